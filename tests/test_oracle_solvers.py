@@ -1,0 +1,171 @@
+"""Pins of oracle/solvers.py: tau_0, g, Alg. 1-5, energies (no GPU)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import layout, ops, solvers as S, spectral
+from tvs_synth import random_field, random_image, step_image, disk_on_ramp
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "operators.json")))
+
+
+def test_tau0_divergence_structure():
+    """Interior div tau_0 = 0 (mixed differences commute); boundary dual rows/cols are not, so
+    tau_0 is not in K in general -- the reason for pre-projecting (reading A1)."""
+    d = random_image(7, 9, 3)
+    dv = ops.div(S.tau0(d))
+    assert np.abs(dv[1:-1, 1:-1]).max() < 1e-15
+    assert np.abs(dv).max() > 0.1
+
+
+def test_g_round_trip():
+    """g(tau_0(d_0)) = d_0 - mean (reading A3, C-12): backward-difference integration inverts tau_0."""
+    d = random_image(8, 11, 5).astype(np.float64)
+    g = S.g_from_tau(S.tau0(d), 8, 11)
+    assert np.abs(g - (d - d.mean())).max() < 1e-13
+
+
+def test_schwarz_1x1_equals_chambolle():
+    """Alg. 2 with M = 1x1 (theta = 1, alpha-hat = 1) is S*K Chambolle iterations."""
+    d0 = random_image(12, 10, 7).astype(np.float64)
+    lay = layout.Layout(12, 10, 1, 1, 0, 0)
+    ta, pa, _ = S.dd_step1(d0, 0.05, lay, 5, 4)
+    tb, pb = S.chambolle_tfs(d0, 0.05, 20)
+    assert np.abs(ta - tb).max() < 1e-12 and np.abs(pa - pb).max() < 1e-12
+    da, _, _ = S.dd_step2(d0, tb, 0.1, lay, 5, 4)
+    db, _ = S.chambolle_irv2(d0, tb, 0.1, 20)
+    assert np.abs(da - db).max() < 1e-12
+
+
+@pytest.mark.parametrize("m2,m1", [(2, 2), (1, 3), (3, 1)])
+def test_localized_tfs_equals_full_grid(m2, m1):
+    """Alg. 5 (localized, block-DCT projection) == Alg. 4 (full grid) per subdomain."""
+    d0 = random_image(12, 10, 7)
+    lay = layout.Layout(12, 10, m2, m1, 2, 2)
+    n2t, n1t = 13, 11
+    whole = S.full_rect(n2t, n1t)
+    p = 0.3 * random_field((2, 2, n2t, n1t), 9)
+    f = spectral.project(S.tau0(d0)) / 0.05
+    r = f - spectral.project(ops.multidiv(p))
+    for m in lay.subdomains():
+        s = lay.rect(m, True)
+        q0 = 0.2 * random_field((2, 2) + S.rect_shape(s), 11) * S.restrict(lay.theta(m, True), whole, s)
+        vl = S._tfs_inner_local(m, lay, p, r, q0, 3, 0.125)
+        vg = S.tfs_inner_global(m, lay, p, f, S.extend(q0, s, whole), 3, 0.125)
+        assert np.abs(S.extend(vl, s, whole) - vg).max() < 1e-12
+
+
+@pytest.mark.parametrize("m2,m1", [(2, 2), (1, 3), (3, 1)])
+def test_localized_irv2_equals_full_grid(m2, m1):
+    d0 = random_image(12, 10, 7)
+    lay = layout.Layout(12, 10, m2, m1, 2, 2)
+    whole = S.full_rect(12, 10)
+    _, _, f = S.irv2_data(d0, S.tau0(d0), 0.1)
+    p = 0.3 * random_field((2, 12, 10), 4)
+    for m in lay.subdomains():
+        s = lay.rect(m, False)
+        q0 = 0.2 * random_field((2,) + S.rect_shape(s), 11) * S.restrict(lay.theta(m, False), whole, s)
+        vl = S._irv2_inner_local(m, lay, p, f, q0, 4, 0.125)
+        vg = S.irv2_inner_global(m, lay, p, f, S.extend(q0, s, whole), 4, 0.125)
+        assert np.abs(S.extend(vl, s, whole) - vg).max() < 1e-12
+
+
+def test_constant_image_fixed_point():
+    d0 = np.full((10, 12), 0.37)
+    lay = layout.Layout(10, 12, 2, 2, 3, 3)
+    tau, p1, _ = S.dd_step1(d0, 0.05, lay, 3, 3)
+    assert np.abs(tau).max() == 0 and np.abs(p1).max() == 0
+    d, p2, _ = S.dd_step2(d0, tau, 0.1, lay, 3, 3)
+    assert np.abs(d - d0).max() < 1e-15
+
+
+def test_feasibility_and_far_boundary():
+    """|p_k| <= 1 pointwise every sweep (B^h); the x-dual on the last column and the
+    y-dual on the last row never move (D+ is 0 there)."""
+    d0 = random_image(14, 12, 2)
+    lay = layout.Layout(14, 12, 2, 2, 4, 4)
+    tau, p1, _ = S.dd_step1(d0, 0.05, lay, 4, 5)
+    for k in range(2):
+        assert np.sqrt(p1[k, 0] ** 2 + p1[k, 1] ** 2).max() <= 1 + 1e-12
+        assert np.all(p1[k, 0][:, -1] == 0) and np.all(p1[k, 1][-1, :] == 0)
+    d, p2, _ = S.dd_step2(d0, tau, 0.1, lay, 4, 5)
+    assert np.sqrt(p2[0] ** 2 + p2[1] ** 2).max() <= 1 + 1e-12
+    assert np.all(p2[0][:, -1] == 0) and np.all(p2[1][-1, :] == 0)
+
+
+def test_tau_divergence_free():
+    d0 = random_image(10, 9, 4)
+    lay = layout.Layout(10, 9, 2, 2, 3, 3)
+    tau, _, _ = S.dd_step1(d0, 0.05, lay, 3, 4)
+    assert np.abs(ops.div(tau)).max() < 1e-10
+
+
+def test_single_domain_monotone_and_gap():
+    """Chambolle's dual energy is non-increasing for t <= 1/8 and the duality gap
+    (C-15) is >= 0 and decreases towards 0."""
+    d0 = random_image(10, 12, 6)
+    _, _, e1 = S.chambolle_tfs(d0, 0.05, 60, trace=True)
+    assert all(b <= a + 1e-9 * a for a, b in zip(e1, e1[1:]))
+    tau, _ = S.chambolle_tfs(d0, 0.05, 400)
+    _, _, e2 = S.chambolle_irv2(d0, tau, 0.1, 60, trace=True)
+    assert all(b <= a + 1e-9 * a for a, b in zip(e2, e2[1:]))
+    gaps = []
+    for it in (20, 200, 2000):
+        d, p = S.chambolle_irv2(d0, tau, 0.1, it)
+        g = S.g_from_tau(tau, 10, 12)
+        gaps.append(S.duality_gap(d - g, p))
+    assert min(gaps) >= -1e-10 and gaps[0] > gaps[1] > gaps[2]
+    gt = []
+    for it in (20, 200, 2000):
+        t, p = S.chambolle_tfs(d0, 0.05, it)
+        gt.append(S.duality_gap(t, p))
+    assert min(gt) >= -1e-10 and gt[0] > gt[1] > gt[2]
+
+
+def test_rof_step_closed_form():
+    """tau = 0 reduces IRV2 to ROF; the vertical step has the exact solution 1/(aL), 1 - 1/(aR)."""
+    g = GOLD["rof_step"]
+    d0 = step_image(g["n2"], g["left"] + g["right"], g["left"])
+    tau = np.zeros((2, g["n2"] + 1, g["left"] + g["right"] + 1))
+    d, _ = S.chambolle_irv2(d0, tau, 1.0 / g["alpha"], 4000)
+    assert np.abs(d[:, :g["left"]] - g["low"]).max() < 1e-6
+    assert np.abs(d[:, g["left"]:] - g["high"]).max() < 1e-6
+
+
+def test_dd_irv2_converges_to_single_domain():
+    """Alg. 2 converges to the single-domain solution (O(n^-1/2)) on a tiny image."""
+    d0 = random_image(16, 16, 8)
+    tau = S.tau0(d0) * 0.0
+    lay = layout.Layout(16, 16, 2, 2, 4, 4)
+    d_ref, _ = S.chambolle_irv2(d0, tau, 0.1, 20000)
+    errs = []
+    for sweeps in (20, 200, 800):
+        d, _, _ = S.dd_step2(d0, tau, 0.1, lay, sweeps, 10)
+        errs.append(np.abs(d - d_ref).max())
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 2e-3
+
+
+def test_dd_tfs_converges_to_single_domain():
+    d0 = random_image(10, 10, 9)
+    lay = layout.Layout(10, 10, 2, 2, 3, 3)
+    t_ref, _ = S.chambolle_tfs(d0, 0.05, 6000)
+    errs = []
+    for sweeps in (10, 60, 240):
+        t, _, _ = S.dd_step1(d0, 0.05, lay, sweeps, 10)
+        errs.append(np.abs(t - t_ref).max())
+    assert errs[0] > errs[1] > errs[2]
+
+
+def test_dd_energy_monotone_diagnostic():
+    """Reading A18: monotone DD energy is a diagnostic (held in all our runs)."""
+    d0 = disk_on_ramp(32, 11)
+    lay = layout.Layout(32, 32, 2, 2, 4, 4)
+    _, _, info = S.dd_step1(d0, 0.05, lay, 10, 5, trace=True)
+    e = info["energies"]
+    assert all(b <= a * (1 + 1e-9) for a, b in zip(e, e[1:]))
+    tau = S.dd_step1(d0, 0.05, lay, 10, 5)[0]
+    _, _, info2 = S.dd_step2(d0, tau, 0.1, lay, 10, 5, trace=True)
+    e = info2["energies"]
+    assert all(b <= a * (1 + 1e-9) for a, b in zip(e, e[1:]))
