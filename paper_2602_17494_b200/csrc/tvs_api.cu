@@ -1,0 +1,832 @@
+// Host driver and C-ABI of the B200-native TV-Stokes Schwarz dual iteration.
+// See include/tvstokes.h for the contract; citations P:<line> refer to PAPER.md.
+#include "../../include/tvstokes.h"
+#include "tvs_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+using namespace tvs;
+
+namespace {
+
+// ----------------------------------------------------------------------------- layout (host)
+
+// Core cuts c_k = floor(k n / m) and inclusive subdomain ranges
+// [c_k - floor(s/2), c_{k+1} - 1 + ceil(s/2)] clipped (readings A6, A8).
+bool axis_ranges(int n, int m, int s, std::vector<int> &lo, std::vector<int> &hi,
+                 std::string &err) {
+  if (m < 1 || n < 2 || m > n) {
+    err = "layout: need 1 <= m <= n and n >= 2";
+    return false;
+  }
+  std::vector<long long> cut(m + 1);
+  for (int k = 0; k <= m; ++k) cut[k] = (long long)k * n / m;
+  if (m > 1) {
+    if (s < 1) {
+      err = "layout: overlap must be >= 1 when m > 1";
+      return false;
+    }
+    for (int k = 0; k < m; ++k)
+      if (cut[k + 1] - cut[k] <= s) {
+        err = "layout: core width must exceed the overlap (reading A17)";
+        return false;
+      }
+  }
+  lo.assign(m, 0);
+  hi.assign(m, 0);
+  for (int k = 0; k < m; ++k) {
+    long long a = cut[k] - (k > 0 ? s / 2 : 0);
+    long long b = cut[k + 1] - 1 + (k < m - 1 ? (s + 1) / 2 : 0);
+    lo[k] = (int)std::max(0LL, a);
+    hi[k] = (int)std::min((long long)n - 1, b);
+  }
+  return true;
+}
+
+// Partition of unity (reading A7 of P:1303-1308): linear ramps across each shared band [L, R]:
+// theta_k = (R - x + 1)/(s + 1), theta_{k+1} = (x - L + 1)/(s + 1); 1 elsewhere in the range.
+double axis_theta(const std::vector<int> &lo, const std::vector<int> &hi, int s, int k, int x) {
+  int m = (int)lo.size();
+  if (x < lo[k] || x > hi[k]) return 0.0;
+  if (k + 1 < m && x >= lo[k + 1]) return (double)(hi[k] - x + 1) / (s + 1.0);
+  if (k > 0 && x <= hi[k - 1]) return (double)(x - lo[k] + 1) / (s + 1.0);
+  return 1.0;
+}
+
+float alpha_hat(int m2, int m1) {
+  if (m1 == 1 && m2 == 1) return 1.f;
+  if (m1 == 1 || m2 == 1) return 0.5f;
+  return 0.25f;
+}
+
+inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// ----------------------------------------------------------------------------- device memory
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct ProjBatch {
+  int ntiles = 0, AT = 0, AP = 0, ldn = 0, nchains = 0;
+  std::vector<ProjTile> tiles;
+  ProjTile *d_tiles = nullptr;
+  int *d_first = nullptr;
+  float *q = nullptr;       // input, [tile][AT][ldq]
+  int ldq = 0;
+  float *G = nullptr;       // output, [tile][2][AP][ldG]
+  int ldG = 0;
+  float *qhat = nullptr;
+  double *z = nullptr, *rinv = nullptr;
+  float *phx = nullptr, *phy = nullptr;
+  GemmDesc *d_fwd = nullptr, *d_inv = nullptr;
+  int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
+  double fwd_flops = 0, inv_flops = 0, solve_bytes = 0;
+};
+
+struct Plan {
+  int n2 = 0, n1 = 0, step = 0;
+  tvs_layout L{};
+  int G2 = 0, G1 = 0;   // step grid
+  int M2 = 0, M1 = 0, M = 0;
+  float ahat = 1.f;
+  std::vector<SubDesc> subs;
+  Geo geo{};
+  int ld = 0;           // pitch of global planes
+  int planes = 0;       // dual planes (2 or 4)
+  SubDesc *d_subs = nullptr;
+  float *d_thy = nullptr, *d_thx = nullptr;
+  int2 *d_covy = nullptr, *d_covx = nullptr;
+  int *d_loy = nullptr, *d_lox = nullptr;
+  float *v[2] = {nullptr, nullptr};
+  float *om = nullptr, *p = nullptr, *f = nullptr;
+  double *g0 = nullptr;
+  int *d_bad = nullptr;
+  // step 1 only
+  float *vtmp = nullptr, *q = nullptr, *gphi = nullptr;
+  float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
+  ProjBatch local, global;
+  int64_t sum_S = 0, sum_T = 0;
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+};
+
+struct Tables {
+  int n = 0, ld = 0;
+  float *cf = nullptr, *cn = nullptr, *sn = nullptr;
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+};
+
+struct PendingEv {
+  int fam;
+  cudaEvent_t a, b;
+  double bytes, flops;
+};
+
+}  // namespace
+
+struct tvs_ctx {
+  int device = 0, rank = 0, world = 1;
+  std::string err;
+  std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
+  std::map<int, std::unique_ptr<Tables>> tables;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<PendingEv> pending;
+  int64_t counts[TVS_NUM_KERNEL_FAMILIES] = {0};
+  double ms[TVS_NUM_KERNEL_FAMILIES] = {0}, bytes[TVS_NUM_KERNEL_FAMILIES] = {0},
+         flops[TVS_NUM_KERNEL_FAMILIES] = {0};
+  int64_t launches = 0;
+  // scratch for denoise / host variants
+  std::unique_ptr<DevBuf> tau_scratch, h_d0, h_d, h_tau;
+};
+
+namespace {
+
+enum Fam { F_SWEEP2 = 0, F_SWEEP1, F_PREDIV, F_FWD, F_SOLVE, F_INV, F_OTHER };
+
+tvs_status fail(tvs_ctx *c, tvs_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? TVS_ENOMEM : TVS_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                      \
+  } while (0)
+
+template <class T>
+tvs_status dalloc(tvs_ctx *ctx, std::vector<std::unique_ptr<DevBuf>> &owner, T **out, size_t n) {
+  auto b = std::make_unique<DevBuf>();
+  size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&b->p, bytes);
+  if (e != cudaSuccess)
+    return fail(ctx, TVS_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+  e = cudaMemset(b->p, 0, bytes);
+  if (e != cudaSuccess) return fail(ctx, TVS_ECUDA, "cudaMemset: %s", cudaGetErrorString(e));
+  b->bytes = bytes;
+  *out = reinterpret_cast<T *>(b->p);
+  owner.push_back(std::move(b));
+  return TVS_OK;
+}
+
+template <class T>
+tvs_status upload(tvs_ctx *ctx, std::vector<std::unique_ptr<DevBuf>> &owner, T **out,
+                  const std::vector<T> &host) {
+  tvs_status st = dalloc(ctx, owner, out, host.size());
+  if (st) return st;
+  if (!host.empty()) CK(cudaMemcpy(*out, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return TVS_OK;
+}
+
+#define TRY(x)                  \
+  do {                          \
+    tvs_status s_ = (x);        \
+    if (s_ != TVS_OK) return s_; \
+  } while (0)
+
+// Kernel launch bracketed by profiling events (on the launching stream) when enabled.
+template <class F>
+tvs_status run(tvs_ctx *ctx, cudaStream_t s, int fam, double bytes, double flops, F &&launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (ctx->profiling) {
+    while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->ev_pool.push_back(e);
+    }
+    a = ctx->ev_pool[ctx->ev_used++];
+    b = ctx->ev_pool[ctx->ev_used++];
+    CK(cudaEventRecord(a, s));
+  }
+  cudaError_t e = launch();
+  if (e != cudaSuccess) return fail(ctx, TVS_ECUDA, "kernel launch (family %d): %s", fam, cudaGetErrorString(e));
+  ctx->launches++;
+  if (ctx->profiling) {
+    CK(cudaEventRecord(b, s));
+    ctx->pending.push_back({fam, a, b, bytes, flops});
+  }
+  return TVS_OK;
+}
+
+tvs_status collect_profile(tvs_ctx *ctx) {
+  for (auto &p : ctx->pending) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    ctx->counts[p.fam]++;
+    ctx->ms[p.fam] += ms;
+    ctx->bytes[p.fam] += p.bytes;
+    ctx->flops[p.fam] += p.flops;
+  }
+  ctx->pending.clear();
+  ctx->ev_used = 0;
+  return TVS_OK;
+}
+
+// ----------------------------------------------------------------------------- plans
+
+tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
+  auto it = ctx->tables.find(n);
+  if (it != ctx->tables.end()) {
+    *out = it->second.get();
+    return TVS_OK;
+  }
+  auto t = std::make_unique<Tables>();
+  t->n = n;
+  t->ld = round_up(n, 4);
+  size_t el = (size_t)n * t->ld;
+  TRY(dalloc(ctx, t->bufs, &t->cf, el));
+  TRY(dalloc(ctx, t->bufs, &t->cn, el));
+  TRY(dalloc(ctx, t->bufs, &t->sn, el));
+  CK(launch_dct_tables(n, t->cf, t->cn, t->sn, t->ld, 0));
+  CK(cudaDeviceSynchronize());
+  *out = t.get();
+  ctx->tables[n] = std::move(t);
+  return TVS_OK;
+}
+
+// Build the projection batch for tiles (chains = distinct row ranges).
+tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
+                      int n2t, int n1t, float *q, int ldq, float *G, int ldG, const Tables *T) {
+  B.tiles = tiles_in;
+  B.ntiles = (int)tiles_in.size();
+  std::map<std::pair<int, int>, int> chain_of;
+  std::vector<int> first;
+  for (int i = 0; i < B.ntiles; ++i) {
+    auto key = std::make_pair(B.tiles[i].ty0, B.tiles[i].ty1);
+    auto it = chain_of.find(key);
+    if (it == chain_of.end()) {
+      chain_of[key] = (int)first.size();
+      first.push_back(i);
+    }
+    B.tiles[i].chain = chain_of[key];
+    B.AT = std::max(B.AT, B.tiles[i].ty1 - B.tiles[i].ty0 + 1);
+    B.AP = std::max(B.AP, B.tiles[i].py1 - B.tiles[i].ty0 + 1);
+  }
+  B.nchains = (int)first.size();
+  B.ldn = round_up(n1t, 4);
+  B.q = q;
+  B.ldq = ldq;
+  B.G = G;
+  B.ldG = ldG;
+  TRY(upload(ctx, P.bufs, &B.d_tiles, B.tiles));
+  TRY(upload(ctx, P.bufs, &B.d_first, first));
+  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.z, (size_t)B.ntiles * B.AT * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
+  std::vector<GemmDesc> fwd, inv;
+  for (int i = 0; i < B.ntiles; ++i) {
+    const ProjTile &t = B.tiles[i];
+    int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
+    int no = t.py1 - t.ty0 + 1, bo = t.px1 - t.tx0 + 1;
+    fwd.push_back({q + (size_t)i * B.AT * ldq, T->cf + (size_t)t.tx0 * T->ld,
+                   B.qhat + (size_t)i * B.AT * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
+    inv.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->sn + t.tx0,
+                   G + ((size_t)i * 2 + 0) * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+    inv.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cn + t.tx0,
+                   G + ((size_t)i * 2 + 1) * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+    B.fwdM = std::max(B.fwdM, nt);
+    B.fwdN = std::max(B.fwdN, n1t);
+    B.invM = std::max(B.invM, no);
+    B.invN = std::max(B.invN, bo);
+    B.fwd_flops += 2.0 * nt * bt * n1t;
+    B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
+    // fp64 solve: read qhat (4) + rinv twice (16) + z write/read (16) + phx/phy (8)
+    B.solve_bytes += (double)nt * n1t * 44.0;
+  }
+  TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
+  TRY(upload(ctx, P.bufs, &B.d_inv, inv));
+  CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
+  CK(cudaDeviceSynchronize());
+  return TVS_OK;
+}
+
+tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan **out) {
+  auto key = std::make_tuple(n2, n1, L.m2, L.m1, L.overlap_y, L.overlap_x, step);
+  auto it = ctx->plans.find(key);
+  if (it != ctx->plans.end()) {
+    *out = it->second.get();
+    return TVS_OK;
+  }
+  auto P = std::make_unique<Plan>();
+  P->n2 = n2;
+  P->n1 = n1;
+  P->L = L;
+  P->step = step;
+  P->G2 = step == 1 ? n2 + 1 : n2;
+  P->G1 = step == 1 ? n1 + 1 : n1;
+  P->M2 = L.m2;
+  P->M1 = L.m1;
+  P->M = L.m2 * L.m1;
+  P->ahat = alpha_hat(L.m2, L.m1);
+  P->planes = step == 1 ? 4 : 2;
+  std::vector<int> ly, hy, lx, hx;
+  std::string err;
+  // the layout lives on Omega~ (reading A6); Omega_m = Omega~_m cap Omega
+  if (!axis_ranges(n2 + 1, L.m2, L.overlap_y, ly, hy, err) ||
+      !axis_ranges(n1 + 1, L.m1, L.overlap_x, lx, hx, err))
+    return fail(ctx, TVS_ELAYOUT, "%s", err.c_str());
+  const int G2 = P->G2, G1 = P->G1;
+  Geo &g = P->geo;
+  g.M = P->M;
+  std::vector<float> thy, thx;
+  for (int a = 0; a < L.m2; ++a)
+    for (int b = 0; b < L.m1; ++b) {
+      SubDesc s{};
+      s.y0 = ly[a];
+      s.y1 = std::min(hy[a], G2 - 1);
+      s.x0 = lx[b];
+      s.x1 = std::min(hx[b], G1 - 1);
+      s.py1 = std::min(s.y1 + 1, G2 - 1);
+      s.px1 = std::min(s.x1 + 1, G1 - 1);
+      s.ty1 = std::min(s.py1 + 1, G2 - 1);
+      s.tx1 = std::min(s.px1 + 1, G1 - 1);
+      s.iy = a;
+      s.ix = b;
+      if (s.y1 - s.y0 + 1 < 2 || s.x1 - s.x0 + 1 < 2)
+        return fail(ctx, TVS_ELAYOUT, "layout: subdomain smaller than 2 x 2");
+      P->subs.push_back(s);
+      g.A = std::max(g.A, s.y1 - s.y0 + 1);
+      g.B = std::max(g.B, s.x1 - s.x0 + 1);
+      g.AP = std::max(g.AP, s.py1 - s.y0 + 1);
+      g.BP = std::max(g.BP, s.px1 - s.x0 + 1);
+      g.AT = std::max(g.AT, s.ty1 - s.y0 + 1);
+      g.BT = std::max(g.BT, s.tx1 - s.x0 + 1);
+      P->sum_S += (int64_t)(s.y1 - s.y0 + 1) * (s.x1 - s.x0 + 1);
+      P->sum_T += (int64_t)(s.ty1 - s.y0 + 1) * (s.tx1 - s.x0 + 1);
+    }
+  g.ldS = round_up(g.B, 4);
+  g.ldP = round_up(g.BP, 4);
+  g.ldT = round_up(g.BT, 4);
+  thy.assign((size_t)L.m2 * g.A, 0.f);
+  thx.assign((size_t)L.m1 * g.B, 0.f);
+  for (int a = 0; a < L.m2; ++a)
+    for (int i = ly[a]; i <= std::min(hy[a], G2 - 1); ++i)
+      thy[(size_t)a * g.A + (i - ly[a])] = (float)axis_theta(ly, hy, L.overlap_y, a, i);
+  for (int b = 0; b < L.m1; ++b)
+    for (int j = lx[b]; j <= std::min(hx[b], G1 - 1); ++j)
+      thx[(size_t)b * g.B + (j - lx[b])] = (float)axis_theta(lx, hx, L.overlap_x, b, j);
+  // coverage of every grid row / column by subdomain indices (at most 2 per axis)
+  std::vector<int2> covy(G2), covx(G1);
+  for (int i = 0; i < G2; ++i) {
+    int k0 = -1, c = 0;
+    for (int a = 0; a < L.m2; ++a)
+      if (i >= ly[a] && i <= hy[a]) {
+        if (k0 < 0) k0 = a;
+        ++c;
+      }
+    covy[i] = make_int2(k0, c);
+  }
+  for (int j = 0; j < G1; ++j) {
+    int k0 = -1, c = 0;
+    for (int b = 0; b < L.m1; ++b)
+      if (j >= lx[b] && j <= hx[b]) {
+        if (k0 < 0) k0 = b;
+        ++c;
+      }
+    covx[j] = make_int2(k0, c);
+  }
+  P->ld = round_up(G1, 4);
+  TRY(upload(ctx, P->bufs, &P->d_subs, P->subs));
+  TRY(upload(ctx, P->bufs, &P->d_thy, thy));
+  TRY(upload(ctx, P->bufs, &P->d_thx, thx));
+  TRY(upload(ctx, P->bufs, &P->d_covy, covy));
+  TRY(upload(ctx, P->bufs, &P->d_covx, covx));
+  TRY(upload(ctx, P->bufs, &P->d_loy, ly));
+  TRY(upload(ctx, P->bufs, &P->d_lox, lx));
+  const int C = P->planes;
+  size_t vsz = (size_t)g.M * C * g.A * g.ldS;
+  TRY(dalloc(ctx, P->bufs, &P->v[0], vsz));
+  TRY(dalloc(ctx, P->bufs, &P->v[1], vsz));
+  TRY(dalloc(ctx, P->bufs, &P->p, (size_t)C * G2 * P->ld));
+  TRY(dalloc(ctx, P->bufs, &P->d_bad, 1));
+  if (step == 2) {
+    TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * g.AP * g.ldP));
+    TRY(dalloc(ctx, P->bufs, &P->f, (size_t)G2 * P->ld));
+    TRY(dalloc(ctx, P->bufs, &P->g0, (size_t)G1));
+  } else {
+    Tables *T = nullptr;
+    TRY(get_tables(ctx, G1, &T));
+    TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * 2 * g.AP * g.ldP));
+    TRY(dalloc(ctx, P->bufs, &P->vtmp, vsz));
+    TRY(dalloc(ctx, P->bufs, &P->q, (size_t)g.M * g.AT * g.ldT));
+    TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)g.M * 2 * g.AP * g.ldP));
+    size_t pl = (size_t)G2 * P->ld;
+    TRY(dalloc(ctx, P->bufs, &P->f, 2 * pl));
+    TRY(dalloc(ctx, P->bufs, &P->t0, 2 * pl));
+    TRY(dalloc(ctx, P->bufs, &P->w, 2 * pl));
+    TRY(dalloc(ctx, P->bufs, &P->r, 2 * pl));
+    TRY(dalloc(ctx, P->bufs, &P->qg, pl));
+    TRY(dalloc(ctx, P->bufs, &P->Gg, 2 * pl));
+    std::vector<ProjTile> lt;
+    for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
+    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T));
+    std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, G2 - 1, G1 - 1, 0, 0}};
+    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->ld, P->Gg, P->ld, T));
+  }
+  *out = P.get();
+  ctx->plans[key] = std::move(P);
+  return TVS_OK;
+}
+
+// grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).
+tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s) {
+  const int G2 = P.G2, G1 = P.G1;
+  TRY(run(ctx, s, F_FWD, 0, B.fwd_flops,
+          [&] { return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s); }));
+  TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
+    return launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z, B.phx,
+                             B.phy, B.AP, s);
+  }));
+  TRY(run(ctx, s, F_INV, 0, B.inv_flops,
+          [&] { return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s); }));
+  return TVS_OK;
+}
+
+tvs_status check_common(tvs_ctx *ctx, int32_t n2, int32_t n1, tvs_layout L, tvs_iters it) {
+  if (!ctx) return TVS_EINVAL;
+  if (n2 < 2 || n1 < 2) return fail(ctx, TVS_EINVAL, "image must be at least 2 x 2");
+  if (!(it.t > 0.f && it.t <= 0.125f))
+    return fail(ctx, TVS_EINVAL, "dual step t must lie in (0, 1/8] (P:784)");
+  if (it.sweeps < 0 || it.inner < 0) return fail(ctx, TVS_EINVAL, "negative schedule");
+  if (L.m2 < 1 || L.m1 < 1) return fail(ctx, TVS_ELAYOUT, "layout needs m2, m1 >= 1");
+  return TVS_OK;
+}
+
+struct CallTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~CallTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+tvs_status finish_call(tvs_ctx *ctx, Plan &P, cudaStream_t s, CallTimer &tm, tvs_stats *st,
+                       int64_t launches0) {
+  CK(cudaEventRecord(tm.b, s));
+  CK(cudaStreamSynchronize(s));
+  TRY(collect_profile(ctx));
+  int bad = 0;
+  CK(cudaMemcpy(&bad, P.d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (st) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, tm.a, tm.b));
+    st->seconds = ms * 1e-3;
+    st->launches = ctx->launches - launches0;
+  }
+  if (bad) return fail(ctx, TVS_ENUMERIC, "non-finite value in the dual after a sweep");
+  return TVS_OK;
+}
+
+tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2, int32_t n1,
+                      float lambda, tvs_layout L, tvs_iters it, float *d, float *p_out,
+                      tvs_stats *st, cudaStream_t s) {
+  TRY(check_common(ctx, n2, n1, L, it));
+  if (!(lambda > 0.f)) return fail(ctx, TVS_EINVAL, "lambda must be > 0");
+  if (!tau || !d0 || !d) return fail(ctx, TVS_EINVAL, "null pointer");
+  Plan *P = nullptr;
+  TRY(get_plan(ctx, n2, n1, L, 2, &P));
+  CallTimer tm;
+  CK(cudaEventCreate(&tm.a));
+  CK(cudaEventCreate(&tm.b));
+  CK(cudaEventRecord(tm.a, s));
+  const int64_t l0 = ctx->launches;
+  const Geo g = P->geo;
+  const int ld = P->ld, ldt = n1 + 1;
+  const float alpha = 1.f / lambda;                       // reading A4
+  const size_t pl = (size_t)n2 * ld;
+  const float *tau1 = tau, *tau2 = tau + (size_t)(n2 + 1) * (n1 + 1);
+  CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_g_row0(tau2, ldt, n1, P->g0, s); }));
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, s);
+  }));
+  CK(cudaMemsetAsync(P->p, 0, 2 * pl * sizeof(float), s));
+  CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 2 * g.A * g.ldS * sizeof(float), s));
+  int cur = 0;
+  const double sweep_bytes = 20.0 * (double)P->sum_S;    // v read 8 + omega0 4 + v write 8
+  for (int n = 0; n < it.sweeps; ++n) {
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_omega0_2(P->d_subs, g, P->d_thy, P->d_thx, P->f, P->p, P->p + pl, ld, n2, n1,
+                             P->om, s);
+    }));
+    for (int k = 0; k < it.inner; ++k) {
+      TRY(run(ctx, s, F_SWEEP2, sweep_bytes, 0, [&] {
+        return launch_sweep2(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->om, P->v[cur ^ 1],
+                             n2, n1, it.t, s);
+      }));
+      cur ^= 1;
+    }
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_combine(P->d_subs, g, 2, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M1,
+                            P->v[cur], P->p, ld, n2, n1, P->ahat, P->d_bad, s);
+    }));
+  }
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha, d, s);
+  }));
+  if (p_out)
+    for (int c = 0; c < 2; ++c)
+      CK(cudaMemcpy2DAsync(p_out + (size_t)c * n2 * n1, n1 * sizeof(float), P->p + c * pl,
+                           ld * sizeof(float), n1 * sizeof(float), n2, cudaMemcpyDeviceToDevice, s));
+  if (st) {
+    memset(st, 0, sizeof *st);
+    st->pixel_updates = P->sum_S * (int64_t)it.sweeps * it.inner;
+    st->bytes_sweep = sweep_bytes * it.sweeps * it.inner;
+  }
+  return finish_call(ctx, *P, s, tm, st, l0);
+}
+
+tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
+                      tvs_layout L, tvs_iters it, float *tau_out, float *p_out, tvs_stats *st,
+                      cudaStream_t s) {
+  TRY(check_common(ctx, n2, n1, L, it));
+  if (!(delta > 0.f)) return fail(ctx, TVS_EINVAL, "delta must be > 0");
+  if (!d0 || !tau_out) return fail(ctx, TVS_EINVAL, "null pointer");
+  Plan *P = nullptr;
+  TRY(get_plan(ctx, n2, n1, L, 1, &P));
+  CallTimer tm;
+  CK(cudaEventCreate(&tm.a));
+  CK(cudaEventCreate(&tm.b));
+  CK(cudaEventRecord(tm.a, s));
+  const int64_t l0 = ctx->launches;
+  const Geo g = P->geo;
+  const int G2 = P->G2, G1 = P->G1, ld = P->ld;
+  const size_t pl = (size_t)G2 * ld;
+  CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
+  // f = delta^{-1} P tau_0 (tau_0 pre-projected, reading A1)
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_tau0(d0, n2, n1, P->t0, ld, s); }));
+  TRY(run(ctx, s, F_OTHER, 0, 0,
+          [&] { return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, s); }));
+  TRY(project_batch(ctx, *P, P->global, s));
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_axpby2(P->t0, P->Gg, nullptr, ld, G2, G1, 1.f / delta, -1.f / delta, 0.f, P->f,
+                         s);
+  }));
+  CK(cudaMemsetAsync(P->p, 0, 4 * pl * sizeof(float), s));
+  CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 4 * g.A * g.ldS * sizeof(float), s));
+  // r = f - P multidiv p = f - w + grad phi, phi = Delta^dagger div w (global, once per sweep)
+  auto residual = [&](float *out, float scale) -> tvs_status {
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, s); }));
+    TRY(run(ctx, s, F_OTHER, 0, 0,
+            [&] { return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, s); }));
+    TRY(project_batch(ctx, *P, P->global, s));
+    return run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, s);
+    });
+  };
+  int cur = 0;
+  const double prediv_bytes = 16.0 * P->sum_S + 4.0 * P->sum_T;
+  const double sweep_bytes = 48.0 * (double)P->sum_S;
+  for (int n = 0; n < it.sweeps; ++n) {
+    TRY(residual(P->r, 1.f));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_load_tp(P->d_subs, g, P->d_thy, P->d_thx, P->p, ld, G2, G1, P->vtmp, s);
+    }));
+    TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
+            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, s); }));
+    TRY(project_batch(ctx, *P, P->local, s));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_omega0_1(P->d_subs, g, P->r, ld, P->vtmp, P->gphi, g.ldP, G2, G1, P->om, s);
+    }));
+    for (int k = 0; k < it.inner; ++k) {
+      TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
+              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, s); }));
+      TRY(project_batch(ctx, *P, P->local, s));
+      TRY(run(ctx, s, F_SWEEP1, sweep_bytes, 0, [&] {
+        return launch_sweep1(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->gphi, g.ldP, P->om,
+                             P->v[cur ^ 1], G2, G1, it.t, s);
+      }));
+      cur ^= 1;
+    }
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_combine(P->d_subs, g, 4, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M1,
+                            P->v[cur], P->p, ld, G2, G1, P->ahat, P->d_bad, s);
+    }));
+  }
+  // tau = P tau_0 - delta P multidiv p = delta r^S
+  TRY(residual(P->r, delta));
+  for (int c = 0; c < 2; ++c)
+    CK(cudaMemcpy2DAsync(tau_out + (size_t)c * G2 * G1, G1 * sizeof(float), P->r + c * pl,
+                         ld * sizeof(float), G1 * sizeof(float), G2, cudaMemcpyDeviceToDevice, s));
+  if (p_out)
+    for (int c = 0; c < 4; ++c)
+      CK(cudaMemcpy2DAsync(p_out + (size_t)c * G2 * G1, G1 * sizeof(float), P->p + c * pl,
+                           ld * sizeof(float), G1 * sizeof(float), G2, cudaMemcpyDeviceToDevice, s));
+  if (st) {
+    memset(st, 0, sizeof *st);
+    st->pixel_updates = P->sum_S * (int64_t)it.sweeps * it.inner;
+    st->bytes_sweep = (sweep_bytes + prediv_bytes) * it.sweeps * it.inner;
+    st->flops_proj = (P->local.fwd_flops + P->local.inv_flops) * it.sweeps * (it.inner + 1) +
+                     (P->global.fwd_flops + P->global.inv_flops) * (it.sweeps + 2);
+  }
+  return finish_call(ctx, *P, s, tm, st, l0);
+}
+
+}  // namespace
+
+// ============================================================================= C ABI
+
+extern "C" {
+
+tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint8_t *nccl_id) {
+  if (!out) return TVS_EINVAL;
+  *out = nullptr;
+  if (world != 1 || rank != 0) {
+    (void)nccl_id;
+    return TVS_EINVAL;   // multi-GPU contexts are created by the NCCL-enabled build (see DESIGN)
+  }
+  auto *c = new tvs_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return TVS_ECUDA;
+  }
+  *out = c;
+  return TVS_OK;
+}
+
+tvs_status tvs_destroy(tvs_ctx *ctx) {
+  if (!ctx) return TVS_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  delete ctx;
+  return TVS_OK;
+}
+
+const char *tvs_last_error(const tvs_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+tvs_status tvs_nccl_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return TVS_EINVAL;
+  memset(id_out, 0, 128);
+  return TVS_ENCCL;
+}
+
+tvs_status tvs_owned_rows(int32_t n2, int32_t n1, const tvs_layout *Lp, int rank, int world,
+                          int32_t *row_begin, int32_t *row_end) {
+  (void)n1;
+  if (!Lp || !row_begin || !row_end || world < 1 || rank < 0 || rank >= world) return TVS_EINVAL;
+  const tvs_layout L = *Lp;
+  if (L.m2 < world) return TVS_ELAYOUT;
+  int n = n2 + 1;
+  int k0 = (int)((long long)rank * L.m2 / world), k1 = (int)((long long)(rank + 1) * L.m2 / world);
+  *row_begin = (int32_t)((long long)k0 * n / L.m2);
+  *row_end = (int32_t)((long long)k1 * n / L.m2);
+  return TVS_OK;
+}
+
+tvs_status tvs_layout_range(int32_t n, int32_t m, int32_t s, int32_t k, int32_t *lo, int32_t *hi) {
+  std::vector<int> l, h;
+  std::string err;
+  if (!lo || !hi) return TVS_EINVAL;
+  if (!axis_ranges(n, m, s, l, h, err)) return TVS_ELAYOUT;
+  if (k < 0 || k >= m) return TVS_EINVAL;
+  *lo = l[k];
+  *hi = h[k];
+  return TVS_OK;
+}
+
+tvs_status tvs_layout_theta(int32_t n, int32_t m, int32_t s, int32_t k, int32_t x, double *theta) {
+  std::vector<int> l, h;
+  std::string err;
+  if (!theta) return TVS_EINVAL;
+  if (!axis_ranges(n, m, s, l, h, err)) return TVS_ELAYOUT;
+  if (k < 0 || k >= m || x < 0 || x >= n) return TVS_EINVAL;
+  *theta = axis_theta(l, h, s, k, x);
+  return TVS_OK;
+}
+
+tvs_status tv_stokes_step1(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
+                           const tvs_layout *L, const tvs_iters *it, float *tau, float *p,
+                           tvs_stats *st, void *cuda_stream) {
+  if (!ctx) return TVS_EINVAL;
+  if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
+  cudaSetDevice(ctx->device);
+  return step1_impl(ctx, d0, n2, n1, delta, *L, *it, tau, p, st, (cudaStream_t)cuda_stream);
+}
+
+tvs_status tv_stokes_step2(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2,
+                           int32_t n1, float lambda, const tvs_layout *L, const tvs_iters *it,
+                           float *d, float *p, tvs_stats *st, void *cuda_stream) {
+  if (!ctx) return TVS_EINVAL;
+  if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
+  cudaSetDevice(ctx->device);
+  return step2_impl(ctx, tau, d0, n2, n1, lambda, *L, *it, d, p, st, (cudaStream_t)cuda_stream);
+}
+
+tvs_status tv_stokes_denoise(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
+                             float lambda, const tvs_layout *Lp, const tvs_iters *it1p,
+                             const tvs_iters *it2p, float *d, float *tau, tvs_stats *st1,
+                             tvs_stats *st2, void *cuda_stream) {
+  if (!ctx) return TVS_EINVAL;
+  if (!Lp || !it1p || !it2p) return fail(ctx, TVS_EINVAL, "null layout or schedule");
+  const tvs_layout L = *Lp;
+  const tvs_iters it1 = *it1p, it2 = *it2p;
+  cudaSetDevice(ctx->device);
+  float *tau_buf = tau;
+  if (!tau_buf) {
+    size_t need = (size_t)2 * (n2 + 1) * (n1 + 1) * sizeof(float);
+    if (!ctx->tau_scratch || ctx->tau_scratch->bytes < need) {
+      ctx->tau_scratch = std::make_unique<DevBuf>();
+      if (cudaMalloc(&ctx->tau_scratch->p, need) != cudaSuccess)
+        return fail(ctx, TVS_ENOMEM, "cudaMalloc tau scratch");
+      ctx->tau_scratch->bytes = need;
+    }
+    tau_buf = (float *)ctx->tau_scratch->p;
+  }
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  tvs_status st = step1_impl(ctx, d0, n2, n1, delta, L, it1, tau_buf, nullptr, st1, s);
+  if (st) return st;
+  return step2_impl(ctx, tau_buf, d0, n2, n1, lambda, L, it2, d, nullptr, st2, s);
+}
+
+static tvs_status ensure(tvs_ctx *ctx, std::unique_ptr<DevBuf> &b, size_t bytes) {
+  if (!b || b->bytes < bytes) {
+    b = std::make_unique<DevBuf>();
+    if (cudaMalloc(&b->p, bytes) != cudaSuccess) return fail(ctx, TVS_ENOMEM, "cudaMalloc host-staging");
+    b->bytes = bytes;
+  }
+  return TVS_OK;
+}
+
+tvs_status tv_stokes_denoise_host(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1,
+                                  float delta, float lambda, const tvs_layout *L,
+                                  const tvs_iters *it1, const tvs_iters *it2, float *d,
+                                  float *tau, tvs_stats *st1, tvs_stats *st2, void *cuda_stream) {
+  if (!ctx || !d0 || !d) return TVS_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  size_t img = (size_t)n2 * n1 * sizeof(float), tb = (size_t)2 * (n2 + 1) * (n1 + 1) * sizeof(float);
+  TRY(ensure(ctx, ctx->h_d0, img));
+  TRY(ensure(ctx, ctx->h_d, img));
+  TRY(ensure(ctx, ctx->h_tau, tb));
+  CK(cudaMemcpyAsync(ctx->h_d0->p, d0, img, cudaMemcpyHostToDevice, s));
+  tvs_status st = tv_stokes_denoise(ctx, (const float *)ctx->h_d0->p, n2, n1, delta, lambda, L,
+                                    it1, it2, (float *)ctx->h_d->p, (float *)ctx->h_tau->p, st1,
+                                    st2, cuda_stream);
+  if (st) return st;
+  CK(cudaMemcpyAsync(d, ctx->h_d->p, img, cudaMemcpyDeviceToHost, s));
+  if (tau) CK(cudaMemcpyAsync(tau, ctx->h_tau->p, tb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return TVS_OK;
+}
+
+tvs_status tvs_set_profiling(tvs_ctx *ctx, int enable) {
+  if (!ctx) return TVS_EINVAL;
+  ctx->profiling = enable != 0;
+  return TVS_OK;
+}
+
+tvs_status tvs_kernel_times(tvs_ctx *ctx, int64_t counts[TVS_NUM_KERNEL_FAMILIES],
+                            double ms[TVS_NUM_KERNEL_FAMILIES],
+                            double bytes[TVS_NUM_KERNEL_FAMILIES],
+                            double flops[TVS_NUM_KERNEL_FAMILIES]) {
+  if (!ctx) return TVS_EINVAL;
+  for (int i = 0; i < TVS_NUM_KERNEL_FAMILIES; ++i) {
+    if (counts) counts[i] = ctx->counts[i];
+    if (ms) ms[i] = ctx->ms[i];
+    if (bytes) bytes[i] = ctx->bytes[i];
+    if (flops) flops[i] = ctx->flops[i];
+  }
+  return TVS_OK;
+}
+
+tvs_status tvs_reset_kernel_times(tvs_ctx *ctx) {
+  if (!ctx) return TVS_EINVAL;
+  for (int i = 0; i < TVS_NUM_KERNEL_FAMILIES; ++i) {
+    ctx->counts[i] = 0;
+    ctx->ms[i] = ctx->bytes[i] = ctx->flops[i] = 0;
+  }
+  return TVS_OK;
+}
+
+}  // extern "C"

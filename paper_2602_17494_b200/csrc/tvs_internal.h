@@ -1,0 +1,91 @@
+// Internal declarations shared by the kernels (tvs_kernels.cu) and the host driver (tvs_api.cu).
+// Nothing here is part of the ABI (see include/tvstokes.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tvs {
+
+// One overlapping subdomain Gamma_m of the step grid (Omega~ for step 1, Omega for step 2).
+// S = [y0, y1] x [x0, x1]; S+ = [y0, py1] x [x0, px1] (one more row/col, clipped, reading A12);
+// T = [y0, ty1] x [x0, tx1] (S+ plus one more row/col, clipped: support of div E_{S+}).
+struct SubDesc {
+  int y0, y1, x0, x1;
+  int py1, px1;
+  int ty1, tx1;
+  int iy, ix;   // subdomain indices (m2, m1)
+};
+
+// One tile of the batched projection phi = R_T Delta^dagger E_T q, grad phi on [ty0..py1]x[tx0..px1].
+struct ProjTile {
+  int ty0, ty1, tx0, tx1;
+  int py1, px1;
+  int chain;    // index of the precomputed Thomas pivots (distinct row range [ty0, ty1])
+  int pad;
+};
+
+// Batched fp32 GEMM descriptor: C[M x N] = A[M x K] * B[K x N], all row-major.
+struct GemmDesc {
+  const float *A;
+  const float *B;
+  float *C;
+  int M, N, K;
+  int lda, ldb, ldc;
+};
+
+// Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
+struct Geo {
+  int M;          // number of subdomains in the batch
+  int A, B;       // rows/cols of S (max)
+  int AP, BP;     // rows/cols of S+ (max)
+  int AT, BT;     // rows/cols of T (max)
+  int ldS, ldP, ldT;  // pitches (floats) of S, S+, T planes
+};
+
+// ---------------------------------------------------------------- launchers (tvs_kernels.cu)
+// all return cudaGetLastError() of the launch; `s` is the stream.
+cudaError_t launch_tau0(const float *d0, int n2, int n1, float *tau, int ldt, cudaStream_t s);
+cudaError_t launch_g_row0(const float *tau2, int ldt, int n1, double *g_row0, cudaStream_t s);
+cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, const float *d0,
+                          int n2, int n1, float alpha, float *f, int ldf, cudaStream_t s);
+
+cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                            const float *f, const float *p1, const float *p2, int ld, int n2,
+                            int n1, float *om, cudaStream_t s);
+cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                          const float *vin, const float *om, float *vout, int n2, int n1, float t,
+                          cudaStream_t s);
+cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
+                           const int2 *covx, const int *loy, const int *lox, int m1,
+                           const float *q, float *p, int ld, int n2, int n1, float ahat,
+                           int *bad, cudaStream_t s);
+cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
+                            int n1, float inv_alpha, float *d, cudaStream_t s);
+
+// step 1
+cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cudaStream_t s);
+cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
+                       cudaStream_t s);
+cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
+                          float sa, float sb, float sc, float *out, cudaStream_t s);
+cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                           const float *p, int ld, int n2, int n1, float *v, cudaStream_t s);
+cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
+                           cudaStream_t s);
+cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
+                            const float *gphi, int ldg, int n2, int n1, float *om,
+                            cudaStream_t s);
+cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                          const float *vin, const float *gphi, int ldg, const float *om,
+                          float *vout, int n2, int n1, float t, cudaStream_t s);
+
+// projection (kernel b)
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, int ld, cudaStream_t s);
+cudaError_t launch_pivots(const ProjTile *chains_tiles, const int *chain_first_tile, int nchains,
+                          int n2, int n1, double *rinv, int ldn, int AT, cudaStream_t s);
+cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s);
+cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
+                              const float *qhat, int AT, int ldn, const double *rinv,
+                              double *z, float *phx, float *phy, int AP, cudaStream_t s);
+
+}  // namespace tvs

@@ -1,0 +1,674 @@
+// Hand-written sm_100a kernels of the TV-Stokes Schwarz dual iteration (arXiv 2602.17494).
+// Citations P:<line> refer to PAPER.md.  Index conventions: row i (y), column j (x), 0-based.
+// Global fields are planes of n2 rows with row pitch `ld` floats; batched per-subdomain buffers
+// use the uniform geometry of tvs::Geo (see tvs_internal.h).
+#include "tvs_internal.h"
+
+#include <math.h>
+
+namespace tvs {
+
+// ----------------------------------------------------------------------------- helpers
+
+__device__ __forceinline__ float theta_at(const float *thy, const float *thx, const SubDesc &sd,
+                                          const Geo &g, int li, int lj) {
+  return thy[sd.iy * g.A + li] * thx[sd.ix * g.B + lj];
+}
+
+// Value of a per-subdomain plane on S at local (li, lj), zero outside S (extension E_S).
+__device__ __forceinline__ float vS(const float *__restrict__ plane, int li, int lj, int a, int b,
+                                    int ld) {
+  return (li >= 0 && li < a && lj >= 0 && lj < b) ? __ldg(plane + (size_t)li * ld + lj) : 0.f;
+}
+
+// Global discrete divergence (Eq. defDivDis P:594 with the three-case D-) of a
+// 2-vector field that vanishes outside S, evaluated at local (li, lj) = global (gi, gj).
+// (x-part: [gj < n1-1] u(gj) - [gj > 0] u(gj-1); the u outside S are zero.)
+__device__ __forceinline__ float div_S(const float *vx, const float *vy, int li, int lj, int gi,
+                                       int gj, int a, int b, int ld, int n2, int n1) {
+  float dx = (gj < n1 - 1 ? vS(vx, li, lj, a, b, ld) : 0.f) - vS(vx, li, lj - 1, a, b, ld);
+  float dy = (gi < n2 - 1 ? vS(vy, li, lj, a, b, ld) : 0.f) - vS(vy, li - 1, lj, a, b, ld);
+  return dx + dy;
+}
+
+// Row-wise projection of Alg. 3/5:
+// v <- (theta v + t theta psi) / (theta + t |psi|); theta = 0 -> 0 (reading A13).
+__device__ __forceinline__ void ball_update(float th, float t, float psx, float psy, float &vx,
+                                            float &vy) {
+  if (th > 0.f) {
+    float nrm = sqrtf(psx * psx + psy * psy);
+    float inv = 1.f / (th + t * nrm);
+    vx = (th * vx + t * th * psx) * inv;
+    vy = (th * vy + t * th * psy) * inv;
+  } else {
+    vx = 0.f;
+    vy = 0.f;
+  }
+}
+
+// ----------------------------------------------------------------------------- step data
+
+// tau_0 = (-D_y^{neum-} d0, D_x^{neum-} d0) on Omega~ (Eq. def:backdiffNeumann P:576-591).
+__global__ void k_tau0(const float *__restrict__ d0, int n2, int n1, float *__restrict__ tau,
+                       int ldt) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i > n2 || j > n1) return;
+  float dxv = 0.f, dyv = 0.f;
+  if (j != 0 && j != n1) {
+    int r = i < n2 ? i : n2 - 1;                    // mirrored extra row
+    dxv = d0[(size_t)r * n1 + j] - d0[(size_t)r * n1 + j - 1];
+  }
+  if (i != 0 && i != n2) {
+    int c = j < n1 ? j : n1 - 1;                    // mirrored extra column
+    dyv = d0[(size_t)i * n1 + c] - d0[(size_t)(i - 1) * n1 + c];
+  }
+  size_t plane = (size_t)(n2 + 1) * ldt;
+  tau[(size_t)i * ldt + j] = -dyv;
+  tau[plane + (size_t)i * ldt + j] = dxv;
+}
+
+// g on row 0 by backward-difference integration along x (reading A3): g[0][j] = sum tau_2[0][1..j].
+__global__ void k_g_row0(const float *__restrict__ tau2, int n1, double *__restrict__ g0) {
+  __shared__ double part[1024];
+  int tid = threadIdx.x, nt = blockDim.x;
+  int chunk = (n1 + nt - 1) / nt;
+  int a = tid * chunk, b = min(n1, a + chunk);
+  double s = 0.0;
+  for (int j = a; j < b; ++j) s += (j >= 1) ? (double)tau2[j] : 0.0;
+  part[tid] = s;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {          // inclusive Hillis-Steele scan
+    double add = tid >= off ? part[tid - off] : 0.0;
+    __syncthreads();
+    part[tid] += add;
+    __syncthreads();
+  }
+  double acc = tid > 0 ? part[tid - 1] : 0.0;
+  for (int j = a; j < b; ++j) {
+    acc += (j >= 1) ? (double)tau2[j] : 0.0;
+    g0[j] = acc;
+  }
+}
+
+// f = alpha (d0 - g) (Eq. ir2dualdis), g integrated down each column with
+// g[i][j] = g[i-1][j] - tau_1[i][j] (reading A3), accumulated in fp64.
+__global__ void k_irv2_f(const float *__restrict__ tau1, int ldt, const double *__restrict__ g0,
+                         const float *__restrict__ d0, int n2, int n1, float alpha,
+                         float *__restrict__ f, int ldf) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n1) return;
+  double acc = g0[j];
+  f[j] = alpha * (float)((double)d0[j] - acc);
+#pragma unroll 8
+  for (int i = 1; i < n2; ++i) {
+    acc -= (double)tau1[(size_t)i * ldt + j];
+    f[(size_t)i * ldf + j] = (float)((double)alpha * ((double)d0[(size_t)i * n1 + j] - acc));
+  }
+}
+
+// ----------------------------------------------------------------------------- step 2 (IRV2)
+
+// omega0_m = R_{S+}(f - div p^n + div(theta_m p^n)) (Alg. 3 with Lambda = div, P:1348,
+// localized by resDiv P:1417).  One plane per subdomain on S+.
+__global__ void k_omega0_2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+                           const float *__restrict__ thx, const float *__restrict__ f,
+                           const float *__restrict__ p1, const float *__restrict__ p2, int ld,
+                           int n2, int n1, float *__restrict__ om) {
+  const SubDesc sd = subs[blockIdx.z];
+  int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  int li = blockIdx.y * blockDim.y + threadIdx.y;
+  int gi = sd.y0 + li, gj = sd.x0 + lj;
+  if (gi > sd.py1 || gj > sd.px1) return;
+  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  auto P1 = [&](int i, int j) { return p1[(size_t)i * ld + j]; };
+  auto P2 = [&](int i, int j) { return p2[(size_t)i * ld + j]; };
+  float divp = (gj < n1 - 1 ? P1(gi, gj) : 0.f) - (gj > 0 ? P1(gi, gj - 1) : 0.f) +
+               (gi < n2 - 1 ? P2(gi, gj) : 0.f) - (gi > 0 ? P2(gi - 1, gj) : 0.f);
+  auto U1 = [&](int i, int j) {   // theta_m p_1 extended by zero outside S (local coords)
+    return (i >= 0 && i < a && j >= 0 && j < b)
+               ? theta_at(thy, thx, sd, g, i, j) * P1(sd.y0 + i, sd.x0 + j) : 0.f;
+  };
+  auto U2 = [&](int i, int j) {
+    return (i >= 0 && i < a && j >= 0 && j < b)
+               ? theta_at(thy, thx, sd, g, i, j) * P2(sd.y0 + i, sd.x0 + j) : 0.f;
+  };
+  float divu = (gj < n1 - 1 ? U1(li, lj) : 0.f) - U1(li, lj - 1) +
+               (gi < n2 - 1 ? U2(li, lj) : 0.f) - U2(li - 1, lj);
+  om[((size_t)blockIdx.z * g.AP + li) * g.ldP + lj] = f[(size_t)gi * ld + gj] - divp + divu;
+}
+
+// Kernel (a): one fused IRV2 dual sweep of Alg. 3 for every subdomain:
+//   u = div_{S+}(E_S v) - omega0 on S+;  psi = R_S grad_{S+} u;  v <- ball_update.
+// CTA = 32 x 8 tile of S; v (2 planes, 1-px halo) and omega0 staged through shared memory.
+constexpr int SW_TX = 32, SW_TY = 8;
+__global__ void __launch_bounds__(SW_TX *SW_TY)
+k_sweep2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+         const float *__restrict__ thx, const float *__restrict__ vin,
+         const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+  __shared__ float sv1[SW_TY + 2][SW_TX + 2];
+  __shared__ float sv2[SW_TY + 2][SW_TX + 2];
+  __shared__ float su[SW_TY + 1][SW_TX + 1];
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int r0 = blockIdx.y * SW_TY, c0 = blockIdx.x * SW_TX;
+  if (r0 >= a || c0 >= b) return;
+  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  const float *v2 = v1 + (size_t)g.A * g.ldS;
+  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
+  const int tid = threadIdx.y * SW_TX + threadIdx.x;
+  for (int e = tid; e < (SW_TY + 2) * (SW_TX + 2); e += SW_TX * SW_TY) {
+    int rr = e / (SW_TX + 2), cc = e % (SW_TX + 2);
+    int li = r0 - 1 + rr, lj = c0 - 1 + cc;
+    sv1[rr][cc] = vS(v1, li, lj, a, b, g.ldS);
+    sv2[rr][cc] = vS(v2, li, lj, a, b, g.ldS);
+  }
+  __syncthreads();
+  for (int e = tid; e < (SW_TY + 1) * (SW_TX + 1); e += SW_TX * SW_TY) {
+    int rr = e / (SW_TX + 1), cc = e % (SW_TX + 1);
+    int li = r0 + rr, lj = c0 + cc;
+    float u = 0.f;
+    if (li < ap && lj < bp) {
+      int gi = sd.y0 + li, gj = sd.x0 + lj;
+      float dx = (gj < n1 - 1 ? sv1[rr + 1][cc + 1] : 0.f) - sv1[rr + 1][cc];
+      float dy = (gi < n2 - 1 ? sv2[rr + 1][cc + 1] : 0.f) - sv2[rr][cc + 1];
+      u = dx + dy - __ldg(omm + (size_t)li * g.ldP + lj);
+    }
+    su[rr][cc] = u;
+  }
+  __syncthreads();
+  const int li = r0 + threadIdx.y, lj = c0 + threadIdx.x;
+  if (li >= a || lj >= b) return;
+  const int rr = threadIdx.y, cc = threadIdx.x;
+  float psx = (lj + 1 < bp) ? su[rr][cc + 1] - su[rr][cc] : 0.f;
+  float psy = (li + 1 < ap) ? su[rr + 1][cc] - su[rr][cc] : 0.f;
+  float vx = sv1[rr + 1][cc + 1], vy = sv2[rr + 1][cc + 1];
+  ball_update(theta_at(thy, thx, sd, g, li, lj), t, psx, psy, vx, vy);
+  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  o1[(size_t)li * g.ldS + lj] = vx;
+  o1[(size_t)g.A * g.ldS + (size_t)li * g.ldS + lj] = vy;
+}
+
+// p^{n+1} = (1 - ahat) p^n + ahat sum_m E qhat_m (Alg. 2), summed in fixed subdomain
+// order (m2 ascending, then m1) so overlaps are bitwise reproducible.  Flags non-finite values.
+__global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
+                          const int2 *__restrict__ covy, const int2 *__restrict__ covx,
+                          const int *__restrict__ loy, const int *__restrict__ lox, int m1,
+                          const float *__restrict__ q, float *__restrict__ p, int ld, int n2,
+                          int n1, float ahat, int *bad) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  int2 cy = covy[i], cx = covx[j];
+  for (int c = 0; c < planes; ++c) {
+    float acc = 0.f;
+    for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
+      for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
+        int m = ky * m1 + kx;
+        int li = i - loy[ky], lj = j - lox[kx];
+        acc += q[(((size_t)m * planes + c) * g.A + li) * g.ldS + lj];
+      }
+    }
+    size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
+    float v = (1.f - ahat) * p[idx] + ahat * acc;
+    if (!isfinite(v)) atomicOr(bad, 1);
+    p[idx] = v;
+  }
+}
+
+// d = d0 - div p / alpha.
+__global__ void k_recover2(const float *__restrict__ d0, const float *__restrict__ p1,
+                           const float *__restrict__ p2, int ld, int n2, int n1, float inv_alpha,
+                           float *__restrict__ d) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  auto P1 = [&](int a, int b) { return p1[(size_t)a * ld + b]; };
+  auto P2 = [&](int a, int b) { return p2[(size_t)a * ld + b]; };
+  float dv = (j < n1 - 1 ? P1(i, j) : 0.f) - (j > 0 ? P1(i, j - 1) : 0.f) +
+             (i < n2 - 1 ? P2(i, j) : 0.f) - (i > 0 ? P2(i - 1, j) : 0.f);
+  d[(size_t)i * n1 + j] = d0[(size_t)i * n1 + j] - dv * inv_alpha;
+}
+
+// ----------------------------------------------------------------------------- step 1 (TFS)
+
+// w = multidiv p: w_k = div(p_k1, p_k2); p has 4 planes [p11 p12 p21 p22].
+__global__ void k_multidiv(const float *__restrict__ p, int ld, int n2, int n1,
+                           float *__restrict__ w) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  size_t pl = (size_t)n2 * ld;
+  for (int k = 0; k < 2; ++k) {
+    const float *px = p + (2 * k) * pl, *py = p + (2 * k + 1) * pl;
+    float dv = (j < n1 - 1 ? px[(size_t)i * ld + j] : 0.f) - (j > 0 ? px[(size_t)i * ld + j - 1] : 0.f) +
+               (i < n2 - 1 ? py[(size_t)i * ld + j] : 0.f) - (i > 0 ? py[(size_t)(i - 1) * ld + j] : 0.f);
+    w[k * pl + (size_t)i * ld + j] = dv;
+  }
+}
+
+// q = div w.
+__global__ void k_div(const float *__restrict__ w1, const float *__restrict__ w2, int ld, int n2,
+                      int n1, float *__restrict__ q) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  float dv = (j < n1 - 1 ? w1[(size_t)i * ld + j] : 0.f) - (j > 0 ? w1[(size_t)i * ld + j - 1] : 0.f) +
+             (i < n2 - 1 ? w2[(size_t)i * ld + j] : 0.f) - (i > 0 ? w2[(size_t)(i - 1) * ld + j] : 0.f);
+  q[(size_t)i * ld + j] = dv;
+}
+
+// out = sa a + sb b (+ sc c), two planes.
+__global__ void k_axpby2(const float *__restrict__ a, const float *__restrict__ b,
+                         const float *__restrict__ c, int ld, int n2, int n1, float sa, float sb,
+                         float sc, float *__restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  size_t pl = (size_t)n2 * ld;
+  for (int k = 0; k < 2; ++k) {
+    size_t idx = k * pl + (size_t)i * ld + j;
+    float v = sa * a[idx] + sb * b[idx];
+    if (c) v += sc * c[idx];
+    out[idx] = v;
+  }
+}
+
+// v_m = R_S (theta_m p^n) (4 planes) -- the argument of the omega0 projection (Alg. 5).
+__global__ void k_load_tp(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+                          const float *__restrict__ thx, const float *__restrict__ p, int ld,
+                          int n2, float *__restrict__ v) {
+  const SubDesc sd = subs[blockIdx.z];
+  int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  int li = blockIdx.y * blockDim.y + threadIdx.y;
+  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  if (li >= a || lj >= b) return;
+  float th = theta_at(thy, thx, sd, g, li, lj);
+  size_t pl = (size_t)n2 * ld;
+  for (int c = 0; c < 4; ++c)
+    v[(((size_t)blockIdx.z * 4 + c) * g.A + li) * g.ldS + lj] =
+        th * p[c * pl + (size_t)(sd.y0 + li) * ld + sd.x0 + lj];
+}
+
+// Pre-div of Alg. 5: q = div_T E_{S+} multidiv_{S+} E_S v on T.  Both divergences use
+// the global rules (resDiv), so the result equals the global div of the
+// zero-extended field restricted to T.
+__device__ __forceinline__ float w_S(const float *vb, int k, int li, int lj, int gi, int gj,
+                                     int a, int b, const Geo &g, int n2, int n1) {
+  const float *vx = vb + (size_t)(2 * k) * g.A * g.ldS;
+  const float *vy = vx + (size_t)g.A * g.ldS;
+  return div_S(vx, vy, li, lj, gi, gj, a, b, g.ldS, n2, n1);
+}
+
+__global__ void k_prediv1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
+                          int n2, int n1, float *__restrict__ q) {
+  const SubDesc sd = subs[blockIdx.z];
+  int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  int li = blockIdx.y * blockDim.y + threadIdx.y;
+  int gi = sd.y0 + li, gj = sd.x0 + lj;
+  if (gi > sd.ty1 || gj > sd.tx1) return;
+  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const float *vb = v + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  float dv = (gj < n1 - 1 ? w_S(vb, 0, li, lj, gi, gj, a, b, g, n2, n1) : 0.f) -
+             (gj > 0 ? w_S(vb, 0, li, lj - 1, gi, gj - 1, a, b, g, n2, n1) : 0.f) +
+             (gi < n2 - 1 ? w_S(vb, 1, li, lj, gi, gj, a, b, g, n2, n1) : 0.f) -
+             (gi > 0 ? w_S(vb, 1, li - 1, lj, gi - 1, gj, a, b, g, n2, n1) : 0.f);
+  q[((size_t)blockIdx.z * g.AT + li) * g.ldT + lj] = dv;
+}
+
+// omega0_loc = R_{S+} r^n + (R_{S+} P E_{S+}) multidiv_{S+} E_S (theta_m p^n)  (Alg. 5, P:1740;
+// r^n = f - P multidiv p^n is the global part, reading A11), with P w = w - grad phi.
+__global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ r,
+                           int ld, const float *__restrict__ v, const float *__restrict__ gphi,
+                           int ldg, int n2, int n1, float *__restrict__ om) {
+  const SubDesc sd = subs[blockIdx.z];
+  int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  int li = blockIdx.y * blockDim.y + threadIdx.y;
+  int gi = sd.y0 + li, gj = sd.x0 + lj;
+  if (gi > sd.py1 || gj > sd.px1) return;
+  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const float *vb = v + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  size_t pl = (size_t)n2 * ld;
+  for (int k = 0; k < 2; ++k) {
+    float w = w_S(vb, k, li, lj, gi, gj, a, b, g, n2, n1);
+    float gp = gphi[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * ldg + lj];
+    om[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * g.ldP + lj] =
+        r[k * pl + (size_t)gi * ld + gj] + (w - gp);
+  }
+}
+
+// Kernel (a'): fused TFS dual sweep of Alg. 5:
+//   rho_k = (w_k - grad phi_k) - omega0_k on S+ with w = multidiv E_S v (recomputed),
+//   psi_k = R_S grad_{S+} rho_k,  v_k <- ball_update (row-wise, k = 1, 2).
+__global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+                         const float *__restrict__ thx, const float *__restrict__ vin,
+                         const float *__restrict__ gphi, int ldg, const float *__restrict__ om,
+                         float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  int li = blockIdx.y * blockDim.y + threadIdx.y;
+  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  if (li >= a || lj >= b) return;
+  int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const float *vb = vin + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  float *ob = vout + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  float th = theta_at(thy, thx, sd, g, li, lj);
+  for (int k = 0; k < 2; ++k) {
+    const float *gk = gphi + ((size_t)blockIdx.z * 2 + k) * g.AP * ldg;
+    const float *ok = om + ((size_t)blockIdx.z * 2 + k) * g.AP * g.ldP;
+    auto rho = [&](int i, int j) {
+      return w_S(vb, k, i, j, sd.y0 + i, sd.x0 + j, a, b, g, n2, n1) -
+             __ldg(gk + (size_t)i * ldg + j) - __ldg(ok + (size_t)i * g.ldP + j);
+    };
+    float r0 = rho(li, lj);
+    float psx = (lj + 1 < bp) ? rho(li, lj + 1) - r0 : 0.f;
+    float psy = (li + 1 < ap) ? rho(li + 1, lj) - r0 : 0.f;
+    float vx = vb[(size_t)(2 * k) * g.A * g.ldS + (size_t)li * g.ldS + lj];
+    float vy = vb[(size_t)(2 * k + 1) * g.A * g.ldS + (size_t)li * g.ldS + lj];
+    ball_update(th, t, psx, psy, vx, vy);
+    ob[(size_t)(2 * k) * g.A * g.ldS + (size_t)li * g.ldS + lj] = vx;
+    ob[(size_t)(2 * k + 1) * g.A * g.ldS + (size_t)li * g.ldS + lj] = vy;
+  }
+}
+
+// ----------------------------------------------------------------------------- projection (b)
+//
+// phi = R_T Delta^dagger E_T q (Eq. locglobprojpart3/invLaplLowCapLong),
+// refactored exactly: Delta = L_y (+) L_x is separable and C_{N1} diagonalises L_x, so
+//   R_T Delta^dagger E_T = sum_j [R_Ty (L_y - s_j)^{-1} E_Ty] (x) [R_Tx c_j c_j^T E_Tx],
+// s_j = sigma_{N1,j}^2 (j = 0: the Neumann pseudo-inverse L_y^dagger).  The restricted y-inverse
+// is a tridiagonal solve on T's rows whose end diagonals carry the exact Schur complement of the
+// rows outside T.  Only grad phi is ever formed (precision rule C-10): the x-derivative
+// spectrally (c_j(x+1) - c_j(x) = -s_j sigma_j sin(pi j (x+1)/N)), the y-derivative by fp64
+// differencing of the solved column.
+
+// Tables: cf[x][j] = cos(pi j (2x+1) / (2n)) (forward), cn[j][x] (same, transposed) and
+// sn[j][x] = sin(pi j (x+1) / n), evaluated in fp64 with exact integer argument reduction.
+__global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ cn,
+                             float *__restrict__ sn, int ld) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= n || j >= n) return;
+  long long mc = ((long long)j * (2LL * x + 1)) % (4LL * n);
+  long long ms = ((long long)j * (x + 1LL)) % (2LL * n);
+  double c = cospi((double)mc / (2.0 * n));
+  double s = sinpi((double)ms / (double)n);
+  cf[(size_t)x * ld + j] = (float)c;
+  cn[(size_t)j * ld + x] = (float)c;
+  sn[(size_t)j * ld + x] = (float)s;
+}
+
+// Thomas pivots of the Schur-corrected tridiagonal M_T(s_j) on rows [ty0, ty1] of an axis of
+// length n2 (Neumann Laplacian L_y), one thread per (chain, j >= 1):
+//   exterior chain of length L (far end Neumann): e_1 = -1 - s, e_k = -2 - s - 1/e_{k-1};
+//   the Schur complement adds -1/e_L to T's end diagonal; rinv_k = 1 / (Thomas pivot k).
+__global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restrict__ first,
+                         int nchains, int n2, int n1, double *__restrict__ rinv, int ldn, int AT) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int c = blockIdx.y;
+  if (j >= n1 || c >= nchains) return;
+  const ProjTile tl = tiles[first[c]];
+  double *out = rinv + (size_t)c * AT * ldn;
+  int nt = tl.ty1 - tl.ty0 + 1;
+  if (j == 0) {
+    for (int k = 0; k < nt; ++k) out[(size_t)k * ldn] = 0.0;
+    return;
+  }
+  double sg = 2.0 * sinpi((double)j / (2.0 * n1));
+  double s = sg * sg;
+  auto chain_corr = [&](int L) {
+    double e = -1.0 - s;
+    for (int k = 2; k <= L; ++k) e = -2.0 - s - 1.0 / e;
+    return -1.0 / e;
+  };
+  double dtop = tl.ty0 > 0 ? (-2.0 - s + chain_corr(tl.ty0)) : (-1.0 - s);
+  double dbot = tl.ty1 < n2 - 1 ? (-2.0 - s + chain_corr(n2 - 1 - tl.ty1)) : (-1.0 - s);
+  double e = dtop;
+  out[j] = 1.0 / e;
+  for (int k = 1; k < nt; ++k) {
+    double dk = (k == nt - 1) ? dbot : (-2.0 - s);
+    e = dk - 1.0 / e;
+    out[(size_t)k * ldn + j] = 1.0 / e;
+  }
+}
+
+// Per-frequency y-solves (fp64), one thread per (tile, j).  Input: raw partial x-DCT
+// qhat[k][j] = sum_x q[k][x] cos(pi j (2x+1)/(2 n1)).  Output on the rows of S+:
+//   phx[k][j] = -s_j^2 sigma_j u_k,  phy[k][j] = s_j^2 (u_{k+1} - u_k)  (0 on the global last
+// row), with s_j = sqrt(2/n1) w_j the DCT normalisation (Eq. form:DCTmat).
+__global__ void k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
+                             const float *__restrict__ qhat, int AT, int ldn,
+                             const double *__restrict__ rinv, double *__restrict__ z,
+                             float *__restrict__ phx, float *__restrict__ phy, int AP) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int tix = blockIdx.y;
+  if (j >= n1) return;
+  const ProjTile tl = tiles[tix];
+  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1;
+  const float *b = qhat + (size_t)tix * AT * ldn + j;
+  float *ox = phx + (size_t)tix * AP * ldn + j;
+  float *oy = phy + (size_t)tix * AP * ldn + j;
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;          // s_j^2
+  if (j == 0) {
+    // L_y^dagger b: D+_y u = w, w_y = sum_{l<=y} b_l - mu (y+1), mu = mean of b over n2 rows.
+    double tot = 0.0;
+    for (int k = 0; k < nt; ++k) tot += (double)b[(size_t)k * ldn];
+    double mu = tot / (double)n2, pre = 0.0;
+    for (int k = 0; k < nout; ++k) {
+      pre += (double)b[(size_t)k * ldn];
+      int y = tl.ty0 + k;
+      double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
+      ox[(size_t)k * ldn] = 0.f;
+      oy[(size_t)k * ldn] = (float)(s2 * w);
+    }
+    return;
+  }
+  const double sg = 2.0 * sinpi((double)j / (2.0 * n1));
+  const double cx = -s2 * sg;
+  const double *ri = rinv + (size_t)tl.chain * AT * ldn + j;
+  double *zz = z + (size_t)tix * AT * ldn + j;
+  double zp = (double)b[0];
+  zz[0] = zp;
+  for (int k = 1; k < nt; ++k) {
+    zp = (double)b[(size_t)k * ldn] - zp * ri[(size_t)(k - 1) * ldn];
+    zz[(size_t)k * ldn] = zp;
+  }
+  double u = zp * ri[(size_t)(nt - 1) * ldn];
+  if (nt - 1 < nout) {                       // T = S+ in y: global last row, D+_y = 0
+    ox[(size_t)(nt - 1) * ldn] = (float)(cx * u);
+    oy[(size_t)(nt - 1) * ldn] = 0.f;
+  }
+  for (int k = nt - 2; k >= 0; --k) {
+    double uk = (zz[(size_t)k * ldn] - u) * ri[(size_t)k * ldn];
+    if (k < nout) {
+      ox[(size_t)k * ldn] = (float)(cx * uk);
+      oy[(size_t)k * ldn] = (float)(s2 * (u - uk));
+    }
+    u = uk;
+  }
+}
+
+// Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
+// register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
+constexpr int GBM = 128, GBN = 128, GBK = 8;
+__global__ void __launch_bounds__(256) k_gemm(const GemmDesc *__restrict__ descs) {
+  const GemmDesc d = descs[blockIdx.z];
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  if (m0 >= d.M || n0 >= d.N) return;
+  __shared__ __align__(16) float As[2][GBK][GBM];
+  __shared__ __align__(16) float Bs[2][GBK][GBN];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  float ra[4], rb[4];
+  auto load_global = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int idx = tid + e * 256;
+      int r = idx / GBK, kk = idx % GBK;
+      int gm = m0 + r, gk = k0 + kk;
+      ra[e] = (gm < d.M && gk < d.K) ? __ldg(d.A + (size_t)gm * d.lda + gk) : 0.f;
+      int kb = idx / GBN, cb = idx % GBN;
+      int gkb = k0 + kb, gn = n0 + cb;
+      rb[e] = (gkb < d.K && gn < d.N) ? __ldg(d.B + (size_t)gkb * d.ldb + gn) : 0.f;
+    }
+  };
+  auto store_shared = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int idx = tid + e * 256;
+      As[buf][idx % GBK][idx / GBK] = ra[e];
+      Bs[buf][idx / GBN][idx % GBN] = rb[e];
+    }
+  };
+  int nk = (d.K + GBK - 1) / GBK;
+  load_global(0);
+  store_shared(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    int buf = kt & 1;
+    if (kt + 1 < nk) load_global((kt + 1) * GBK);
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+      float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4 + 64]);
+      float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+      float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4 + 64]);
+      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) {
+      store_shared(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (gm >= d.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (gn < d.N) d.C[(size_t)gm * d.ldc + gn] = acc[i][j];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- launchers
+
+static inline dim3 grid2(int nx, int ny, int bx, int by, int z = 1) {
+  return dim3((nx + bx - 1) / bx, (ny + by - 1) / by, z);
+}
+
+cudaError_t launch_tau0(const float *d0, int n2, int n1, float *tau, int ldt, cudaStream_t s) {
+  k_tau0<<<grid2(n1 + 1, n2 + 1, 32, 8), dim3(32, 8), 0, s>>>(d0, n2, n1, tau, ldt);
+  return cudaGetLastError();
+}
+cudaError_t launch_g_row0(const float *tau2, int ldt, int n1, double *g_row0, cudaStream_t s) {
+  (void)ldt;
+  k_g_row0<<<1, 1024, 0, s>>>(tau2, n1, g_row0);
+  return cudaGetLastError();
+}
+cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, const float *d0,
+                          int n2, int n1, float alpha, float *f, int ldf, cudaStream_t s) {
+  k_irv2_f<<<(n1 + 127) / 128, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf);
+  return cudaGetLastError();
+}
+cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                            const float *f, const float *p1, const float *p2, int ld, int n2,
+                            int n1, float *om, cudaStream_t s) {
+  k_omega0_2<<<grid2(g.BP, g.AP, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, f, p1, p2,
+                                                                   ld, n2, n1, om);
+  return cudaGetLastError();
+}
+cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                          const float *vin, const float *om, float *vout, int n2, int n1, float t,
+                          cudaStream_t s) {
+  k_sweep2<<<grid2(g.B, g.A, SW_TX, SW_TY, g.M), dim3(SW_TX, SW_TY), 0, s>>>(
+      subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  return cudaGetLastError();
+}
+cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
+                           const int2 *covx, const int *loy, const int *lox, int m1,
+                           const float *q, float *p, int ld, int n2, int n1, float ahat, int *bad,
+                           cudaStream_t s) {
+  k_combine<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(subs, g, planes, covy, covx, loy, lox,
+                                                         m1, q, p, ld, n2, n1, ahat, bad);
+  return cudaGetLastError();
+}
+cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
+                            int n1, float inv_alpha, float *d, cudaStream_t s) {
+  k_recover2<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(d0, p1, p2, ld, n2, n1, inv_alpha, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cudaStream_t s) {
+  k_multidiv<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(p, ld, n2, n1, w);
+  return cudaGetLastError();
+}
+cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
+                       cudaStream_t s) {
+  k_div<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(w1, w2, ld, n2, n1, q);
+  return cudaGetLastError();
+}
+cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
+                          float sa, float sb, float sc, float *out, cudaStream_t s) {
+  k_axpby2<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(a, b, c, ld, n2, n1, sa, sb, sc, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                           const float *p, int ld, int n2, int n1, float *v, cudaStream_t s) {
+  (void)n1;
+  k_load_tp<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, p, ld, n2, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
+                           cudaStream_t s) {
+  k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q);
+  return cudaGetLastError();
+}
+cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
+                            const float *gphi, int ldg, int n2, int n1, float *om,
+                            cudaStream_t s) {
+  k_omega0_1<<<grid2(g.BP, g.AP, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, r, ld, v, gphi, ldg,
+                                                                   n2, n1, om);
+  return cudaGetLastError();
+}
+cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                          const float *vin, const float *gphi, int ldg, const float *om,
+                          float *vout, int n2, int n1, float t, cudaStream_t s) {
+  k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
+                                                               ldg, om, vout, n2, n1, t);
+  return cudaGetLastError();
+}
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, int ld, cudaStream_t s) {
+  k_dct_tables<<<grid2(n, n, 32, 8), dim3(32, 8), 0, s>>>(n, cf, cn, sn, ld);
+  return cudaGetLastError();
+}
+cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, int n2, int n1,
+                          double *rinv, int ldn, int AT, cudaStream_t s) {
+  k_pivots<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, n2, n1, rinv,
+                                                           ldn, AT);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s) {
+  k_gemm<<<dim3((maxN + GBN - 1) / GBN, (maxM + GBM - 1) / GBM, batch), 256, 0, s>>>(descs);
+  return cudaGetLastError();
+}
+cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
+                              const float *qhat, int AT, int ldn, const double *rinv, double *z,
+                              float *phx, float *phy, int AP, cudaStream_t s) {
+  k_proj_solve<<<dim3((n1 + 127) / 128, ntiles), 128, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv,
+                                                              z, phx, phy, AP);
+  return cudaGetLastError();
+}
+
+}  // namespace tvs

@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded inputs
+and the same fixed schedule.  Tolerances (BASELINE.json north_star): max-abs <= 1e-4 on d and tau
+([0,1]-scaled images), <= 1e-4 relative on the final primal energies."""
+import numpy as np
+import pytest
+
+from oracle import layout as olayout, ops, solvers as S, spectral
+from tvs_synth import CONFIGS, random_image, disk_on_ramp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_17494_b200 as pkg
+    c = pkg.Context(0)
+    yield c
+    c.close()
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _primal1(tau, d0, delta):
+    ptau0 = spectral.project(S.tau0(d0))
+    return S.primal_energy_tfs(tau, ptau0, delta)
+
+
+def _primal2(d, d0, tau, lam):
+    alpha, g, _ = S.irv2_data(d0, tau, lam)
+    return S.primal_energy_irv2(d, d0, g, alpha)
+
+
+def check_step1(ctx, img, delta, L, sweeps, inner, t=0.125):
+    n2, n1 = img.shape
+    lay = olayout.Layout(n2, n1, *L)
+    tau_ref, p_ref, _ = S.dd_step1(img.astype(np.float64), delta, lay, sweeps, inner, t)
+    tau, p, st = ctx.tv_stokes_step1(_dev(img), delta, L, (sweeps, inner, t), want_p=True)
+    tau, p = tau.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
+    e_tau = np.abs(tau - tau_ref).max()
+    e_p = np.abs(p.reshape(2, 2, n2 + 1, n1 + 1) - p_ref).max()
+    E_ref = _primal1(tau_ref, img.astype(np.float64), delta)
+    E_gpu = _primal1(tau, img.astype(np.float64), delta)
+    rel = abs(E_gpu - E_ref) / abs(E_ref) if E_ref else abs(E_gpu)
+    assert e_tau <= TOL, f"max|tau - oracle| = {e_tau}"
+    assert e_p <= 10 * TOL, f"max|p - oracle| = {e_p}"
+    assert rel <= TOL, f"relative E1 error {rel}"
+    return tau_ref, st
+
+
+def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125):
+    n2, n1 = img.shape
+    lay = olayout.Layout(n2, n1, *L)
+    d_ref, p_ref, _ = S.dd_step2(img.astype(np.float64), tau, lam, lay, sweeps, inner, t)
+    d, p, st = ctx.tv_stokes_step2(_dev(tau), _dev(img), lam, L, (sweeps, inner, t), want_p=True)
+    d, p = d.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
+    e_d = np.abs(d - d_ref).max()
+    e_p = np.abs(p - p_ref).max()
+    E_ref = _primal2(d_ref, img.astype(np.float64), tau, lam)
+    E_gpu = _primal2(d, img.astype(np.float64), tau, lam)
+    rel = abs(E_gpu - E_ref) / abs(E_ref)
+    assert e_d <= TOL, f"max|d - oracle| = {e_d}"
+    assert e_p <= 10 * TOL, f"max|p - oracle| = {e_p}"
+    assert rel <= TOL, f"relative E2 error {rel}"
+    return st
+
+
+# ----------------------------------------------------------------------------- small / edge cases
+
+@pytest.mark.parametrize("shape,L", [((16, 16), (1, 1, 0, 0)), ((24, 20), (2, 2, 4, 4)),
+                                     ((37, 53), (3, 2, 3, 5)), ((40, 18), (4, 1, 4, 0)),
+                                     ((18, 40), (1, 4, 0, 3)), ((33, 35), (2, 3, 2, 2)),
+                                     ((2, 2), (1, 1, 0, 0)), ((5, 9), (1, 2, 0, 2))])
+def test_step2_small(ctx, shape, L):
+    img = random_image(*shape, seed=shape[0] * 100 + shape[1])
+    tau, _ = S.chambolle_tfs(img.astype(np.float64), 0.05, 30)
+    check_step2(ctx, img, tau, 0.1, L, 4, 5)
+
+
+@pytest.mark.parametrize("shape,L", [((16, 16), (1, 1, 0, 0)), ((24, 20), (2, 2, 4, 4)),
+                                     ((37, 53), (3, 2, 3, 5)), ((40, 18), (4, 1, 4, 0)),
+                                     ((18, 40), (1, 4, 0, 3)), ((33, 35), (2, 3, 2, 2)),
+                                     ((2, 2), (1, 1, 0, 0)), ((5, 9), (1, 2, 0, 2))])
+def test_step1_small(ctx, shape, L):
+    img = random_image(*shape, seed=shape[0] * 7 + shape[1])
+    check_step1(ctx, img, 0.05, L, 3, 4)
+
+
+def test_global_projection_only(ctx):
+    """sweeps = 1, inner = 0: tau = P tau_0 exactly (qhat stays 0) -- isolates the global P."""
+    img = random_image(45, 61, 3)
+    tau, _, _ = ctx.tv_stokes_step1(_dev(img), 0.05, (2, 2, 4, 4), (1, 0, 0.125))
+    ref = spectral.project(S.tau0(img.astype(np.float64)))
+    assert np.abs(tau.cpu().numpy() - ref).max() < 1e-5
+    assert np.abs(ops.div(tau.cpu().numpy().astype(np.float64))).max() < 1e-5
+
+
+def test_constant_image(ctx):
+    img = np.full((20, 24), 0.42, np.float32)
+    d, tau, _, _ = ctx.tv_stokes_denoise(_dev(img), 0.05, 0.1, (2, 2, 3, 3), (3, 3, 0.125),
+                                         (3, 3, 0.125), want_tau=True)
+    assert np.abs(tau.cpu().numpy()).max() == 0.0
+    assert np.abs(d.cpu().numpy() - img).max() < 1e-6
+
+
+def test_small_t_and_odd_overlap(ctx):
+    img = random_image(30, 30, 5)
+    check_step1(ctx, img, 0.1, (2, 2, 5, 3), 2, 3, t=0.05)
+    tau, _ = S.chambolle_tfs(img.astype(np.float64), 0.1, 20)
+    check_step2(ctx, img, tau, 0.2, (2, 2, 5, 3), 3, 3, t=0.05)
+
+
+def test_errors(ctx):
+    import paper_2602_17494_b200 as pkg
+    img = _dev(random_image(16, 16, 1))
+    with pytest.raises(pkg.TvsError) as e:
+        ctx.tv_stokes_step1(img, 0.05, (2, 2, 4, 4), (1, 1, 0.2))
+    assert e.value.code == 1
+    with pytest.raises(pkg.TvsError) as e:
+        ctx.tv_stokes_step1(img, 0.05, (4, 4, 4, 4), (1, 1, 0.125))
+    assert e.value.code == 2
+    with pytest.raises(pkg.TvsError) as e:
+        ctx.tv_stokes_step1(img, -1.0, (2, 2, 4, 4), (1, 1, 0.125))
+    assert e.value.code == 1
+
+
+def test_determinism(ctx):
+    img = _dev(random_image(40, 40, 9))
+    a = ctx.tv_stokes_denoise(img, 0.05, 0.1, (2, 2, 4, 4), (3, 3, 0.125), (3, 3, 0.125))[0]
+    b = ctx.tv_stokes_denoise(img, 0.05, 0.1, (2, 2, 4, 4), (3, 3, 0.125), (3, 3, 0.125))[0]
+    assert torch.equal(a, b)
+
+
+def test_host_entry_point(ctx):
+    img = random_image(24, 28, 2)
+    dd = ctx.tv_stokes_denoise(_dev(img), 0.05, 0.1, (2, 2, 4, 4), (2, 3, 0.125), (2, 3, 0.125))[0]
+    dh, _, _ = ctx.tv_stokes_denoise_host(img, 0.05, 0.1, (2, 2, 4, 4), (2, 3, 0.125), (2, 3, 0.125))
+    assert np.array_equal(dd.cpu().numpy(), dh)
+
+
+# ----------------------------------------------------------------------------- BASELINE configs
+
+def test_config1_full(ctx):
+    c = CONFIGS["c1"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    tau_ref, _ = check_step1(ctx, img, c.delta, L, c.sweeps, c.inner)
+    check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner)
+    # single-domain comparison run of config 1 (400 Chambolle iterations per step)
+    tau_ref1, _ = check_step1(ctx, img, c.delta, (1, 1, 0, 0), 20, 20)
+    check_step2(ctx, img, tau_ref1, c.lam, (1, 1, 0, 0), 20, 20)
+
+
+def test_config1_denoise_end_to_end(ctx):
+    c = CONFIGS["c1"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    lay = olayout.Layout(c.n, c.n, *L)
+    d_ref, tau_ref, _, _ = S.dd_denoise(img.astype(np.float64), c.delta, c.lam, lay,
+                                        (c.sweeps, c.inner), (c.sweeps, c.inner))
+    d, tau, s1, s2 = ctx.tv_stokes_denoise(_dev(img), c.delta, c.lam, L, (c.sweeps, c.inner, c.t),
+                                           (c.sweeps, c.inner, c.t), want_tau=True)
+    assert np.abs(tau.cpu().numpy() - tau_ref).max() <= TOL
+    assert np.abs(d.cpu().numpy() - d_ref).max() <= TOL
+    assert s1.pixel_updates == sum((b - a + 1) * (y - x + 1) for (a, b) in lay.ry for (x, y) in lay.rx) * 400
+
+
+def test_config2_full(ctx):
+    c = CONFIGS["c2"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    tau_ref, _ = check_step1(ctx, img, c.delta, L, c.sweeps, c.inner)
+    check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner)
+
+
+def test_config3_full_size_short_schedule(ctx):
+    """Config 3 at full size (2048^2, 8x8, s=16) in the bench launch configuration, with the
+    schedule shortened so the oracle finishes (step 1: 1 sweep x 2; step 2: 3 sweeps x 10)."""
+    c = CONFIGS["c3"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    tau_ref, _ = check_step1(ctx, img, c.delta, L, 1, 2)
+    check_step2(ctx, img, tau_ref, c.lam, L, 3, c.inner)
