@@ -1,0 +1,379 @@
+#!/usr/bin/env python3
+"""Benchmark of the TV-Stokes overlapping-Schwarz dual iteration on B200.
+
+One *step* = one full pass of the hot path: tv_stokes_denoise =
+step 1 (TFS, Alg. 2 + Alg. 5) then step 2 (IRV2, Alg. 2 + Alg. 3) on BASELINE config 3
+(2048 x 2048 Voronoi image, 8 x 8 subdomains, overlap 16, 50 sweeps x 10 inner per step).
+
+metric: dual pixel-updates/s (sum over subdomains of |Gamma_m| per inner update, overlap counted
+per subdomain, both steps), whole job over all ranks.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+       [--workload c1|c2|c3]
+N > 1 is launched by torchrun (one process per GPU); see DESIGN.md for the multi-GPU status.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from tvs_synth import CONFIGS  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP32 SIMT peak: 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FALLBACK_HBM_GBS = 6650.0
+
+
+def measured_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": FALLBACK_HBM_GBS}, "fallback"
+
+
+def workload(name):
+    c = CONFIGS[name]
+    return c, (c.m2, c.m1, c.overlap, c.overlap), (c.sweeps, c.inner, c.t)
+
+
+def sum_sub(n, L, extended):
+    from paper_2602_17494_b200 import layout_range
+    m2, m1, sy, sx = L
+    ys = [layout_range(n + 1, m2, sy, k) for k in range(m2)]
+    xs = [layout_range(n + 1, m1, sx, k) for k in range(m1)]
+    lim = n if extended else n - 1
+    return sum((min(b, lim) - a + 1) for a, b in ys) * sum((min(b, lim) - a + 1) for a, b in xs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)   # 256 MB write > 126 MB L2
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2602_17494_b200 as pkg
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    c, L, it = workload(args.workload)
+    img = c.image()
+    ctx = pkg.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    d0 = torch.from_numpy(img).cuda()
+    out = torch.empty_like(d0)
+    flush = torch.empty(64 * 1024 * 1024, device="cuda", dtype=torch.float32)
+    n = c.n
+    upd_step = (sum_sub(n, L, True) + sum_sub(n, L, False)) * it[0] * it[1]
+
+    def step():
+        return ctx.tv_stokes_denoise(d0, c.delta, c.lam, L, it, it, out=out)
+
+    for _ in range(args.warmup):
+        flush_l2(flush)
+        step()
+    torch.cuda.synchronize()
+    # ---- timed region: K steps, device events on the launching stream, L2 flushed between steps
+    ctx.reset_kernel_times()
+    ctx.set_profiling(True)
+    launches = 0
+    step_ms = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, _, s1, s2 = step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            launches += s1.launches + s2.launches
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ctx.set_profiling(False)
+    kt = ctx.kernel_times()
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * upd_step * args.steps / (total_ms / 1e3)
+
+    # ---- e2e: same metric through the host-buffer C-ABI call (H2D of d0 + D2H of d inside)
+    h_in = torch.from_numpy(img).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.tv_stokes_denoise_host(h_in.numpy(), c.delta, c.lam, L, it, it, out=h_out.numpy())
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_t = statistics.median(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_t], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel family (largest share of device time)
+    peaks, peak_src = measured_peaks()
+    fam_ms = kt.ms
+    dom = max(range(len(fam_ms)), key=lambda i: fam_ms[i])
+    names = pkg.KERNEL_FAMILIES
+    kern = {}
+    for i, nm in enumerate(names):
+        if kt.counts[i] == 0:
+            continue
+        avg = kt.ms[i] / kt.counts[i]
+        entry = {"launches": kt.counts[i], "avg_us": round(avg * 1e3, 3),
+                 "share": round(kt.ms[i] / max(total_ms, 1e-9), 4)}
+        if kt.flops[i] > 0:
+            entry["tflops"] = round(kt.flops[i] / (kt.ms[i] / 1e3) / 1e12, 3)
+        if kt.bytes[i] > 0:
+            entry["gbs"] = round(kt.bytes[i] / (kt.ms[i] / 1e3) / 1e9, 1)
+        kern[nm] = entry
+    if kt.flops[dom] > 0 and os.environ.get("TVS_GEMM", "tc") != "simt":
+        # 3xTF32 tcgen05 contraction: tf32 dense peak = measured bf16 burst x (1.1/2.25 nominal),
+        # and one fp32-accurate flop costs 3 tf32 flops
+        tf32 = peaks.get("bf16_tflops", 1590.0) * (1.1 / 2.25)
+        pk = tf32 / 3.0
+        ach = kt.flops[dom] / (kt.ms[dom] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(pk, 1),
+                "unit": "TFLOP/s", "frac": round(ach / pk, 4), "traffic": None, "kernel": names[dom],
+                "peak_source": f"tf32 = bf16_tflops ({peak_src}) x 1.1/2.25 = {tf32:.0f}; fp32-equivalent "
+                               "of 3xTF32 = tf32/3; achieved counts algorithmic fp32 flops 2MNK"}
+    elif kt.flops[dom] > 0:
+        ach = kt.flops[dom] / (kt.ms[dom] / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(FP32_SIMT_PEAK_TFLOPS, 1),
+                "unit": "TFLOP/s", "frac": round(ach / FP32_SIMT_PEAK_TFLOPS, 4),
+                "traffic": None, "kernel": names[dom],
+                "peak_source": "FP32 SIMT: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md)"}
+    else:
+        ach = kt.bytes[dom] / (kt.ms[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "kernel": names[dom],
+                "peak_source": f"hbm_gbs ({peak_src}) MEASURED_PEAKS.json"}
+    line = {
+        "metric": "dual pixel-updates/s (step 1 + step 2, overlap counted per subdomain)",
+        "value": value, "unit": "pixel-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f32 (fp64 y-solves)", "data": "synthetic",
+        "config": {"workload": f"{c.name}: {n}x{n} Voronoi-{c.cells}, {c.m2}x{c.m1} subdomains, "
+                               f"overlap {c.overlap}, {c.sweeps}x{c.inner} per step, delta {c.delta}, "
+                               f"lambda {c.lam}, t {c.t}",
+                   "pixel_updates_per_step": upd_step, "l2": "flushed (256 MB write) between steps",
+                   "parallelism": "replicas" if world > 1 else "1 GPU"},
+        "gpu_launches": launches,
+        "e2e": {"value": world * upd_step / (e2e_t / 1e3), "unit": "pixel-updates/s",
+                "h2d_bytes_per_step": int(img.nbytes), "d2h_bytes_per_step": int(img.nbytes),
+                "ms_per_step": e2e_t},
+        "roofline": roof,
+        "kernels": kern,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(c, L, it, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(c, L, it, step1_subs=1):
+    """Time the fp64 oracle on a bounded sample of the workload and extrapolate the rate:
+    step 2: one outer sweep x `inner` updates over ALL subdomains (Alg. 2 + Alg. 3);
+    step 1: `inner`=1 localized Alg. 5 update on `step1_subs` subdomain(s) (plus its omega0),
+    with the per-sweep global residual r^n timed once.  Returns (rate, sample description)."""
+    from oracle import layout as olayout, ops, solvers as S, spectral
+    img = c.image().astype(np.float64)
+    n = c.n
+    lay = olayout.Layout(n, n, *L)
+    # step 2 sample
+    tau0 = S.tau0(img) * 0.0
+    t0 = time.perf_counter()
+    S.dd_step2(img, tau0, c.lam, lay, 1, it[1], it[2])
+    t2 = time.perf_counter() - t0
+    u2 = sum((min(b, n - 1) - a + 1) for a, b in lay.ry) * sum((min(b, n - 1) - a + 1) for a, b in lay.rx) * it[1]
+    # step 1 sample
+    n2t = n + 1
+    whole = S.full_rect(n2t, n2t)
+    t0 = time.perf_counter()
+    f = spectral.project(S.tau0(img)) / c.delta
+    p = np.zeros((2, 2, n2t, n2t))
+    r = f - spectral.project(ops.multidiv(p))
+    tg = time.perf_counter() - t0
+    u1 = 0
+    t0 = time.perf_counter()
+    for m in lay.subdomains()[:step1_subs]:
+        s = lay.rect(m, True)
+        q0 = np.zeros((2, 2) + S.rect_shape(s))
+        S._tfs_inner_local(m, lay, p, r, q0, 1, it[2])
+        u1 += S.rect_shape(s)[0] * S.rect_shape(s)[1]
+    t1 = time.perf_counter() - t0
+    # per-update costs -> rate for the full workload (updates of both steps / extrapolated time)
+    nsub = len(lay.subdomains())
+    sweeps, inner = it[0], it[1]
+    full_u1 = sum((b - a + 1) for a, b in lay.ry) * sum((b - a + 1) for a, b in lay.rx) * sweeps * inner
+    full_u2 = u2 * sweeps
+    # one Alg.5 update (with omega0 share) per subdomain costs ~t1/(2*step1_subs) each
+    per_sub_update = t1 / (2.0 * step1_subs)
+    full_t1 = per_sub_update * nsub * sweeps * (inner + 1) + tg * (sweeps + 2) / 2.0
+    full_t2 = t2 * sweeps
+    rate = (full_u1 + full_u2) / (full_t1 + full_t2)
+    desc = (f"{c.name}: step 2 = 1 sweep x {inner} on all {nsub} subdomains ({t2:.1f} s); step 1 = "
+            f"1 Alg.5 update + omega0 on {step1_subs} subdomain(s) ({t1:.1f} s) + 2 global P "
+            f"({tg:.1f} s); rate extrapolated to the full {sweeps}x{inner} schedule of both steps")
+    return rate, desc, t1 + t2 + tg
+
+
+def cpu_baseline(c, L, it, budget_s=30.0):
+    rate, desc, secs = oracle_sample(c, L, it)
+    return {"value": rate, "unit": "pixel-updates/s", "cores": _blas_threads(), "kind": "oracle",
+            "sample": desc, "sample_seconds": round(secs, 1),
+            "cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    c, L, it = workload(args.workload)
+    for _ in range(args.warmup):
+        oracle_sample(c, L, it)
+    rates, secs = [], 0.0
+    for _ in range(args.steps):
+        r, desc, s = oracle_sample(c, L, it)
+        rates.append(r)
+        secs += s
+    value = statistics.median(rates)
+    c_name = c.name
+    line = {
+        "impl": "reference", "metric": "dual pixel-updates/s (step 1 + step 2, overlap counted per subdomain)",
+        "value": value, "unit": "pixel-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c_name, "note": "fp64 CPU oracle on a bounded sample per step"},
+        "cpu_baseline": {"value": value, "unit": "pixel-updates/s", "cores": _blas_threads(),
+                         "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "pixel-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

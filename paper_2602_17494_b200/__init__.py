@@ -22,7 +22,7 @@ ABI_SYMBOLS = [
     "tvs_create", "tvs_destroy", "tvs_last_error", "tvs_nccl_unique_id", "tvs_owned_rows",
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
-    "tvs_reset_kernel_times",
+    "tvs_reset_kernel_times", "tvs_selftest_gemm",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
     arr7d = ctypes.c_double * 7
     lib.tvs_kernel_times.argtypes = [P, arr7i, arr7d, arr7d, arr7d]
     lib.tvs_reset_kernel_times.argtypes = [P]
+    lib.tvs_selftest_gemm.argtypes = [P, i32, i32, i32, i32, ctypes.c_uint64,
+                                      ctypes.POINTER(ctypes.c_double)]
     for name in ABI_SYMBOLS:
         if name != "tvs_last_error":
             getattr(lib, name).restype = ctypes.c_int
@@ -255,6 +257,12 @@ class Context:
             ctypes.c_void_p(d.ctypes.data), None,
             ctypes.byref(s1), ctypes.byref(s2), self._stream(stream)), "tv_stokes_denoise_host")
         return d, s1, s2
+
+    def selftest_gemm(self, M, N, K, impl, seed=1):
+        err = ctypes.c_double()
+        self._check(self.lib.tvs_selftest_gemm(self.h, M, N, K, impl, seed, ctypes.byref(err)),
+                    "tvs_selftest_gemm")
+        return err.value
 
     def set_profiling(self, on: bool):
         self._check(self.lib.tvs_set_profiling(self.h, 1 if on else 0), "tvs_set_profiling")

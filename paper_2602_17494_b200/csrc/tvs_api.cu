@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -94,8 +95,10 @@ struct ProjBatch {
   float *qhat = nullptr;
   double *z = nullptr, *rinv = nullptr;
   float *phx = nullptr, *phy = nullptr;
-  GemmDesc *d_fwd = nullptr, *d_inv = nullptr;
+  GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
+  GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
+  int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
   double fwd_flops = 0, inv_flops = 0, solve_bytes = 0;
 };
 
@@ -127,7 +130,7 @@ struct Plan {
 
 struct Tables {
   int n = 0, ld = 0;
-  float *cf = nullptr, *cn = nullptr, *sn = nullptr;
+  float *cf = nullptr, *cn = nullptr, *sn = nullptr, *snT = nullptr;
   std::vector<std::unique_ptr<DevBuf>> bufs;
 };
 
@@ -145,6 +148,7 @@ struct tvs_ctx {
   std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
   std::map<int, std::unique_ptr<Tables>> tables;
   bool profiling = false;
+  bool gemm_tc = true;   // TVS_GEMM=simt selects the SIMT fp32 GEMM (A/B comparisons)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<PendingEv> pending;
@@ -261,7 +265,8 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
   TRY(dalloc(ctx, t->bufs, &t->cf, el));
   TRY(dalloc(ctx, t->bufs, &t->cn, el));
   TRY(dalloc(ctx, t->bufs, &t->sn, el));
-  CK(launch_dct_tables(n, t->cf, t->cn, t->sn, t->ld, 0));
+  TRY(dalloc(ctx, t->bufs, &t->snT, el));
+  CK(launch_dct_tables(n, t->cf, t->cn, t->sn, t->snT, t->ld, 0));
   CK(cudaDeviceSynchronize());
   *out = t.get();
   ctx->tables[n] = std::move(t);
@@ -299,7 +304,30 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
-  std::vector<GemmDesc> fwd, inv;
+  std::vector<GemmDesc> fwd, inv, fwd_tc, inv_tc;
+  // ∇φ output is plane-major: G[c][tile][AP][ldG]
+  const size_t gplane = (size_t)B.ntiles * B.AP * ldG;
+  for (int i = 0; i < B.ntiles;) {
+    // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
+    int j = i + 1;
+    while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
+           B.tiles[j].px1 == B.tiles[i].px1)
+      ++j;
+    const ProjTile &t = B.tiles[i];
+    const int cnt = j - i;
+    const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
+    const int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
+    const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1);
+    fwd_tc.push_back({q + (size_t)i * B.AT * ldq, T->cn + t.tx0,
+                      B.qhat + (size_t)i * B.AT * B.ldn, Mf, n1t, bt, ldq, T->ld, B.ldn});
+    inv_tc.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->snT + (size_t)t.tx0 * T->ld,
+                      G + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+    inv_tc.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cf + (size_t)t.tx0 * T->ld,
+                      G + gplane + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+    B.tcM_fwd = std::max(B.tcM_fwd, Mf);
+    B.tcM_inv = std::max(B.tcM_inv, Mi);
+    i = j;
+  }
   for (int i = 0; i < B.ntiles; ++i) {
     const ProjTile &t = B.tiles[i];
     int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
@@ -307,9 +335,9 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     fwd.push_back({q + (size_t)i * B.AT * ldq, T->cf + (size_t)t.tx0 * T->ld,
                    B.qhat + (size_t)i * B.AT * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
     inv.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->sn + t.tx0,
-                   G + ((size_t)i * 2 + 0) * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+                   G + (size_t)i * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
     inv.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cn + t.tx0,
-                   G + ((size_t)i * 2 + 1) * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+                   G + gplane + (size_t)i * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
     B.fwdM = std::max(B.fwdM, nt);
     B.fwdN = std::max(B.fwdN, n1t);
     B.invM = std::max(B.invM, no);
@@ -321,6 +349,9 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   }
   TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
   TRY(upload(ctx, P.bufs, &B.d_inv, inv));
+  B.nstack = (int)fwd_tc.size();
+  TRY(upload(ctx, P.bufs, &B.d_fwd_tc, fwd_tc));
+  TRY(upload(ctx, P.bufs, &B.d_inv_tc, inv_tc));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   CK(cudaDeviceSynchronize());
   return TVS_OK;
@@ -355,8 +386,11 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   Geo &g = P->geo;
   g.M = P->M;
   std::vector<float> thy, thx;
-  for (int a = 0; a < L.m2; ++a)
-    for (int b = 0; b < L.m1; ++b) {
+  // subdomains are stored column-major (m = m1_index * M2 + m2_index) so the tiles of one layout
+  // column -- which share their x-range and hence the DCT operand of kernel (b) -- are contiguous
+  // and their partial-DCT GEMMs can be stacked into one.
+  for (int b = 0; b < L.m1; ++b)
+    for (int a = 0; a < L.m2; ++a) {
       SubDesc s{};
       s.y0 = ly[a];
       s.y1 = std::min(hy[a], G2 - 1);
@@ -457,14 +491,19 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
 // grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).
 tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s) {
   const int G2 = P.G2, G1 = P.G1;
-  TRY(run(ctx, s, F_FWD, 0, B.fwd_flops,
-          [&] { return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s); }));
+  const bool tc = ctx->gemm_tc;
+  TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
+    return tc ? launch_gemm_tc(B.d_fwd_tc, B.nstack, B.tcM_fwd, B.fwdN, 144, false, s)
+              : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
+  }));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
     return launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z, B.phx,
                              B.phy, B.AP, s);
   }));
-  TRY(run(ctx, s, F_INV, 0, B.inv_flops,
-          [&] { return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s); }));
+  TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
+    return tc ? launch_gemm_tc(B.d_inv_tc, 2 * B.nstack, B.tcM_inv, B.invN, 144, true, s)
+              : launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
+  }));
   return TVS_OK;
 }
 
@@ -543,7 +582,7 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       cur ^= 1;
     }
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_combine(P->d_subs, g, 2, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M1,
+      return launch_combine(P->d_subs, g, 2, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M2,
                             P->v[cur], P->p, ld, n2, n1, P->ahat, P->d_bad, s);
     }));
   }
@@ -625,7 +664,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       cur ^= 1;
     }
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_combine(P->d_subs, g, 4, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M1,
+      return launch_combine(P->d_subs, g, 4, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M2,
                             P->v[cur], P->p, ld, G2, G1, P->ahat, P->d_bad, s);
     }));
   }
@@ -665,6 +704,8 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->device = device;
   c->rank = rank;
   c->world = world;
+  const char *g = getenv("TVS_GEMM");
+  c->gemm_tc = !(g && strcmp(g, "simt") == 0);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;
@@ -797,6 +838,57 @@ tvs_status tv_stokes_denoise_host(tvs_ctx *ctx, const float *d0, int32_t n2, int
   CK(cudaMemcpyAsync(d, ctx->h_d->p, img, cudaMemcpyDeviceToHost, s));
   if (tau) CK(cudaMemcpyAsync(tau, ctx->h_tau->p, tb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return TVS_OK;
+}
+
+tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int32_t impl,
+                             uint64_t seed, double *max_rel_err) {
+  if (!ctx || !max_rel_err || M < 1 || N < 1 || K < 1) return TVS_EINVAL;
+  cudaSetDevice(ctx->device);
+  const int lda = (K + 3) / 4 * 4;
+  std::vector<float> A((size_t)M * lda, 0.f), Bt((size_t)N * lda, 0.f), C((size_t)M * N, 0.f);
+  uint64_t z = seed ? seed : 1;
+  auto rnd = [&]() {
+    z = z * 6364136223846793005ULL + 1442695040888963407ULL;
+    return (float)((double)(z >> 11) / 9007199254740992.0 * 2.0 - 1.0);
+  };
+  for (int i = 0; i < M; ++i)
+    for (int k = 0; k < K; ++k) A[(size_t)i * lda + k] = rnd();
+  for (int j = 0; j < N; ++j)
+    for (int k = 0; k < K; ++k) Bt[(size_t)j * lda + k] = rnd();
+  std::vector<std::unique_ptr<DevBuf>> own;
+  float *dA, *dB, *dC, *dBk;
+  GemmDesc *dd;
+  TRY(dalloc(ctx, own, &dA, A.size()));
+  TRY(dalloc(ctx, own, &dB, Bt.size()));
+  TRY(dalloc(ctx, own, &dBk, (size_t)K * N));
+  TRY(dalloc(ctx, own, &dC, C.size()));
+  CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice));
+  std::vector<float> Bk((size_t)K * N);
+  for (int k = 0; k < K; ++k)
+    for (int j = 0; j < N; ++j) Bk[(size_t)k * N + j] = Bt[(size_t)j * lda + k];
+  CK(cudaMemcpy(dBk, Bk.data(), Bk.size() * 4, cudaMemcpyHostToDevice));
+  std::vector<GemmDesc> desc = {
+      {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
+  TRY(upload(ctx, own, &dd, desc));
+  cudaError_t e = impl == 0 ? launch_gemm(dd, 1, M, N, 0)
+                            : launch_gemm_tc(dd, 1, M, N, impl == 2 ? 144 : 128, true, 0);
+  if (e != cudaSuccess) return fail(ctx, TVS_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost));
+  double worst = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      double ref = 0, mag = 0;
+      for (int k = 0; k < K; ++k) {
+        double p = (double)A[(size_t)i * lda + k] * (double)Bt[(size_t)j * lda + k];
+        ref += p;
+        mag += fabs(p);
+      }
+      worst = std::max(worst, fabs((double)C[(size_t)i * N + j] - ref) / std::max(mag, 1e-30));
+    }
+  *max_rel_err = worst;
   return TVS_OK;
 }
 

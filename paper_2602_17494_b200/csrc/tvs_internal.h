@@ -56,7 +56,7 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s);
 cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
-                           const int2 *covx, const int *loy, const int *lox, int m1,
+                           const int2 *covx, const int *loy, const int *lox, int m2,
                            const float *q, float *p, int ld, int n2, int n1, float ahat,
                            int *bad, cudaStream_t s);
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
@@ -80,10 +80,14 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
                           float *vout, int n2, int n1, float t, cudaStream_t s);
 
 // projection (kernel b)
-cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, int ld, cudaStream_t s);
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, int ld,
+                              cudaStream_t s);
 cudaError_t launch_pivots(const ProjTile *chains_tiles, const int *chain_first_tile, int nchains,
                           int n2, int n1, double *rinv, int ldn, int AT, cudaStream_t s);
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s);
+// tcgen05 3xTF32 GEMM: C = A * Bt^T, Bt given as [N][K] row-major (tvs_gemm_tc.cu)
+cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                           bool b_aligned, cudaStream_t s);
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
                               const float *qhat, int AT, int ldn, const double *rinv,
                               double *z, float *phx, float *phy, int AP, cudaStream_t s);

@@ -194,7 +194,7 @@ k_sweep2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
 // order (m2 ascending, then m1) so overlaps are bitwise reproducible.  Flags non-finite values.
 __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
                           const int2 *__restrict__ covy, const int2 *__restrict__ covx,
-                          const int *__restrict__ loy, const int *__restrict__ lox, int m1,
+                          const int *__restrict__ loy, const int *__restrict__ lox, int m2,
                           const float *__restrict__ q, float *__restrict__ p, int ld, int n2,
                           int n1, float ahat, int *bad) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -205,7 +205,7 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
     float acc = 0.f;
     for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
       for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
-        int m = ky * m1 + kx;
+        int m = kx * m2 + ky;   // subdomains are stored column-major (see tvs_api.cu)
         int li = i - loy[ky], lj = j - lox[kx];
         acc += q[(((size_t)m * planes + c) * g.A + li) * g.ldS + lj];
       }
@@ -332,7 +332,7 @@ __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float 
   size_t pl = (size_t)n2 * ld;
   for (int k = 0; k < 2; ++k) {
     float w = w_S(vb, k, li, lj, gi, gj, a, b, g, n2, n1);
-    float gp = gphi[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * ldg + lj];
+    float gp = gphi[(((size_t)k * g.M + blockIdx.z) * g.AP + li) * ldg + lj];
     om[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * g.ldP + lj] =
         r[k * pl + (size_t)gi * ld + gj] + (w - gp);
   }
@@ -355,7 +355,7 @@ __global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *_
   float *ob = vout + (size_t)blockIdx.z * 4 * g.A * g.ldS;
   float th = theta_at(thy, thx, sd, g, li, lj);
   for (int k = 0; k < 2; ++k) {
-    const float *gk = gphi + ((size_t)blockIdx.z * 2 + k) * g.AP * ldg;
+    const float *gk = gphi + ((size_t)k * g.M + blockIdx.z) * g.AP * ldg;
     const float *ok = om + ((size_t)blockIdx.z * 2 + k) * g.AP * g.ldP;
     auto rho = [&](int i, int j) {
       return w_S(vb, k, i, j, sd.y0 + i, sd.x0 + j, a, b, g, n2, n1) -
@@ -383,10 +383,11 @@ __global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *_
 // spectrally (c_j(x+1) - c_j(x) = -s_j sigma_j sin(pi j (x+1)/N)), the y-derivative by fp64
 // differencing of the solved column.
 
-// Tables: cf[x][j] = cos(pi j (2x+1) / (2n)) (forward), cn[j][x] (same, transposed) and
-// sn[j][x] = sin(pi j (x+1) / n), evaluated in fp64 with exact integer argument reduction.
+// Tables: cf[x][j] = cos(pi j (2x+1) / (2n)) (forward), cn[j][x] (same, transposed),
+// sn[j][x] = sin(pi j (x+1) / n) and snT[x][j] (transposed), evaluated in fp64 with exact
+// integer argument reduction.
 __global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ cn,
-                             float *__restrict__ sn, int ld) {
+                             float *__restrict__ sn, float *__restrict__ snT, int ld) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= n || j >= n) return;
@@ -397,6 +398,7 @@ __global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ 
   cf[(size_t)x * ld + j] = (float)c;
   cn[(size_t)j * ld + x] = (float)c;
   sn[(size_t)j * ld + x] = (float)s;
+  snT[(size_t)x * ld + j] = (float)s;
 }
 
 // Thomas pivots of the Schur-corrected tridiagonal M_T(s_j) on rows [ty0, ty1] of an axis of
@@ -598,11 +600,11 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
   return cudaGetLastError();
 }
 cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
-                           const int2 *covx, const int *loy, const int *lox, int m1,
+                           const int2 *covx, const int *loy, const int *lox, int m2,
                            const float *q, float *p, int ld, int n2, int n1, float ahat, int *bad,
                            cudaStream_t s) {
   k_combine<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(subs, g, planes, covy, covx, loy, lox,
-                                                         m1, q, p, ld, n2, n1, ahat, bad);
+                                                         m2, q, p, ld, n2, n1, ahat, bad);
   return cudaGetLastError();
 }
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
@@ -649,8 +651,9 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
                                                                ldg, om, vout, n2, n1, t);
   return cudaGetLastError();
 }
-cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, int ld, cudaStream_t s) {
-  k_dct_tables<<<grid2(n, n, 32, 8), dim3(32, 8), 0, s>>>(n, cf, cn, sn, ld);
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, int ld,
+                              cudaStream_t s) {
+  k_dct_tables<<<grid2(n, n, 32, 8), dim3(32, 8), 0, s>>>(n, cf, cn, sn, snT, ld);
   return cudaGetLastError();
 }
 cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, int n2, int n1,
