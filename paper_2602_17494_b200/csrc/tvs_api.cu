@@ -88,14 +88,16 @@ struct ProjBatch {
   std::vector<ProjTile> tiles;
   ProjTile *d_tiles = nullptr;
   int *d_first = nullptr;
-  float *q = nullptr;       // input, [tile][AT][ldq]
+  float *q = nullptr;       // input, [tile][AT][ldq] (hi plane in 3xTF32 mode)
+  float *qlo = nullptr;     // lo plane (3xTF32 mode)
   int ldq = 0;
   float *G = nullptr;       // output, [tile][2][AP][ldG]
   int ldG = 0;
   float *qhat = nullptr;
   double *z = nullptr, *rinv = nullptr;
-  float *phx = nullptr, *phy = nullptr;
+  float *phx = nullptr, *phy = nullptr, *phx_lo = nullptr, *phy_lo = nullptr;
   GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
+  GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
   GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
   int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
@@ -121,7 +123,7 @@ struct Plan {
   double *g0 = nullptr;
   int *d_bad = nullptr;
   // step 1 only
-  float *vtmp = nullptr, *q = nullptr, *gphi = nullptr;
+  float *vtmp = nullptr, *q = nullptr, *qlo = nullptr, *gphi = nullptr, *qglo = nullptr;
   float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
   ProjBatch local, global;
   int64_t sum_S = 0, sum_T = 0;
@@ -131,6 +133,8 @@ struct Plan {
 struct Tables {
   int n = 0, ld = 0;
   float *cf = nullptr, *cn = nullptr, *sn = nullptr, *snT = nullptr;
+  float *split6 = nullptr;   // [cf_hi, cf_lo, cn_hi, cn_lo, snT_hi, snT_lo], each n x ld
+  float *part(int k) const { return split6 + (size_t)k * n * ld; }
   std::vector<std::unique_ptr<DevBuf>> bufs;
 };
 
@@ -266,7 +270,8 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
   TRY(dalloc(ctx, t->bufs, &t->cn, el));
   TRY(dalloc(ctx, t->bufs, &t->sn, el));
   TRY(dalloc(ctx, t->bufs, &t->snT, el));
-  CK(launch_dct_tables(n, t->cf, t->cn, t->sn, t->snT, t->ld, 0));
+  TRY(dalloc(ctx, t->bufs, &t->split6, 6 * el));
+  CK(launch_dct_tables(n, t->cf, t->cn, t->sn, t->snT, t->split6, t->ld, 0));
   CK(cudaDeviceSynchronize());
   *out = t.get();
   ctx->tables[n] = std::move(t);
@@ -275,7 +280,8 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
 
 // Build the projection batch for tiles (chains = distinct row ranges).
 tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
-                      int n2t, int n1t, float *q, int ldq, float *G, int ldG, const Tables *T) {
+                      int n2t, int n1t, float *q, float *qlo, int ldq, float *G, int ldG,
+                      const Tables *T) {
   B.tiles = tiles_in;
   B.ntiles = (int)tiles_in.size();
   std::map<std::pair<int, int>, int> chain_of;
@@ -294,6 +300,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   B.nchains = (int)first.size();
   B.ldn = round_up(n1t, 4);
   B.q = q;
+  B.qlo = qlo;
   B.ldq = ldq;
   B.G = G;
   B.ldG = ldG;
@@ -304,7 +311,10 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phx_lo, (size_t)B.ntiles * B.AP * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phy_lo, (size_t)B.ntiles * B.AP * B.ldn));
   std::vector<GemmDesc> fwd, inv, fwd_tc, inv_tc;
+  std::vector<GemmDesc2> fwd2, inv2;
   // ∇φ output is plane-major: G[c][tile][AP][ldG]
   const size_t gplane = (size_t)B.ntiles * B.AP * ldG;
   for (int i = 0; i < B.ntiles;) {
@@ -324,6 +334,18 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
                       G + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
     inv_tc.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cf + (size_t)t.tx0 * T->ld,
                       G + gplane + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+    // 3xTF32 pre-split forms; q carries a leading zero offset of (tx0 & 3) columns so the table
+    // rows start 16-byte aligned: K = bt + off, tables from column tx0 - off
+    const int off = t.tx0 & 3;
+    fwd2.push_back({q + (size_t)i * B.AT * ldq, qlo + (size_t)i * B.AT * ldq,
+                    T->part(2) + (t.tx0 - off), T->part(3) + (t.tx0 - off),
+                    B.qhat + (size_t)i * B.AT * B.ldn, Mf, n1t, bt + off, ldq, T->ld, B.ldn});
+    inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, B.phx_lo + (size_t)i * B.AP * B.ldn,
+                    T->part(4) + (size_t)t.tx0 * T->ld, T->part(5) + (size_t)t.tx0 * T->ld,
+                    G + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+    inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, B.phy_lo + (size_t)i * B.AP * B.ldn,
+                    T->part(0) + (size_t)t.tx0 * T->ld, T->part(1) + (size_t)t.tx0 * T->ld,
+                    G + gplane + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
     B.tcM_fwd = std::max(B.tcM_fwd, Mf);
     B.tcM_inv = std::max(B.tcM_inv, Mi);
     i = j;
@@ -332,7 +354,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     const ProjTile &t = B.tiles[i];
     int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
     int no = t.py1 - t.ty0 + 1, bo = t.px1 - t.tx0 + 1;
-    fwd.push_back({q + (size_t)i * B.AT * ldq, T->cf + (size_t)t.tx0 * T->ld,
+    fwd.push_back({q + (size_t)i * B.AT * ldq + (t.tx0 & 3), T->cf + (size_t)t.tx0 * T->ld,
                    B.qhat + (size_t)i * B.AT * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
     inv.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->sn + t.tx0,
                    G + (size_t)i * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
@@ -352,6 +374,8 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   B.nstack = (int)fwd_tc.size();
   TRY(upload(ctx, P.bufs, &B.d_fwd_tc, fwd_tc));
   TRY(upload(ctx, P.bufs, &B.d_inv_tc, inv_tc));
+  TRY(upload(ctx, P.bufs, &B.d_fwd2, fwd2));
+  TRY(upload(ctx, P.bufs, &B.d_inv2, inv2));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   CK(cudaDeviceSynchronize());
   return TVS_OK;
@@ -416,7 +440,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     }
   g.ldS = round_up(g.B, 4);
   g.ldP = round_up(g.BP, 4);
-  g.ldT = round_up(g.BT, 4);
+  g.ldT = round_up(g.BT + 3, 4);   // + column offset (x0 & 3) of the forward GEMM operand
   thy.assign((size_t)L.m2 * g.A, 0.f);
   thx.assign((size_t)L.m1 * g.B, 0.f);
   for (int a = 0; a < L.m2; ++a)
@@ -469,6 +493,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * 2 * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->vtmp, vsz));
     TRY(dalloc(ctx, P->bufs, &P->q, (size_t)g.M * g.AT * g.ldT));
+    TRY(dalloc(ctx, P->bufs, &P->qlo, (size_t)g.M * g.AT * g.ldT));
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)g.M * 2 * g.AP * g.ldP));
     size_t pl = (size_t)G2 * P->ld;
     TRY(dalloc(ctx, P->bufs, &P->f, 2 * pl));
@@ -476,12 +501,13 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->w, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->r, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->qg, pl));
+    TRY(dalloc(ctx, P->bufs, &P->qglo, pl));
     TRY(dalloc(ctx, P->bufs, &P->Gg, 2 * pl));
     std::vector<ProjTile> lt;
     for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
-    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T));
+    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, P->qlo, g.ldT, P->gphi, g.ldP, T));
     std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, G2 - 1, G1 - 1, 0, 0}};
-    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->ld, P->Gg, P->ld, T));
+    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->qglo, P->ld, P->Gg, P->ld, T));
   }
   *out = P.get();
   ctx->plans[key] = std::move(P);
@@ -493,15 +519,15 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s) {
   const int G2 = P.G2, G1 = P.G1;
   const bool tc = ctx->gemm_tc;
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
-    return tc ? launch_gemm_tc(B.d_fwd_tc, B.nstack, B.tcM_fwd, B.fwdN, 144, false, s)
+    return tc ? launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
               : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
   }));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
     return launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z, B.phx,
-                             B.phy, B.AP, s);
+                             B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
   }));
   TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
-    return tc ? launch_gemm_tc(B.d_inv_tc, 2 * B.nstack, B.tcM_inv, B.invN, 144, true, s)
+    return tc ? launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
               : launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
   }));
   return TVS_OK;
@@ -617,11 +643,12 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   const Geo g = P->geo;
   const int G2 = P->G2, G1 = P->G1, ld = P->ld;
   const size_t pl = (size_t)G2 * ld;
+  const bool tc = ctx->gemm_tc;
   CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
   // f = delta^{-1} P tau_0 (tau_0 pre-projected, reading A1)
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_tau0(d0, n2, n1, P->t0, ld, s); }));
   TRY(run(ctx, s, F_OTHER, 0, 0,
-          [&] { return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, s); }));
+          [&] { return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, s); }));
   TRY(project_batch(ctx, *P, P->global, s));
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
     return launch_axpby2(P->t0, P->Gg, nullptr, ld, G2, G1, 1.f / delta, -1.f / delta, 0.f, P->f,
@@ -633,7 +660,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   auto residual = [&](float *out, float scale) -> tvs_status {
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, s); }));
     TRY(run(ctx, s, F_OTHER, 0, 0,
-            [&] { return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, s); }));
+            [&] { return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, s); }));
     TRY(project_batch(ctx, *P, P->global, s));
     return run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, s);
@@ -648,14 +675,14 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       return launch_load_tp(P->d_subs, g, P->d_thy, P->d_thx, P->p, ld, G2, G1, P->vtmp, s);
     }));
     TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, s); }));
+            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, tc ? P->qlo : nullptr, s); }));
     TRY(project_batch(ctx, *P, P->local, s));
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_omega0_1(P->d_subs, g, P->r, ld, P->vtmp, P->gphi, g.ldP, G2, G1, P->om, s);
     }));
     for (int k = 0; k < it.inner; ++k) {
       TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, s); }));
+              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, tc ? P->qlo : nullptr, s); }));
       TRY(project_batch(ctx, *P, P->local, s));
       TRY(run(ctx, s, F_SWEEP1, sweep_bytes, 0, [&] {
         return launch_sweep1(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->gphi, g.ldP, P->om,
@@ -872,8 +899,32 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
   std::vector<GemmDesc> desc = {
       {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
   TRY(upload(ctx, own, &dd, desc));
-  cudaError_t e = impl == 0 ? launch_gemm(dd, 1, M, N, 0)
-                            : launch_gemm_tc(dd, 1, M, N, impl == 2 ? 144 : 128, true, 0);
+  cudaError_t e;
+  if (impl == 3) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
+    auto rna = [](float x) {
+      uint32_t u;
+      memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      float h;
+      memcpy(&h, &u, 4);
+      return h;
+    };
+    std::vector<float> Ah(A.size()), Al(A.size()), Bh(Bt.size()), Bl(Bt.size());
+    for (size_t i = 0; i < A.size(); ++i) { Ah[i] = rna(A[i]); Al[i] = A[i] - Ah[i]; }
+    for (size_t i = 0; i < Bt.size(); ++i) { Bh[i] = rna(Bt[i]); Bl[i] = Bt[i] - Bh[i]; }
+    float *dAh, *dAl, *dBh, *dBl;
+    GemmDesc2 *dd2;
+    TRY(upload(ctx, own, &dAh, Ah));
+    TRY(upload(ctx, own, &dAl, Al));
+    TRY(upload(ctx, own, &dBh, Bh));
+    TRY(upload(ctx, own, &dBl, Bl));
+    std::vector<GemmDesc2> d2 = {{dAh, dAl, dBh, dBl, dC, M, N, K, lda, lda, N}};
+    TRY(upload(ctx, own, &dd2, d2));
+    e = launch_gemm_tc2(dd2, 1, M, N, 144, 0);
+  } else {
+    e = impl == 0 ? launch_gemm(dd, 1, M, N, 0)
+                  : launch_gemm_tc(dd, 1, M, N, impl == 2 ? 144 : 128, true, 0);
+  }
   if (e != cudaSuccess) return fail(ctx, TVS_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost));

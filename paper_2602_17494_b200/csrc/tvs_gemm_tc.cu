@@ -266,6 +266,173 @@ __global__ void __launch_bounds__(NT) k_gemm_tc(const GemmDesc *__restrict__ des
                  "n"(SM::TMEM_COLS));
 }
 
+// ---------------------------------------------------------------------------------------------
+// v2: operands arrive pre-split (A_hi/A_lo, B_hi/B_lo planes written by their producers, hi
+// exactly representable in tf32).  The mainloop is pure data movement: 16-byte zero-filling
+// cp.async copies straight into the core-matrix layout, a STAGES-deep cp.async group ring, and
+// the same single-thread tcgen05.mma issue + mbarrier commit per stage.
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NT) k_gemm_tc2(const GemmDesc2 *__restrict__ descs) {
+  using SM = Smem<BN>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const GemmDesc2 d = descs[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= d.M || n0 >= d.N) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * SM::STAGE);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + STAGES * SM::STAGE + 64);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(SM::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (d.K + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(smem);
+
+  // one K slice = (A_hi, A_lo: 128 rows x 4 chunks) + (B_hi, B_lo: BN rows x 4 chunks) of 16 B
+  constexpr int A_CH = BM * (BK / 4), B_CH = BN * (BK / 4);
+  constexpr int TOT = 2 * A_CH + 2 * B_CH;
+  auto issue = [&](int s, int kt) {
+    const int k0 = kt * BK;
+    const uint32_t st = sbase + s * SM::STAGE;
+#pragma unroll 1
+    for (int c = tid; c < TOT; c += NT) {
+      int part, rem;
+      if (c < 2 * A_CH) { part = c / A_CH; rem = c - part * A_CH; }
+      else { part = 2 + (c - 2 * A_CH) / B_CH; rem = (c - 2 * A_CH) - (part - 2) * B_CH; }
+      const int row = rem >> 2, kc = rem & 3;
+      const int k = k0 + 4 * kc;
+      const bool isA = part < 2;
+      const int R = isA ? BM : BN;
+      const int grow = (isA ? m0 : n0) + row;
+      const int lim = isA ? d.M : d.N;
+      const float *src = isA ? (part == 0 ? d.Ahi : d.Alo) : (part == 2 ? d.Bhi : d.Blo);
+      const int ld = isA ? d.lda : d.ldb;
+      int valid = d.K - k;
+      valid = valid < 0 ? 0 : (valid > 4 ? 4 : valid);
+      if (grow >= lim) valid = 0;
+      const float *g = valid ? src + (size_t)grow * ld + k : src;
+      const uint32_t off = isA ? (part == 0 ? 0 : SM::A_BYTES) : (2 * SM::A_BYTES + (part == 2 ? 0 : SM::B_BYTES));
+      const uint32_t dst = st + off + core_off(row, 4 * kc, R);
+      cp_async16(dst, g, (uint32_t)(valid * 4));
+    }
+  };
+
+  constexpr uint32_t IDESC = make_idesc(BM, BN);
+  constexpr uint32_t LBO_A = (BM / 8) * 128, LBO_B = (BN / 8) * 128, SBO = 128;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % STAGES;
+    cp_async_wait<STAGES - 2>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = sbase + s * SM::STAGE;
+      const uint32_t ahi = base, alo = base + SM::A_BYTES;
+      const uint32_t bhi = base + 2 * SM::A_BYTES, blo = bhi + SM::B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BK / 8; ++ks) {
+        const uint64_t dah = make_desc(ahi + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t dal = make_desc(alo + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t dbh = make_desc(bhi + ks * 2 * LBO_B, LBO_B, SBO);
+        const uint64_t dbl = make_desc(blo + ks * 2 * LBO_B, LBO_B, SBO);
+        const uint32_t acc0 = (kt > 0 || ks > 0) ? 1u : 0u;
+        mma_tf32(tmem, dal, dbh, IDESC, acc0);
+        mma_tf32(tmem, dah, dbl, IDESC, 1u);
+        mma_tf32(tmem, dah, dbh, IDESC, 1u);
+      }
+      mma_commit(&bars[s]);
+    }
+    __syncwarp();
+    const int kn = kt + STAGES - 1;
+    if (kn < nk) {
+      if (kt >= 1) mbar_wait(&bars[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
+      issue(kn % STAGES, kn);
+    }
+    cp_async_commit();
+  }
+  {
+    const int last = nk - 1;
+    mbar_wait(&bars[last % STAGES], (last / STAGES) & 1);
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < d.M) {
+      float *out = d.C + (size_t)row * d.ldc + n0 + c0;
+      const int nvalid = d.N - (n0 + c0);
+      if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4 *>(out)[q] =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < nvalid) out[j] = __uint_as_float(v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(SM::TMEM_COLS));
+}
+
+template <int BN>
+static cudaError_t launch_two(const GemmDesc2 *descs, int batch, int maxM, int maxN,
+                              cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc2<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((maxN + BN - 1) / BN, (maxM + BM - 1) / BM, batch);
+  k_gemm_tc2<BN><<<grid, NT, Smem<BN>::TOTAL, s>>>(descs);
+  return cudaGetLastError();
+}
+
 template <int BN, bool AL>
 static cudaError_t launch_one(const GemmDesc *descs, int batch, int maxM, int maxN,
                               cudaStream_t s) {
@@ -283,6 +450,12 @@ static cudaError_t launch_one(const GemmDesc *descs, int batch, int maxM, int ma
 }
 
 }  // namespace tc
+
+cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int maxN, int bn,
+                            cudaStream_t s) {
+  return bn == 144 ? tc::launch_two<144>(descs, batch, maxM, maxN, s)
+                   : tc::launch_two<128>(descs, batch, maxM, maxN, s);
+}
 
 // bn: 128 or 144 (tile width); b_aligned: every Bt row start is 16-byte aligned and ldb % 4 == 0.
 cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN, int bn,

@@ -33,6 +33,15 @@ struct GemmDesc {
   int lda, ldb, ldc;
 };
 
+// Pre-split (3xTF32) GEMM descriptor: C = (A_hi + A_lo) (B_hi + B_lo)^T, all K-contiguous,
+// every row start 16-byte aligned; hi planes hold values exactly representable in tf32.
+struct GemmDesc2 {
+  const float *Ahi, *Alo, *Bhi, *Blo;
+  float *C;
+  int M, N, K;
+  int lda, ldb, ldc;
+};
+
 // Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
 struct Geo {
   int M;          // number of subdomains in the batch
@@ -65,13 +74,13 @@ cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, i
 // step 1
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cudaStream_t s);
 cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
-                       cudaStream_t s);
+                       float *qlo, cudaStream_t s);
 cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
                           float sa, float sb, float sc, float *out, cudaStream_t s);
 cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                            const float *p, int ld, int n2, int n1, float *v, cudaStream_t s);
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
-                           cudaStream_t s);
+                           float *qlo, cudaStream_t s);
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
                             const float *gphi, int ldg, int n2, int n1, float *om,
                             cudaStream_t s);
@@ -80,16 +89,19 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
                           float *vout, int n2, int n1, float t, cudaStream_t s);
 
 // projection (kernel b)
-cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, int ld,
-                              cudaStream_t s);
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,
+                              int ld, cudaStream_t s);
 cudaError_t launch_pivots(const ProjTile *chains_tiles, const int *chain_first_tile, int nchains,
                           int n2, int n1, double *rinv, int ldn, int AT, cudaStream_t s);
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s);
 // tcgen05 3xTF32 GEMM: C = A * Bt^T, Bt given as [N][K] row-major (tvs_gemm_tc.cu)
 cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN, int bn,
                            bool b_aligned, cudaStream_t s);
+cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int maxN, int bn,
+                            cudaStream_t s);
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
                               const float *qhat, int AT, int ldn, const double *rinv,
-                              double *z, float *phx, float *phy, int AP, cudaStream_t s);
+                              double *z, float *phx, float *phy, float *phx_lo, float *phy_lo,
+                              int AP, cudaStream_t s);
 
 }  // namespace tvs

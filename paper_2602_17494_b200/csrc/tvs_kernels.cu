@@ -5,10 +5,29 @@
 #include "tvs_internal.h"
 
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 namespace tvs {
 
 // ----------------------------------------------------------------------------- helpers
+
+// round-to-nearest tf32 (low 13 mantissa bits zero): the "hi" half of a 3xTF32 operand split
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
+// store v either as full fp32 (lo == nullptr) or as the exact split hi = tf32(v), lo = v - hi
+__device__ __forceinline__ void store_split(float *hi, float *lo, size_t idx, double v) {
+  if (lo) {
+    float h = tf32_rna((float)v);
+    hi[idx] = h;
+    lo[idx] = (float)(v - (double)h);
+  } else {
+    hi[idx] = (float)v;
+  }
+}
 
 __device__ __forceinline__ float theta_at(const float *thy, const float *thx, const SubDesc &sd,
                                           const Geo &g, int li, int lj) {
@@ -190,6 +209,273 @@ k_sweep2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
   o1[(size_t)g.A * g.ldS + (size_t)li * g.ldS + lj] = vy;
 }
 
+// Kernel (a), streaming form (default): each warp owns 30 output columns of S (lane 0 and lane 31
+// are halo lanes) and walks down RB rows, keeping the previous row of v_2 and the next row of u
+// in registers; x-neighbours come from warp shuffles.  Traffic per update ~= (32/30)*12 B loaded
+// (v_1, v_2, omega0) + 8 B stored, i.e. the algorithmic 20 B plus 6.7 % halo.
+constexpr int SS_OUT = 30, SS_RB = 32, SS_WARPS = 4;
+__global__ void __launch_bounds__(32 * SS_WARPS)
+k_sweep2s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+          const float *__restrict__ thx, const float *__restrict__ vin,
+          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * SS_WARPS + threadIdx.y;
+  const int c0 = strip * SS_OUT;
+  if (c0 >= b) return;
+  const int r0 = blockIdx.y * SS_RB;
+  if (r0 >= a) return;
+  const int r1 = min(a, r0 + SS_RB);              // output rows [r0, r1)
+  const int lj = c0 - 1 + lane;                   // local column of this lane
+  const bool inS = lj >= 0 && lj < b;
+  const bool inSp = lj >= 0 && lj < bp;
+  const bool out_lane = lane >= 1 && lane <= SS_OUT && lj < b;
+  const int gj = sd.x0 + lj;
+  const float xkeep = (gj < n1 - 1) ? 1.f : 0.f;  // global rule of D-_x at the last column
+  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  const float *v2 = v1 + (size_t)g.A * g.ldS;
+  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
+  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  float *o2 = o1 + (size_t)g.A * g.ldS;
+  const float thx_l = (lj >= 0 && lj < b) ? thx[sd.ix * g.B + lj] : 0.f;
+  auto ld1 = [&](int li) { return (inS && li >= 0 && li < a) ? __ldg(v1 + (size_t)li * g.ldS + lj) : 0.f; };
+  auto ld2 = [&](int li) { return (inS && li >= 0 && li < a) ? __ldg(v2 + (size_t)li * g.ldS + lj) : 0.f; };
+  auto ldo = [&](int li) { return (inSp && li < ap) ? __ldg(omm + (size_t)li * g.ldP + lj) : 0.f; };
+  // u(li) for this lane's column, given v1(li), v2(li), v2(li-1), omega0(li)
+  auto ucalc = [&](int li, float a1, float a2, float a2m, float o) {
+    const float left = __shfl_up_sync(0xffffffffu, a1, 1);
+    const float gy = (sd.y0 + li < n2 - 1) ? a2 : 0.f;
+    return (inSp && li < ap) ? (xkeep * a1 - left + gy - a2m - o) : 0.f;
+  };
+  // register ring: row li (c*), row li+1 (n*, loaded one iteration ahead), row li+2 issued at the
+  // top of each iteration so a row of loads is always in flight behind the arithmetic
+  float c1 = ld1(r0), c2 = ld2(r0);
+  const float p2 = ld2(r0 - 1), co = ldo(r0);
+  float n1v = ld1(r0 + 1), n2v = ld2(r0 + 1), no = ldo(r0 + 1);
+  float u_c = ucalc(r0, c1, c2, p2, co);
+  for (int li = r0; li < r1; ++li) {
+    const float m1 = ld1(li + 2), m2 = ld2(li + 2), mo = ldo(li + 2);
+    const float u_n = ucalc(li + 1, n1v, n2v, c2, no);
+    const float u_r = __shfl_down_sync(0xffffffffu, u_c, 1);
+    const float psx = (lj + 1 < bp) ? u_r - u_c : 0.f;
+    const float psy = (li + 1 < ap) ? u_n - u_c : 0.f;
+    if (out_lane) {
+      float vx = c1, vy = c2;
+      ball_update(thy[sd.iy * g.A + li] * thx_l, t, psx, psy, vx, vy);
+      o1[(size_t)li * g.ldS + lj] = vx;
+      o2[(size_t)li * g.ldS + lj] = vy;
+    }
+    c1 = n1v;
+    c2 = n2v;
+    u_c = u_n;
+    n1v = m1;
+    n2v = m2;
+    no = mo;
+  }
+}
+
+// Kernel (a), vectorised streaming form (default): lane l owns the column pair
+// (c0 - 2 + 2l, c0 - 1 + 2l) -> 8-byte loads/stores; a warp produces 60 output columns
+// (lanes 1..30), lane 0 supplies the left halo column and lane 31 the right one.  Two rows of
+// loads are kept in flight ahead of the arithmetic (bytes in flight per SM ~ 3x the scalar form).
+constexpr int SV_OUT = 60, SV_RB = 32, SV_WARPS = 4;
+__global__ void __launch_bounds__(32 * SV_WARPS)
+k_sweep2v(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+          const float *__restrict__ thx, const float *__restrict__ vin,
+          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * SV_WARPS + threadIdx.y;
+  const int c0 = strip * SV_OUT;
+  if (c0 >= b) return;
+  const int r0 = blockIdx.y * SV_RB;
+  if (r0 >= a) return;
+  const int r1 = min(a, r0 + SV_RB);
+  const int jA = c0 - 2 + 2 * lane, jB = jA + 1;          // local columns of this lane
+  // a column pair is loaded as one float2 when both columns lie inside the plane's extent
+  const bool SA = jA >= 0 && jA < b, SB = jB >= 0 && jB < b;
+  const bool PA = jA >= 0 && jA < bp, PB = jB >= 0 && jB < bp;
+  const bool outA = lane >= 1 && lane <= 30 && jA < b;
+  const bool outB = lane >= 1 && lane <= 30 && jB < b;
+  const float xkA = (sd.x0 + jA < n1 - 1) ? 1.f : 0.f, xkB = (sd.x0 + jB < n1 - 1) ? 1.f : 0.f;
+  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  const float *v2 = v1 + (size_t)g.A * g.ldS;
+  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
+  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  float *o2 = o1 + (size_t)g.A * g.ldS;
+  const float thA = SA ? thx[sd.ix * g.B + jA] : 0.f, thB = SB ? thx[sd.ix * g.B + jB] : 0.f;
+  auto ldpair = [&](const float *base, int ld, int li, int rows, bool okA, bool okB) {
+    float2 r = make_float2(0.f, 0.f);
+    if (li < 0 || li >= rows) return r;
+    const float *p = base + (size_t)li * ld + jA;
+    if (okA && okB) return __ldg(reinterpret_cast<const float2 *>(p));
+    if (okA) r.x = __ldg(p);
+    if (okB) r.y = __ldg(p + 1);
+    return r;
+  };
+  struct Row { float2 w1, w2, o; };
+  auto ldrow = [&](int li) {
+    Row r;
+    r.w1 = ldpair(v1, g.ldS, li, a, SA, SB);
+    r.w2 = ldpair(v2, g.ldS, li, a, SA, SB);
+    r.o = ldpair(omm, g.ldP, li, ap, PA, PB);
+    return r;
+  };
+  // u for the lane's pair at row li, given that row and v_2 of the row above
+  auto ucalc = [&](int li, const Row &r, float2 w2m) {
+    const float leftA = __shfl_up_sync(0xffffffffu, r.w1.y, 1);    // v_1 at column jA - 1
+    const bool gy = (sd.y0 + li < n2 - 1);
+    float2 u;
+    u.x = (PA && li < ap) ? (xkA * r.w1.x - leftA + (gy ? r.w2.x : 0.f) - w2m.x - r.o.x) : 0.f;
+    u.y = (PB && li < ap) ? (xkB * r.w1.y - r.w1.x + (gy ? r.w2.y : 0.f) - w2m.y - r.o.y) : 0.f;
+    return u;
+  };
+  Row c = ldrow(r0), n = ldrow(r0 + 1);
+  const Row pr = ldrow(r0 - 1);
+  float2 u_c = ucalc(r0, c, pr.w2);
+  for (int li = r0; li < r1; ++li) {
+    const Row m = ldrow(li + 2);                     // two rows in flight
+    const float2 u_n = ucalc(li + 1, n, c.w2);
+    const float urA = __shfl_down_sync(0xffffffffu, u_c.x, 1);   // u at column jB + 1
+    const float psxA = (jA + 1 < bp) ? u_c.y - u_c.x : 0.f;
+    const float psxB = (jB + 1 < bp) ? urA - u_c.y : 0.f;
+    const float psyA = (li + 1 < ap) ? u_n.x - u_c.x : 0.f;
+    const float psyB = (li + 1 < ap) ? u_n.y - u_c.y : 0.f;
+    const float ty = thy[sd.iy * g.A + li];
+    float2 nv1 = c.w1, nv2 = c.w2;
+    ball_update(ty * thA, t, psxA, psyA, nv1.x, nv2.x);
+    ball_update(ty * thB, t, psxB, psyB, nv1.y, nv2.y);
+    float *q1 = o1 + (size_t)li * g.ldS + jA, *q2 = o2 + (size_t)li * g.ldS + jA;
+    if (outA && outB) {
+      *reinterpret_cast<float2 *>(q1) = nv1;
+      *reinterpret_cast<float2 *>(q2) = nv2;
+    } else {
+      if (outA) { q1[0] = nv1.x; q2[0] = nv2.x; }
+      if (outB) { q1[1] = nv1.y; q2[1] = nv2.y; }
+    }
+    c = n;
+    n = m;
+    u_c = u_n;
+  }
+}
+
+// ball update with a fast reciprocal (MUFU.RCP, <= 2 ulp): v <- (th v + t th psi) / (th + t|psi|)
+__device__ __forceinline__ void ball_update_fast(float th, float t, float psx, float psy,
+                                                 float &vx, float &vy) {
+  const float nrm = __fsqrt_rn(psx * psx + psy * psy);
+  const float inv = __fdividef(th, th + t * nrm);
+  const float nx = (vx + t * psx) * inv, ny = (vy + t * psy) * inv;
+  vx = th > 0.f ? nx : 0.f;
+  vy = th > 0.f ? ny : 0.f;
+}
+
+// Kernel (a), 4 columns per lane (default): lane l owns columns c0-4+4l .. c0-1+4l (16-byte loads
+// and stores); lanes 1..30 produce 120 output columns, lane 0 / lane 31 are the halo columns.
+// Two rows of loads in flight ahead of the arithmetic; registers capped for 50 % occupancy.
+constexpr int SQ_OUT = 120, SQ_RB = 64, SQ_WARPS = 4;
+__global__ void __launch_bounds__(32 * SQ_WARPS, 8)
+k_sweep2q(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+          const float *__restrict__ thx, const float *__restrict__ vin,
+          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * SQ_WARPS + threadIdx.y;
+  const int c0 = strip * SQ_OUT;
+  if (c0 >= b) return;
+  const int r0 = blockIdx.y * SQ_RB;
+  if (r0 >= a) return;
+  const int r1 = min(a, r0 + SQ_RB);
+  const int j0 = c0 - 4 + 4 * lane;                   // first local column of this lane
+  // per-column masks (S for v, S+ for u / omega0), output lanes, global D-_x rule at n1 - 1
+  float mS[4], mP[4], xk[4], thc[4];
+  bool fullS = true, fullP = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = j0 + q;
+    const bool s_ = j >= 0 && j < b, p_ = j >= 0 && j < bp;
+    mS[q] = s_ ? 1.f : 0.f;
+    mP[q] = p_ ? 1.f : 0.f;
+    fullS &= s_;
+    fullP &= p_;
+    xk[q] = (sd.x0 + j < n1 - 1) ? 1.f : 0.f;
+    thc[q] = s_ ? thx[sd.ix * g.B + j] : 0.f;
+  }
+  const bool out_lane = lane >= 1 && lane <= 30;
+  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  const float *v2 = v1 + (size_t)g.A * g.ldS;
+  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
+  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  float *o2 = o1 + (size_t)g.A * g.ldS;
+  auto ld4 = [&](const float *base, int ld, int li, int rows, bool full, const float *m) {
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (li < 0 || li >= rows) return r;
+    const float *p = base + (size_t)li * ld + j0;
+    if (full) return __ldg(reinterpret_cast<const float4 *>(p));
+    if (m[0] != 0.f) r.x = __ldg(p);
+    if (m[1] != 0.f) r.y = __ldg(p + 1);
+    if (m[2] != 0.f) r.z = __ldg(p + 2);
+    if (m[3] != 0.f) r.w = __ldg(p + 3);
+    return r;
+  };
+  struct Row { float4 w1, w2, o; };
+  auto ldrow = [&](int li) {
+    Row r;
+    r.w1 = ld4(v1, g.ldS, li, a, fullS, mS);
+    r.w2 = ld4(v2, g.ldS, li, a, fullS, mS);
+    r.o = ld4(omm, g.ldP, li, ap, fullP, mP);
+    return r;
+  };
+  auto ucalc = [&](int li, const Row &r, float4 w2m) {
+    const float left = __shfl_up_sync(0xffffffffu, r.w1.w, 1);   // v_1 at column j0 - 1
+    const float gy = (sd.y0 + li < n2 - 1) ? 1.f : 0.f;
+    const float rowok = (li < ap) ? 1.f : 0.f;
+    float4 u;
+    u.x = rowok * mP[0] * (xk[0] * r.w1.x - left + gy * r.w2.x - w2m.x - r.o.x);
+    u.y = rowok * mP[1] * (xk[1] * r.w1.y - r.w1.x + gy * r.w2.y - w2m.y - r.o.y);
+    u.z = rowok * mP[2] * (xk[2] * r.w1.z - r.w1.y + gy * r.w2.z - w2m.z - r.o.z);
+    u.w = rowok * mP[3] * (xk[3] * r.w1.w - r.w1.z + gy * r.w2.w - w2m.w - r.o.w);
+    return u;
+  };
+  Row c = ldrow(r0), n = ldrow(r0 + 1);
+  const float4 pw2 = ld4(v2, g.ldS, r0 - 1, a, fullS, mS);
+  float4 u_c = ucalc(r0, c, pw2);
+  const bool lastx[4] = {j0 + 1 >= bp, j0 + 2 >= bp, j0 + 3 >= bp, j0 + 4 >= bp};
+  for (int li = r0; li < r1; ++li) {
+    const Row m = ldrow(li + 2);
+    const float4 u_n = ucalc(li + 1, n, c.w2);
+    const float ur = __shfl_down_sync(0xffffffffu, u_c.x, 1);      // u at column j0 + 4
+    const float ydiff = (li + 1 < ap) ? 1.f : 0.f;
+    const float psx0 = lastx[0] ? 0.f : u_c.y - u_c.x, psy0 = ydiff * (u_n.x - u_c.x);
+    const float psx1 = lastx[1] ? 0.f : u_c.z - u_c.y, psy1 = ydiff * (u_n.y - u_c.y);
+    const float psx2 = lastx[2] ? 0.f : u_c.w - u_c.z, psy2 = ydiff * (u_n.z - u_c.z);
+    const float psx3 = lastx[3] ? 0.f : ur - u_c.w, psy3 = ydiff * (u_n.w - u_c.w);
+    const float ty = thy[sd.iy * g.A + li];
+    float4 a1 = c.w1, a2 = c.w2;
+    ball_update_fast(ty * thc[0], t, psx0, psy0, a1.x, a2.x);
+    ball_update_fast(ty * thc[1], t, psx1, psy1, a1.y, a2.y);
+    ball_update_fast(ty * thc[2], t, psx2, psy2, a1.z, a2.z);
+    ball_update_fast(ty * thc[3], t, psx3, psy3, a1.w, a2.w);
+    if (out_lane) {
+      float *q1 = o1 + (size_t)li * g.ldS + j0, *q2 = o2 + (size_t)li * g.ldS + j0;
+      if (fullS) {
+        *reinterpret_cast<float4 *>(q1) = a1;
+        *reinterpret_cast<float4 *>(q2) = a2;
+      } else {
+        if (mS[0] != 0.f) { q1[0] = a1.x; q2[0] = a2.x; }
+        if (mS[1] != 0.f) { q1[1] = a1.y; q2[1] = a2.y; }
+        if (mS[2] != 0.f) { q1[2] = a1.z; q2[2] = a2.z; }
+        if (mS[3] != 0.f) { q1[3] = a1.w; q2[3] = a2.w; }
+      }
+    }
+    c = n;
+    n = m;
+    u_c = u_n;
+  }
+}
+
 // p^{n+1} = (1 - ahat) p^n + ahat sum_m E qhat_m (Alg. 2), summed in fixed subdomain
 // order (m2 ascending, then m1) so overlaps are bitwise reproducible.  Flags non-finite values.
 __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
@@ -250,13 +536,13 @@ __global__ void k_multidiv(const float *__restrict__ p, int ld, int n2, int n1,
 
 // q = div w.
 __global__ void k_div(const float *__restrict__ w1, const float *__restrict__ w2, int ld, int n2,
-                      int n1, float *__restrict__ q) {
+                      int n1, float *__restrict__ q, float *__restrict__ qlo) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   int i = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= n2 || j >= n1) return;
   float dv = (j < n1 - 1 ? w1[(size_t)i * ld + j] : 0.f) - (j > 0 ? w1[(size_t)i * ld + j - 1] : 0.f) +
              (i < n2 - 1 ? w2[(size_t)i * ld + j] : 0.f) - (i > 0 ? w2[(size_t)(i - 1) * ld + j] : 0.f);
-  q[(size_t)i * ld + j] = dv;
+  store_split(q, qlo, (size_t)i * ld + j, dv);
 }
 
 // out = sa a + sb b (+ sc c), two planes.
@@ -302,7 +588,7 @@ __device__ __forceinline__ float w_S(const float *vb, int k, int li, int lj, int
 }
 
 __global__ void k_prediv1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
-                          int n2, int n1, float *__restrict__ q) {
+                          int n2, int n1, float *__restrict__ q, float *__restrict__ qlo) {
   const SubDesc sd = subs[blockIdx.z];
   int lj = blockIdx.x * blockDim.x + threadIdx.x;
   int li = blockIdx.y * blockDim.y + threadIdx.y;
@@ -314,7 +600,9 @@ __global__ void k_prediv1(const SubDesc *__restrict__ subs, Geo g, const float *
              (gj > 0 ? w_S(vb, 0, li, lj - 1, gi, gj - 1, a, b, g, n2, n1) : 0.f) +
              (gi < n2 - 1 ? w_S(vb, 1, li, lj, gi, gj, a, b, g, n2, n1) : 0.f) -
              (gi > 0 ? w_S(vb, 1, li - 1, lj, gi - 1, gj, a, b, g, n2, n1) : 0.f);
-  q[((size_t)blockIdx.z * g.AT + li) * g.ldT + lj] = dv;
+  // column offset x0 & 3 keeps the forward GEMM's DCT-table rows 16-byte aligned (the leading
+  // columns stay zero)
+  store_split(q, qlo, ((size_t)blockIdx.z * g.AT + li) * g.ldT + lj + (sd.x0 & 3), dv);
 }
 
 // omega0_loc = R_{S+} r^n + (R_{S+} P E_{S+}) multidiv_{S+} E_S (theta_m p^n)  (Alg. 5, P:1740;
@@ -387,7 +675,8 @@ __global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *_
 // sn[j][x] = sin(pi j (x+1) / n) and snT[x][j] (transposed), evaluated in fp64 with exact
 // integer argument reduction.
 __global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ cn,
-                             float *__restrict__ sn, float *__restrict__ snT, int ld) {
+                             float *__restrict__ sn, float *__restrict__ snT,
+                             float *__restrict__ split6, int ld) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= n || j >= n) return;
@@ -399,6 +688,11 @@ __global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ 
   cn[(size_t)j * ld + x] = (float)c;
   sn[(size_t)j * ld + x] = (float)s;
   snT[(size_t)x * ld + j] = (float)s;
+  // 3xTF32 splits: [cf_hi, cf_lo, cn_hi, cn_lo, snT_hi, snT_lo], each n x ld
+  const size_t pl = (size_t)n * ld;
+  store_split(split6 + 0 * pl, split6 + 1 * pl, (size_t)x * ld + j, c);
+  store_split(split6 + 2 * pl, split6 + 3 * pl, (size_t)j * ld + x, c);
+  store_split(split6 + 4 * pl, split6 + 5 * pl, (size_t)x * ld + j, s);
 }
 
 // Thomas pivots of the Schur-corrected tridiagonal M_T(s_j) on rows [ty0, ty1] of an axis of
@@ -439,18 +733,23 @@ __global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restri
 // qhat[k][j] = sum_x q[k][x] cos(pi j (2x+1)/(2 n1)).  Output on the rows of S+:
 //   phx[k][j] = -s_j^2 sigma_j u_k,  phy[k][j] = s_j^2 (u_{k+1} - u_k)  (0 on the global last
 // row), with s_j = sqrt(2/n1) w_j the DCT normalisation (Eq. form:DCTmat).
-__global__ void k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
+__global__ void __launch_bounds__(128, 8)
+k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
                              const float *__restrict__ qhat, int AT, int ldn,
                              const double *__restrict__ rinv, double *__restrict__ z,
-                             float *__restrict__ phx, float *__restrict__ phy, int AP) {
+                             float *__restrict__ phx, float *__restrict__ phy,
+                             float *__restrict__ phx_lo, float *__restrict__ phy_lo, int AP) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   int tix = blockIdx.y;
   if (j >= n1) return;
   const ProjTile tl = tiles[tix];
   const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1;
-  const float *b = qhat + (size_t)tix * AT * ldn + j;
-  float *ox = phx + (size_t)tix * AP * ldn + j;
-  float *oy = phy + (size_t)tix * AP * ldn + j;
+  const float *__restrict__ b = qhat + (size_t)tix * AT * ldn + j;
+  const size_t obase = (size_t)tix * AP * ldn + j;
+  float *__restrict__ ox = phx + obase;
+  float *__restrict__ oy = phy + obase;
+  float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
+  float *__restrict__ oyl = phy_lo ? phy_lo + obase : nullptr;
   const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;          // s_j^2
   if (j == 0) {
     // L_y^dagger b: D+_y u = w, w_y = sum_{l<=y} b_l - mu (y+1), mu = mean of b over n2 rows.
@@ -461,31 +760,69 @@ __global__ void k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
       pre += (double)b[(size_t)k * ldn];
       int y = tl.ty0 + k;
       double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
-      ox[(size_t)k * ldn] = 0.f;
-      oy[(size_t)k * ldn] = (float)(s2 * w);
+      store_split(ox, oxl, (size_t)k * ldn, 0.0);
+      store_split(oy, oyl, (size_t)k * ldn, s2 * w);
     }
     return;
   }
   const double sg = 2.0 * sinpi((double)j / (2.0 * n1));
   const double cx = -s2 * sg;
-  const double *ri = rinv + (size_t)tl.chain * AT * ldn + j;
-  double *zz = z + (size_t)tix * AT * ldn + j;
-  double zp = (double)b[0];
+  const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * ldn + j;
+  double *__restrict__ zz = z + (size_t)tix * AT * ldn + j;
+  const float *__restrict__ bb = b;
+  // forward substitution z_k = b_k - z_{k-1} r_{k-1}; loads batched U rows ahead so the only
+  // serial dependence is one DFMA per row (pointers are __restrict__, so they can be hoisted)
+  constexpr int U = 4;
+  double zp = (double)bb[0];
   zz[0] = zp;
-  for (int k = 1; k < nt; ++k) {
-    zp = (double)b[(size_t)k * ldn] - zp * ri[(size_t)(k - 1) * ldn];
+  int k = 1;
+  for (; k + U <= nt; k += U) {
+    float bv[U];
+    double rv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bv[u] = bb[(size_t)(k + u) * ldn];
+      rv[u] = ri[(size_t)(k + u - 1) * ldn];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      zp = fma(-zp, rv[u], (double)bv[u]);
+      zz[(size_t)(k + u) * ldn] = zp;
+    }
+  }
+  for (; k < nt; ++k) {
+    zp = fma(-zp, ri[(size_t)(k - 1) * ldn], (double)bb[(size_t)k * ldn]);
     zz[(size_t)k * ldn] = zp;
   }
   double u = zp * ri[(size_t)(nt - 1) * ldn];
   if (nt - 1 < nout) {                       // T = S+ in y: global last row, D+_y = 0
-    ox[(size_t)(nt - 1) * ldn] = (float)(cx * u);
-    oy[(size_t)(nt - 1) * ldn] = 0.f;
+    store_split(ox, oxl, (size_t)(nt - 1) * ldn, cx * u);
+    store_split(oy, oyl, (size_t)(nt - 1) * ldn, 0.0);
   }
-  for (int k = nt - 2; k >= 0; --k) {
-    double uk = (zz[(size_t)k * ldn] - u) * ri[(size_t)k * ldn];
+  // back substitution u_k = (z_k - u_{k+1}) r_k, k = nt-2 .. 0, batched the same way
+  k = nt - 2;
+  for (; k - U + 1 >= 0; k -= U) {
+    double zv[U], rv[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      zv[q] = zz[(size_t)(k - q) * ldn];
+      rv[q] = ri[(size_t)(k - q) * ldn];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const double uk = (zv[q] - u) * rv[q];
+      if (k - q < nout) {
+        store_split(ox, oxl, (size_t)(k - q) * ldn, cx * uk);
+        store_split(oy, oyl, (size_t)(k - q) * ldn, s2 * (u - uk));
+      }
+      u = uk;
+    }
+  }
+  for (; k >= 0; --k) {
+    const double uk = (zz[(size_t)k * ldn] - u) * ri[(size_t)k * ldn];
     if (k < nout) {
-      ox[(size_t)k * ldn] = (float)(cx * uk);
-      oy[(size_t)k * ldn] = (float)(s2 * (u - uk));
+      store_split(ox, oxl, (size_t)k * ldn, cx * uk);
+      store_split(oy, oyl, (size_t)k * ldn, s2 * (u - uk));
     }
     u = uk;
   }
@@ -595,8 +932,25 @@ cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const 
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s) {
-  k_sweep2<<<grid2(g.B, g.A, SW_TX, SW_TY, g.M), dim3(SW_TX, SW_TY), 0, s>>>(
-      subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  static const bool tiled = getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "tiled") == 0;
+  if (tiled) {
+    k_sweep2<<<grid2(g.B, g.A, SW_TX, SW_TY, g.M), dim3(SW_TX, SW_TY), 0, s>>>(
+        subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  } else if (getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "scalar") == 0) {
+    const int strips = (g.B + SS_OUT - 1) / SS_OUT;
+    dim3 grid((strips + SS_WARPS - 1) / SS_WARPS, (g.A + SS_RB - 1) / SS_RB, g.M);
+    k_sweep2s<<<grid, dim3(32, SS_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  } else if ((getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "pair") == 0) ||
+             (!getenv("TVS_SWEEP2") && g.B < 512)) {
+    // narrow subdomains (L2-resident regime): the 2-column form keeps more warps in flight
+    const int strips = (g.B + SV_OUT - 1) / SV_OUT;
+    dim3 grid((strips + SV_WARPS - 1) / SV_WARPS, (g.A + SV_RB - 1) / SV_RB, g.M);
+    k_sweep2v<<<grid, dim3(32, SV_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  } else {
+    const int strips = (g.B + SQ_OUT - 1) / SQ_OUT;
+    dim3 grid((strips + SQ_WARPS - 1) / SQ_WARPS, (g.A + SQ_RB - 1) / SQ_RB, g.M);
+    k_sweep2q<<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
@@ -617,8 +971,8 @@ cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cu
   return cudaGetLastError();
 }
 cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
-                       cudaStream_t s) {
-  k_div<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(w1, w2, ld, n2, n1, q);
+                       float *qlo, cudaStream_t s) {
+  k_div<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(w1, w2, ld, n2, n1, q, qlo);
   return cudaGetLastError();
 }
 cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
@@ -633,8 +987,8 @@ cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const f
   return cudaGetLastError();
 }
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
-                           cudaStream_t s) {
-  k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q);
+                           float *qlo, cudaStream_t s) {
+  k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
   return cudaGetLastError();
 }
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
@@ -651,9 +1005,9 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
                                                                ldg, om, vout, n2, n1, t);
   return cudaGetLastError();
 }
-cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, int ld,
-                              cudaStream_t s) {
-  k_dct_tables<<<grid2(n, n, 32, 8), dim3(32, 8), 0, s>>>(n, cf, cn, sn, snT, ld);
+cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,
+                              int ld, cudaStream_t s) {
+  k_dct_tables<<<grid2(n, n, 32, 8), dim3(32, 8), 0, s>>>(n, cf, cn, sn, snT, split6, ld);
   return cudaGetLastError();
 }
 cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, int n2, int n1,
@@ -668,9 +1022,11 @@ cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cu
 }
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
                               const float *qhat, int AT, int ldn, const double *rinv, double *z,
-                              float *phx, float *phy, int AP, cudaStream_t s) {
-  k_proj_solve<<<dim3((n1 + 127) / 128, ntiles), 128, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv,
-                                                              z, phx, phy, AP);
+                              float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
+                              cudaStream_t s) {
+  const int nt = ntiles >= 16 ? 128 : 32;   // few tiles (global P): spread columns over more SMs
+  k_proj_solve<<<dim3((n1 + nt - 1) / nt, ntiles), nt, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv,
+                                                               z, phx, phy, phx_lo, phy_lo, AP);
   return cudaGetLastError();
 }
 

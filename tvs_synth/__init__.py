@@ -109,8 +109,7 @@ def ellipses_on_sinusoid(n: int = 512, seed: int = 1002, sigma: float = 0.08,
     return np.clip(img, 0.0, 1.0).astype(np.float32)
 
 
-def voronoi(n: int, cells: int, seed: int, sigma: float = 0.1) -> np.ndarray:
-    """Configs 3-5: jittered-grid Voronoi, each cell an affine ramp, + noise."""
+def _voronoi_geometry(n, cells, seed):
     g = int(round(np.sqrt(cells)))
     assert g * g == cells
     geo = _Seq(seed)
@@ -123,12 +122,19 @@ def voronoi(n: int, cells: int, seed: int, sigma: float = 0.1) -> np.ndarray:
     c0 = 0.2 + 0.6 * prm[..., 0]
     ga = -1e-3 + 2e-3 * prm[..., 1]
     gb = -1e-3 + 2e-3 * prm[..., 2]
-    img = np.empty((n, n), dtype=np.float64)
+    return g, sy, sx, c0, ga, gb
+
+
+def _voronoi_rows(args):
+    """Rows [r0, r1) of the Voronoi image (+ noise, clipped) -- exact for any row split."""
+    n, cells, seed, sigma, r0_all, r1_all = args
+    g, sy, sx, c0, ga, gb = _voronoi_geometry(n, cells, seed)
+    out = np.empty((r1_all - r0_all, n), dtype=np.float32)
     cols = np.arange(n, dtype=np.float64)
     bcol = np.minimum((cols * g / n).astype(np.int64), g - 1)
     step = max(1, (1 << 21) // n)
-    for r0 in range(0, n, step):
-        r1 = min(n, r0 + step)
+    for r0 in range(r0_all, r1_all, step):
+        r1 = min(r1_all, r0 + step)
         rows = np.arange(r0, r1, dtype=np.float64)
         arow = np.minimum((rows * g / n).astype(np.int64), g - 1)
         best = np.full((r1 - r0, n), np.inf)
@@ -147,10 +153,29 @@ def voronoi(n: int, cells: int, seed: int, sigma: float = 0.1) -> np.ndarray:
                 best = np.where(better, d2, best)
                 bidx = np.where(better, idx, bidx)
         ka, kb = bidx // g, bidx % g
-        img[r0:r1] = (c0[ka, kb] + ga[ka, kb] * (cols[None, :] - sx[ka, kb])
-                      + gb[ka, kb] * (rows[:, None] - sy[ka, kb]))
-    img += gaussian_field(seed, n, n, sigma)
-    return np.clip(img, 0.0, 1.0).astype(np.float32)
+        img = (c0[ka, kb] + ga[ka, kb] * (cols[None, :] - sx[ka, kb])
+               + gb[ka, kb] * (rows[:, None] - sy[ka, kb]))
+        img += gaussian_field(seed, r1 - r0, n, sigma, row0=r0)
+        out[r0 - r0_all:r1 - r0_all] = np.clip(img, 0.0, 1.0)
+    return out
+
+
+def voronoi(n: int, cells: int, seed: int, sigma: float = 0.1, workers: int = 0) -> np.ndarray:
+    """Configs 3-5: jittered-grid Voronoi, each cell an affine ramp, + noise.
+
+    ``workers`` > 1 splits the rows over processes; the result is bit-identical for any split
+    (every pixel depends only on its coordinates and the seed)."""
+    import os
+    if workers == 0:
+        workers = min(16, os.cpu_count() or 1) if n >= 4096 else 1
+    if workers <= 1:
+        return _voronoi_rows((n, cells, seed, sigma, 0, n))
+    from concurrent.futures import ProcessPoolExecutor
+    bounds = [(n * k) // workers for k in range(workers + 1)]
+    jobs = [(n, cells, seed, sigma, bounds[k], bounds[k + 1]) for k in range(workers)]
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        parts = list(ex.map(_voronoi_rows, jobs))
+    return np.concatenate(parts, axis=0)
 
 
 @dataclass(frozen=True)
