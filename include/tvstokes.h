@@ -91,6 +91,15 @@ tvs_status tvs_nccl_unique_id(uint8_t id_out[128]);
 tvs_status tvs_owned_rows(int32_t n2, int32_t n1, const tvs_layout *L, int rank, int world,
                           int32_t *row_begin, int32_t *row_end);
 
+/* Slab decomposition of the step grid for `rank` of `world` (host only, no GPU; step 1 = Omega~,
+ * step 2 = Omega).  out = {k0, k1, R0, R1, E0, E1, V0, V1, us0, us1, ur0, ur1, ds0, ds1, dr0, dr1}:
+ * layout rows [k0,k1) of this rank, core (output) rows [R0,R1), rows covered by its subdomains
+ * [E0,E1), rows where it keeps p valid [V0,V1) = E +- 1, and the band rows whose partial sums it
+ * sends to / receives from rank-1 (us/ur) and rank+1 (ds/dr) every sweep.
+ * TVS_ELAYOUT if the layout cannot be split over `world` ranks (m2 < world, overlap < 2, ...). */
+tvs_status tvs_dist_rows(int32_t n2, int32_t n1, const tvs_layout *L, int32_t step, int rank,
+                         int world, int32_t out[16]);
+
 /* Layout query (host only): inclusive ranges of subdomain k along an axis of length n with
  * m subdomains and overlap s (reading A8), and the partition-of-unity weight theta_k(x)
  * (reading A7).  Used by tests to check the ABI agrees with the paper's layout rules. */

@@ -22,7 +22,7 @@ ABI_SYMBOLS = [
     "tvs_create", "tvs_destroy", "tvs_last_error", "tvs_nccl_unique_id", "tvs_owned_rows",
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
-    "tvs_reset_kernel_times", "tvs_selftest_gemm",
+    "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
     lib.tvs_nccl_unique_id.argtypes = [P]
     lib.tvs_owned_rows.argtypes = [i32, i32, ctypes.POINTER(Layout), ctypes.c_int, ctypes.c_int,
                                    ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.tvs_dist_rows.argtypes = [i32, i32, LP, i32, ctypes.c_int, ctypes.c_int, ctypes.c_int32 * 16]
     lib.tvs_layout_range.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.tvs_layout_theta.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(ctypes.c_double)]
     lib.tv_stokes_step1.argtypes = [P, P, i32, i32, f32, LP, IP, P, P,
@@ -129,6 +130,29 @@ def owned_rows(n2, n1, layout, rank, world):
     return a.value, b.value
 
 
+DIST_FIELDS = ["k0", "k1", "R0", "R1", "E0", "E1", "V0", "V1", "us0", "us1", "ur0", "ur1",
+               "ds0", "ds1", "dr0", "dr1"]
+
+
+def dist_rows(n2, n1, layout, step, rank, world):
+    """Slab decomposition rows of `rank` (host only; see tvs_dist_rows in include/tvstokes.h)."""
+    lib = load_library()
+    out = (ctypes.c_int32 * 16)()
+    st = lib.tvs_dist_rows(n2, n1, ctypes.byref(_layout(layout)), step, rank, world, out)
+    if st:
+        raise TvsError(st, "tvs_dist_rows")
+    return dict(zip(DIST_FIELDS, list(out)))
+
+
+def nccl_unique_id():
+    lib = load_library()
+    buf = (ctypes.c_uint8 * 128)()
+    st = lib.tvs_nccl_unique_id(buf)
+    if st:
+        raise TvsError(st, "tvs_nccl_unique_id")
+    return bytes(buf)
+
+
 def _layout(L):
     if isinstance(L, Layout):
         return L
@@ -158,14 +182,15 @@ class Context:
     """Owns a tvs_ctx on one CUDA device.  Arrays are torch CUDA float32 tensors (device entry
     points) or numpy float32 arrays (``*_host``)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("tvstokes needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         self.device = device
         h = ctypes.c_void_p()
-        st = self.lib.tvs_create(ctypes.byref(h), device, 0, 1, None)
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        st = self.lib.tvs_create(ctypes.byref(h), device, rank, world, idbuf)
         if st:
             raise TvsError(st, "tvs_create")
         self.h = h

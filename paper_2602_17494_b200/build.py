@@ -9,12 +9,24 @@ LIB = os.path.join(HERE, "libtvstokes.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("tvs_kernels.cu", "tvs_gemm_tc.cu", "tvs_api.cu")]
 HEADERS = [os.path.join(HERE, "csrc", "tvs_internal.h"), os.path.join(ROOT, "include", "tvstokes.h")]
 
+NCCL_DIR = None
+for _cand in [os.path.join(os.path.dirname(os.__file__), "site-packages", "nvidia", "nccl"),
+              "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"]:
+    if os.path.exists(os.path.join(_cand, "include", "nccl.h")):
+        NCCL_DIR = _cand
+        break
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-I", os.path.join(ROOT, "include"),
 ]
+if NCCL_DIR:   # the torch-bundled NCCL (same library torch loads); rpath so no LD_LIBRARY_PATH needed
+    NVCC_FLAGS += ["-I", os.path.join(NCCL_DIR, "include"), "-L", os.path.join(NCCL_DIR, "lib"),
+                   "-Xlinker", "-rpath=" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2"]
+else:
+    NVCC_FLAGS += ["-lnccl"]
 
 
 def nvcc():

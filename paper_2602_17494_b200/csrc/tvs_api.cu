@@ -4,6 +4,7 @@
 #include "tvs_internal.h"
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -73,6 +74,87 @@ float alpha_hat(int m2, int m1) {
 
 inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
+// Row bookkeeping of one rank in a slab decomposition of whole layout rows, on the
+// step grid of G2 rows.  world == 1 gives k = [0, M2), every row range = [0, G2), no exchange.
+struct Dist {
+  int rank = 0, world = 1;
+  int k0 = 0, k1 = 0;                      // local layout rows
+  int R0 = 0, R1 = 0;                      // core rows: output rows this rank owns
+  int E0 = 0, E1 = 0;                      // rows covered by the local subdomains
+  int V0 = 0, V1 = 0;                      // rows where p is kept valid: E +- 1 (clipped)
+  int us0 = 0, us1 = 0, ur0 = 0, ur1 = 0;  // rows sent to / received from rank - 1
+  int ds0 = 0, ds1 = 0, dr0 = 0, dr1 = 0;  // rows sent to / received from rank + 1
+  std::vector<int> Rlo, Rhi;               // core rows of every rank (all-gathers)
+};
+
+// cuts: core cuts of the layout axis (on the N~ grid); ly/hy: subdomain ranges; G2: step rows.
+bool compute_dist(int G2, int M2, const std::vector<int> &ly, const std::vector<int> &hy,
+                  int naxis, int rank, int world, Dist &d, std::string &err) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    err = "bad rank/world";
+    return false;
+  }
+  if (M2 < world) {
+    err = "multi-GPU needs at least one layout row (m2) per rank";
+    return false;
+  }
+  auto rows = [&](int r, int &k0, int &k1, int &R0, int &R1, int &E0, int &E1, int &V0, int &V1) {
+    k0 = (int)((long long)r * M2 / world);
+    k1 = (int)((long long)(r + 1) * M2 / world);
+    R0 = std::min(G2, (int)((long long)k0 * naxis / M2));
+    R1 = (r == world - 1) ? G2 : std::min(G2, (int)((long long)k1 * naxis / M2));
+    E0 = ly[k0];
+    E1 = std::min(hy[k1 - 1], G2 - 1) + 1;
+    V0 = std::max(0, E0 - 1);
+    V1 = std::min(G2, E1 + 1);
+  };
+  d = Dist();
+  d.rank = rank;
+  d.world = world;
+  int k0, k1, R0, R1, E0, E1, V0, V1;
+  for (int r = 0; r < world; ++r) {
+    rows(r, k0, k1, R0, R1, E0, E1, V0, V1);
+    d.Rlo.push_back(R0);
+    d.Rhi.push_back(R1);
+  }
+  rows(rank, d.k0, d.k1, d.R0, d.R1, d.E0, d.E1, d.V0, d.V1);
+  auto isect = [](int a0, int a1, int b0, int b1, int &o0, int &o1) {
+    o0 = std::max(a0, b0);
+    o1 = std::min(a1, b1);
+    if (o1 < o0) o1 = o0;
+  };
+  if (rank > 0) {
+    rows(rank - 1, k0, k1, R0, R1, E0, E1, V0, V1);
+    isect(d.E0, d.E1, V0, V1, d.us0, d.us1);
+    isect(E0, E1, d.V0, d.V1, d.ur0, d.ur1);
+  }
+  if (rank < world - 1) {
+    rows(rank + 1, k0, k1, R0, R1, E0, E1, V0, V1);
+    isect(d.E0, d.E1, V0, V1, d.ds0, d.ds1);
+    isect(E0, E1, d.V0, d.V1, d.dr0, d.dr1);
+  }
+  // every valid row must be covered only by local layout rows or by the neighbours' rows whose
+  // partial sums this rank receives; the core rows' stencil rows R0-2 .. R1 must be valid
+  const int ku0 = rank > 0 ? (int)((long long)(rank - 1) * M2 / world) : d.k0;
+  const int kd1 = rank < world - 1 ? (int)((long long)(rank + 2) * M2 / world) : d.k1;
+  for (int i = d.V0; i < d.V1; ++i)
+    for (int ky = 0; ky < M2; ++ky) {
+      if (i < ly[ky] || i > hy[ky]) continue;
+      const bool local = ky >= d.k0 && ky < d.k1;
+      const bool from_up = ky >= ku0 && ky < d.k0 && i >= d.ur0 && i < d.ur1;
+      const bool from_dn = ky >= d.k1 && ky < kd1 && i >= d.dr0 && i < d.dr1;
+      if (!local && !from_up && !from_dn) {
+        err = "layout too fine for this GPU count (a band reaches past the slab neighbour)";
+        return false;
+      }
+    }
+  if ((d.k0 > 0 && d.R0 - 2 < d.V0) || d.R1 > d.V1) {
+    err = "multi-GPU needs overlap >= 2";
+    return false;
+  }
+  return true;
+}
+
 // ----------------------------------------------------------------------------- device memory
 
 struct DevBuf {
@@ -127,6 +209,9 @@ struct Plan {
   float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
   ProjBatch local, global;
   int64_t sum_S = 0, sum_T = 0;
+  Dist dist;
+  int m2loc = 0;                       // local layout rows (k1 - k0)
+  float *send_up = nullptr, *send_dn = nullptr, *recv_up = nullptr, *recv_dn = nullptr;
   std::vector<std::unique_ptr<DevBuf>> bufs;
 };
 
@@ -162,6 +247,7 @@ struct tvs_ctx {
   int64_t launches = 0;
   // scratch for denoise / host variants
   std::unique_ptr<DevBuf> tau_scratch, h_d0, h_d, h_tau;
+  ncclComm_t nccl = nullptr;   // world > 1 only
 };
 
 namespace {
@@ -279,9 +365,11 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
 }
 
 // Build the projection batch for tiles (chains = distinct row ranges).
+// fr0/fr1 (global batch only): rows whose partial x-DCT this rank computes (its core rows; the
+// rest of qhat arrives by all-gather); gplane: plane stride of G (0 = ntiles * AP * ldG).
 tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
                       int n2t, int n1t, float *q, float *qlo, int ldq, float *G, int ldG,
-                      const Tables *T) {
+                      const Tables *T, int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0) {
   B.tiles = tiles_in;
   B.ntiles = (int)tiles_in.size();
   std::map<std::pair<int, int>, int> chain_of;
@@ -295,7 +383,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     }
     B.tiles[i].chain = chain_of[key];
     B.AT = std::max(B.AT, B.tiles[i].ty1 - B.tiles[i].ty0 + 1);
-    B.AP = std::max(B.AP, B.tiles[i].py1 - B.tiles[i].ty0 + 1);
+    B.AP = std::max(B.AP, B.tiles[i].py1 - B.tiles[i].ty0 + 1 - B.tiles[i].po);
   }
   B.nchains = (int)first.size();
   B.ldn = round_up(n1t, 4);
@@ -316,7 +404,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   std::vector<GemmDesc> fwd, inv, fwd_tc, inv_tc;
   std::vector<GemmDesc2> fwd2, inv2;
   // ∇φ output is plane-major: G[c][tile][AP][ldG]
-  const size_t gplane = (size_t)B.ntiles * B.AP * ldG;
+  const size_t gplane = gplane_arg ? gplane_arg : (size_t)B.ntiles * B.AP * ldG;
   for (int i = 0; i < B.ntiles;) {
     // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
     int j = i + 1;
@@ -326,26 +414,33 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     const ProjTile &t = B.tiles[i];
     const int cnt = j - i;
     const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
-    const int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
-    const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1);
-    fwd_tc.push_back({q + (size_t)i * B.AT * ldq, T->cn + t.tx0,
-                      B.qhat + (size_t)i * B.AT * B.ldn, Mf, n1t, bt, ldq, T->ld, B.ldn});
+    int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
+    const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1 - B.tiles[j - 1].po);
+    // forward rows [f0, f0 + Mf) of the stacked operand; inverse output rows start at po
+    int f0 = 0;
+    if (fr0 >= 0) {
+      f0 = fr0;
+      Mf = fr1 - fr0;
+    }
+    const size_t goff = (size_t)t.po * ldG;
+    fwd_tc.push_back({q + ((size_t)i * B.AT + f0) * ldq, T->cn + t.tx0,
+                      B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t, bt, ldq, T->ld, B.ldn});
     inv_tc.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->snT + (size_t)t.tx0 * T->ld,
-                      G + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+                      G + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
     inv_tc.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cf + (size_t)t.tx0 * T->ld,
-                      G + gplane + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+                      G + gplane + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
     // 3xTF32 pre-split forms; q carries a leading zero offset of (tx0 & 3) columns so the table
     // rows start 16-byte aligned: K = bt + off, tables from column tx0 - off
     const int off = t.tx0 & 3;
-    fwd2.push_back({q + (size_t)i * B.AT * ldq, qlo + (size_t)i * B.AT * ldq,
+    fwd2.push_back({q + ((size_t)i * B.AT + f0) * ldq, qlo + ((size_t)i * B.AT + f0) * ldq,
                     T->part(2) + (t.tx0 - off), T->part(3) + (t.tx0 - off),
-                    B.qhat + (size_t)i * B.AT * B.ldn, Mf, n1t, bt + off, ldq, T->ld, B.ldn});
+                    B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t, bt + off, ldq, T->ld, B.ldn});
     inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, B.phx_lo + (size_t)i * B.AP * B.ldn,
                     T->part(4) + (size_t)t.tx0 * T->ld, T->part(5) + (size_t)t.tx0 * T->ld,
-                    G + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+                    G + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
     inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, B.phy_lo + (size_t)i * B.AP * B.ldn,
                     T->part(0) + (size_t)t.tx0 * T->ld, T->part(1) + (size_t)t.tx0 * T->ld,
-                    G + gplane + (size_t)i * B.AP * ldG, Mi, bo, n1t, B.ldn, T->ld, ldG});
+                    G + gplane + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
     B.tcM_fwd = std::max(B.tcM_fwd, Mf);
     B.tcM_inv = std::max(B.tcM_inv, Mi);
     i = j;
@@ -353,13 +448,19 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   for (int i = 0; i < B.ntiles; ++i) {
     const ProjTile &t = B.tiles[i];
     int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
-    int no = t.py1 - t.ty0 + 1, bo = t.px1 - t.tx0 + 1;
-    fwd.push_back({q + (size_t)i * B.AT * ldq + (t.tx0 & 3), T->cf + (size_t)t.tx0 * T->ld,
-                   B.qhat + (size_t)i * B.AT * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
+    int no = t.py1 - t.ty0 + 1 - t.po, bo = t.px1 - t.tx0 + 1;
+    int f0 = 0;
+    if (fr0 >= 0) {
+      f0 = fr0;
+      nt = fr1 - fr0;
+    }
+    const size_t goff = (size_t)t.po * ldG;
+    fwd.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3), T->cf + (size_t)t.tx0 * T->ld,
+                   B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
     inv.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->sn + t.tx0,
-                   G + (size_t)i * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+                   G + (size_t)i * B.AP * ldG + goff, no, bo, n1t, B.ldn, T->ld, ldG});
     inv.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cn + t.tx0,
-                   G + gplane + (size_t)i * B.AP * ldG, no, bo, n1t, B.ldn, T->ld, ldG});
+                   G + gplane + (size_t)i * B.AP * ldG + goff, no, bo, n1t, B.ldn, T->ld, ldG});
     B.fwdM = std::max(B.fwdM, nt);
     B.fwdN = std::max(B.fwdN, n1t);
     B.invM = std::max(B.invM, no);
@@ -407,14 +508,20 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
       !axis_ranges(n1 + 1, L.m1, L.overlap_x, lx, hx, err))
     return fail(ctx, TVS_ELAYOUT, "%s", err.c_str());
   const int G2 = P->G2, G1 = P->G1;
+  if (!compute_dist(G2, L.m2, ly, hy, n2 + 1, ctx->rank, ctx->world, P->dist, err))
+    return fail(ctx, TVS_ELAYOUT, "%s", err.c_str());
+  const Dist &D = P->dist;
+  P->m2loc = D.k1 - D.k0;
+  P->M = P->m2loc * L.m1;
   Geo &g = P->geo;
   g.M = P->M;
   std::vector<float> thy, thx;
-  // subdomains are stored column-major (m = m1_index * M2 + m2_index) so the tiles of one layout
-  // column -- which share their x-range and hence the DCT operand of kernel (b) -- are contiguous
-  // and their partial-DCT GEMMs can be stacked into one.
+  // this rank's subdomains (layout rows [k0, k1)) stored column-major
+  // (m = m1_index * m2loc + (m2_index - k0)) so the tiles of one layout column -- which share their
+  // x-range and hence the DCT operand of kernel (b) -- are contiguous and their partial-DCT GEMMs
+  // can be stacked into one.
   for (int b = 0; b < L.m1; ++b)
-    for (int a = 0; a < L.m2; ++a) {
+    for (int a = D.k0; a < D.k1; ++a) {
       SubDesc s{};
       s.y0 = ly[a];
       s.y1 = std::min(hy[a], G2 - 1);
@@ -483,6 +590,12 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   TRY(dalloc(ctx, P->bufs, &P->v[1], vsz));
   TRY(dalloc(ctx, P->bufs, &P->p, (size_t)C * G2 * P->ld));
   TRY(dalloc(ctx, P->bufs, &P->d_bad, 1));
+  if (D.world > 1) {   // partial-sum band buffers [planes][rows][ld]
+    TRY(dalloc(ctx, P->bufs, &P->send_up, (size_t)C * std::max(1, D.us1 - D.us0) * P->ld));
+    TRY(dalloc(ctx, P->bufs, &P->recv_up, (size_t)C * std::max(1, D.ur1 - D.ur0) * P->ld));
+    TRY(dalloc(ctx, P->bufs, &P->send_dn, (size_t)C * std::max(1, D.ds1 - D.ds0) * P->ld));
+    TRY(dalloc(ctx, P->bufs, &P->recv_dn, (size_t)C * std::max(1, D.dr1 - D.dr0) * P->ld));
+  }
   if (step == 2) {
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->f, (size_t)G2 * P->ld));
@@ -506,22 +619,85 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     std::vector<ProjTile> lt;
     for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
     TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, P->qlo, g.ldT, P->gphi, g.ldP, T));
-    std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, G2 - 1, G1 - 1, 0, 0}};
-    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->qglo, P->ld, P->Gg, P->ld, T));
+    // global projection: the y-solves span every row; this rank transforms its core rows
+    // (qhat of the others arrives by all-gather) and needs grad phi only on its valid rows V
+    std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, D.V1 - 1, G1 - 1, 0, D.V0}};
+    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->qglo, P->ld, P->Gg, P->ld, T, D.R0,
+                   D.R1, pl));
   }
   *out = P.get();
   ctx->plans[key] = std::move(P);
   return TVS_OK;
 }
 
-// grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).
-tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s) {
+tvs_status nccl_ck(tvs_ctx *ctx, ncclResult_t r, const char *what) {
+  if (r != ncclSuccess) return fail(ctx, TVS_ENCCL, "%s: %s", what, ncclGetErrorString(r));
+  return TVS_OK;
+}
+
+// All-gather of row slabs: rank q contributes rows [Rlo[q], Rhi[q]) of every plane of `buf`
+// (row pitch ld, plane stride ps), in place -- one ncclBroadcast per (root, plane) in a group.
+tvs_status allgather_rows(tvs_ctx *ctx, const Dist &D, float *buf, int planes, size_t ps, int ld,
+                          cudaStream_t s) {
+  if (D.world == 1) return TVS_OK;
+  TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
+  for (int q = 0; q < D.world; ++q)
+    for (int c = 0; c < planes; ++c) {
+      float *ptr = buf + (size_t)c * ps + (size_t)D.Rlo[q] * ld;
+      size_t cnt = (size_t)(D.Rhi[q] - D.Rlo[q]) * ld;
+      if (cnt) TRY(nccl_ck(ctx, ncclBroadcast(ptr, ptr, cnt, ncclFloat, q, ctx->nccl, s), "ncclBroadcast"));
+    }
+  return nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// Alg. 2 combine on this rank's valid rows, after exchanging the partial sums of the
+// band rows with the slab neighbours (NCCL send/recv over NVLink).
+tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
+  const Dist &D = P.dist;
+  const int C = P.planes;
+  const Geo g = P.geo;
+  if (D.world > 1) {
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_partial(P.d_subs, g, C, P.d_covy, P.d_covx, P.d_loy, P.d_lox, P.m2loc, D.k0,
+                            D.k1, q, D.us0, D.us1, P.G1, P.ld, P.send_up, s);
+    }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_partial(P.d_subs, g, C, P.d_covy, P.d_covx, P.d_loy, P.d_lox, P.m2loc, D.k0,
+                            D.k1, q, D.ds0, D.ds1, P.G1, P.ld, P.send_dn, s);
+    }));
+    TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
+    auto cnt = [&](int a, int b) { return (size_t)C * (b - a) * P.ld; };
+    if (D.rank > 0) {
+      if (D.us1 > D.us0)
+        TRY(nccl_ck(ctx, ncclSend(P.send_up, cnt(D.us0, D.us1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclSend"));
+      if (D.ur1 > D.ur0)
+        TRY(nccl_ck(ctx, ncclRecv(P.recv_up, cnt(D.ur0, D.ur1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclRecv"));
+    }
+    if (D.rank < D.world - 1) {
+      if (D.ds1 > D.ds0)
+        TRY(nccl_ck(ctx, ncclSend(P.send_dn, cnt(D.ds0, D.ds1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclSend"));
+      if (D.dr1 > D.dr0)
+        TRY(nccl_ck(ctx, ncclRecv(P.recv_dn, cnt(D.dr0, D.dr1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclRecv"));
+    }
+    TRY(nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd"));
+  }
+  return run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_combine(P.d_subs, g, C, P.d_covy, P.d_covx, P.d_loy, P.d_lox, P.m2loc, D.k0,
+                          D.k1, q, P.p, P.ld, P.G2, D.V0, D.V1, P.G1, P.ahat, P.d_bad,
+                          P.recv_up, D.ur0, D.ur1, P.recv_dn, D.dr0, D.dr1, s);
+  });
+}
+
+// grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).  For the
+// global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
+tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
   const bool tc = ctx->gemm_tc;
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
     return tc ? launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
               : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
   }));
+  if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
     return launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z, B.phx,
                              B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
@@ -607,14 +783,14 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       }));
       cur ^= 1;
     }
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_combine(P->d_subs, g, 2, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M2,
-                            P->v[cur], P->p, ld, n2, n1, P->ahat, P->d_bad, s);
-    }));
+    TRY(combine_step(ctx, *P, P->v[cur], s));
   }
+  const Dist &D = P->dist;
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-    return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha, d, s);
+    return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha, d, D.R0, D.R1, s);
   }));
+  TRY(allgather_rows(ctx, D, d, 1, 0, n1, s));
+  if (p_out) TRY(allgather_rows(ctx, D, P->p, 2, pl, ld, s));
   if (p_out)
     for (int c = 0; c < 2; ++c)
       CK(cudaMemcpy2DAsync(p_out + (size_t)c * n2 * n1, n1 * sizeof(float), P->p + c * pl,
@@ -647,23 +823,29 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
   // f = delta^{-1} P tau_0 (tau_0 pre-projected, reading A1)
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_tau0(d0, n2, n1, P->t0, ld, s); }));
-  TRY(run(ctx, s, F_OTHER, 0, 0,
-          [&] { return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, s); }));
-  TRY(project_batch(ctx, *P, P->global, s));
+  const Dist &D = P->dist;
+  const bool gather = D.world > 1;
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, s);
+  }));
+  TRY(project_batch(ctx, *P, P->global, s, gather));
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
     return launch_axpby2(P->t0, P->Gg, nullptr, ld, G2, G1, 1.f / delta, -1.f / delta, 0.f, P->f,
-                         s);
+                         D.E0, D.V1, s);
   }));
   CK(cudaMemsetAsync(P->p, 0, 4 * pl * sizeof(float), s));
   CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 4 * g.A * g.ldS * sizeof(float), s));
   // r = f - P multidiv p = f - w + grad phi, phi = Delta^dagger div w (global, once per sweep)
+  // rows: w on [E0, V1) (needs p on [V0, V1)); q on the core rows; r on [E0, V1)
   auto residual = [&](float *out, float scale) -> tvs_status {
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, s); }));
     TRY(run(ctx, s, F_OTHER, 0, 0,
-            [&] { return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, s); }));
-    TRY(project_batch(ctx, *P, P->global, s));
+            [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, D.E0, D.V1, s); }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, s);
+    }));
+    TRY(project_batch(ctx, *P, P->global, s, gather));
     return run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, s);
+      return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, D.E0, D.V1, s);
     });
   };
   int cur = 0;
@@ -690,13 +872,12 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       }));
       cur ^= 1;
     }
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_combine(P->d_subs, g, 4, P->d_covy, P->d_covx, P->d_loy, P->d_lox, P->M2,
-                            P->v[cur], P->p, ld, G2, G1, P->ahat, P->d_bad, s);
-    }));
+    TRY(combine_step(ctx, *P, P->v[cur], s));
   }
-  // tau = P tau_0 - delta P multidiv p = delta r^S
+  // tau = P tau_0 - delta P multidiv p = delta r^S; every rank ends with the full field
   TRY(residual(P->r, delta));
+  TRY(allgather_rows(ctx, D, P->r, 2, pl, ld, s));
+  if (p_out) TRY(allgather_rows(ctx, D, P->p, 4, pl, ld, s));
   for (int c = 0; c < 2; ++c)
     CK(cudaMemcpy2DAsync(tau_out + (size_t)c * G2 * G1, G1 * sizeof(float), P->r + c * pl,
                          ld * sizeof(float), G1 * sizeof(float), G2, cudaMemcpyDeviceToDevice, s));
@@ -723,10 +904,7 @@ extern "C" {
 tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint8_t *nccl_id) {
   if (!out) return TVS_EINVAL;
   *out = nullptr;
-  if (world != 1 || rank != 0) {
-    (void)nccl_id;
-    return TVS_EINVAL;   // multi-GPU contexts are created by the NCCL-enabled build (see DESIGN)
-  }
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) return TVS_EINVAL;
   auto *c = new tvs_ctx();
   c->device = device;
   c->rank = rank;
@@ -738,6 +916,14 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
     delete c;
     return TVS_ECUDA;
   }
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    if (ncclCommInitRank(&c->nccl, world, id, rank) != ncclSuccess) {
+      delete c;
+      return TVS_ENCCL;
+    }
+  }
   *out = c;
   return TVS_OK;
 }
@@ -747,6 +933,7 @@ tvs_status tvs_destroy(tvs_ctx *ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->nccl) ncclCommDestroy(ctx->nccl);
   delete ctx;
   return TVS_OK;
 }
@@ -755,8 +942,27 @@ const char *tvs_last_error(const tvs_ctx *ctx) { return ctx ? ctx->err.c_str() :
 
 tvs_status tvs_nccl_unique_id(uint8_t id_out[128]) {
   if (!id_out) return TVS_EINVAL;
-  memset(id_out, 0, 128);
-  return TVS_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TVS_ENCCL;
+  memcpy(id_out, &id, 128);
+  return TVS_OK;
+}
+
+tvs_status tvs_dist_rows(int32_t n2, int32_t n1, const tvs_layout *L, int32_t step, int rank,
+                         int world, int32_t out[16]) {
+  if (!L || !out || (step != 1 && step != 2)) return TVS_EINVAL;
+  std::vector<int> ly, hy;
+  std::string err;
+  if (!axis_ranges(n2 + 1, L->m2, L->overlap_y, ly, hy, err)) return TVS_ELAYOUT;
+  (void)n1;
+  const int G2 = step == 1 ? n2 + 1 : n2;
+  Dist d;
+  if (!compute_dist(G2, L->m2, ly, hy, n2 + 1, rank, world, d, err)) return TVS_ELAYOUT;
+  const int v[16] = {d.k0, d.k1, d.R0, d.R1, d.E0, d.E1, d.V0, d.V1,
+                     d.us0, d.us1, d.ur0, d.ur1, d.ds0, d.ds1, d.dr0, d.dr1};
+  memcpy(out, v, sizeof v);
+  return TVS_OK;
 }
 
 tvs_status tvs_owned_rows(int32_t n2, int32_t n1, const tvs_layout *Lp, int rank, int world,

@@ -21,7 +21,7 @@ struct ProjTile {
   int ty0, ty1, tx0, tx1;
   int py1, px1;
   int chain;    // index of the precomputed Thomas pivots (distinct row range [ty0, ty1])
-  int pad;
+  int po;       // first output row relative to ty0 (output rows [ty0 + po, py1], stored from 0)
 };
 
 // Batched fp32 GEMM descriptor: C[M x N] = A[M x K] * B[K x N], all row-major.
@@ -65,18 +65,26 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s);
 cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
-                           const int2 *covx, const int *loy, const int *lox, int m2,
-                           const float *q, float *p, int ld, int n2, int n1, float ahat,
-                           int *bad, cudaStream_t s);
+                           const int2 *covx, const int *loy, const int *lox, int m2loc, int k0,
+                           int k1, const float *q, float *p, int ld, int n2, int row0, int row1,
+                           int n1, float ahat, int *bad, const float *up, int up_r0, int up_r1,
+                           const float *dn, int dn_r0, int dn_r1, cudaStream_t s);
+cudaError_t launch_partial(const SubDesc *subs, Geo g, int planes, const int2 *covy,
+                           const int2 *covx, const int *loy, const int *lox, int m2loc, int k0,
+                           int k1, const float *q, int ra, int rb, int n1, int ld, float *out,
+                           cudaStream_t s);
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
-                            int n1, float inv_alpha, float *d, cudaStream_t s);
+                            int n1, float inv_alpha, float *d, int row0, int row1,
+                            cudaStream_t s);
 
 // step 1
-cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cudaStream_t s);
+cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,
+                            cudaStream_t s);
 cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
-                       float *qlo, cudaStream_t s);
+                       float *qlo, int row0, int row1, cudaStream_t s);
 cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
-                          float sa, float sb, float sc, float *out, cudaStream_t s);
+                          float sa, float sb, float sc, float *out, int row0, int row1,
+                          cudaStream_t s);
 cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                            const float *p, int ld, int n2, int n1, float *v, cudaStream_t s);
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,

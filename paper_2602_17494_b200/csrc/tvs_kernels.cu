@@ -476,25 +476,47 @@ k_sweep2q(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   }
 }
 
-// p^{n+1} = (1 - ahat) p^n + ahat sum_m E qhat_m (Alg. 2), summed in fixed subdomain
-// order (m2 ascending, then m1) so overlaps are bitwise reproducible.  Flags non-finite values.
+// Sum over the local layout-row ky of sum_kx qhat (subdomains stored column-major per rank:
+// m = kx * m2loc + (ky - k0)).
+__device__ __forceinline__ float ky_part(const float *__restrict__ q, const Geo &g, int planes,
+                                         int c, int ky, int k0, int m2loc, int i, int j,
+                                         int2 cx, const int *__restrict__ loy,
+                                         const int *__restrict__ lox) {
+  float part = 0.f;
+  for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
+    const int m = kx * m2loc + (ky - k0);
+    const int li = i - loy[ky], lj = j - lox[kx];
+    part += q[(((size_t)m * planes + c) * g.A + li) * g.ldS + lj];
+  }
+  return part;
+}
+
+// p^{n+1} = (1 - ahat) p^n + ahat sum_m E qhat_m (Alg. 2) on rows [row0, row1).  The sum
+// is grouped as sum_ky (sum_kx qhat) in ascending ky, where the parts of layout rows owned by the
+// slab neighbours (ky < k0: `up`, ky >= k1: `dn`, rows [*_r0, *_r1)) arrive as partial sums over
+// NCCL -- so overlaps are bitwise identical for every GPU count.  Flags non-finite values.
 __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
                           const int2 *__restrict__ covy, const int2 *__restrict__ covx,
-                          const int *__restrict__ loy, const int *__restrict__ lox, int m2,
-                          const float *__restrict__ q, float *__restrict__ p, int ld, int n2,
-                          int n1, float ahat, int *bad) {
+                          const int *__restrict__ loy, const int *__restrict__ lox, int m2loc,
+                          int k0, int k1, const float *__restrict__ q, float *__restrict__ p,
+                          int ld, int n2, int row0, int row1, int n1, float ahat, int *bad,
+                          const float *__restrict__ up, int up_r0, int up_r1,
+                          const float *__restrict__ dn, int dn_r0, int dn_r1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= n2 || j >= n1) return;
+  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= row1 || j >= n1) return;
   int2 cy = covy[i], cx = covx[j];
   for (int c = 0; c < planes; ++c) {
     float acc = 0.f;
     for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
-      for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
-        int m = kx * m2 + ky;   // subdomains are stored column-major (see tvs_api.cu)
-        int li = i - loy[ky], lj = j - lox[kx];
-        acc += q[(((size_t)m * planes + c) * g.A + li) * g.ldS + lj];
-      }
+      float part;
+      if (ky < k0)
+        part = (i >= up_r0 && i < up_r1) ? up[((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + j] : 0.f;
+      else if (ky >= k1)
+        part = (i >= dn_r0 && i < dn_r1) ? dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j] : 0.f;
+      else
+        part = ky_part(q, g, planes, c, ky, k0, m2loc, i, j, cx, loy, lox);
+      acc += part;
     }
     size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
     float v = (1.f - ahat) * p[idx] + ahat * acc;
@@ -503,13 +525,32 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
   }
 }
 
+// Partial sums of the local subdomains on rows [ra, rb) for a slab neighbour:
+// out[c][i - ra][j] = sum_{local ky covering i} sum_kx qhat (same grouping as k_combine).
+__global__ void k_partial(const SubDesc *__restrict__ subs, Geo g, int planes,
+                          const int2 *__restrict__ covy, const int2 *__restrict__ covx,
+                          const int *__restrict__ loy, const int *__restrict__ lox, int m2loc,
+                          int k0, int k1, const float *__restrict__ q, int ra, int rb, int n1,
+                          int ld, float *__restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = ra + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= rb || j >= n1) return;
+  int2 cy = covy[i], cx = covx[j];
+  for (int c = 0; c < planes; ++c) {
+    float acc = 0.f;
+    for (int ky = cy.x; ky < cy.x + cy.y; ++ky)
+      if (ky >= k0 && ky < k1) acc += ky_part(q, g, planes, c, ky, k0, m2loc, i, j, cx, loy, lox);
+    out[((size_t)c * (rb - ra) + (i - ra)) * ld + j] = acc;
+  }
+}
+
 // d = d0 - div p / alpha.
 __global__ void k_recover2(const float *__restrict__ d0, const float *__restrict__ p1,
                            const float *__restrict__ p2, int ld, int n2, int n1, float inv_alpha,
-                           float *__restrict__ d) {
+                           float *__restrict__ d, int row0, int row1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= n2 || j >= n1) return;
+  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= row1 || j >= n1) return;
   auto P1 = [&](int a, int b) { return p1[(size_t)a * ld + b]; };
   auto P2 = [&](int a, int b) { return p2[(size_t)a * ld + b]; };
   float dv = (j < n1 - 1 ? P1(i, j) : 0.f) - (j > 0 ? P1(i, j - 1) : 0.f) +
@@ -521,10 +562,10 @@ __global__ void k_recover2(const float *__restrict__ d0, const float *__restrict
 
 // w = multidiv p: w_k = div(p_k1, p_k2); p has 4 planes [p11 p12 p21 p22].
 __global__ void k_multidiv(const float *__restrict__ p, int ld, int n2, int n1,
-                           float *__restrict__ w) {
+                           float *__restrict__ w, int row0, int row1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= n2 || j >= n1) return;
+  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= row1 || j >= n1) return;
   size_t pl = (size_t)n2 * ld;
   for (int k = 0; k < 2; ++k) {
     const float *px = p + (2 * k) * pl, *py = p + (2 * k + 1) * pl;
@@ -536,10 +577,10 @@ __global__ void k_multidiv(const float *__restrict__ p, int ld, int n2, int n1,
 
 // q = div w.
 __global__ void k_div(const float *__restrict__ w1, const float *__restrict__ w2, int ld, int n2,
-                      int n1, float *__restrict__ q, float *__restrict__ qlo) {
+                      int n1, float *__restrict__ q, float *__restrict__ qlo, int row0, int row1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= n2 || j >= n1) return;
+  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= row1 || j >= n1) return;
   float dv = (j < n1 - 1 ? w1[(size_t)i * ld + j] : 0.f) - (j > 0 ? w1[(size_t)i * ld + j - 1] : 0.f) +
              (i < n2 - 1 ? w2[(size_t)i * ld + j] : 0.f) - (i > 0 ? w2[(size_t)(i - 1) * ld + j] : 0.f);
   store_split(q, qlo, (size_t)i * ld + j, dv);
@@ -548,10 +589,10 @@ __global__ void k_div(const float *__restrict__ w1, const float *__restrict__ w2
 // out = sa a + sb b (+ sc c), two planes.
 __global__ void k_axpby2(const float *__restrict__ a, const float *__restrict__ b,
                          const float *__restrict__ c, int ld, int n2, int n1, float sa, float sb,
-                         float sc, float *__restrict__ out) {
+                         float sc, float *__restrict__ out, int row0, int row1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= n2 || j >= n1) return;
+  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= row1 || j >= n1) return;
   size_t pl = (size_t)n2 * ld;
   for (int k = 0; k < 2; ++k) {
     size_t idx = k * pl + (size_t)i * ld + j;
@@ -744,8 +785,9 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
   if (j >= n1) return;
   const ProjTile tl = tiles[tix];
   const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1;
+  const int po = tl.po;   // output rows are [po, nout) relative to ty0, stored from row 0
   const float *__restrict__ b = qhat + (size_t)tix * AT * ldn + j;
-  const size_t obase = (size_t)tix * AP * ldn + j;
+  const size_t obase = (size_t)tix * AP * ldn + j - (size_t)po * ldn;
   float *__restrict__ ox = phx + obase;
   float *__restrict__ oy = phy + obase;
   float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
@@ -760,8 +802,10 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
       pre += (double)b[(size_t)k * ldn];
       int y = tl.ty0 + k;
       double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
-      store_split(ox, oxl, (size_t)k * ldn, 0.0);
-      store_split(oy, oyl, (size_t)k * ldn, s2 * w);
+      if (k >= po) {
+        store_split(ox, oxl, (size_t)k * ldn, 0.0);
+        store_split(oy, oyl, (size_t)k * ldn, s2 * w);
+      }
     }
     return;
   }
@@ -795,7 +839,7 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
     zz[(size_t)k * ldn] = zp;
   }
   double u = zp * ri[(size_t)(nt - 1) * ldn];
-  if (nt - 1 < nout) {                       // T = S+ in y: global last row, D+_y = 0
+  if (nt - 1 < nout && nt - 1 >= po) {       // T = S+ in y: global last row, D+_y = 0
     store_split(ox, oxl, (size_t)(nt - 1) * ldn, cx * u);
     store_split(oy, oyl, (size_t)(nt - 1) * ldn, 0.0);
   }
@@ -811,7 +855,7 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const double uk = (zv[q] - u) * rv[q];
-      if (k - q < nout) {
+      if (k - q < nout && k - q >= po) {
         store_split(ox, oxl, (size_t)(k - q) * ldn, cx * uk);
         store_split(oy, oyl, (size_t)(k - q) * ldn, s2 * (u - uk));
       }
@@ -820,7 +864,7 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
   }
   for (; k >= 0; --k) {
     const double uk = (zz[(size_t)k * ldn] - u) * ri[(size_t)k * ldn];
-    if (k < nout) {
+    if (k < nout && k >= po) {
       store_split(ox, oxl, (size_t)k * ldn, cx * uk);
       store_split(oy, oyl, (size_t)k * ldn, s2 * (u - uk));
     }
@@ -954,30 +998,53 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
   return cudaGetLastError();
 }
 cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *covy,
-                           const int2 *covx, const int *loy, const int *lox, int m2,
-                           const float *q, float *p, int ld, int n2, int n1, float ahat, int *bad,
+                           const int2 *covx, const int *loy, const int *lox, int m2loc, int k0,
+                           int k1, const float *q, float *p, int ld, int n2, int row0, int row1,
+                           int n1, float ahat, int *bad, const float *up, int up_r0, int up_r1,
+                           const float *dn, int dn_r0, int dn_r1, cudaStream_t s) {
+  if (row1 <= row0) return cudaSuccess;
+  k_combine<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
+      subs, g, planes, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat,
+      bad, up, up_r0, up_r1, dn, dn_r0, dn_r1);
+  return cudaGetLastError();
+}
+cudaError_t launch_partial(const SubDesc *subs, Geo g, int planes, const int2 *covy,
+                           const int2 *covx, const int *loy, const int *lox, int m2loc, int k0,
+                           int k1, const float *q, int ra, int rb, int n1, int ld, float *out,
                            cudaStream_t s) {
-  k_combine<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(subs, g, planes, covy, covx, loy, lox,
-                                                         m2, q, p, ld, n2, n1, ahat, bad);
+  if (rb <= ra) return cudaSuccess;
+  k_partial<<<grid2(n1, rb - ra, 32, 8), dim3(32, 8), 0, s>>>(subs, g, planes, covy, covx, loy,
+                                                              lox, m2loc, k0, k1, q, ra, rb, n1,
+                                                              ld, out);
   return cudaGetLastError();
 }
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
-                            int n1, float inv_alpha, float *d, cudaStream_t s) {
-  k_recover2<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(d0, p1, p2, ld, n2, n1, inv_alpha, d);
+                            int n1, float inv_alpha, float *d, int row0, int row1,
+                            cudaStream_t s) {
+  if (row1 <= row0) return cudaSuccess;
+  k_recover2<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(d0, p1, p2, ld, n2, n1,
+                                                                   inv_alpha, d, row0, row1);
   return cudaGetLastError();
 }
-cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, cudaStream_t s) {
-  k_multidiv<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(p, ld, n2, n1, w);
+cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,
+                            cudaStream_t s) {
+  if (row1 <= row0) return cudaSuccess;
+  k_multidiv<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(p, ld, n2, n1, w, row0, row1);
   return cudaGetLastError();
 }
 cudaError_t launch_div(const float *w1, const float *w2, int ld, int n2, int n1, float *q,
-                       float *qlo, cudaStream_t s) {
-  k_div<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(w1, w2, ld, n2, n1, q, qlo);
+                       float *qlo, int row0, int row1, cudaStream_t s) {
+  if (row1 <= row0) return cudaSuccess;
+  k_div<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(w1, w2, ld, n2, n1, q, qlo, row0,
+                                                              row1);
   return cudaGetLastError();
 }
 cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld, int n2, int n1,
-                          float sa, float sb, float sc, float *out, cudaStream_t s) {
-  k_axpby2<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(a, b, c, ld, n2, n1, sa, sb, sc, out);
+                          float sa, float sb, float sc, float *out, int row0, int row1,
+                          cudaStream_t s) {
+  if (row1 <= row0) return cudaSuccess;
+  k_axpby2<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(a, b, c, ld, n2, n1, sa, sb, sc,
+                                                                 out, row0, row1);
   return cudaGetLastError();
 }
 cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
