@@ -180,6 +180,7 @@ struct ProjBatch {
   float *phx = nullptr, *phy = nullptr, *phx_lo = nullptr, *phy_lo = nullptr;
   GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
   GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
+  TmaGemmDesc *d_fwd3 = nullptr, *d_inv3 = nullptr;   // same, TMA tensor maps
   GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
   int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
@@ -237,7 +238,9 @@ struct tvs_ctx {
   std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
   std::map<int, std::unique_ptr<Tables>> tables;
   bool profiling = false;
-  bool gemm_tc = true;   // TVS_GEMM=simt selects the SIMT fp32 GEMM (A/B comparisons)
+  // projection contractions: TVS_GEMM = tma (default: TMA + tcgen05 3xTF32), cpasync (cp.async +
+  // tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
+  bool gemm_tc = true, gemm_tma = true;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<PendingEv> pending;
@@ -477,6 +480,11 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(upload(ctx, P.bufs, &B.d_inv_tc, inv_tc));
   TRY(upload(ctx, P.bufs, &B.d_fwd2, fwd2));
   TRY(upload(ctx, P.bufs, &B.d_inv2, inv2));
+  std::vector<TmaGemmDesc> fwd3(fwd2.size()), inv3(inv2.size());
+  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
+  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
+  TRY(upload(ctx, P.bufs, &B.d_fwd3, fwd3));
+  TRY(upload(ctx, P.bufs, &B.d_inv3, inv3));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   CK(cudaDeviceSynchronize());
   return TVS_OK;
@@ -693,9 +701,11 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
 tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
   const bool tc = ctx->gemm_tc;
+  const bool tma = ctx->gemm_tma;
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
-    return tc ? launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
-              : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
+    return tma  ? launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
+           : tc ? launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
+                : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
@@ -703,8 +713,9 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
                              B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
   }));
   TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
-    return tc ? launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
-              : launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
+    return tma  ? launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
+           : tc ? launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
+                : launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
   }));
   return TVS_OK;
 }
@@ -911,6 +922,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->world = world;
   const char *g = getenv("TVS_GEMM");
   c->gemm_tc = !(g && strcmp(g, "simt") == 0);
+  c->gemm_tma = c->gemm_tc && !(g && strcmp(g, "cpasync") == 0);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;
@@ -1106,7 +1118,7 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
       {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
   TRY(upload(ctx, own, &dd, desc));
   cudaError_t e;
-  if (impl == 3) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
+  if (impl == 3 || impl == 4) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
     auto rna = [](float x) {
       uint32_t u;
       memcpy(&u, &x, 4);
@@ -1127,6 +1139,14 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
     std::vector<GemmDesc2> d2 = {{dAh, dAl, dBh, dBl, dC, M, N, K, lda, lda, N}};
     TRY(upload(ctx, own, &dd2, d2));
     e = launch_gemm_tc2(dd2, 1, M, N, 144, 0);
+    if (impl == 4) {   // same operands through the TMA pipeline
+      std::vector<TmaGemmDesc> d3(1);
+      CK(make_tma_desc(&d3[0], d2[0], 144));
+      TmaGemmDesc *dd3;
+      TRY(upload(ctx, own, &dd3, d3));
+      CK(cudaMemset(dC, 0, C.size() * 4));
+      e = launch_gemm_tma(dd3, 1, M, N, 144, 0);
+    }
   } else {
     e = impl == 0 ? launch_gemm(dd, 1, M, N, 0)
                   : launch_gemm_tc(dd, 1, M, N, impl == 2 ? 144 : 128, true, 0);

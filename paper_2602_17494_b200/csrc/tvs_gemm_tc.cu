@@ -19,6 +19,7 @@
 #include "tvs_internal.h"
 
 #include <stdint.h>
+#include <string.h>
 
 namespace tvs {
 namespace tc {
@@ -310,32 +311,46 @@ __global__ void __launch_bounds__(NT) k_gemm_tc2(const GemmDesc2 *__restrict__ d
   const int nk = (d.K + BK - 1) / BK;
   const uint32_t sbase = smem_u32(smem);
 
-  // one K slice = (A_hi, A_lo: 128 rows x 4 chunks) + (B_hi, B_lo: BN rows x 4 chunks) of 16 B
+  // one K slice = (A_hi, A_lo: 128 rows x 4 chunks) + (B_hi, B_lo: BN rows x 4 chunks) of 16 B.
+  // Chunk c = tid + NT*i: its 16-byte column kc = tid & 3 is the same for every i (A_CH, B_CH and
+  // NT are multiples of 4), so each thread's source rows and smem slots are fixed across k-tiles
+  // and precomputed here; per k-tile a copy costs one pointer add and one cp.async.
   constexpr int A_CH = BM * (BK / 4), B_CH = BN * (BK / 4);
   constexpr int TOT = 2 * A_CH + 2 * B_CH;
+  constexpr int PER = (TOT + NT - 1) / NT;
+  const int kc = tid & 3;
+  const float *src[PER];
+  uint32_t dst[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = tid + NT * i;
+    src[i] = nullptr;
+    dst[i] = 0xFFFFFFFFu;
+    if (c >= TOT) continue;
+    int part, rem;
+    if (c < 2 * A_CH) { part = c / A_CH; rem = c - part * A_CH; }
+    else { part = 2 + (c - 2 * A_CH) / B_CH; rem = (c - 2 * A_CH) - (part - 2) * B_CH; }
+    const int row = rem >> 2;
+    const bool isA = part < 2;
+    const int grow = (isA ? m0 : n0) + row;
+    const int lim = isA ? d.M : d.N;
+    const float *base = isA ? (part == 0 ? d.Ahi : d.Alo) : (part == 2 ? d.Bhi : d.Blo);
+    const int ld = isA ? d.lda : d.ldb;
+    if (grow < lim) src[i] = base + (size_t)grow * ld + 4 * kc;
+    const uint32_t off = isA ? (part == 0 ? 0 : SM::A_BYTES) : (2 * SM::A_BYTES + (part == 2 ? 0 : SM::B_BYTES));
+    dst[i] = off + core_off(row, 4 * kc, isA ? BM : BN);
+  }
   auto issue = [&](int s, int kt) {
     const int k0 = kt * BK;
     const uint32_t st = sbase + s * SM::STAGE;
-#pragma unroll 1
-    for (int c = tid; c < TOT; c += NT) {
-      int part, rem;
-      if (c < 2 * A_CH) { part = c / A_CH; rem = c - part * A_CH; }
-      else { part = 2 + (c - 2 * A_CH) / B_CH; rem = (c - 2 * A_CH) - (part - 2) * B_CH; }
-      const int row = rem >> 2, kc = rem & 3;
-      const int k = k0 + 4 * kc;
-      const bool isA = part < 2;
-      const int R = isA ? BM : BN;
-      const int grow = (isA ? m0 : n0) + row;
-      const int lim = isA ? d.M : d.N;
-      const float *src = isA ? (part == 0 ? d.Ahi : d.Alo) : (part == 2 ? d.Bhi : d.Blo);
-      const int ld = isA ? d.lda : d.ldb;
-      int valid = d.K - k;
-      valid = valid < 0 ? 0 : (valid > 4 ? 4 : valid);
-      if (grow >= lim) valid = 0;
-      const float *g = valid ? src + (size_t)grow * ld + k : src;
-      const uint32_t off = isA ? (part == 0 ? 0 : SM::A_BYTES) : (2 * SM::A_BYTES + (part == 2 ? 0 : SM::B_BYTES));
-      const uint32_t dst = st + off + core_off(row, 4 * kc, R);
-      cp_async16(dst, g, (uint32_t)(valid * 4));
+    int valid = d.K - (k0 + 4 * kc);
+    valid = valid < 0 ? 0 : (valid > 4 ? 4 : valid);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (dst[i] == 0xFFFFFFFFu) continue;
+      const bool ok = src[i] != nullptr && valid > 0;
+      cp_async16(st + dst[i], ok ? (const void *)(src[i] + k0) : (const void *)d.Ahi,
+                 ok ? (uint32_t)(valid * 4) : 0u);
     }
   };
 
@@ -449,7 +464,224 @@ static cudaError_t launch_one(const GemmDesc *descs, int batch, int maxM, int ma
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// v3 (default): TMA + tcgen05, warp-specialised.  Per stage one cp.async.bulk.tensor per operand
+// plane (box = {32 fp32 = 128 B, rows}, SWIZZLE_128B, OOB zero-fill handles every M/N/K tail);
+// warp 0 lane 0 produces (full[s] with expect_tx), warp 1 lane 0 issues 4 k-steps x 3 MMAs per
+// stage and commits to empty[s]; after the last stage a commit to `accum` releases the epilogue.
+// K-major SWIZZLE_128B smem descriptors: LBO field 1, SBO = 1024 B (8 rows x 128 B), start
+// address advanced by 32 B per k-step inside the 128-B swizzle atom (tiles 1024-B aligned).
+constexpr int TBK = 32, TSTAGES = 3;
+
+template <int BN>
+struct TSmem {
+  static constexpr int A_BYTES = BM * TBK * 4;      // 16 KB
+  static constexpr int B_BYTES = BN * TBK * 4;      // 18 KB for BN = 144
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int TOTAL = TSTAGES * STAGE + 256 + 1024;   // barriers + alignment slack
+  static constexpr int TMEM_COLS = BN <= 128 ? 128 : 256;
+};
+
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;                 // LBO (unused for swizzled K-major) = 1
+  d |= (uint64_t)(1024u >> 4) << 32;       // SBO = 1024 B between 8-row groups
+  d |= (uint64_t)1u << 46;                 // version (Blackwell)
+  d |= (uint64_t)2u << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NT, 1) k_gemm_tma(const TmaGemmDesc *__restrict__ descs) {
+  using SM = TSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const TmaGemmDesc *dp = descs + blockIdx.z;
+  const int M = dp->M, N = dp->N, K = dp->K, ldc = dp->ldc;
+  float *C = dp->C;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M || n0 >= N) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TSTAGES * SM::STAGE);
+  uint64_t *empty = full + TSTAGES;
+  uint64_t *accum = empty + TSTAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(SM::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&dp->a_hi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&dp->b_hi)));
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (K + TBK - 1) / TBK;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TSTAGES;
+      if (kt >= TSTAGES) mbar_wait(&empty[s], ((kt / TSTAGES) - 1) & 1);
+      mbar_expect_tx(&full[s], SM::STAGE);
+      const uint32_t st = sbase + s * SM::STAGE;
+      tma_load_2d(st, &dp->a_hi, kt * TBK, m0, &full[s]);
+      tma_load_2d(st + SM::A_BYTES, &dp->a_lo, kt * TBK, m0, &full[s]);
+      tma_load_2d(st + 2 * SM::A_BYTES, &dp->b_hi, kt * TBK, n0, &full[s]);
+      tma_load_2d(st + 2 * SM::A_BYTES + SM::B_BYTES, &dp->b_lo, kt * TBK, n0, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDESC = make_idesc(BM, BN);
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TSTAGES;
+      mbar_wait(&full[s], (kt / TSTAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t st = sbase + s * SM::STAGE;
+      const uint32_t ahi = st, alo = st + SM::A_BYTES;
+      const uint32_t bhi = st + 2 * SM::A_BYTES, blo = bhi + SM::B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < TBK / 8; ++ks) {
+        const uint64_t dah = make_desc_sw128(ahi + 32 * ks), dal = make_desc_sw128(alo + 32 * ks);
+        const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
+        mma_tf32(tmem, dal, dbh, IDESC, (kt > 0 || ks > 0) ? 1u : 0u);
+        mma_tf32(tmem, dah, dbl, IDESC, 1u);
+        mma_tf32(tmem, dah, dbh, IDESC, 1u);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(accum);
+  }
+  __syncwarp();
+  // ------------------------------------------------------------------ epilogue (all 4 warps)
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+      float *out = C + (size_t)row * ldc + n0 + c0;
+      const int nvalid = N - (n0 + c0);
+      if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4 *>(out)[q] =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < nvalid) out[j] = __uint_as_float(v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(SM::TMEM_COLS));
+}
+
+template <int BN>
+static cudaError_t launch_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                              cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TSmem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((maxN + BN - 1) / BN, (maxM + BM - 1) / BM, batch);
+  k_gemm_tma<BN><<<grid, NT, TSmem<BN>::TOTAL, s>>>(descs);
+  return cudaGetLastError();
+}
+
 }  // namespace tc
+
+cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                            cudaStream_t s) {
+  return bn == 144 ? tc::launch_tma<144>(descs, batch, maxM, maxN, s)
+                   : tc::launch_tma<128>(descs, batch, maxM, maxN, s);
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static cudaError_t encode_2d(CUtensorMap *map, const float *base, int cols, int rows, int ld,
+                             int box_rows) {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !p) return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+    fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)(cols > 0 ? cols : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)tc::TBK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn) {
+  memset(out, 0, sizeof *out);
+  cudaError_t e;
+  if ((e = encode_2d(&out->a_hi, d.Ahi, d.K, d.M, d.lda, tc::BM)) != cudaSuccess) return e;
+  if ((e = encode_2d(&out->a_lo, d.Alo, d.K, d.M, d.lda, tc::BM)) != cudaSuccess) return e;
+  if ((e = encode_2d(&out->b_hi, d.Bhi, d.K, d.N, d.ldb, bn)) != cudaSuccess) return e;
+  if ((e = encode_2d(&out->b_lo, d.Blo, d.K, d.N, d.ldb, bn)) != cudaSuccess) return e;
+  out->C = d.C;
+  out->M = d.M;
+  out->N = d.N;
+  out->K = d.K;
+  out->ldc = d.ldc;
+  return cudaSuccess;
+}
 
 cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s) {

@@ -1,6 +1,7 @@
 // Internal declarations shared by the kernels (tvs_kernels.cu) and the host driver (tvs_api.cu).
 // Nothing here is part of the ABI (see include/tvstokes.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,16 @@ struct GemmDesc2 {
   int M, N, K;
   int lda, ldb, ldc;
 };
+
+// TMA form of a pre-split GEMM: one 2D tensor map per operand plane (fp32 elements, 128-byte
+// swizzle, box {32, rows}, out-of-bounds elements read as zero).  Lives in device memory.
+struct alignas(64) TmaGemmDesc {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+  float *C;
+  int M, N, K, ldc;
+};
+// host: encode the four tensor maps of d for a tile of width bn
+cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn);
 
 // Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
 struct Geo {
@@ -106,6 +117,8 @@ cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cu
 cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN, int bn,
                            bool b_aligned, cudaStream_t s);
 cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int maxN, int bn,
+                            cudaStream_t s);
+cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
                               const float *qhat, int AT, int ldn, const double *rinv,
