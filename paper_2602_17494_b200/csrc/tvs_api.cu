@@ -241,6 +241,9 @@ struct tvs_ctx {
   // projection contractions: TVS_GEMM = tma (default: TMA + tcgen05 3xTF32), cpasync (cp.async +
   // tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
   bool gemm_tc = true, gemm_tma = true;
+  // y-solve variant: global fp64 z scratch (default; faster at config 3) or TVS_SOLVE=chunked
+  // (z checkpoints + chunk recompute in shared memory: less traffic, lower occupancy)
+  bool solve_v1 = true;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<PendingEv> pending;
@@ -470,8 +473,9 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.invN = std::max(B.invN, bo);
     B.fwd_flops += 2.0 * nt * bt * n1t;
     B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
-    // fp64 solve: read qhat (4) + rinv twice (16) + z write/read (16) + phx/phy (8)
-    B.solve_bytes += (double)nt * n1t * 44.0;
+    // solve, algorithmic bytes per (row, frequency): qhat 4 + pivots 8 + grad outputs 16 (hi/lo);
+    // the default variant also round-trips an fp64 z scratch (16 B) -- not counted
+    B.solve_bytes += (double)nt * n1t * 28.0;
   }
   TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
   TRY(upload(ctx, P.bufs, &B.d_inv, inv));
@@ -709,8 +713,13 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    return launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z, B.phx,
-                             B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
+    return ctx->solve_v1
+               ? launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
+                                   B.phx, B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr,
+                                   B.AP, s)
+               : launch_proj_solve2(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
+                                    B.phx, B.phy, tc ? B.phx_lo : nullptr,
+                                    tc ? B.phy_lo : nullptr, B.AP, s);
   }));
   TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
     return tma  ? launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
@@ -923,6 +932,8 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   const char *g = getenv("TVS_GEMM");
   c->gemm_tc = !(g && strcmp(g, "simt") == 0);
   c->gemm_tma = c->gemm_tc && !(g && strcmp(g, "cpasync") == 0);
+  const char *sv = getenv("TVS_SOLVE");
+  c->solve_v1 = !(sv && strcmp(sv, "chunked") == 0);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;

@@ -872,6 +872,102 @@ k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
   }
 }
 
+// Chunked form of the per-frequency y-solve (default): no global fp64 scratch.  The forward
+// substitution keeps z only at chunk boundaries (every SC rows, in shared memory); the backward
+// substitution recomputes each chunk's z (and caches its pivots) in shared memory from the
+// checkpoint, then back-substitutes it.  Global traffic per (row, frequency): qhat 2 x 4 B,
+// pivots 2 x 8 B (L2-resident, shared by the tiles of a layout row), outputs 16 B.
+constexpr int SC = 32;
+__global__ void k_proj_solve2(const ProjTile *__restrict__ tiles, int n2, int n1,
+                              const float *__restrict__ qhat, int AT, int ldn,
+                              const double *__restrict__ rinv, float *__restrict__ phx,
+                              float *__restrict__ phy, float *__restrict__ phx_lo,
+                              float *__restrict__ phy_lo, int AP, int nch) {
+  extern __shared__ double sm_solve[];
+  const int nth = blockDim.x, tid = threadIdx.x;
+  double *ck = sm_solve;                       // [nch][nth]: z_{cSC-1}
+  double *zc = ck + (size_t)nch * nth;         // [SC][nth]
+  double *rc = zc + (size_t)SC * nth;          // [SC][nth]
+  const int j = blockIdx.x * nth + tid;
+  const int tix = blockIdx.y;
+  if (j >= n1) return;
+  const ProjTile tl = tiles[tix];
+  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
+  const float *__restrict__ b = qhat + (size_t)tix * AT * ldn + j;
+  const size_t obase = (size_t)tix * AP * ldn + j - (size_t)po * ldn;
+  float *__restrict__ ox = phx + obase;
+  float *__restrict__ oy = phy + obase;
+  float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
+  float *__restrict__ oyl = phy_lo ? phy_lo + obase : nullptr;
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
+  if (j == 0) {   // L_y^dagger: D+_y u = prefix(b) - mu (y + 1)
+    double tot = 0.0;
+    for (int k = 0; k < nt; ++k) tot += (double)b[(size_t)k * ldn];
+    double mu = tot / (double)n2, pre = 0.0;
+    for (int k = 0; k < nout; ++k) {
+      pre += (double)b[(size_t)k * ldn];
+      const int y = tl.ty0 + k;
+      const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
+      if (k >= po) {
+        store_split(ox, oxl, (size_t)k * ldn, 0.0);
+        store_split(oy, oyl, (size_t)k * ldn, s2 * w);
+      }
+    }
+    return;
+  }
+  const double sg = 2.0 * sinpi((double)j / (2.0 * n1));
+  const double cx = -s2 * sg;
+  const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * ldn + j;
+  // forward sweep: checkpoints ck[c] = z_{c*SC - 1}
+  constexpr int U = 8;
+  double zp = (double)b[0];
+  int k = 1;
+  for (; k + U <= nt; k += U) {
+    float bv[U];
+    double rv[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      bv[q] = b[(size_t)(k + q) * ldn];
+      rv[q] = ri[(size_t)(k + q - 1) * ldn];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if ((k + q) % SC == 0) ck[(size_t)((k + q) / SC) * nth + tid] = zp;
+      zp = fma(-zp, rv[q], (double)bv[q]);
+    }
+  }
+  for (; k < nt; ++k) {
+    if (k % SC == 0) ck[(size_t)(k / SC) * nth + tid] = zp;
+    zp = fma(-zp, ri[(size_t)(k - 1) * ldn], (double)b[(size_t)k * ldn]);
+  }
+  // backward sweep, chunk by chunk from the bottom
+  double u_next = 0.0;
+  for (int c = (nt - 1) / SC; c >= 0; --c) {
+    const int k0 = c * SC, k1 = min(nt, k0 + SC);
+    double zprev = (c == 0) ? 0.0 : ck[(size_t)c * nth + tid];
+    double rprev = (c == 0) ? 0.0 : ri[(size_t)(k0 - 1) * ldn];
+#pragma unroll 8
+    for (int kk = k0; kk < k1; ++kk) {
+      const double r = ri[(size_t)kk * ldn];
+      const double z = fma(-zprev, rprev, (double)b[(size_t)kk * ldn]);
+      zc[(size_t)(kk - k0) * nth + tid] = z;
+      rc[(size_t)(kk - k0) * nth + tid] = r;
+      zprev = z;
+      rprev = r;
+    }
+    for (int kk = k1 - 1; kk >= k0; --kk) {
+      const double z = zc[(size_t)(kk - k0) * nth + tid], r = rc[(size_t)(kk - k0) * nth + tid];
+      const double u = (kk == nt - 1) ? z * r : (z - u_next) * r;
+      if (kk >= po && kk < nout) {
+        store_split(ox, oxl, (size_t)kk * ldn, cx * u);
+        // D+_y u = u_{k+1} - u_k; 0 on the global last row (T = S+ in y there)
+        store_split(oy, oyl, (size_t)kk * ldn, (kk == nt - 1) ? 0.0 : s2 * (u_next - u));
+      }
+      u_next = u;
+    }
+  }
+}
+
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
 constexpr int GBM = 128, GBN = 128, GBK = 8;
@@ -1085,6 +1181,23 @@ cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, 
 }
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s) {
   k_gemm<<<dim3((maxN + GBN - 1) / GBN, (maxM + GBM - 1) / GBM, batch), 256, 0, s>>>(descs);
+  return cudaGetLastError();
+}
+cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,
+                               const float *qhat, int AT, int ldn, const double *rinv, float *phx,
+                               float *phy, float *phx_lo, float *phy_lo, int AP, cudaStream_t s) {
+  const int nth = ntiles >= 16 ? 64 : 32;
+  const int nch = (AT + SC - 1) / SC;
+  const size_t smem = (size_t)(nch + 2 * SC) * nth * sizeof(double);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_proj_solve2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k_proj_solve2<<<dim3((n1 + nth - 1) / nth, ntiles), nth, smem, s>>>(
+      tiles, n2, n1, qhat, AT, ldn, rinv, phx, phy, phx_lo, phy_lo, AP, nch);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
