@@ -701,6 +701,191 @@ __global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *_
   }
 }
 
+// Streaming forms of the step-1 stencils (default): lane l owns the column pair
+// (c0 - 2 + 2l, c0 - 1 + 2l) of the subdomain-local grid, lanes 1..30 produce 60 output
+// columns, lane 0 / lane 31 are halo columns, and each warp walks RB rows with the next rows'
+// loads in flight (same scheme as k_sweep2v).
+constexpr int S1_OUT = 60, S1_RB = 32, S1_WARPS = 4;
+
+struct PairCtx {
+  int jA, jB;
+  bool SA, SB, PA, PB;
+  float xkA, xkB;
+};
+
+__device__ __forceinline__ float2 ld_pair(const float *__restrict__ base, int ld, int li, int rows,
+                                          const PairCtx &pc, bool okA, bool okB) {
+  float2 r = make_float2(0.f, 0.f);
+  if (li < 0 || li >= rows) return r;
+  const float *p = base + (size_t)li * ld + pc.jA;
+  if (okA && okB) return __ldg(reinterpret_cast<const float2 *>(p));
+  if (okA) r.x = __ldg(p);
+  if (okB) r.y = __ldg(p + 1);
+  return r;
+}
+
+// global-rule divergence of (vx, vy) for the lane's pair at row li, given vy of row li - 1
+__device__ __forceinline__ float2 div_pair(const PairCtx &pc, int gi, int n2, float2 vx, float2 vy,
+                                           float2 vym) {
+  const float leftA = __shfl_up_sync(0xffffffffu, vx.y, 1);
+  const float gy = (gi < n2 - 1) ? 1.f : 0.f;
+  return make_float2(pc.xkA * vx.x - leftA + gy * vy.x - vym.x,
+                     pc.xkB * vx.y - vx.x + gy * vy.y - vym.y);
+}
+
+// q = div_T E_{S+} multidiv E_S v on T (Alg. 5 pre-div)
+__global__ void __launch_bounds__(32 * S1_WARPS)
+k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v, int n2, int n1,
+           float *__restrict__ q, float *__restrict__ qlo) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int at = sd.ty1 - sd.y0 + 1, bt = sd.tx1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * S1_WARPS + threadIdx.y;
+  const int c0 = strip * S1_OUT;
+  if (c0 >= bt) return;
+  const int r0 = blockIdx.y * S1_RB;
+  if (r0 >= at) return;
+  const int r1 = min(at, r0 + S1_RB);
+  PairCtx pc;
+  pc.jA = c0 - 2 + 2 * lane;
+  pc.jB = pc.jA + 1;
+  pc.SA = pc.jA >= 0 && pc.jA < b;
+  pc.SB = pc.jB >= 0 && pc.jB < b;
+  pc.xkA = (sd.x0 + pc.jA < n1 - 1) ? 1.f : 0.f;
+  pc.xkB = (sd.x0 + pc.jB < n1 - 1) ? 1.f : 0.f;
+  const bool outA = lane >= 1 && lane <= 30 && pc.jA < bt;
+  const bool outB = lane >= 1 && lane <= 30 && pc.jB < bt;
+  const float *vb = v + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  const size_t pl = (size_t)g.A * g.ldS;
+  struct Row { float2 a11, a12, a21, a22; };
+  auto ldrow = [&](int li) {
+    Row r;
+    r.a11 = ld_pair(vb, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a12 = ld_pair(vb + pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a21 = ld_pair(vb + 2 * pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a22 = ld_pair(vb + 3 * pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    return r;
+  };
+  // w_k = div(v_k1, v_k2) at row li needs v_k2 at li - 1
+  Row pm = ldrow(r0 - 2), c = ldrow(r0 - 1);
+  float2 w2p = div_pair(pc, sd.y0 + r0 - 1, n2, c.a21, c.a22, pm.a22);   // w_2 at row r0 - 1
+  Row n = ldrow(r0);
+  const int qo = sd.x0 & 3;
+  float *qb = q + (size_t)blockIdx.z * g.AT * g.ldT + qo;
+  float *qlb = qlo ? qlo + (size_t)blockIdx.z * g.AT * g.ldT + qo : nullptr;
+  for (int li = r0; li < r1; ++li) {
+    const Row m = ldrow(li + 1);
+    const int gi = sd.y0 + li;
+    const float2 w1 = div_pair(pc, gi, n2, n.a11, n.a12, c.a12);
+    const float2 w2 = div_pair(pc, gi, n2, n.a21, n.a22, c.a22);
+    const float w1left = __shfl_up_sync(0xffffffffu, w1.y, 1);
+    const float gxA = (sd.x0 + pc.jA > 0) ? 1.f : 0.f;
+    const float gyk = (gi < n2 - 1) ? 1.f : 0.f, gyp = (gi > 0) ? 1.f : 0.f;
+    const float qA = pc.xkA * w1.x - gxA * w1left + gyk * w2.x - gyp * w2p.x;
+    const float qB = pc.xkB * w1.y - w1.x + gyk * w2.y - gyp * w2p.y;
+    const size_t o = (size_t)li * g.ldT + pc.jA;
+    if (outA) store_split(qb, qlb, o, qA);
+    if (outB) store_split(qb, qlb, o + 1, qB);
+    w2p = w2;
+    c = n;
+    n = m;
+  }
+}
+
+// Kernel (a') streaming form: rho_k = w_k - grad phi_k - omega0_k on S+, psi_k = grad rho_k,
+// row-wise ball update of (v_k1, v_k2) (Alg. 5)
+__global__ void __launch_bounds__(32 * S1_WARPS)
+k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+          const float *__restrict__ thx, const float *__restrict__ vin,
+          const float *__restrict__ gphi, int ldg, const float *__restrict__ om,
+          float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * S1_WARPS + threadIdx.y;
+  const int c0 = strip * S1_OUT;
+  if (c0 >= b) return;
+  const int r0 = blockIdx.y * S1_RB;
+  if (r0 >= a) return;
+  const int r1 = min(a, r0 + S1_RB);
+  PairCtx pc;
+  pc.jA = c0 - 2 + 2 * lane;
+  pc.jB = pc.jA + 1;
+  pc.SA = pc.jA >= 0 && pc.jA < b;
+  pc.SB = pc.jB >= 0 && pc.jB < b;
+  pc.PA = pc.jA >= 0 && pc.jA < bp;
+  pc.PB = pc.jB >= 0 && pc.jB < bp;
+  pc.xkA = (sd.x0 + pc.jA < n1 - 1) ? 1.f : 0.f;
+  pc.xkB = (sd.x0 + pc.jB < n1 - 1) ? 1.f : 0.f;
+  const bool outA = lane >= 1 && lane <= 30 && pc.jA < b;
+  const bool outB = lane >= 1 && lane <= 30 && pc.jB < b;
+  const float *vb = vin + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  float *ob = vout + (size_t)blockIdx.z * 4 * g.A * g.ldS;
+  const size_t pl = (size_t)g.A * g.ldS;
+  const float *g1 = gphi + ((size_t)0 * g.M + blockIdx.z) * g.AP * ldg;
+  const float *g2 = gphi + ((size_t)1 * g.M + blockIdx.z) * g.AP * ldg;
+  const float *o1 = om + ((size_t)blockIdx.z * 2 + 0) * g.AP * g.ldP;
+  const float *o2 = om + ((size_t)blockIdx.z * 2 + 1) * g.AP * g.ldP;
+  const float thA = pc.SA ? thx[sd.ix * g.B + pc.jA] : 0.f;
+  const float thB = pc.SB ? thx[sd.ix * g.B + pc.jB] : 0.f;
+  struct Row { float2 a11, a12, a21, a22, h1, h2; };   // h_k = grad phi_k + omega0_k
+  auto ldrow = [&](int li) {
+    Row r;
+    r.a11 = ld_pair(vb, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a12 = ld_pair(vb + pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a21 = ld_pair(vb + 2 * pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    r.a22 = ld_pair(vb + 3 * pl, g.ldS, li, a, pc, pc.SA, pc.SB);
+    const float2 ga = ld_pair(g1, ldg, li, ap, pc, pc.PA, pc.PB);
+    const float2 gb = ld_pair(g2, ldg, li, ap, pc, pc.PA, pc.PB);
+    const float2 oa = ld_pair(o1, g.ldP, li, ap, pc, pc.PA, pc.PB);
+    const float2 obb = ld_pair(o2, g.ldP, li, ap, pc, pc.PA, pc.PB);
+    r.h1 = make_float2(ga.x + oa.x, ga.y + oa.y);
+    r.h2 = make_float2(gb.x + obb.x, gb.y + obb.y);
+    return r;
+  };
+  auto rho = [&](int li, const Row &r, float2 v12m, float2 v22m, float2 &r1o, float2 &r2o) {
+    const int gi = sd.y0 + li;
+    const float2 w1 = div_pair(pc, gi, n2, r.a11, r.a12, v12m);
+    const float2 w2 = div_pair(pc, gi, n2, r.a21, r.a22, v22m);
+    const bool row_ok = li < ap;
+    r1o = make_float2((row_ok && pc.PA) ? w1.x - r.h1.x : 0.f, (row_ok && pc.PB) ? w1.y - r.h1.y : 0.f);
+    r2o = make_float2((row_ok && pc.PA) ? w2.x - r.h2.x : 0.f, (row_ok && pc.PB) ? w2.y - r.h2.y : 0.f);
+  };
+  Row c = ldrow(r0), n = ldrow(r0 + 1);
+  const Row pr = ldrow(r0 - 1);
+  float2 rc1, rc2;
+  rho(r0, c, pr.a12, pr.a22, rc1, rc2);
+  for (int li = r0; li < r1; ++li) {
+    const Row m = ldrow(li + 2);
+    float2 rn1, rn2;
+    rho(li + 1, n, c.a12, c.a22, rn1, rn2);
+    const float rr1 = __shfl_down_sync(0xffffffffu, rc1.x, 1);
+    const float rr2 = __shfl_down_sync(0xffffffffu, rc2.x, 1);
+    const bool xa = pc.jA + 1 < bp, xb = pc.jB + 1 < bp, yd = li + 1 < ap;
+    const float ty = thy[sd.iy * g.A + li];
+    // channel 1: (v11, v12); channel 2: (v21, v22)
+    float2 a11 = c.a11, a12 = c.a12, a21 = c.a21, a22 = c.a22;
+    ball_update_fast(ty * thA, t, xa ? rc1.y - rc1.x : 0.f, yd ? rn1.x - rc1.x : 0.f, a11.x, a12.x);
+    ball_update_fast(ty * thB, t, xb ? rr1 - rc1.y : 0.f, yd ? rn1.y - rc1.y : 0.f, a11.y, a12.y);
+    ball_update_fast(ty * thA, t, xa ? rc2.y - rc2.x : 0.f, yd ? rn2.x - rc2.x : 0.f, a21.x, a22.x);
+    ball_update_fast(ty * thB, t, xb ? rr2 - rc2.y : 0.f, yd ? rn2.y - rc2.y : 0.f, a21.y, a22.y);
+    const size_t o = (size_t)li * g.ldS + pc.jA;
+    if (outA && outB) {
+      *reinterpret_cast<float2 *>(ob + o) = a11;
+      *reinterpret_cast<float2 *>(ob + pl + o) = a12;
+      *reinterpret_cast<float2 *>(ob + 2 * pl + o) = a21;
+      *reinterpret_cast<float2 *>(ob + 3 * pl + o) = a22;
+    } else {
+      if (outA) { ob[o] = a11.x; ob[pl + o] = a12.x; ob[2 * pl + o] = a21.x; ob[3 * pl + o] = a22.x; }
+      if (outB) { ob[o + 1] = a11.y; ob[pl + o + 1] = a12.y; ob[2 * pl + o + 1] = a21.y; ob[3 * pl + o + 1] = a22.y; }
+    }
+    c = n;
+    n = m;
+    rc1 = rn1;
+    rc2 = rn2;
+  }
+}
+
 // ----------------------------------------------------------------------------- projection (b)
 //
 // phi = R_T Delta^dagger E_T q (Eq. locglobprojpart3/invLaplLowCapLong),
@@ -1151,7 +1336,14 @@ cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const f
 }
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
                            float *qlo, cudaStream_t s) {
-  k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
+  static const bool naive = getenv("TVS_STENCIL1") && strcmp(getenv("TVS_STENCIL1"), "naive") == 0;
+  if (naive) {
+    k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
+  } else {
+    const int strips = (g.BT + S1_OUT - 1) / S1_OUT;
+    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + S1_RB - 1) / S1_RB, g.M);
+    k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
@@ -1164,8 +1356,16 @@ cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, 
 cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *gphi, int ldg, const float *om,
                           float *vout, int n2, int n1, float t, cudaStream_t s) {
-  k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
-                                                               ldg, om, vout, n2, n1, t);
+  static const bool naive = getenv("TVS_STENCIL1") && strcmp(getenv("TVS_STENCIL1"), "naive") == 0;
+  if (naive) {
+    k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
+                                                                 ldg, om, vout, n2, n1, t);
+  } else {
+    const int strips = (g.B + S1_OUT - 1) / S1_OUT;
+    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + S1_RB - 1) / S1_RB, g.M);
+    k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
+                                                  n2, n1, t);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,
