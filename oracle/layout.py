@@ -91,3 +91,9 @@ class Layout:
         if not extended:
             th = th[:self.n2, :self.n1]
         return th
+
+    def theta_rect(self, m, extended):
+        """theta_m restricted to its own rectangle Gamma_m (the same products as ``theta``)."""
+        a, b = m
+        (y0, y1), (x0, x1) = self.rect(m, extended)
+        return self.ty[a][y0:y1 + 1, None] * self.tx[b][None, x0:x1 + 1]

@@ -157,11 +157,21 @@ def _irv2_inner_local(m, lay, p, f, qhat_m, inner, t):
     n2, n1 = lay.n2, lay.n1
     s = lay.rect(m, extended=False)
     sp = rect_plus(s, n2, n1)
-    th = restrict(lay.theta(m, extended=False), full_rect(n2, n1), s)
+    th = lay.theta_rect(m, extended=False)
     p_s = restrict(p, full_rect(n2, n1), s)
     omega0 = (restrict(f - ops.div(p), full_rect(n2, n1), sp)
               + ops.div(extend(th * p_s, s, sp)))
-    v = np.array(qhat_m, np.float64)
+    return irv2_local_iterations(lay, m, omega0, qhat_m, inner, t)
+
+
+def irv2_local_iterations(lay, m, omega0, v0, inner, t):
+    """The inner loop of the localized Alg. 3 given omega0 on S+ = R_{S+}(...):
+    ``inner`` times psi = R_S grad_{S+}(div_{S+} E v - omega0); v <- (theta v + t theta psi) /
+    (theta + t |psi|).  Only arrays on S / S+ are touched."""
+    s = lay.rect(m, extended=False)
+    sp = rect_plus(s, lay.n2, lay.n1)
+    th = lay.theta_rect(m, extended=False)
+    v = np.array(v0, np.float64)
     for _ in range(inner):
         u = ops.div(extend(v, s, sp)) - omega0
         psi = restrict(ops.grad(u), sp, s)
@@ -229,7 +239,7 @@ def _tfs_inner_local(m, lay, p, r_global, qhat_m, inner, t):
     s = lay.rect(m, extended=True)
     sp = rect_plus(s, n2t, n1t)
     whole = full_rect(n2t, n1t)
-    th = restrict(lay.theta(m, extended=True), whole, s)
+    th = lay.theta_rect(m, extended=True)
     tp = th * restrict(p, whole, s)
     w_m = ops.multidiv(extend(tp, s, sp))
     omega0 = restrict(r_global, whole, sp) + local_projection(w_m, sp, n2t, n1t, cy, cx)

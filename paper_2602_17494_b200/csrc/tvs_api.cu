@@ -241,9 +241,9 @@ struct tvs_ctx {
   // projection contractions: TVS_GEMM = tma (default: TMA + tcgen05 3xTF32), cpasync (cp.async +
   // tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
   bool gemm_tc = true, gemm_tma = true;
-  // y-solve variant: global fp64 z scratch (default; faster at config 3) or TVS_SOLVE=chunked
-  // (z checkpoints + chunk recompute in shared memory: less traffic, lower occupancy)
-  bool solve_v1 = true;
+  // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
+  // thread per frequency, fp64 z scratch) or TVS_SOLVE=chunked (z checkpoints in shared memory)
+  int solve_impl = 3;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<PendingEv> pending;
@@ -713,7 +713,11 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    return ctx->solve_v1
+    if (ctx->solve_impl == 3)
+      return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
+                                reinterpret_cast<float *>(B.z), B.phx, B.phy,
+                                tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
+    return ctx->solve_impl == 1
                ? launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
                                    B.phx, B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr,
                                    B.AP, s)
@@ -933,7 +937,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->gemm_tc = !(g && strcmp(g, "simt") == 0);
   c->gemm_tma = c->gemm_tc && !(g && strcmp(g, "cpasync") == 0);
   const char *sv = getenv("TVS_SOLVE");
-  c->solve_v1 = !(sv && strcmp(sv, "chunked") == 0);
+  c->solve_impl = sv && strcmp(sv, "chunked") == 0 ? 2 : sv && strcmp(sv, "serial") == 0 ? 1 : 3;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;

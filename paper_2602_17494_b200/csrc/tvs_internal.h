@@ -123,6 +123,11 @@ cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int m
 cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *phx,
                                float *phy, float *phx_lo, float *phy_lo, int AP, cudaStream_t s);
+// segmented y-solve (default): fp32 z scratch [tile][AT][ldn]
+cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
+                               const float *qhat, int AT, int ldn, const double *rinv, float *z,
+                               float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
+                               cudaStream_t s);
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
                               const float *qhat, int AT, int ldn, const double *rinv,
                               double *z, float *phx, float *phy, float *phx_lo, float *phy_lo,

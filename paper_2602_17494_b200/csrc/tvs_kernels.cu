@@ -4,6 +4,7 @@
 // use the uniform geometry of tvs::Geo (see tvs_internal.h).
 #include "tvs_internal.h"
 
+#include <algorithm>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1153,6 +1154,229 @@ __global__ void k_proj_solve2(const ProjTile *__restrict__ tiles, int n2, int n1
   }
 }
 
+// Segmented form of the per-frequency y-solve (default).  Both Thomas sweeps are first-order
+// linear recurrences in the precomputed pivots r_k = 1/e_k:
+//   forward   z_k = b_k - r_{k-1} z_{k-1}         (z_0 = b_0)
+//   backward  u_k = r_k (z_k - u_{k+1})           (u_nt = 0)
+// so the rows of T are cut into nseg segments per frequency (one warp per segment, 32 frequencies
+// per CTA): every segment runs its recurrence from a zero carry and records (end value, product of
+// coefficients); one fp64 scan over the segments in shared memory gives every segment its exact
+// carry; the segment then re-runs with it.  Same operator as one serial sweep, different rounding
+// order.  z is kept in an fp32 scratch: its rounding moves grad phi by < 1e-7 of max|grad phi|
+// (flat in N).  j = 0 (singular Neumann L_y^dagger) uses the same skeleton for
+// its prefix sums: D+_y u = prefix(b) - mu (y + 1), mu = sum(b) / n2.
+constexpr int SJB = 32, SSEG_MAX = 16, SU = 8;
+// SMEM = true: the CTA's column block of qhat is staged in shared memory by the first pass and
+// overwritten in place by z (fp32), so qhat is read from HBM once and z never leaves the SM
+// (AT x 128 B of dynamic shared memory; used when that fits).  SMEM = false: z in a global
+// scratch.
+template <bool SMEM>
+__global__ void __launch_bounds__(SJB *SSEG_MAX)
+k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
+              int AT, int ldn, const double *__restrict__ rinv, float *__restrict__ zs,
+              float *__restrict__ phx, float *__restrict__ phy, float *__restrict__ phx_lo,
+              float *__restrict__ phy_lo, int AP) {
+  __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
+  __shared__ double sh_tot[SJB];
+  extern __shared__ float sbuf[];   // SMEM: [AT][SJB]
+  const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
+  const int j = blockIdx.x * SJB + tx;
+  const int tix = blockIdx.y;
+  const bool valid = j < n1;
+  const ProjTile tl = tiles[tix];
+  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
+  const int LS = (nt + nseg - 1) / nseg;
+  const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
+  const int jj = valid ? j : 0;
+  const size_t st = (size_t)ldn;   // row stride of every global plane
+  const float *__restrict__ b = qhat + (size_t)tix * AT * st + jj;
+  const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * st + jj;
+  // z (and, in SMEM mode, the staged b) live at zb with row stride zst
+  float *zb = SMEM ? sbuf + tx : zs + (size_t)tix * AT * st + jj;
+  const size_t zst = SMEM ? (size_t)SJB : st;
+  const float *bb = SMEM ? zb : b;   // second read of b
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;   // s_j^2 (Eq. form:DCTmat normalisation)
+
+  // ---- forward, local pass from a zero carry: end value a and coefficient product g
+  double a = 0.0, g = 1.0;
+  if (valid) {
+    if (j == 0) {
+      const float *bp = b + (size_t)k0 * st;
+      for (int k = k0; k < k1; ++k, bp += st) {
+        const float bk = *bp;
+        if constexpr (SMEM) zb[(size_t)k * zst] = bk;
+        a += (double)bk;
+      }
+    } else {
+      int k = k0;
+      if (k == 0 && k < k1) {   // z_0 = b_0 (no coupling above row 0 of T)
+        const float b0 = b[0];
+        if constexpr (SMEM) zb[0] = b0;
+        a = (double)b0;
+        g = 0.0;
+        k = 1;
+      }
+      const float *bp = b + (size_t)k * st;
+      const double *rp = ri + (size_t)(k - 1) * st;
+      for (; k + SU <= k1; k += SU, bp += SU * st, rp += SU * st) {
+        float bv[SU];
+        double rv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {   // the whole batch of loads first (latency-bound)
+          bv[u] = bp[u * st];
+          rv[u] = rp[u * st];
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          if constexpr (SMEM) zb[(size_t)(k + u) * zst] = bv[u];
+          a = fma(-rv[u], a, (double)bv[u]);
+          g *= -rv[u];
+        }
+      }
+      for (; k < k1; ++k, bp += st, rp += st) {
+        const double r = *rp;
+        const float bk = *bp;
+        if constexpr (SMEM) zb[(size_t)k * zst] = bk;
+        a = fma(-r, a, (double)bk);
+        g *= -r;
+      }
+    }
+  }
+  sh_a[sg][tx] = a;
+  sh_c[sg][tx] = g;
+  __syncthreads();
+  if (sg == 0) {   // carry into segment s: Z_{s-1};  Z_s = a_s + g_s Z_{s-1}
+    double Z = 0.0;
+    for (int s = 0; s < nseg; ++s) {
+      const double as = sh_a[s][tx], gs = sh_c[s][tx];
+      sh_c[s][tx] = Z;
+      Z = fma(gs, Z, as);
+    }
+    sh_tot[tx] = Z;
+  }
+  __syncthreads();
+  const double fcarry = sh_c[sg][tx];
+
+  // ---- forward, final pass with the exact carry: z (fp32)
+  if (valid && j > 0 && k0 < k1) {
+    double zc = fcarry;
+    int k = k0;
+    if (k == 0) {
+      zc = (double)bb[0];
+      zb[0] = (float)zc;
+      k = 1;
+    }
+    const float *bp = bb + (size_t)k * zst;
+    const double *rp = ri + (size_t)(k - 1) * st;
+    float *zp = zb + (size_t)k * zst;
+    for (; k + SU <= k1; k += SU, bp += SU * zst, rp += SU * st, zp += SU * zst) {
+      float bv[SU];
+      double rv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        bv[u] = bp[u * zst];
+        rv[u] = rp[u * st];
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        zc = fma(-rv[u], zc, (double)bv[u]);
+        zp[u * zst] = (float)zc;
+      }
+    }
+    for (; k < k1; ++k, bp += zst, rp += st, zp += zst) {
+      zc = fma(-*rp, zc, (double)*bp);
+      *zp = (float)zc;
+    }
+  }
+  // ---- backward, local pass from a zero carry (u_{k1} = 0)
+  a = 0.0;
+  g = 1.0;
+  if (valid && j > 0 && k0 < k1) {
+    int k = k1 - 1;
+    const float *zp = zb + (size_t)k * zst;
+    const double *rp = ri + (size_t)k * st;
+    for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst, rp -= SU * st) {
+      float zv[SU];
+      double rv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        zv[u] = zp[-(ptrdiff_t)(u * zst)];
+        rv[u] = rp[-(ptrdiff_t)(u * st)];
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        a = rv[u] * ((double)zv[u] - a);
+        g *= -rv[u];
+      }
+    }
+    for (; k >= k0; --k, zp -= zst, rp -= st) {
+      const double r = *rp;
+      a = r * ((double)*zp - a);
+      g *= -r;
+    }
+  }
+  __syncthreads();   // every thread has read its forward carry
+  sh_a[sg][tx] = a;
+  sh_c[sg][tx] = g;
+  __syncthreads();
+  if (sg == 0) {   // carry into segment s from below: U_{s+1};  U_s = a_s + g_s U_{s+1}
+    double U = 0.0;
+    for (int s = nseg - 1; s >= 0; --s) {
+      const double as = sh_a[s][tx], gs = sh_c[s][tx];
+      sh_c[s][tx] = U;
+      U = fma(gs, U, as);
+    }
+  }
+  __syncthreads();
+  if (!valid || k0 >= k1) return;
+  const size_t obase = (size_t)tix * AP * st + jj - (size_t)po * st;
+  float *__restrict__ ox = phx + obase;
+  float *__restrict__ oy = phy + obase;
+  float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
+  float *__restrict__ oyl = phy_lo ? phy_lo + obase : nullptr;
+  if (j == 0) {   // L_y^dagger: D+_y u = prefix(b) - mu (y + 1), mu = sum(b) / n2
+    const double mu = sh_tot[tx] / (double)n2;
+    double pre = fcarry;
+    for (int k = k0; k < min(k1, nout); ++k) {
+      pre += (double)bb[(size_t)k * zst];
+      const int y = tl.ty0 + k;
+      const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
+      if (k >= po) {
+        store_split(ox, oxl, (size_t)k * st, 0.0);
+        store_split(oy, oyl, (size_t)k * st, s2 * w);
+      }
+    }
+    return;
+  }
+  const double sg_j = 2.0 * sinpi((double)j / (2.0 * n1));
+  const double cx = -s2 * sg_j;
+  // ---- backward, final pass with the exact carry; outputs on rows [po, nout)
+  double un = sh_c[sg][tx];
+  int k = k1 - 1;
+  const float *zp = zb + (size_t)k * zst;
+  const double *rp = ri + (size_t)k * st;
+  auto emit = [&](int kk, double uk) {
+    if (kk >= po && kk < nout) {
+      store_split(ox, oxl, (size_t)kk * st, cx * uk);
+      // D+_y u = u_{k+1} - u_k; 0 on the global last row (T = S+ in y there)
+      store_split(oy, oyl, (size_t)kk * st, (kk == nt - 1) ? 0.0 : s2 * (un - uk));
+    }
+    un = uk;
+  };
+  for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst, rp -= SU * st) {
+    float zv[SU];
+    double rv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      zv[u] = zp[-(ptrdiff_t)(u * zst)];
+      rv[u] = rp[-(ptrdiff_t)(u * st)];
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) emit(k - u, rv[u] * ((double)zv[u] - un));
+  }
+  for (; k >= k0; --k, zp -= zst, rp -= st) emit(k, *rp * ((double)*zp - un));
+}
+
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
 constexpr int GBM = 128, GBN = 128, GBK = 8;
@@ -1398,6 +1622,30 @@ cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1
   }
   k_proj_solve2<<<dim3((n1 + nth - 1) / nth, ntiles), nth, smem, s>>>(
       tiles, n2, n1, qhat, AT, ldn, rinv, phx, phy, phx_lo, phy_lo, AP, nch);
+  return cudaGetLastError();
+}
+cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
+                               const float *qhat, int AT, int ldn, const double *rinv, float *z,
+                               float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
+                               cudaStream_t s) {
+  // one warp per segment of ~32 rows, at most SSEG_MAX segments (the max tile height AT decides)
+  const int nseg = std::min(SSEG_MAX, std::max(1, (AT + 31) / 32));
+  const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);
+  const size_t smem = (size_t)AT * SJB * sizeof(float);
+  if (smem <= 160 * 1024) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaError_t e = cudaFuncSetAttribute(k_proj_solve3<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    k_proj_solve3<true><<<grid, block, smem, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
+                                                   phx_lo, phy_lo, AP);
+  } else {
+    k_proj_solve3<false><<<grid, block, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
+                                                 phx_lo, phy_lo, AP);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
