@@ -181,6 +181,7 @@ struct ProjBatch {
   GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
   GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
   TmaGemmDesc *d_fwd3 = nullptr, *d_inv3 = nullptr;   // same, TMA tensor maps
+  TmaGemmDesc *d_fwd4 = nullptr, *d_inv4 = nullptr;   // persistent: A as one fp32 plane
   GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
   int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
@@ -238,9 +239,12 @@ struct tvs_ctx {
   std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
   std::map<int, std::unique_ptr<Tables>> tables;
   bool profiling = false;
-  // projection contractions: TVS_GEMM = tma (default: TMA + tcgen05 3xTF32), cpasync (cp.async +
+  // projection contractions: TVS_GEMM = persistent (default: TMA + tcgen05 3xTF32, A split in
+  // shared memory, overlapped epilogue), tma (pre-split hi/lo operand planes), cpasync (cp.async +
   // tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
-  bool gemm_tc = true, gemm_tma = true;
+  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3 };
+  int gemm = G_PERSIST;
+  bool presplit() const { return gemm == G_CPASYNC || gemm == G_TMA; }
   // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
   // thread per frequency, fp64 z scratch) or TVS_SOLVE=chunked (z checkpoints in shared memory)
   int solve_impl = 3;
@@ -489,6 +493,13 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
   TRY(upload(ctx, P.bufs, &B.d_fwd3, fwd3));
   TRY(upload(ctx, P.bufs, &B.d_inv3, inv3));
+  // persistent kernel: the A operand is the single fp32 plane (split in shared memory)
+  for (auto &d : fwd2) d.Alo = nullptr;
+  for (auto &d : inv2) d.Alo = nullptr;
+  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
+  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
+  TRY(upload(ctx, P.bufs, &B.d_fwd4, fwd3));
+  TRY(upload(ctx, P.bufs, &B.d_inv4, inv3));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   CK(cudaDeviceSynchronize());
   return TVS_OK;
@@ -704,12 +715,15 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
 // global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
 tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
-  const bool tc = ctx->gemm_tc;
-  const bool tma = ctx->gemm_tma;
+  const bool tc = ctx->presplit();   // solve writes hi/lo planes
+  const int gm = ctx->gemm;
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
-    return tma  ? launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
-           : tc ? launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s)
-                : launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
+    switch (gm) {
+      case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
+      case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
+      case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
+      default: return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
+    }
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
@@ -726,9 +740,12 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
                                     tc ? B.phy_lo : nullptr, B.AP, s);
   }));
   TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
-    return tma  ? launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
-           : tc ? launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s)
-                : launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
+    switch (gm) {
+      case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+      case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+      case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+      default: return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
+    }
   }));
   return TVS_OK;
 }
@@ -843,7 +860,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   const Geo g = P->geo;
   const int G2 = P->G2, G1 = P->G1, ld = P->ld;
   const size_t pl = (size_t)G2 * ld;
-  const bool tc = ctx->gemm_tc;
+  const bool tc = ctx->presplit();   // operand planes pre-split into hi/lo
   CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
   // f = delta^{-1} P tau_0 (tau_0 pre-projected, reading A1)
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_tau0(d0, n2, n1, P->t0, ld, s); }));
@@ -934,8 +951,11 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->rank = rank;
   c->world = world;
   const char *g = getenv("TVS_GEMM");
-  c->gemm_tc = !(g && strcmp(g, "simt") == 0);
-  c->gemm_tma = c->gemm_tc && !(g && strcmp(g, "cpasync") == 0);
+  c->gemm = !g                          ? tvs_ctx::G_PERSIST
+            : strcmp(g, "simt") == 0    ? tvs_ctx::G_SIMT
+            : strcmp(g, "cpasync") == 0 ? tvs_ctx::G_CPASYNC
+            : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
+                                        : tvs_ctx::G_PERSIST;
   const char *sv = getenv("TVS_SOLVE");
   c->solve_impl = sv && strcmp(sv, "chunked") == 0 ? 2 : sv && strcmp(sv, "serial") == 0 ? 1 : 3;
   cudaError_t e = cudaSetDevice(device);
@@ -1133,7 +1153,27 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
       {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
   TRY(upload(ctx, own, &dd, desc));
   cudaError_t e;
-  if (impl == 3 || impl == 4) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
+  if (impl == 5) {   // persistent TMA kernel: A as one fp32 plane, split in shared memory
+    auto rna = [](float x) {
+      uint32_t u;
+      memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      float h;
+      memcpy(&h, &u, 4);
+      return h;
+    };
+    std::vector<float> Bh(Bt.size()), Bl(Bt.size());
+    for (size_t i = 0; i < Bt.size(); ++i) { Bh[i] = rna(Bt[i]); Bl[i] = Bt[i] - Bh[i]; }
+    float *dBh, *dBl;
+    TRY(upload(ctx, own, &dBh, Bh));
+    TRY(upload(ctx, own, &dBl, Bl));
+    GemmDesc2 g2 = {dA, nullptr, dBh, dBl, dC, M, N, K, lda, lda, N};
+    std::vector<TmaGemmDesc> d3(1);
+    CK(make_tma_desc(&d3[0], g2, 144));
+    TmaGemmDesc *dd3;
+    TRY(upload(ctx, own, &dd3, d3));
+    e = launch_gemm_tma_p(dd3, 1, M, N, 144, 0);
+  } else if (impl == 3 || impl == 4) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
     auto rna = [](float x) {
       uint32_t u;
       memcpy(&u, &x, 4);

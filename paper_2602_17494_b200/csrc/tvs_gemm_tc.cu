@@ -635,7 +635,243 @@ static cudaError_t launch_tma(const TmaGemmDesc *descs, int batch, int maxM, int
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent form (default): one CTA per SM loops over the (desc, m-block, n-block) tiles.
+// Warp roles (10 warps):
+//   warp 0      TMA producer: A (raw fp32, one plane) + B_hi + B_lo per K slice of 32
+//   warps 6..9  split A in shared memory: hi = tf32_rna(a) in place, lo = a - hi (exact), then
+//               fence.proxy.async so the tensor core sees the generic-proxy stores
+//   warp 1      MMA issuer: 4 k-steps x 3 tcgen05.mma per stage into one of two TMEM accumulators
+//   warps 2..5  epilogue: tcgen05.ld of the finished accumulator (warp w owns TMEM lanes
+//               32 (w % 4) ..), float4 stores; it overlaps the next tile's main loop.
+// The A operand therefore streams from HBM/L2 once, in fp32 (half the bytes of pre-split hi/lo
+// planes); B (DCT tables, L2-resident) stays pre-split.  Same arithmetic as k_gemm_tma.
+constexpr int PSTAGES = 3, PNT = 320;
+
+template <int BN>
+struct PSmem {
+  static constexpr int A_BYTES = BM * TBK * 4;                 // 16 KB
+  static constexpr int B_BYTES = BN * TBK * 4;                 // 18 KB for BN = 144
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;      // A (-> hi), A lo, B hi, B lo
+  static constexpr int TX = A_BYTES + 2 * B_BYTES;             // bytes landed by TMA per stage
+  static constexpr int TOTAL = PSTAGES * STAGE + 256 + 1024;
+  static constexpr int ACC = BN <= 128 ? 128 : 256;            // TMEM columns per accumulator
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(PNT, 1)
+k_gemm_tma_p(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int nblocks) {
+  using SM = PSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + PSTAGES * SM::STAGE);
+  uint64_t *conv = full + PSTAGES;
+  uint64_t *empty = conv + PSTAGES;
+  uint64_t *accf = empty + PSTAGES;   // [2]
+  uint64_t *acce = accf + 2;          // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(2 * SM::ACC));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  const int per = mblocks * nblocks, ntiles = batch * per;
+  // tile decode shared by every role (n fastest: neighbouring CTAs share the A rows)
+  auto decode = [&](int t, const TmaGemmDesc *&dp, int &m0, int &n0) {
+    const int z = t / per, r = t - z * per;
+    dp = descs + z;
+    m0 = (r / nblocks) * BM;
+    n0 = (r % nblocks) * BN;
+    return m0 < dp->M && n0 < dp->N;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TmaGemmDesc *dp;
+        int m0, n0;
+        if (!decode(t, dp, m0, n0)) continue;
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int s = it % PSTAGES;
+          if (it >= PSTAGES) mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
+          mbar_expect_tx(&full[s], SM::TX);
+          const uint32_t st = sbase + s * SM::STAGE;
+          tma_load_2d(st, &dp->a_hi, kt * TBK, m0, &full[s]);
+          tma_load_2d(st + 2 * SM::A_BYTES, &dp->b_hi, kt * TBK, n0, &full[s]);
+          tma_load_2d(st + 2 * SM::A_BYTES + SM::B_BYTES, &dp->b_lo, kt * TBK, n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ------------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC = make_idesc(BM, BN);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TmaGemmDesc *dp;
+        int m0, n0;
+        if (!decode(t, dp, m0, n0)) continue;
+        const int b = tc & 1;
+        if (tc >= 2) mbar_wait(&acce[b], ((tc >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + (uint32_t)(b * SM::ACC);
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int s = it % PSTAGES;
+          mbar_wait(&conv[s], (it / PSTAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = sbase + s * SM::STAGE;
+          const uint32_t ahi = st, alo = st + SM::A_BYTES;
+          const uint32_t bhi = st + 2 * SM::A_BYTES, blo = bhi + SM::B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < TBK / 8; ++ks) {
+            const uint64_t dah = make_desc_sw128(ahi + 32 * ks), dal = make_desc_sw128(alo + 32 * ks);
+            const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
+            mma_tf32(acc, dal, dbh, IDESC, (kt > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(acc, dah, dbl, IDESC, 1u);
+            mma_tf32(acc, dah, dbh, IDESC, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf[b]);
+        ++tc;
+      }
+    }
+  } else if (warp >= 6) {   // ----------------------------------------------- A split
+    const int ct = tid - 6 * 32;   // 0..127
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TmaGemmDesc *dp;
+      int m0, n0;
+      if (!decode(t, dp, m0, n0)) continue;
+      const int nk = (dp->K + TBK - 1) / TBK;
+      for (int kt = 0; kt < nk; ++kt, ++it) {
+        const int s = it % PSTAGES;
+        mbar_wait(&full[s], (it / PSTAGES) & 1);
+        float4 *a = reinterpret_cast<float4 *>(smem + s * SM::STAGE);
+        float4 *lo = reinterpret_cast<float4 *>(smem + s * SM::STAGE + SM::A_BYTES);
+#pragma unroll
+        for (int q = 0; q < SM::A_BYTES / 16 / 128; ++q) {   // element-wise: layout agnostic
+          const int i = ct + q * 128;
+          float4 x = a[i], h, l;
+          split(x.x, h.x, l.x);
+          split(x.y, h.y, l.y);
+          split(x.z, h.z, l.z);
+          split(x.w, h.w, l.w);
+          a[i] = h;
+          lo[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ct == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else {   // warps 2..5 ------------------------------------------------------ epilogue
+    const int q4 = warp & 3;   // TMEM lane quarter this warp may access
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TmaGemmDesc *dp;
+      int m0, n0;
+      if (!decode(t, dp, m0, n0)) continue;
+      const int b = tc & 1;
+      mbar_wait(&accf[b], (tc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int M = dp->M, N = dp->N, ldc = dp->ldc;
+      float *C = dp->C;
+      const int row = m0 + q4 * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * SM::ACC + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+          float *out = C + (size_t)row * ldc + n0 + c0;
+          const int nvalid = N - (n0 + c0);
+          if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<float4 *>(out)[q] =
+                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nvalid) out[j] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++tc;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * SM::ACC));
+}
+
+template <int BN>
+static cudaError_t launch_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                                cudaStream_t s) {
+  static int nsm = 0;
+  if (!nsm) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_p<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PSmem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int mb = (maxM + BM - 1) / BM, nb = (maxN + BN - 1) / BN;
+  const int ntiles = batch * mb * nb;
+  const int grid = ntiles < nsm ? ntiles : nsm;
+  k_gemm_tma_p<BN><<<grid, PNT, PSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
+  return cudaGetLastError();
+}
+
 }  // namespace tc
+
+cudaError_t launch_gemm_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                              cudaStream_t s) {
+  return bn == 144 ? tc::launch_tma_p<144>(descs, batch, maxM, maxN, s)
+                   : tc::launch_tma_p<128>(descs, batch, maxM, maxN, s);
+}
 
 cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s) {
@@ -672,7 +908,7 @@ cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn) {
   memset(out, 0, sizeof *out);
   cudaError_t e;
   if ((e = encode_2d(&out->a_hi, d.Ahi, d.K, d.M, d.lda, tc::BM)) != cudaSuccess) return e;
-  if ((e = encode_2d(&out->a_lo, d.Alo, d.K, d.M, d.lda, tc::BM)) != cudaSuccess) return e;
+  if (d.Alo && (e = encode_2d(&out->a_lo, d.Alo, d.K, d.M, d.lda, tc::BM)) != cudaSuccess) return e;
   if ((e = encode_2d(&out->b_hi, d.Bhi, d.K, d.N, d.ldb, bn)) != cudaSuccess) return e;
   if ((e = encode_2d(&out->b_lo, d.Blo, d.K, d.N, d.ldb, bn)) != cudaSuccess) return e;
   out->C = d.C;

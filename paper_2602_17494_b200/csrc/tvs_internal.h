@@ -118,6 +118,9 @@ cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN,
                            bool b_aligned, cudaStream_t s);
 cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
+// persistent warp-specialised form: A given as ONE fp32 plane (a_hi map), split in shared memory
+cudaError_t launch_gemm_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                              cudaStream_t s);
 cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
 cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,

@@ -37,6 +37,16 @@ def ctx():
 _IMG = {}
 
 
+def _log(kind, **kw):
+    import json
+    import os
+    path = os.environ.get("TVS_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"check": kind, **{k: (float(v) if isinstance(v, (float, np.floating))
+                                                     else v) for k, v in kw.items()}}) + "\n")
+
+
 def _image(name):
     if name not in _IMG:
         _IMG[name] = CONFIGS[name].image()
@@ -82,6 +92,7 @@ def test_config4_step2_first_sweep_sampled(ctx):
         # d on rows whose div stencil (rows i-1, i) lies in the core
         d_ref = d0[lo + 1:hi] - ops.div(p_ref)[:, :][1:-1] / alpha
         e_d = np.abs(d_g[lo + 1:hi].cpu().numpy() - d_ref).max()
+        _log("c4_step2_sweep1", m=list(m), p_err=e_p, d_err=e_d)
         assert e_p <= TOL, (m, e_p)
         assert e_d <= TOL, (m, e_d)
 
@@ -130,11 +141,13 @@ def test_config4_step1_first_sweep_sampled(ctx):
         assert e_p <= TOL, (m, e_p)
     # tau = delta r^1 is divergence-free up to the fp32 projection error
     e_div = np.abs(ops.div(tau_g.cpu().numpy().astype(np.float64))).max()
+    _log("c4_step1_div_tau", div=e_div)
     assert e_div <= TOL, e_div
     # the global projection alone at full size: sweeps = 1, inner = 0 leaves p = 0 and
     # tau = P tau_0 = delta f (element-wise parity of the 8193^2 projection)
     tau_p, _, _ = ctx.tv_stokes_step1(torch.from_numpy(img).cuda(), c.delta, _layout(c), (1, 0, c.t))
     e_P = np.abs(tau_p.cpu().numpy().astype(np.float64) - c.delta * f).max()
+    _log("c4_global_P", err=e_P)
     assert e_P <= TOL, e_P
 
 
@@ -166,6 +179,7 @@ def test_config5_step2_sampled_and_properties(ctx):
         p_ref = lay.alpha_hat * v[:, ylo - y0:yhi - y0 + 1, xlo - x0:xhi - x0 + 1]
         p_gpu = p_g[:, ylo:yhi + 1, xlo:xhi + 1].cpu().numpy().astype(np.float64)
         e_p = np.abs(p_gpu - p_ref).max()
+        _log("c5_step2_sweep1", m=list(m), p_err=e_p)
         assert e_p <= TOL, (m, e_p)
     del d_g, p_g
     # full schedule: properties that hold at any size
