@@ -237,6 +237,7 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "kernel": names[dom],
                 "peak_source": f"hbm_gbs ({peak_src}) MEASURED_PEAKS.json"}
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(c.name, roof["kernel"])
     line = {
         "metric": "dual pixel-updates/s (step 1 + step 2, overlap counted per subdomain)",
         "value": value, "unit": "pixel-updates/s", "n_gpus": world, "steps": args.steps,
@@ -263,6 +264,18 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def ncu_traffic(workload, family):
+    """DRAM bytes (read + write) per launch of the dominant kernel family, from the committed
+    `ncu --set full` capture summarised in profiles/ncu_traffic.json (one launch of the local
+    projection batch of this workload); None when no capture of that family exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)[workload][family]
+        return t["dram_bytes"], t["source"]
+    except Exception:
+        return None, None
 
 
 def aux_kernel_a(ctx, pkg, img, peaks, peak_src, flush):

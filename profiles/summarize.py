@@ -2,6 +2,7 @@
 
 usage: python profiles/summarize.py launches <launches.csv> <out.txt>
        python profiles/summarize.py full <report.ncu-rep> <out.txt>
+       python profiles/summarize.py traffic <report.ncu-rep> <workload> <family> <ncu_traffic.json> [index]
 """
 import collections
 import csv
@@ -56,5 +57,28 @@ def full(path, out):
                     f.write(f"    {w:70s} {r[i]:>16s} {units[i]}\n")
 
 
+
+
+def traffic(rep, workload, family, out_json, index="0"):
+    """Record dram__bytes_read.sum + dram__bytes_write.sum of the first kernel in an ncu report
+    as the per-launch traffic of a kernel family (read by bench.py's roofline.traffic)."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units, v = rows[0], rows[1], rows[2 + int(index)]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = h.index(m)
+        tot += float(v[i].replace(",", "")) * scale[units[i]]
+    name = v[h.index("Kernel Name")].split("(")[0]
+    t = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    t.setdefault(workload, {})[family] = {"dram_bytes": tot, "kernel": name,
+                                          "source": f"{os.path.basename(rep)} launch {index}"}
+    json.dump(t, open(out_json, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
