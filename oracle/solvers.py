@@ -114,6 +114,52 @@ def irv2_data(d0, tau, lam):
     return alpha, g, alpha * (np.asarray(d0, np.float64) - g)
 
 
+def xi_from_tau(tau, n2, n1, eps):
+    """xi^h of Eq. defXi2:discrete: tau_perp = R_Omega (tau_2, -tau_1) and
+    xi = tau_perp / sqrt(|tau_perp|^2 + eps) pointwise on Omega (N2 x N1)."""
+    t1 = np.asarray(tau[0], np.float64)[:n2, :n1]
+    t2 = np.asarray(tau[1], np.float64)[:n2, :n1]
+    den = np.sqrt(t2 ** 2 + t1 ** 2 + eps)
+    return np.stack([t2 / den, -t1 / den])
+
+
+def irv1_data(d0, tau, mu, eps):
+    """IRV1 (Eq. ir1dualdis, P:677): alpha = 1/mu (P:930), xi from tau (Eq. defXi2:discrete),
+    f = alpha d_0 - div xi.  Returns (alpha, div xi, f)."""
+    n2, n1 = d0.shape
+    alpha = 1.0 / mu
+    dxi = ops.div(xi_from_tau(tau, n2, n1, eps))
+    return alpha, dxi, alpha * np.asarray(d0, np.float64) - dxi
+
+
+def step2_data(d0, tau, lam, variant="irv2", eps=1e-3):
+    """Data of the step-2 dual min ||div p - f||^2 and the shift of the primal recovery
+    d = d_0 - (div p + shift) / alpha: IRV2 (f = alpha (d_0 - g), shift 0) or IRV1
+    (f = alpha d_0 - div xi, shift = div xi, Eq. tau_hat)."""
+    if variant == "irv1":
+        alpha, dxi, f = irv1_data(d0, tau, lam, eps)
+        return alpha, f, dxi
+    alpha, _, f = irv2_data(d0, tau, lam)
+    return alpha, f, np.zeros_like(f)
+
+
+def chambolle_irv1(d0, tau, mu, eps, iters, t=0.125, trace=False):
+    """Chambolle's iteration for the IRV1 dual (Cor. irdual P:403-417, Eq. ir1dualdis):
+    psi = grad(div p - f), p <- (p + t psi)/(1 + t |psi|); d = d_0 - (div p + div xi)/alpha."""
+    n2, n1 = d0.shape
+    alpha, dxi, f = irv1_data(d0, tau, mu, eps)
+    p = np.zeros((2, n2, n1))
+    one = np.ones((n2, n1))
+    energies = []
+    for _ in range(iters):
+        r = ops.div(p) - f
+        if trace:
+            energies.append(ops.inner(r, r))
+        p = rowwise_update(p, ops.grad(r), one, t)
+    d = np.asarray(d0, np.float64) - (ops.div(p) + dxi) / alpha
+    return (d, p, energies) if trace else (d, p)
+
+
 def chambolle_irv2(d0, tau, lam, iters, t=0.125, trace=False):
     """Chambolle's iteration for the IRV2 dual (P:504-510, P:679): psi = grad(div p - f);
     p <- (p + t psi)/(1 + t |psi|); d = d_0 - div p / alpha."""
@@ -192,14 +238,15 @@ def irv2_inner_global(m, lay, p, f, v0_full, inner, t):
 
 
 def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False,
-             subdomains=None):
-    """Alg. 2 for IRV2 on Gamma = Omega with the localized Alg. 3.
+             subdomains=None, variant="irv2", eps=1e-3):
+    """Alg. 2 for step 2 on Gamma = Omega with the localized Alg. 3; IRV2 (default,
+    the variant the paper adopts) or IRV1 (``variant='irv1'``, xi smoothing ``eps``).
 
     Warm start v^0 = R_S qhat_m from the previous sweep, qhat = 0 initially (reading A9;
     ``warm='theta_p'`` uses R_S theta_m p^n instead).  Fixed schedule, no stopping test (A10).
-    Returns (d, p, info) with d = d_0 - div p / alpha."""
+    Returns (d, p, info) with d = d_0 - (div p + shift) / alpha (IRV1: Eq. tau_hat)."""
     n2, n1 = d0.shape
-    alpha, g, f = irv2_data(d0, tau, lam)
+    alpha, f, shift = step2_data(d0, tau, lam, variant, eps)
     p = np.zeros((2, n2, n1))
     qhat = {}
     for m in lay.subdomains():
@@ -219,8 +266,8 @@ def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", tra
         if trace:
             r = ops.div(p) - f
             energies.append(ops.inner(r, r))
-    d = np.asarray(d0, np.float64) - ops.div(p) / alpha
-    info = {"alpha": alpha, "g": g, "f": f, "energies": energies, "qhat": qhat}
+    d = np.asarray(d0, np.float64) - (ops.div(p) + shift) / alpha
+    info = {"alpha": alpha, "shift": shift, "f": f, "energies": energies, "qhat": qhat}
     return d, p, info
 
 
@@ -338,6 +385,20 @@ def primal_energy_irv2(d, d0, g, alpha):
     """E_2 = TV(d - g) + alpha/2 ||d - d_0||^2 (Eq. modifiedStep2, P:475-479)."""
     dd = np.asarray(d, np.float64) - d0
     return tv(np.asarray(d, np.float64) - g) + 0.5 * alpha * ops.inner(dd, dd)
+
+
+def primal_energy_irv1(d, d0, dxi, alpha):
+    """E = TV(d) + <d, div xi> + alpha/2 ||d - d_0||^2 (Eq. IRPXi)."""
+    d = np.asarray(d, np.float64)
+    dd = d - d0
+    return tv(d) + ops.inner(d, dxi) + 0.5 * alpha * ops.inner(dd, dd)
+
+
+def dual_value_irv1(p, d0, f, alpha):
+    """The dual function whose maximiser Cor. irdual characterises:
+    G(p) = alpha/2 ||d_0||^2 - ||div p - f||^2 / (2 alpha) <= min E (weak duality)."""
+    r = ops.div(p) - f
+    return 0.5 * alpha * ops.inner(d0, d0) - ops.inner(r, r) / (2.0 * alpha)
 
 
 def duality_gap(u, p):

@@ -169,3 +169,67 @@ def test_dd_energy_monotone_diagnostic():
     _, _, info2 = S.dd_step2(d0, tau, 0.1, lay, 10, 5, trace=True)
     e = info2["energies"]
     assert all(b <= a * (1 + 1e-9) for a, b in zip(e, e[1:]))
+
+
+# ----------------------------------------------------------------------------- IRV1 (NEXT row 2)
+
+def test_xi_is_smoothed_unit_normal_of_a_ramp():
+    """tau_0 = grad^perp d_0 so tau_0^perp = (tau_2, -tau_1) = grad d_0 and xi of Eq.
+    defXi2:discrete is the smoothed unit normal: for the x-ramp d_0 = c j every
+    interior xi equals (c / sqrt(c^2 + eps), 0).  Pins the perp orientation and the eps placement."""
+    c, eps = 0.3, 1e-3
+    d0 = c * np.tile(np.arange(9, dtype=np.float64), (7, 1))
+    xi = S.xi_from_tau(S.tau0(d0), 7, 9, eps)
+    assert np.allclose(xi[0][:, 1:], c / np.sqrt(c * c + eps), atol=1e-15)
+    assert np.abs(xi[1]).max() == 0.0
+    assert np.all(xi[0][:, 0] == 0.0)      # tau_0's zero Neumann column
+
+
+def test_xi_strictly_inside_unit_ball():
+    """||xi||_inf < 1 holds automatically for eps > 0 (Rem. IRPW11)."""
+    tau = random_field((2, 12, 15), 4, 3.0)
+    xi = S.xi_from_tau(tau, 11, 14, 1e-3)
+    assert np.sqrt(xi[0] ** 2 + xi[1] ** 2).max() < 1.0
+
+
+def test_irv1_with_zero_tangent_field_is_rof():
+    """tau = 0 gives xi = 0, so IRV1 and IRV2 (g = 0) are both the ROF dual of
+    Chambolle 2004 with alpha = 1/mu = 1/lambda (reading A4): identical iterates."""
+    d0 = random_image(9, 11, 3).astype(np.float64)
+    tau = np.zeros((2, 10, 12))
+    d1, p1 = S.chambolle_irv1(d0, tau, 0.1, 1e-3, 50)
+    d2, p2 = S.chambolle_irv2(d0, tau, 0.1, 50)
+    assert np.abs(d1 - d2).max() < 1e-14 and np.abs(p1 - p2).max() < 1e-14
+
+
+def test_irv1_weak_duality_gap_closes():
+    """Weak duality between Eq. IRPXi and the dual of Cor. irdual:
+    E(d) >= G(p) for every feasible p; Chambolle's iterates drive E(d(p)) - G(p) to 0.  A wrong
+    sign or a dropped div xi in f or in the recovery d = d_0 - (div p + div xi)/alpha leaves a
+    gap that does not close."""
+    d0 = disk_on_ramp(16, 1001).astype(np.float64)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 300)
+    mu, eps = 0.1, 1e-3
+    alpha, dxi, f = S.irv1_data(d0, tau, mu, eps)
+    gaps = []
+    for it in (10, 100, 3000):
+        d, p = S.chambolle_irv1(d0, tau, mu, eps, it)
+        gaps.append(S.primal_energy_irv1(d, d0, dxi, alpha) - S.dual_value_irv1(p, d0, f, alpha))
+    assert min(gaps) >= -1e-9
+    assert gaps[0] > gaps[1] > gaps[2] and gaps[2] < 1e-3 * gaps[0]
+
+
+def test_irv1_schwarz_1x1_equals_chambolle_and_dd_converges():
+    """Alg. 2 with one subdomain is plain Chambolle (alpha_hat = 1, theta = 1), and the 2 x 2 DD
+    iterate approaches the single-domain IRV1 solution."""
+    d0 = random_image(12, 12, 8).astype(np.float64)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 100)
+    one = layout.Layout(12, 12, 1, 1, 0, 0)
+    d_dd, _, _ = S.dd_step2(d0, tau, 0.1, one, 6, 5, variant="irv1")
+    d_ch, _ = S.chambolle_irv1(d0, tau, 0.1, 1e-3, 30)
+    assert np.abs(d_dd - d_ch).max() < 1e-13
+    ref, _ = S.chambolle_irv1(d0, tau, 0.1, 1e-3, 20000)
+    lay = layout.Layout(12, 12, 2, 2, 4, 4)
+    e = [np.abs(S.dd_step2(d0, tau, 0.1, lay, n, 10, variant="irv1")[0] - ref).max()
+         for n in (10, 300)]
+    assert e[1] < 0.2 * e[0]
