@@ -119,6 +119,16 @@ tvs_status tv_stokes_step2(tvs_ctx *ctx, const float *tau, const float *d0, int3
                            float *d,
                            float *p, tvs_stats *st, void *cuda_stream);
 
+/* Step 2, variant IRV1 (Eq. ir1dualdis; Cor. irdual P:403-417): same dual iteration with
+ * f = alpha d0 - div xi, xi = tau_perp / sqrt(|tau_perp|^2 + epsilon), tau_perp = R_Omega(tau_2,
+ * -tau_1) (Eq. defXi2:discrete P:683-686), and d = d0 - (div p + div xi)/alpha.  mu = 1/alpha
+ * (P:930); epsilon > 0 (the paper's DD run uses 1e-3).  Arguments, layouts,
+ * ownership and errors as tv_stokes_step2 (TVS_EINVAL also for epsilon <= 0). */
+tvs_status tv_stokes_step2_irv1(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2,
+                                int32_t n1, float mu, float epsilon, const tvs_layout *L,
+                                const tvs_iters *it, float *d, float *p, tvs_stats *st,
+                                void *cuda_stream);
+
 /* Step 1 then step 2 on the same splitting.  tau (nullable) receives step 1's field. */
 tvs_status tv_stokes_denoise(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
                              float lambda, const tvs_layout *L, const tvs_iters *it1,

@@ -22,7 +22,7 @@ ABI_SYMBOLS = [
     "tvs_create", "tvs_destroy", "tvs_last_error", "tvs_nccl_unique_id", "tvs_owned_rows",
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
-    "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows",
+    "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows", "tv_stokes_step2_irv1",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH):
                                     ctypes.POINTER(Stats), P]
     lib.tv_stokes_step2.argtypes = [P, P, P, i32, i32, f32, LP, IP, P, P,
                                     ctypes.POINTER(Stats), P]
+    lib.tv_stokes_step2_irv1.argtypes = [P, P, P, i32, i32, f32, f32, LP, IP, P, P,
+                                         ctypes.POINTER(Stats), P]
     lib.tv_stokes_denoise.argtypes = [P, P, i32, i32, f32, f32, LP, IP, IP, P, P,
                                       ctypes.POINTER(Stats), ctypes.POINTER(Stats), P]
     lib.tv_stokes_denoise_host.argtypes = lib.tv_stokes_denoise.argtypes
@@ -240,7 +242,10 @@ class Context:
                     "tv_stokes_step1")
         return tau, p, st
 
-    def tv_stokes_step2(self, tau, d0, lam, layout, iters, want_p=False, stream=None):
+    def tv_stokes_step2(self, tau, d0, lam, layout, iters, want_p=False, stream=None,
+                        variant="irv2", eps=1e-3):
+        """Step 2: ``variant='irv2'`` (tv_stokes_step2, lam = 1/alpha) or ``'irv1'``
+        (tv_stokes_step2_irv1, lam = mu = 1/alpha, xi smoothing ``eps``)."""
         import torch
         n2, n1 = d0.shape
         self._dev(d0, (n2, n1))
@@ -248,10 +253,19 @@ class Context:
         d = torch.empty((n2, n1), device=d0.device, dtype=torch.float32)
         p = torch.empty((2, n2, n1), device=d0.device, dtype=torch.float32) if want_p else None
         st = Stats()
-        self._check(self.lib.tv_stokes_step2(self.h, self._ptr(tau), self._ptr(d0), n2, n1,
-                                             float(lam), ctypes.byref(_layout(layout)), ctypes.byref(_iters(iters)),
-                                             self._ptr(d), self._ptr(p), ctypes.byref(st),
-                                             self._stream(stream)), "tv_stokes_step2")
+        L, it = ctypes.byref(_layout(layout)), ctypes.byref(_iters(iters))
+        if variant == "irv1":
+            self._check(self.lib.tv_stokes_step2_irv1(self.h, self._ptr(tau), self._ptr(d0), n2, n1,
+                                                      float(lam), float(eps), L, it, self._ptr(d),
+                                                      self._ptr(p), ctypes.byref(st),
+                                                      self._stream(stream)), "tv_stokes_step2_irv1")
+        elif variant == "irv2":
+            self._check(self.lib.tv_stokes_step2(self.h, self._ptr(tau), self._ptr(d0), n2, n1,
+                                                 float(lam), L, it, self._ptr(d), self._ptr(p),
+                                                 ctypes.byref(st), self._stream(stream)),
+                        "tv_stokes_step2")
+        else:
+            raise ValueError(f"unknown step-2 variant {variant!r}")
         return d, p, st
 
     def tv_stokes_denoise(self, d0, delta, lam, layout, it1, it2, want_tau=False, stream=None,

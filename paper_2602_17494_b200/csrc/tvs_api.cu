@@ -204,6 +204,7 @@ struct Plan {
   int *d_loy = nullptr, *d_lox = nullptr;
   float *v[2] = {nullptr, nullptr};
   float *om = nullptr, *p = nullptr, *f = nullptr;
+  float *dxi = nullptr;   // IRV1: div xi (allocated on first use)
   double *g0 = nullptr;
   int *d_bad = nullptr;
   // step 1 only
@@ -477,9 +478,9 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.invN = std::max(B.invN, bo);
     B.fwd_flops += 2.0 * nt * bt * n1t;
     B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
-    // solve, algorithmic bytes per (row, frequency): qhat 4 + pivots 8 + grad outputs 16 (hi/lo);
-    // the default variant also round-trips an fp64 z scratch (16 B) -- not counted
-    B.solve_bytes += (double)nt * n1t * 28.0;
+    // solve, algorithmic bytes per (row, frequency): qhat 4 + pivots 8 + two fp32 grad planes 8
+    // (the z scratch stays on chip in the default segmented kernel)
+    B.solve_bytes += (double)nt * n1t * 20.0;
   }
   TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
   TRY(upload(ctx, P.bufs, &B.d_inv, inv));
@@ -785,11 +786,13 @@ tvs_status finish_call(tvs_ctx *ctx, Plan &P, cudaStream_t s, CallTimer &tm, tvs
   return TVS_OK;
 }
 
+// variant 2 = IRV2 (the paper's adopted step 2), 1 = IRV1 (xi smoothing eps > 0)
 tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2, int32_t n1,
                       float lambda, tvs_layout L, tvs_iters it, float *d, float *p_out,
-                      tvs_stats *st, cudaStream_t s) {
+                      tvs_stats *st, cudaStream_t s, int variant = 2, float eps = 0.f) {
   TRY(check_common(ctx, n2, n1, L, it));
   if (!(lambda > 0.f)) return fail(ctx, TVS_EINVAL, "lambda must be > 0");
+  if (variant == 1 && !(eps > 0.f)) return fail(ctx, TVS_EINVAL, "IRV1 needs epsilon > 0 (P:260)");
   if (!tau || !d0 || !d) return fail(ctx, TVS_EINVAL, "null pointer");
   Plan *P = nullptr;
   TRY(get_plan(ctx, n2, n1, L, 2, &P));
@@ -804,10 +807,17 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
   const size_t pl = (size_t)n2 * ld;
   const float *tau1 = tau, *tau2 = tau + (size_t)(n2 + 1) * (n1 + 1);
   CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
-  TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_g_row0(tau2, ldt, n1, P->g0, s); }));
-  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-    return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, s);
-  }));
+  if (variant == 1) {   // IRV1: f = alpha d0 - div xi
+    if (!P->dxi) TRY(dalloc(ctx, P->bufs, &P->dxi, pl));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_irv1_f(tau1, tau2, ldt, d0, n2, n1, alpha, eps, P->f, P->dxi, ld, s);
+    }));
+  } else {              // IRV2: f = alpha (d0 - g)
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_g_row0(tau2, ldt, n1, P->g0, s); }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, s);
+    }));
+  }
   CK(cudaMemsetAsync(P->p, 0, 2 * pl * sizeof(float), s));
   CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 2 * g.A * g.ldS * sizeof(float), s));
   int cur = 0;
@@ -828,7 +838,8 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
   }
   const Dist &D = P->dist;
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-    return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha, d, D.R0, D.R1, s);
+    return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha,
+                           variant == 1 ? P->dxi : nullptr, d, D.R0, D.R1, s);
   }));
   TRY(allgather_rows(ctx, D, d, 1, 0, n1, s));
   if (p_out) TRY(allgather_rows(ctx, D, P->p, 2, pl, ld, s));
@@ -1062,6 +1073,17 @@ tvs_status tv_stokes_step2(tvs_ctx *ctx, const float *tau, const float *d0, int3
   if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
   cudaSetDevice(ctx->device);
   return step2_impl(ctx, tau, d0, n2, n1, lambda, *L, *it, d, p, st, (cudaStream_t)cuda_stream);
+}
+
+tvs_status tv_stokes_step2_irv1(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2,
+                                int32_t n1, float mu, float epsilon, const tvs_layout *L,
+                                const tvs_iters *it, float *d, float *p, tvs_stats *st,
+                                void *cuda_stream) {
+  if (!ctx) return TVS_EINVAL;
+  if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
+  cudaSetDevice(ctx->device);
+  return step2_impl(ctx, tau, d0, n2, n1, mu, *L, *it, d, p, st, (cudaStream_t)cuda_stream, 1,
+                    epsilon);
 }
 
 tvs_status tv_stokes_denoise(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,

@@ -85,8 +85,12 @@ cudaError_t launch_partial(const SubDesc *subs, Geo g, int planes, const int2 *c
                            int k1, const float *q, int ra, int rb, int n1, int ld, float *out,
                            cudaStream_t s);
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
-                            int n1, float inv_alpha, float *d, int row0, int row1,
-                            cudaStream_t s);
+                            int n1, float inv_alpha, const float *shift, float *d, int row0,
+                            int row1, cudaStream_t s);
+// IRV1 data: f = alpha d0 - div xi and div xi (pitch ldf)
+cudaError_t launch_irv1_f(const float *tau1, const float *tau2, int ldt, const float *d0, int n2,
+                          int n1, float alpha, float eps, float *f, float *dxi, int ldf,
+                          cudaStream_t s);
 
 // step 1
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,

@@ -127,6 +127,29 @@ __global__ void k_irv2_f(const float *__restrict__ tau1, int ldt, const double *
   }
 }
 
+// IRV1 data (Eq. ir1dualdis): f = alpha d0 - div xi, xi = tau_perp / sqrt(|tau_perp|^2 + eps)
+// with tau_perp = R_Omega(tau_2, -tau_1) (Eq. defXi2:discrete); div with the three-case
+// D- (P:560-571).  Also stores div xi for the recovery d = d0 - (div p + div xi)/alpha.
+__global__ void k_irv1_f(const float *__restrict__ tau1, const float *__restrict__ tau2, int ldt,
+                         const float *__restrict__ d0, int n2, int n1, float alpha, float eps,
+                         float *__restrict__ f, float *__restrict__ dxi, int ldf) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  auto xi1 = [&](int a, int b) {   // x-component tau_2 / |tau|_eps
+    const float t1 = tau1[(size_t)a * ldt + b], t2 = tau2[(size_t)a * ldt + b];
+    return t2 * rsqrtf(t1 * t1 + t2 * t2 + eps);
+  };
+  auto xi2 = [&](int a, int b) {   // y-component -tau_1 / |tau|_eps
+    const float t1 = tau1[(size_t)a * ldt + b], t2 = tau2[(size_t)a * ldt + b];
+    return -t1 * rsqrtf(t1 * t1 + t2 * t2 + eps);
+  };
+  const float dv = (j < n1 - 1 ? xi1(i, j) : 0.f) - (j > 0 ? xi1(i, j - 1) : 0.f) +
+                   (i < n2 - 1 ? xi2(i, j) : 0.f) - (i > 0 ? xi2(i - 1, j) : 0.f);
+  f[(size_t)i * ldf + j] = alpha * d0[(size_t)i * n1 + j] - dv;
+  dxi[(size_t)i * ldf + j] = dv;
+}
+
 // ----------------------------------------------------------------------------- step 2 (IRV2)
 
 // omega0_m = R_{S+}(f - div p^n + div(theta_m p^n)) (Alg. 3 with Lambda = div, P:1348,
@@ -546,9 +569,11 @@ __global__ void k_partial(const SubDesc *__restrict__ subs, Geo g, int planes,
 }
 
 // d = d0 - div p / alpha.
+// d = d0 - (div p + shift) / alpha (IRV1: shift = div xi, Eq. tau_hat)
 __global__ void k_recover2(const float *__restrict__ d0, const float *__restrict__ p1,
                            const float *__restrict__ p2, int ld, int n2, int n1, float inv_alpha,
-                           float *__restrict__ d, int row0, int row1) {
+                           const float *__restrict__ shift, float *__restrict__ d, int row0,
+                           int row1) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= row1 || j >= n1) return;
@@ -556,7 +581,8 @@ __global__ void k_recover2(const float *__restrict__ d0, const float *__restrict
   auto P2 = [&](int a, int b) { return p2[(size_t)a * ld + b]; };
   float dv = (j < n1 - 1 ? P1(i, j) : 0.f) - (j > 0 ? P1(i, j - 1) : 0.f) +
              (i < n2 - 1 ? P2(i, j) : 0.f) - (i > 0 ? P2(i - 1, j) : 0.f);
-  d[(size_t)i * n1 + j] = d0[(size_t)i * n1 + j] - dv * inv_alpha;
+  const float sh = shift ? shift[(size_t)i * ld + j] : 0.f;
+  d[(size_t)i * n1 + j] = d0[(size_t)i * n1 + j] - (dv + sh) * inv_alpha;
 }
 
 // ----------------------------------------------------------------------------- step 1 (TFS)
@@ -1471,6 +1497,13 @@ cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, cons
   k_irv2_f<<<(n1 + 127) / 128, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf);
   return cudaGetLastError();
 }
+cudaError_t launch_irv1_f(const float *tau1, const float *tau2, int ldt, const float *d0, int n2,
+                          int n1, float alpha, float eps, float *f, float *dxi, int ldf,
+                          cudaStream_t s) {
+  k_irv1_f<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(tau1, tau2, ldt, d0, n2, n1, alpha, eps, f,
+                                                        dxi, ldf);
+  return cudaGetLastError();
+}
 cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                             const float *f, const float *p1, const float *p2, int ld, int n2,
                             int n1, float *om, cudaStream_t s) {
@@ -1524,11 +1557,11 @@ cudaError_t launch_partial(const SubDesc *subs, Geo g, int planes, const int2 *c
   return cudaGetLastError();
 }
 cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, int ld, int n2,
-                            int n1, float inv_alpha, float *d, int row0, int row1,
-                            cudaStream_t s) {
+                            int n1, float inv_alpha, const float *shift, float *d, int row0,
+                            int row1, cudaStream_t s) {
   if (row1 <= row0) return cudaSuccess;
   k_recover2<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(d0, p1, p2, ld, n2, n1,
-                                                                   inv_alpha, d, row0, row1);
+                                                                   inv_alpha, shift, d, row0, row1);
   return cudaGetLastError();
 }
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,

@@ -47,7 +47,10 @@ def _primal1(tau, d0, delta):
     return S.primal_energy_tfs(tau, ptau0, delta)
 
 
-def _primal2(d, d0, tau, lam):
+def _primal2(d, d0, tau, lam, variant="irv2", eps=1e-3):
+    if variant == "irv1":
+        alpha, dxi, _ = S.irv1_data(d0, tau, lam, eps)
+        return S.primal_energy_irv1(d, d0, dxi, alpha)
     alpha, g, _ = S.irv2_data(d0, tau, lam)
     return S.primal_energy_irv2(d, d0, g, alpha)
 
@@ -71,19 +74,23 @@ def check_step1(ctx, img, delta, L, sweeps, inner, t=0.125):
     return tau_ref, st
 
 
-def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125):
+def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125, variant="irv2", eps=1e-3):
     n2, n1 = img.shape
     lay = olayout.Layout(n2, n1, *L)
-    d_ref, p_ref, _ = S.dd_step2(img.astype(np.float64), tau, lam, lay, sweeps, inner, t)
-    d, p, st = ctx.tv_stokes_step2(_dev(tau), _dev(img), lam, L, (sweeps, inner, t), want_p=True)
+    # both sides consume the same fp32 tau
+    tau = np.asarray(tau, np.float32).astype(np.float64)
+    d_ref, p_ref, _ = S.dd_step2(img.astype(np.float64), tau, lam, lay, sweeps, inner, t,
+                                 variant=variant, eps=eps)
+    d, p, st = ctx.tv_stokes_step2(_dev(tau), _dev(img), lam, L, (sweeps, inner, t), want_p=True,
+                                   variant=variant, eps=eps)
     d, p = d.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
     e_d = np.abs(d - d_ref).max()
     e_p = np.abs(p - p_ref).max()
-    E_ref = _primal2(d_ref, img.astype(np.float64), tau, lam)
-    E_gpu = _primal2(d, img.astype(np.float64), tau, lam)
+    E_ref = _primal2(d_ref, img.astype(np.float64), tau, lam, variant, eps)
+    E_gpu = _primal2(d, img.astype(np.float64), tau, lam, variant, eps)
     rel = abs(E_gpu - E_ref) / abs(E_ref)
-    _log("step2", shape=list(img.shape), L=list(L), sweeps=sweeps, inner=inner, d_err=e_d,
-         p_err=e_p, E2_rel=rel)
+    _log("step2" if variant == "irv2" else "step2_irv1", shape=list(img.shape), L=list(L),
+         sweeps=sweeps, inner=inner, d_err=e_d, p_err=e_p, E2_rel=rel)
     assert e_d <= TOL, f"max|d - oracle| = {e_d}"
     assert e_p <= P_TOL, f"max|p - oracle| = {e_p}"
     assert rel <= TOL, f"relative E2 error {rel}"
@@ -109,6 +116,24 @@ def test_step2_small(ctx, shape, L):
 def test_step1_small(ctx, shape, L):
     img = random_image(*shape, seed=shape[0] * 7 + shape[1])
     check_step1(ctx, img, 0.05, L, 3, 4)
+
+
+@pytest.mark.parametrize("shape,L", [((16, 16), (1, 1, 0, 0)), ((24, 20), (2, 2, 4, 4)),
+                                     ((37, 53), (3, 2, 3, 5)), ((5, 9), (1, 2, 0, 2))])
+def test_step2_irv1_small(ctx, shape, L):
+    """IRV1 (Eq. ir1dualdis, xi of Eq. defXi2:discrete) through tv_stokes_step2_irv1."""
+    img = random_image(*shape, seed=shape[0] * 31 + shape[1])
+    tau, _ = S.chambolle_tfs(img.astype(np.float64), 0.05, 30)
+    check_step2(ctx, img, tau, 0.1, L, 4, 5, variant="irv1", eps=1e-3)
+
+
+def test_irv1_errors(ctx):
+    import paper_2602_17494_b200 as pkg
+    img = _dev(random_image(16, 16, 1))
+    tau = torch.zeros((2, 17, 17), device="cuda")
+    with pytest.raises(pkg.TvsError) as e:
+        ctx.tv_stokes_step2(tau, img, 0.1, (2, 2, 4, 4), (1, 1, 0.125), variant="irv1", eps=0.0)
+    assert e.value.code == 1
 
 
 def test_global_projection_only(ctx):
@@ -171,6 +196,7 @@ def test_config1_full(ctx):
     L = (c.m2, c.m1, c.overlap, c.overlap)
     tau_ref, _ = check_step1(ctx, img, c.delta, L, c.sweeps, c.inner)
     check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner)
+    check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner, variant="irv1", eps=1e-3)
     # single-domain comparison run of config 1 (400 Chambolle iterations per step)
     tau_ref1, _ = check_step1(ctx, img, c.delta, (1, 1, 0, 0), 20, 20)
     check_step2(ctx, img, tau_ref1, c.lam, (1, 1, 0, 0), 20, 20)
@@ -196,6 +222,8 @@ def test_config2_full(ctx):
     L = (c.m2, c.m1, c.overlap, c.overlap)
     tau_ref, _ = check_step1(ctx, img, c.delta, L, c.sweeps, c.inner)
     check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner)
+    # IRV1 on the same tangent field, the paper's DD-run smoothing eps = 1e-3
+    check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner, variant="irv1", eps=1e-3)
 
 
 def test_config3_full_size_short_schedule(ctx):
