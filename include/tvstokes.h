@@ -74,6 +74,9 @@ typedef struct {
   int64_t launches;
   double flops_proj;        /* algorithmic fp32 MACs*2 of the projection contractions (step 1) */
   double bytes_sweep;       /* algorithmic HBM bytes of the fused dual-sweep kernels            */
+  double dual_energy;       /* D(p) of the returned dual (Eq. opt_dual_discrete),
+                               fp64 reduction over the whole grid (all ranks)                   */
+  int64_t sweeps_run;       /* outer sweeps performed (< sweeps when a stopping rule fired)     */
 } tvs_stats;
 
 typedef struct tvs_ctx tvs_ctx;   /* opaque: device, plans, scratch, profiling, communicator */
@@ -105,6 +108,16 @@ tvs_status tvs_dist_rows(int32_t n2, int32_t n1, const tvs_layout *L, int32_t st
  * (reading A7).  Used by tests to check the ABI agrees with the paper's layout rules. */
 tvs_status tvs_layout_range(int32_t n, int32_t m, int32_t s, int32_t k, int32_t *lo, int32_t *hi);
 tvs_status tvs_layout_theta(int32_t n, int32_t m, int32_t s, int32_t k, int32_t x, double *theta);
+
+/* Outer-loop stopping rule of this context (default 0: fixed schedule, reading A10).
+ * criterion 1: |D(p^n)^{1/2} - D(p^{n+1})^{1/2}| < c tol with c = (2|Omega~|)^{1/2} for step 1 and
+ *              |Omega|^{1/2} for step 2 (the criteria of section 5.2);
+ * criterion 2: |D(p^n)^2 - D(p^{n+1})^2| / |Gamma| < tol (section 6.3, printed squares,
+ *              reading A19).
+ * D is evaluated on the device after every sweep (one fp64 reduction; step 1 reuses the residual
+ * r^n = f - P multidiv p^n of the next sweep) and read back by the host, so an active rule adds one
+ * stream synchronisation per sweep.  TVS_EINVAL for an unknown criterion or tol < 0. */
+tvs_status tvs_set_stopping(tvs_ctx *ctx, int32_t criterion, double tol);
 
 /* Step 1 (TFS).  d0: device [n2*n1]; tau: device out [2][(n2+1)*(n1+1)];
  * p: device out (nullable) [4][(n2+1)*(n1+1)]. */

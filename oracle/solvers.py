@@ -237,8 +237,20 @@ def irv2_inner_global(m, lay, p, f, v0_full, inner, t):
     return v
 
 
+def stop_rule(criterion, tol, d_prev, d_next, npts, cfac):
+    """Outer stopping tests between consecutive dual energies:
+    1 -- |D_n^{1/2} - D_{n+1}^{1/2}| < (cfac |Gamma|)^{1/2} tol (section 5.2: cfac = 2 for TFS,
+    P:915-919; 1 for IRV1/IRV2); 2 -- |D_n^2 - D_{n+1}^2| / |Gamma| < tol (section 6.3,
+    P:1776, printed with squares, reading A19).  0 never stops (fixed schedule, A10)."""
+    if criterion == 1:
+        return abs(np.sqrt(d_prev) - np.sqrt(d_next)) < np.sqrt(cfac * npts) * tol
+    if criterion == 2:
+        return abs(d_prev ** 2 - d_next ** 2) / npts < tol
+    return False
+
+
 def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False,
-             subdomains=None, variant="irv2", eps=1e-3):
+             subdomains=None, variant="irv2", eps=1e-3, stop=(0, 0.0)):
     """Alg. 2 for step 2 on Gamma = Omega with the localized Alg. 3; IRV2 (default,
     the variant the paper adopts) or IRV1 (``variant='irv1'``, xi smoothing ``eps``).
 
@@ -252,7 +264,9 @@ def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", tra
     for m in lay.subdomains():
         qhat[m] = np.zeros((2,) + rect_shape(lay.rect(m, extended=False)))
     energies = []
-    for _ in range(sweeps):
+    e_prev = ops.inner(f, f)                  # D(p^0) = ||div 0 - f||^2
+    sweeps_run = sweeps
+    for n in range(sweeps):
         acc = np.zeros_like(p)
         for m in lay.subdomains():
             s = lay.rect(m, extended=False)
@@ -263,11 +277,17 @@ def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", tra
             qhat[m] = _irv2_inner_local(m, lay, p, f, v0, inner, t)
             acc += extend(qhat[m], s, full_rect(n2, n1))
         p = (1.0 - lay.alpha_hat) * p + lay.alpha_hat * acc
-        if trace:
+        if trace or stop[0]:
             r = ops.div(p) - f
             energies.append(ops.inner(r, r))
+            if stop_rule(stop[0], stop[1], e_prev, energies[-1], n2 * n1, 1.0):
+                sweeps_run = n + 1
+                break
+            e_prev = energies[-1]
     d = np.asarray(d0, np.float64) - (ops.div(p) + shift) / alpha
-    info = {"alpha": alpha, "shift": shift, "f": f, "energies": energies, "qhat": qhat}
+    r = ops.div(p) - f
+    info = {"alpha": alpha, "shift": shift, "f": f, "energies": energies, "qhat": qhat,
+            "sweeps_run": sweeps_run, "dual_energy": ops.inner(r, r)}
     return d, p, info
 
 
@@ -312,7 +332,8 @@ def tfs_inner_global(m, lay, p, f, v0_full, inner, t):
     return v
 
 
-def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False):
+def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False,
+             stop=(0, 0.0)):
     """Alg. 2 for TFS on Gamma = Omega~ with the localized Alg. 5.
 
     f = delta^{-1} P tau_0.  The global residual r^n = f - P multidiv p^n is
@@ -325,8 +346,16 @@ def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=
     p = np.zeros((2, 2, n2t, n1t))
     qhat = {m: np.zeros((2, 2) + rect_shape(lay.rect(m, True))) for m in lay.subdomains()}
     energies = []
-    for _ in range(sweeps):
+    e_prev = None
+    sweeps_run = sweeps
+    for n in range(sweeps):
         r = f - spectral.project(ops.multidiv(p))
+        if stop[0]:                          # D_TFS(p^n) = ||r^n||^2 (Eq. tfsdualdis)
+            e = ops.inner(r, r)
+            if e_prev is not None and stop_rule(stop[0], stop[1], e_prev, e, n2t * n1t, 2.0):
+                sweeps_run = n
+                break
+            e_prev = e
         acc = np.zeros_like(p)
         for m in lay.subdomains():
             s = lay.rect(m, extended=True)
@@ -341,7 +370,8 @@ def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=
             rr = spectral.project(ops.multidiv(p)) - f
             energies.append(ops.inner(rr, rr))
     tau = delta * (f - spectral.project(ops.multidiv(p)))
-    return tau, p, {"f": f, "energies": energies, "qhat": qhat}
+    return tau, p, {"f": f, "energies": energies, "qhat": qhat, "sweeps_run": sweeps_run,
+                    "dual_energy": ops.inner(tau, tau) / delta ** 2}
 
 
 def dd_denoise(d0, delta, lam, lay: Layout, it1, it2, t=0.125):

@@ -23,6 +23,7 @@ ABI_SYMBOLS = [
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
     "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows", "tv_stokes_step2_irv1",
+    "tvs_set_stopping",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -49,7 +50,8 @@ class Iters(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("seconds", ctypes.c_double), ("pixel_updates", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("flops_proj", ctypes.c_double),
-                ("bytes_sweep", ctypes.c_double)]
+                ("bytes_sweep", ctypes.c_double), ("dual_energy", ctypes.c_double),
+                ("sweeps_run", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -90,6 +92,7 @@ def load_library(path: str = LIB_PATH):
                                       ctypes.POINTER(Stats), ctypes.POINTER(Stats), P]
     lib.tv_stokes_denoise_host.argtypes = lib.tv_stokes_denoise.argtypes
     lib.tvs_set_profiling.argtypes = [P, ctypes.c_int]
+    lib.tvs_set_stopping.argtypes = [P, i32, ctypes.c_double]
     arr7i = ctypes.c_int64 * 7
     arr7d = ctypes.c_double * 7
     lib.tvs_kernel_times.argtypes = [P, arr7i, arr7d, arr7d, arr7d]
@@ -302,6 +305,11 @@ class Context:
         self._check(self.lib.tvs_selftest_gemm(self.h, M, N, K, impl, seed, ctypes.byref(err)),
                     "tvs_selftest_gemm")
         return err.value
+
+    def set_stopping(self, criterion: int, tol: float = 0.0):
+        """Outer-loop stopping rule (tvs_set_stopping): 0 fixed schedule, 1 the sqrt(D) criterion
+        of section 5.2, 2 the D^2 criterion of section 6.3."""
+        self._check(self.lib.tvs_set_stopping(self.h, int(criterion), float(tol)), "tvs_set_stopping")
 
     def set_profiling(self, on: bool):
         self._check(self.lib.tvs_set_profiling(self.h, 1 if on else 0), "tvs_set_profiling")

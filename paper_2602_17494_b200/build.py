@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtvstokes.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("tvs_kernels.cu", "tvs_gemm_tc.cu", "tvs_api.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("tvs_kernels.cu", "tvs_gemm_tc.cu", "tvs_czt.cu", "tvs_api.cu")]
 HEADERS = [os.path.join(HERE, "csrc", "tvs_internal.h"), os.path.join(ROOT, "include", "tvstokes.h")]
 
 NCCL_DIR = None

@@ -184,6 +184,12 @@ struct ProjBatch {
   TmaGemmDesc *d_fwd4 = nullptr, *d_inv4 = nullptr;   // persistent: A as one fp32 plane
   GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
+  // chirp-z form of the two contractions (used when its estimated time is lower, TVS_DCT)
+  bool czt = false;
+  CztGeom gf{}, gi{};
+  CztJob *d_fj = nullptr, *d_ij = nullptr;
+  int nfj = 0, nij = 0, fj_rows = 0, ij_rows = 0;
+  float2 *gtab_f = nullptr, *gtab_i = nullptr, *tw_f = nullptr, *tw_i = nullptr;
   int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
   double fwd_flops = 0, inv_flops = 0, solve_bytes = 0;
 };
@@ -207,6 +213,7 @@ struct Plan {
   float *dxi = nullptr;   // IRV1: div xi (allocated on first use)
   double *g0 = nullptr;
   int *d_bad = nullptr;
+  double *d_part = nullptr, *d_energy = nullptr;   // dual-energy reduction scratch
   // step 1 only
   float *vtmp = nullptr, *q = nullptr, *qlo = nullptr, *gphi = nullptr, *qglo = nullptr;
   float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
@@ -246,6 +253,12 @@ struct tvs_ctx {
   enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3 };
   int gemm = G_PERSIST;
   bool presplit() const { return gemm == G_CPASYNC || gemm == G_TMA; }
+  // partial x-DCTs: 0 = choose per batch by estimated time, 1 = dense GEMM, 2 = chirp-z (TVS_DCT)
+  int dct_mode = 0;
+  int czt_max_m = 16384;
+  double *h_energy = nullptr;   // pinned slot for dual energies
+  int stop_crit = 0;       // tvs_set_stopping
+  double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
   // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
   // thread per frequency, fp64 z scratch) or TVS_SOLVE=chunked (z checkpoints in shared memory)
   int solve_impl = 3;
@@ -482,6 +495,61 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     // (the z scratch stays on chip in the default segmented kernel)
     B.solve_bytes += (double)nt * n1t * 20.0;
   }
+  // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
+  {
+    std::vector<CztJob> fj, ij;
+    int bt_max = 0, bo_max = 0;
+    for (int i = 0; i < B.ntiles; ++i) {
+      const ProjTile &t = B.tiles[i];
+      int nt = t.ty1 - t.ty0 + 1, f0 = 0;
+      if (fr0 >= 0) {
+        f0 = fr0;
+        nt = fr1 - fr0;
+      }
+      const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
+      const int no = t.py1 - t.ty0 + 1 - t.po;
+      const size_t goff = (size_t)t.po * ldG;
+      fj.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3),
+                    B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, ldq, B.ldn, t.tx0, bt, n1t, 0});
+      ij.push_back({B.phx + (size_t)i * B.AP * B.ldn, G + (size_t)i * B.AP * ldG + goff, no, B.ldn,
+                    ldG, t.tx0, n1t, bo, 2});
+      ij.push_back({B.phy + (size_t)i * B.AP * B.ldn, G + gplane + (size_t)i * B.AP * ldG + goff, no,
+                    B.ldn, ldG, t.tx0, n1t, bo, 1});
+      bt_max = std::max(bt_max, bt);
+      bo_max = std::max(bo_max, bo);
+      B.fj_rows = std::max(B.fj_rows, nt);
+      B.ij_rows = std::max(B.ij_rows, no);
+    }
+    B.nfj = (int)fj.size();
+    B.nij = (int)ij.size();
+    const bool okf = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
+    const bool oki = czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
+    // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~3.5 TF/s
+    double t_gemm = 0, t_czt = 0;
+    for (int i = 0; i < B.ntiles; ++i) {
+      t_gemm += 3.0 * (2.0 * fj[i].rows * fj[i].ulen * fj[i].vlen +
+                       2.0 * 2.0 * ij[2 * i].rows * ij[2 * i].ulen * ij[2 * i].vlen) / 400e12;
+      const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)B.gf.M);
+      const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)B.gi.M);
+      t_czt += (fj[i].rows * B.gf.nvp * B.gf.nuc * f1 + 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2) / 3.5e12;
+    }
+    // accuracy: the tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193
+    // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
+    const bool long_axis = n1t > 4096;
+    B.czt = okf && oki && !ctx->presplit() && ctx->gemm != tvs_ctx::G_SIMT &&
+            (ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
+    if (B.czt) {
+      std::vector<float2> gt, tw;
+      czt_tables(B.gf, gt, tw);
+      TRY(upload(ctx, P.bufs, &B.gtab_f, gt));
+      TRY(upload(ctx, P.bufs, &B.tw_f, tw));
+      czt_tables(B.gi, gt, tw);
+      TRY(upload(ctx, P.bufs, &B.gtab_i, gt));
+      TRY(upload(ctx, P.bufs, &B.tw_i, tw));
+      TRY(upload(ctx, P.bufs, &B.d_fj, fj));
+      TRY(upload(ctx, P.bufs, &B.d_ij, ij));
+    }
+  }
   TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
   TRY(upload(ctx, P.bufs, &B.d_inv, inv));
   B.nstack = (int)fwd_tc.size();
@@ -614,6 +682,8 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   TRY(dalloc(ctx, P->bufs, &P->v[1], vsz));
   TRY(dalloc(ctx, P->bufs, &P->p, (size_t)C * G2 * P->ld));
   TRY(dalloc(ctx, P->bufs, &P->d_bad, 1));
+  TRY(dalloc(ctx, P->bufs, &P->d_part, 1024));
+  TRY(dalloc(ctx, P->bufs, &P->d_energy, 4));
   if (D.world > 1) {   // partial-sum band buffers [planes][rows][ld]
     TRY(dalloc(ctx, P->bufs, &P->send_up, (size_t)C * std::max(1, D.us1 - D.us0) * P->ld));
     TRY(dalloc(ctx, P->bufs, &P->recv_up, (size_t)C * std::max(1, D.ur1 - D.ur0) * P->ld));
@@ -712,12 +782,51 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
   });
 }
 
+// Sum the device scalar over ranks (NCCL) and copy it to the pinned host slot; sync = read it now
+// (otherwise the value is valid after the call's final stream synchronisation).
+tvs_status fetch_energy(tvs_ctx *ctx, Plan &P, cudaStream_t s, double *out, bool sync = true) {
+  if (P.dist.world > 1)
+    TRY(nccl_ck(ctx, ncclAllReduce(P.d_energy, P.d_energy, 1, ncclDouble, ncclSum, ctx->nccl, s),
+                "ncclAllReduce"));
+  if (!ctx->h_energy) CK(cudaMallocHost(&ctx->h_energy, 8 * sizeof(double)));
+  CK(cudaMemcpyAsync(ctx->h_energy, P.d_energy, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (sync) {
+    CK(cudaStreamSynchronize(s));
+    *out = ctx->h_energy[0];
+  }
+  return TVS_OK;
+}
+
+// Stopping rule of tvs_set_stopping between consecutive dual energies (npts = |Gamma|; cfac = the
+// c of criterion 1: 2 for step 1 (2|Omega~|), 1 for step 2 (|Omega|)).
+bool stop_now(const tvs_ctx *ctx, double d_prev, double d_next, double npts, double cfac) {
+  if (ctx->stop_crit == 1)
+    return std::fabs(std::sqrt(d_prev) - std::sqrt(d_next)) < std::sqrt(cfac * npts) * ctx->stop_tol;
+  if (ctx->stop_crit == 2)
+    return std::fabs(d_prev * d_prev - d_next * d_next) / npts < ctx->stop_tol;
+  return false;
+}
+
 // grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).  For the
 // global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
 tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
   const bool tc = ctx->presplit();   // solve writes hi/lo planes
   const int gm = ctx->gemm;
+  if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
+    TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
+      return launch_czt(B.d_fj, B.nfj, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
+    }));
+    if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
+    TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
+      return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
+                                reinterpret_cast<float *>(B.z), B.phx, B.phy, nullptr, nullptr,
+                                B.AP, s);
+    }));
+    return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
+      return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
+    });
+  }
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
     switch (gm) {
       case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
@@ -822,6 +931,18 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
   CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 2 * g.A * g.ldS * sizeof(float), s));
   int cur = 0;
   const double sweep_bytes = 20.0 * (double)P->sum_S;    // v read 8 + omega0 4 + v write 8
+  const Dist &D2 = P->dist;
+  auto energy2 = [&](double *out, bool sync) -> tvs_status {   // ||div p - f||^2
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_dual_energy2(P->p, P->p + pl, P->f, ld, n2, n1, D2.R0, D2.R1, P->d_part,
+                                 P->d_energy, s);
+    }));
+    return fetch_energy(ctx, *P, s, out, sync);
+  };
+  const bool stopping = ctx->stop_crit != 0;
+  double e_prev = 0.0;
+  int sweeps_run = it.sweeps;
+  if (stopping) TRY(energy2(&e_prev, true));
   for (int n = 0; n < it.sweeps; ++n) {
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_omega0_2(P->d_subs, g, P->d_thy, P->d_thx, P->f, P->p, P->p + pl, ld, n2, n1,
@@ -835,7 +956,18 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       cur ^= 1;
     }
     TRY(combine_step(ctx, *P, P->v[cur], s));
+    if (stopping) {
+      double e = 0.0;
+      TRY(energy2(&e, true));
+      if (stop_now(ctx, e_prev, e, (double)n2 * n1, 1.0)) {
+        sweeps_run = n + 1;
+        break;
+      }
+      e_prev = e;
+    }
   }
+  double e_final = 0.0;
+  TRY(energy2(&e_final, false));   // read after the final synchronisation
   const Dist &D = P->dist;
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
     return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha,
@@ -849,10 +981,14 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
                            ld * sizeof(float), n1 * sizeof(float), n2, cudaMemcpyDeviceToDevice, s));
   if (st) {
     memset(st, 0, sizeof *st);
-    st->pixel_updates = P->sum_S * (int64_t)it.sweeps * it.inner;
-    st->bytes_sweep = sweep_bytes * it.sweeps * it.inner;
+    st->pixel_updates = P->sum_S * (int64_t)sweeps_run * it.inner;
+    st->bytes_sweep = sweep_bytes * sweeps_run * it.inner;
+    st->sweeps_run = sweeps_run;
   }
-  return finish_call(ctx, *P, s, tm, st, l0);
+  TRY(finish_call(ctx, *P, s, tm, st, l0));
+  (void)e_final;
+  if (st) st->dual_energy = ctx->h_energy[0];
+  return TVS_OK;
 }
 
 tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
@@ -903,8 +1039,27 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   int cur = 0;
   const double prediv_bytes = 16.0 * P->sum_S + 4.0 * P->sum_T;
   const double sweep_bytes = 48.0 * (double)P->sum_S;
+  // D_TFS(p^n) = ||r^n||^2 (Eq. tfsdualdis) on this rank's core rows
+  auto energy1 = [&](double *out, bool sync) -> tvs_status {
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_sumsq2(P->r, pl, ld, G1, D.R0, D.R1, P->d_part, P->d_energy, s);
+    }));
+    return fetch_energy(ctx, *P, s, out, sync);
+  };
+  const bool stopping = ctx->stop_crit != 0;
+  double e_prev = 0.0;
+  int sweeps_run = it.sweeps;
   for (int n = 0; n < it.sweeps; ++n) {
     TRY(residual(P->r, 1.f));
+    if (stopping) {   // r^n is D(p^n)'s residual: test the previous sweep before starting this one
+      double e = 0.0;
+      TRY(energy1(&e, true));
+      if (n > 0 && stop_now(ctx, e_prev, e, (double)G2 * G1, 2.0)) {
+        sweeps_run = n;
+        break;
+      }
+      e_prev = e;
+    }
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_load_tp(P->d_subs, g, P->d_thy, P->d_thx, P->p, ld, G2, G1, P->vtmp, s);
     }));
@@ -928,6 +1083,8 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   }
   // tau = P tau_0 - delta P multidiv p = delta r^S; every rank ends with the full field
   TRY(residual(P->r, delta));
+  double e_final = 0.0;
+  TRY(energy1(&e_final, false));   // ||delta r^S||^2, read after the final synchronisation
   TRY(allgather_rows(ctx, D, P->r, 2, pl, ld, s));
   if (p_out) TRY(allgather_rows(ctx, D, P->p, 4, pl, ld, s));
   for (int c = 0; c < 2; ++c)
@@ -939,12 +1096,16 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
                            ld * sizeof(float), G1 * sizeof(float), G2, cudaMemcpyDeviceToDevice, s));
   if (st) {
     memset(st, 0, sizeof *st);
-    st->pixel_updates = P->sum_S * (int64_t)it.sweeps * it.inner;
-    st->bytes_sweep = (sweep_bytes + prediv_bytes) * it.sweeps * it.inner;
-    st->flops_proj = (P->local.fwd_flops + P->local.inv_flops) * it.sweeps * (it.inner + 1) +
-                     (P->global.fwd_flops + P->global.inv_flops) * (it.sweeps + 2);
+    st->pixel_updates = P->sum_S * (int64_t)sweeps_run * it.inner;
+    st->bytes_sweep = (sweep_bytes + prediv_bytes) * sweeps_run * it.inner;
+    st->flops_proj = (P->local.fwd_flops + P->local.inv_flops) * sweeps_run * (it.inner + 1) +
+                     (P->global.fwd_flops + P->global.inv_flops) * (sweeps_run + 2);
+    st->sweeps_run = sweeps_run;
   }
-  return finish_call(ctx, *P, s, tm, st, l0);
+  TRY(finish_call(ctx, *P, s, tm, st, l0));
+  (void)e_final;
+  if (st) st->dual_energy = ctx->h_energy[0] / ((double)delta * (double)delta);
+  return TVS_OK;
 }
 
 }  // namespace
@@ -967,6 +1128,12 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
             : strcmp(g, "cpasync") == 0 ? tvs_ctx::G_CPASYNC
             : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
                                         : tvs_ctx::G_PERSIST;
+  const char *dm = getenv("TVS_DCT");
+  c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
+  if (const char *mm = getenv("TVS_CZT_MAXM")) {
+    const int v = atoi(mm);
+    if (v >= 16 && v <= 16384 && (v & (v - 1)) == 0 && (__builtin_ctz(v) % 2) == 0) c->czt_max_m = v;
+  }
   const char *sv = getenv("TVS_SOLVE");
   c->solve_impl = sv && strcmp(sv, "chunked") == 0 ? 2 : sv && strcmp(sv, "serial") == 0 ? 1 : 3;
   cudaError_t e = cudaSetDevice(device);
@@ -987,6 +1154,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
 }
 
 tvs_status tvs_destroy(tvs_ctx *ctx) {
+  if (ctx && ctx->h_energy) cudaFreeHost(ctx->h_energy);
   if (!ctx) return TVS_EINVAL;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
@@ -1243,6 +1411,15 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
       worst = std::max(worst, fabs((double)C[(size_t)i * N + j] - ref) / std::max(mag, 1e-30));
     }
   *max_rel_err = worst;
+  return TVS_OK;
+}
+
+tvs_status tvs_set_stopping(tvs_ctx *ctx, int32_t criterion, double tol) {
+  if (!ctx) return TVS_EINVAL;
+  if (criterion < 0 || criterion > 2 || !(tol >= 0.0))
+    return fail(ctx, TVS_EINVAL, "stopping: criterion must be 0, 1 or 2 and tol >= 0");
+  ctx->stop_crit = criterion;
+  ctx->stop_tol = tol;
   return TVS_OK;
 }
 

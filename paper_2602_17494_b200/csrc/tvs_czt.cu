@@ -1,0 +1,267 @@
+// Fast partial x-DCTs of the projection kernel (b) by the chirp-z transform (
+// "Fast DCT could help").  Same operators as the dense contractions of tvs_gemm_tc.cu:
+//   forward  Qhat[j]  = sum_{x in tile} q[x] cos(theta j (2x+1))              j = 0 .. N-1
+//   inverse  out_y[x] = sum_j Phi_y[j] cos(theta j (2x+1))                    x in the tile
+//            out_x[x] = sum_j Phi_x[j] sin(theta j (2x+2))
+// with theta = pi / (2N) (Eq. form:DCTmat, and the spectral x-derivative of
+// DESIGN.md section 5).  With x = tx0 + u (u tile-relative) and 2jv = j^2 + v^2 - (j - v)^2 every
+// sum is  out[v] = Op( post[v] sum_u in[u] pre[u] h[v - u] ),  h[m] = e^{-i theta m^2} (even in m),
+// a linear convolution with a chirp, evaluated by an in-place radix-4 FFT of size M (power of 4)
+// in shared memory: DIF (natural -> digit-reversed), multiply by the precomputed digit-reversed
+// FFT of the circular kernel window, DIT (digit-reversed -> natural).  Inputs are cut into chunks
+// of Uc and outputs into passes of Vp with Uc + Vp - 1 <= M; chunk c / pass p uses the kernel
+// window g[n] = h[(v0 - u0) + n] for n in [-(M - Vp), Vp - 1].  When the tile spans the whole axis
+// and M = 2N - 2 one pass suffices (h even: the one colliding index holds the same value).
+// Cost per row O(M log M) instead of O(width * N): the dense GEMM stays faster for narrow tiles
+// (config 3), the chirp-z for full-width strips and large N (configs 4, 5).  fp32 FFT arithmetic;
+// chirp phases by exact integer reduction mod 4N (in double), kernel FFTs in fp64 on the host.
+#include "tvs_internal.h"
+
+#include <cmath>
+#include <complex>
+#include <vector>
+
+namespace tvs {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+// e^{i theta m}, m = v^2 + c v reduced exactly mod 4N (v^2 + c v < 2^53)
+__device__ __forceinline__ float2 chirp(int v, int c, double n4, double inv_n4, float inv_2n) {
+  const double x = (double)v * (double)v + (double)c * (double)v;
+  double r = x - floor(x * inv_n4) * n4;
+  if (r < 0.0) r += n4;
+  if (r >= n4) r -= n4;
+  float s, co;
+  sincospif((float)r * inv_2n, &s, &co);
+  return make_float2(co, s);
+}
+
+// In-place radix-4 DIF on z[M] (natural order in, base-4 digit-reversed out); tw[n] = e^{-2 pi i n/M}.
+__device__ void fft_dif4(float2 *z, int M, int logM4, const float2 *__restrict__ tw) {
+  const int nth = blockDim.x, tid = threadIdx.x;
+  for (int lg = logM4 - 1; lg >= 0; --lg) {
+    const int L = 1 << (2 * lg), s = M >> (2 * lg + 2);
+    for (int b = tid; b < (M >> 2); b += nth) {
+      const int blk = b >> (2 * lg), k = b & (L - 1);
+      const int i0 = (blk << (2 * lg + 2)) + k;
+      const float2 x0 = z[i0], x1 = z[i0 + L], x2 = z[i0 + 2 * L], x3 = z[i0 + 3 * L];
+      const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
+      const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
+      z[i0] = make_float2(a0.x + a2.x, a0.y + a2.y);
+      const float2 y1 = make_float2(a1.x + a3.y, a1.y - a3.x);   // a1 - i a3
+      const float2 y2 = make_float2(a0.x - a2.x, a0.y - a2.y);
+      const float2 y3 = make_float2(a1.x - a3.y, a1.y + a3.x);   // a1 + i a3
+      if (k == 0) {
+        z[i0 + L] = y1;
+        z[i0 + 2 * L] = y2;
+        z[i0 + 3 * L] = y3;
+      } else {
+        z[i0 + L] = cmul(y1, __ldg(tw + k * s));
+        z[i0 + 2 * L] = cmul(y2, __ldg(tw + 2 * k * s));
+        z[i0 + 3 * L] = cmul(y3, __ldg(tw + 3 * k * s));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
+// transform times M.
+__device__ void fft_dit4_inv(float2 *z, int M, int logM4, const float2 *__restrict__ tw) {
+  const int nth = blockDim.x, tid = threadIdx.x;
+  for (int lg = 0; lg < logM4; ++lg) {
+    const int L = 1 << (2 * lg), s = M >> (2 * lg + 2);
+    for (int b = tid; b < (M >> 2); b += nth) {
+      const int blk = b >> (2 * lg), k = b & (L - 1);
+      const int i0 = (blk << (2 * lg + 2)) + k;
+      const float2 x0 = z[i0];
+      float2 x1 = z[i0 + L], x2 = z[i0 + 2 * L], x3 = z[i0 + 3 * L];
+      if (k != 0) {
+        x1 = cmulc(x1, __ldg(tw + k * s));
+        x2 = cmulc(x2, __ldg(tw + 2 * k * s));
+        x3 = cmulc(x3, __ldg(tw + 3 * k * s));
+      }
+      const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
+      const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
+      z[i0] = make_float2(a0.x + a2.x, a0.y + a2.y);
+      z[i0 + L] = make_float2(a1.x - a3.y, a1.y + a3.x);        // a1 + i a3
+      z[i0 + 2 * L] = make_float2(a0.x - a2.x, a0.y - a2.y);
+      z[i0 + 3 * L] = make_float2(a1.x + a3.y, a1.y - a3.x);    // a1 - i a3
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int CZT_THREADS = 512;
+
+// One CTA per (row, job, output pass).  kind 0: forward cos (pre u^2, post v^2 + v(2tx0+1), Re);
+// kind 1: inverse cos (pre u^2 + u(2tx0+1), post v^2, Re); kind 2: inverse sin (pre u^2 +
+// u(2tx0+2), post v^2, Im).
+__global__ void __launch_bounds__(CZT_THREADS)
+k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gtab,
+      const float2 *__restrict__ tw) {
+  extern __shared__ float2 zsm[];
+  float *acc = reinterpret_cast<float *>(zsm + G.M);
+  const CztJob jb = jobs[blockIdx.y];
+  const int row = blockIdx.x;
+  if (row >= jb.rows) return;
+  const int v0 = blockIdx.z * G.Vp;
+  if (v0 >= jb.vlen) return;
+  const int vcnt = min(G.Vp, jb.vlen - v0);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const double n4 = 4.0 * G.N, inv_n4 = 1.0 / n4;
+  const float inv_2n = 1.0f / (2.0f * (float)G.N);
+  const int cpre = jb.kind == 0 ? 0 : 2 * jb.tx0 + jb.kind;   // kind 1: 2tx0+1, kind 2: 2tx0+2
+  const int cpost = jb.kind == 0 ? 2 * jb.tx0 + 1 : 0;
+  for (int i = tid; i < vcnt; i += nth) acc[i] = 0.f;
+  const float *__restrict__ in = jb.in + (size_t)row * jb.ldin;
+  const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
+  for (int uc = 0; uc < nuc; ++uc) {
+    const int u0 = uc * G.Uc, ucnt = min(G.Uc, jb.ulen - u0);
+    for (int i = tid; i < G.M; i += nth) {
+      float2 a = make_float2(0.f, 0.f);
+      if (i < ucnt) {
+        const float x = in[u0 + i];
+        const float2 c = chirp(u0 + i, cpre, n4, inv_n4, inv_2n);
+        a = make_float2(x * c.x, x * c.y);
+      }
+      zsm[i] = a;
+    }
+    __syncthreads();
+    fft_dif4(zsm, G.M, G.logM4, tw);
+    const float2 *__restrict__ gk = gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M;
+    for (int i = tid; i < G.M; i += nth) zsm[i] = cmul(zsm[i], __ldg(gk + i));
+    __syncthreads();
+    fft_dit4_inv(zsm, G.M, G.logM4, tw);
+    for (int i = tid; i < vcnt; i += nth) {
+      const float2 c = cmul(chirp(v0 + i, cpost, n4, inv_n4, inv_2n), zsm[i]);
+      acc[i] += jb.kind == 2 ? c.y : c.x;
+    }
+    __syncthreads();
+  }
+  float *__restrict__ out = jb.out + (size_t)row * jb.ldout + v0;
+  for (int i = tid; i < vcnt; i += nth) out[i] = acc[i];
+}
+
+// ------------------------------------------------------------------------------------ host side
+
+namespace {
+void fft64(std::vector<std::complex<double>> &a) {   // iterative radix-2, e^{-2 pi i / n}
+  const size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const double ang = -2.0 * M_PI / (double)len;
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < len / 2; ++k) {
+        const std::complex<double> w(std::cos(ang * k), std::sin(ang * k));
+        const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+int digitrev4(int n, int logM4) {
+  int r = 0;
+  for (int d = 0; d < logM4; ++d) {
+    r = r * 4 + (n & 3);
+    n >>= 2;
+  }
+  return r;
+}
+}  // namespace
+
+// Geometry for inputs of length <= ulen_max and outputs of length <= vlen_max on an axis of N.
+bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g) {
+  g->N = N;
+  auto pow4 = [](long long x) {
+    long long m = 4;
+    while (m < x) m <<= 2;
+    return m;
+  };
+  const long long trick = 2LL * N - 2;
+  if (ulen_max == N && vlen_max == N && trick <= max_m && pow4(trick) == trick) {
+    g->M = (int)trick;
+    g->Uc = g->Vp = N;
+  } else {
+    long long m = pow4((long long)ulen_max + vlen_max - 1);
+    if (m <= max_m) {
+      g->M = (int)m;
+      g->Uc = ulen_max;
+      g->Vp = (int)(m - ulen_max + 1);
+    } else {
+      g->M = max_m;
+      if (ulen_max <= max_m / 4) {          // narrow input (forward of a tile): output passes
+        g->Uc = ulen_max;
+        g->Vp = max_m - ulen_max + 1;
+      } else if (vlen_max <= max_m / 4) {   // narrow output (inverse to a tile): input chunks
+        g->Vp = vlen_max;
+        g->Uc = max_m - vlen_max + 1;
+      } else {
+        g->Uc = max_m / 2;
+        g->Vp = max_m / 2;
+      }
+    }
+  }
+  g->logM4 = 0;
+  while ((1 << (2 * g->logM4)) < g->M) ++g->logM4;
+  g->nuc = (ulen_max + g->Uc - 1) / g->Uc;
+  g->nvp = (vlen_max + g->Vp - 1) / g->Vp;
+  return (1 << (2 * g->logM4)) == g->M;
+}
+
+// Kernel tables: for output pass p and input chunk c the digit-reversed FFT of the circular window
+// g[n] = h[(p Vp - c Uc) + n], n in [-(M - Vp), Vp - 1], scaled by 1/M (fp64 on the host).
+void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw) {
+  const int M = g.M;
+  gtab.assign((size_t)g.nvp * g.nuc * M, make_float2(0.f, 0.f));
+  const long long n4 = 4LL * g.N;
+  std::vector<std::complex<double>> a(M);
+  for (int p = 0; p < g.nvp; ++p)
+    for (int c = 0; c < g.nuc; ++c) {
+      const long long d = (long long)p * g.Vp - (long long)c * g.Uc;
+      for (int i = 0; i < M; ++i) {
+        const long long n = i < g.Vp ? i : (long long)i - M;
+        const long long m = d + n;
+        long long r = ((m % n4) * (m % n4)) % n4;   // m^2 mod 4N exactly
+        if (r < 0) r += n4;
+        const double ph = -M_PI * (double)r / (2.0 * g.N);
+        a[i] = std::complex<double>(std::cos(ph), std::sin(ph));
+      }
+      fft64(a);
+      float2 *dst = gtab.data() + (size_t)(p * g.nuc + c) * M;
+      for (int k = 0; k < M; ++k) {
+        const std::complex<double> v = a[k] / (double)M;
+        dst[digitrev4(k, g.logM4)] = make_float2((float)v.real(), (float)v.imag());
+      }
+    }
+  tw.resize((size_t)M);
+  for (int n = 0; n < M; ++n) {
+    const double ph = -2.0 * M_PI * (double)n / (double)M;
+    tw[n] = make_float2((float)std::cos(ph), (float)std::sin(ph));
+  }
+}
+
+cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
+                       const float2 *gtab, const float2 *tw, cudaStream_t s) {
+  const size_t smem = (size_t)g.M * sizeof(float2) + (size_t)g.Vp * sizeof(float);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_czt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
+  k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, g, gtab, tw);
+  return cudaGetLastError();
+}
+
+}  // namespace tvs

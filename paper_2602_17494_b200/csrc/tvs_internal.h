@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace tvs {
 
 // One overlapping subdomain Gamma_m of the step grid (Omega~ for step 1, Omega for step 2).
@@ -53,6 +55,26 @@ struct alignas(64) TmaGemmDesc {
 // host: encode the four tensor maps of d for a tile of width bn
 cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn);
 
+// Chirp-z evaluation of the partial x-DCTs (tvs_czt.cu).  One job = `rows` rows of one tile:
+// out[row][v] = Op(post[v] sum_u in[row][u] pre[u] h[v-u]) for u < ulen, v < vlen (see the file
+// header); kind 0 forward cos, 1 inverse cos, 2 inverse sin; tx0 = first global column of the tile.
+struct CztJob {
+  const float *in;
+  float *out;
+  int rows, ldin, ldout;
+  int tx0, ulen, vlen, kind;
+};
+struct CztGeom {
+  int N;          // axis length (theta = pi / (2N))
+  int M, logM4;   // FFT size (power of 4) and log4 M
+  int Uc, Vp;     // input chunk and output pass lengths (Uc + Vp - 1 <= M, or the M = 2N-2 case)
+  int nuc, nvp;   // numbers of chunks / passes for the largest job
+};
+bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g);
+void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw);
+cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
+                       const float2 *gtab, const float2 *tw, cudaStream_t s);
+
 // Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
 struct Geo {
   int M;          // number of subdomains in the batch
@@ -91,6 +113,13 @@ cudaError_t launch_recover2(const float *d0, const float *p1, const float *p2, i
 cudaError_t launch_irv1_f(const float *tau1, const float *tau2, int ldt, const float *d0, int n2,
                           int n1, float alpha, float eps, float *f, float *dxi, int ldf,
                           cudaStream_t s);
+
+// dual energies (deterministic fp64 reductions; part has >= 592 doubles, out one double)
+cudaError_t launch_dual_energy2(const float *p1, const float *p2, const float *f, int ld, int n2,
+                                int n1, int row0, int row1, double *part, double *out,
+                                cudaStream_t s);
+cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
+                          double *part, double *out, cudaStream_t s);
 
 // step 1
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,

@@ -1,0 +1,73 @@
+"""Chirp-z form of the partial x-DCTs (tvs_czt.cu) forced on every projection
+batch (TVS_DCT=czt) and compared with the fp64 oracle at the north-star tolerances, on ragged
+layouts (several chunk / pass geometries), config 2 in full and config 3 at full size."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import solvers as S
+from tvs_synth import CONFIGS, random_image
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import check_step1, check_step2   # noqa: E402
+
+
+def _context(**env):
+    import paper_2602_17494_b200 as pkg
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return pkg.Context(0)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = _context(TVS_DCT="czt")
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_chunked():
+    """FFT size capped at 64 points: every small case runs several input chunks / output passes."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = _context(TVS_DCT="czt", TVS_CZT_MAXM="64")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("shape,L", [((16, 16), (1, 1, 0, 0)), ((24, 20), (2, 2, 4, 4)),
+                                     ((37, 53), (3, 2, 3, 5)), ((40, 18), (4, 1, 4, 0)),
+                                     ((18, 40), (1, 4, 0, 3)), ((2, 2), (1, 1, 0, 0)),
+                                     ((63, 63), (1, 1, 0, 0)), ((127, 127), (4, 1, 6, 0))])
+def test_step1_czt_small(ctx, ctx_chunked, shape, L):
+    img = random_image(*shape, seed=shape[0] * 7 + shape[1] + 1)
+    check_step1(ctx, img, 0.05, L, 3, 4)
+    check_step1(ctx_chunked, img, 0.05, L, 3, 4)
+
+
+def test_config2_czt(ctx):
+    c = CONFIGS["c2"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    tau_ref, _ = check_step1(ctx, img, c.delta, L, c.sweeps, c.inner)
+    check_step2(ctx, img, tau_ref, c.lam, L, c.sweeps, c.inner)
+
+
+def test_config3_czt_full_size(ctx):
+    c = CONFIGS["c3"]
+    img = c.image()
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    check_step1(ctx, img, c.delta, L, 1, 2)

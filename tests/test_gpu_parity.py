@@ -58,7 +58,7 @@ def _primal2(d, d0, tau, lam, variant="irv2", eps=1e-3):
 def check_step1(ctx, img, delta, L, sweeps, inner, t=0.125):
     n2, n1 = img.shape
     lay = olayout.Layout(n2, n1, *L)
-    tau_ref, p_ref, _ = S.dd_step1(img.astype(np.float64), delta, lay, sweeps, inner, t)
+    tau_ref, p_ref, info = S.dd_step1(img.astype(np.float64), delta, lay, sweeps, inner, t)
     tau, p, st = ctx.tv_stokes_step1(_dev(img), delta, L, (sweeps, inner, t), want_p=True)
     tau, p = tau.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
     e_tau = np.abs(tau - tau_ref).max()
@@ -71,6 +71,10 @@ def check_step1(ctx, img, delta, L, sweeps, inner, t=0.125):
     assert e_tau <= TOL, f"max|tau - oracle| = {e_tau}"
     assert e_p <= P_TOL, f"max|p - oracle| = {e_p}"
     assert rel <= TOL, f"relative E1 error {rel}"
+    # the dual objective D_TFS of the returned p, reduced on the device (tvs_stats.dual_energy)
+    D_ref = info["dual_energy"]
+    assert abs(st.dual_energy - D_ref) <= TOL * max(D_ref, 1e-12), (st.dual_energy, D_ref)
+    assert st.sweeps_run == sweeps
     return tau_ref, st
 
 
@@ -79,8 +83,8 @@ def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125, variant="irv2", e
     lay = olayout.Layout(n2, n1, *L)
     # both sides consume the same fp32 tau
     tau = np.asarray(tau, np.float32).astype(np.float64)
-    d_ref, p_ref, _ = S.dd_step2(img.astype(np.float64), tau, lam, lay, sweeps, inner, t,
-                                 variant=variant, eps=eps)
+    d_ref, p_ref, info = S.dd_step2(img.astype(np.float64), tau, lam, lay, sweeps, inner, t,
+                                    variant=variant, eps=eps)
     d, p, st = ctx.tv_stokes_step2(_dev(tau), _dev(img), lam, L, (sweeps, inner, t), want_p=True,
                                    variant=variant, eps=eps)
     d, p = d.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
@@ -94,6 +98,9 @@ def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125, variant="irv2", e
     assert e_d <= TOL, f"max|d - oracle| = {e_d}"
     assert e_p <= P_TOL, f"max|p - oracle| = {e_p}"
     assert rel <= TOL, f"relative E2 error {rel}"
+    D_ref = info["dual_energy"]
+    assert abs(st.dual_energy - D_ref) <= TOL * max(D_ref, 1e-12), (st.dual_energy, D_ref)
+    assert st.sweeps_run == sweeps
     return st
 
 
@@ -143,6 +150,53 @@ def test_global_projection_only(ctx):
     ref = spectral.project(S.tau0(img.astype(np.float64)))
     assert np.abs(tau.cpu().numpy() - ref).max() < 1e-5
     assert np.abs(ops.div(tau.cpu().numpy().astype(np.float64))).max() < 1e-5
+
+
+def _crit_values(energies, npts, cfac, crit):
+    e = energies
+    if crit == 1:
+        return [abs(np.sqrt(a) - np.sqrt(b)) / np.sqrt(cfac * npts) for a, b in zip(e, e[1:])]
+    return [abs(a * a - b * b) / npts for a, b in zip(e, e[1:])]
+
+
+@pytest.mark.parametrize("crit", [1, 2])
+def test_stopping_rules_match_oracle(ctx, crit):
+    """tvs_set_stopping: the device energies trigger the same outer sweep as the oracle's rule
+    (sections 5.2 / 6.3).  tol sits halfway (geometric mean) between two
+    consecutive criterion values that differ by > 20 %, so fp32 rounding cannot flip the sweep."""
+    img = random_image(40, 36, 12)
+    L = (2, 2, 4, 4)
+    n2, n1 = img.shape
+    lay = olayout.Layout(n2, n1, *L)
+    d0 = img.astype(np.float64)
+    # step 2
+    tau, _ = S.chambolle_tfs(d0, 0.05, 40)
+    tau = tau.astype(np.float32).astype(np.float64)
+    _, _, tr = S.dd_step2(d0, tau, 0.1, lay, 12, 4, trace=True)
+    f = S.step2_data(d0, tau, 0.1)[1]
+    cv = _crit_values([ops.inner(f, f)] + tr["energies"], n2 * n1, 1.0, crit)
+    k = next(i for i in range(3, len(cv)) if cv[i] < 0.8 * cv[i - 1] and min(cv[:i]) > cv[i - 1] * 0.99)
+    tol = float(np.sqrt(cv[k] * cv[k - 1]))
+    _, _, ref = S.dd_step2(d0, tau, 0.1, lay, 12, 4, stop=(crit, tol))
+    try:
+        ctx.set_stopping(crit, tol)
+        _, _, st = ctx.tv_stokes_step2(_dev(tau), _dev(img), 0.1, L, (12, 4, 0.125))
+    finally:
+        ctx.set_stopping(0, 0.0)
+    assert ref["sweeps_run"] < 12 and st.sweeps_run == ref["sweeps_run"], (st.sweeps_run, ref["sweeps_run"])
+    # step 1
+    _, _, tr1 = S.dd_step1(d0, 0.05, lay, 8, 3, trace=True)
+    f1 = tr1["f"]
+    cv1 = _crit_values([ops.inner(f1, f1)] + tr1["energies"], (n2 + 1) * (n1 + 1), 2.0, crit)
+    k1 = next(i for i in range(2, len(cv1)) if cv1[i] < 0.8 * cv1[i - 1] and min(cv1[:i]) > cv1[i - 1] * 0.99)
+    tol1 = float(np.sqrt(cv1[k1] * cv1[k1 - 1]))
+    _, _, ref1 = S.dd_step1(d0, 0.05, lay, 8, 3, stop=(crit, tol1))
+    try:
+        ctx.set_stopping(crit, tol1)
+        _, _, st1 = ctx.tv_stokes_step1(_dev(img), 0.05, L, (8, 3, 0.125))
+    finally:
+        ctx.set_stopping(0, 0.0)
+    assert ref1["sweeps_run"] < 8 and st1.sweeps_run == ref1["sweeps_run"], (st1.sweeps_run, ref1["sweeps_run"])
 
 
 def test_constant_image(ctx):

@@ -233,3 +233,40 @@ def test_irv1_schwarz_1x1_equals_chambolle_and_dd_converges():
     e = [np.abs(S.dd_step2(d0, tau, 0.1, lay, n, 10, variant="irv1")[0] - ref).max()
          for n in (10, 300)]
     assert e[1] < 0.2 * e[0]
+
+
+# ----------------------------------------------------------------------------- stopping rules (NEXT 3)
+
+def test_stopping_rules_bracket_the_fixed_schedule():
+    """tol = 0 never fires (the fixed schedule, reading A10); a huge tol fires after the first
+    comparison (step 2: after sweep 1, step 1: before sweep 2's inner loop, i.e. 1 sweep run); the
+    sweep at which criterion 1 fires is the first n with |D_n^{1/2} - D_{n+1}^{1/2}| below
+    |Omega|^{1/2} tol, recomputed here from the traced energies."""
+    d0 = random_image(14, 13, 3).astype(np.float64)
+    lay = layout.Layout(14, 13, 2, 2, 3, 3)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 50)
+    _, _, i0 = S.dd_step2(d0, tau, 0.1, lay, 12, 4, stop=(1, 0.0))
+    assert i0["sweeps_run"] == 12
+    _, _, i1 = S.dd_step2(d0, tau, 0.1, lay, 12, 4, stop=(1, 1e9))
+    assert i1["sweeps_run"] == 1
+    _, _, tr = S.dd_step2(d0, tau, 0.1, lay, 12, 4, trace=True)
+    e = [S.ops.inner(S.step2_data(d0, tau, 0.1)[1], S.step2_data(d0, tau, 0.1)[1])] + tr["energies"]
+    crit = [abs(np.sqrt(a) - np.sqrt(b)) / np.sqrt(14 * 13) for a, b in zip(e, e[1:])]
+    tol = 0.5 * (crit[4] + crit[5])
+    assert crit[5] < tol and all(c > tol for c in crit[:5])   # the criterion decreases here
+    _, _, i2 = S.dd_step2(d0, tau, 0.1, lay, 12, 4, stop=(1, tol))
+    assert i2["sweeps_run"] == 6
+    _, _, j0 = S.dd_step1(d0, 0.05, lay, 4, 3, stop=(2, 0.0))
+    assert j0["sweeps_run"] == 4
+    _, _, j1 = S.dd_step1(d0, 0.05, lay, 4, 3, stop=(2, 1e30))
+    assert j1["sweeps_run"] == 1
+
+
+def test_reported_dual_energy_is_the_objective():
+    """info['dual_energy'] is D(p) of Eqs. tfsdualdis / ir2dualdis of the returned p."""
+    d0 = random_image(10, 11, 5).astype(np.float64)
+    lay = layout.Layout(10, 11, 2, 2, 3, 3)
+    tau, p1, i1 = S.dd_step1(d0, 0.05, lay, 3, 3)
+    assert abs(i1["dual_energy"] - S.dual_energy_tfs(p1, i1["f"])) < 1e-10 * i1["dual_energy"]
+    d, p2, i2 = S.dd_step2(d0, tau, 0.1, lay, 3, 3)
+    assert abs(i2["dual_energy"] - S.dual_energy_irv2(p2, i2["f"])) < 1e-10 * i2["dual_energy"]
