@@ -171,7 +171,8 @@ tvs_status tvs_reset_kernel_times(tvs_ctx *ctx);
 /* Diagnostics: run the projection GEMM (impl 0 = SIMT fp32, 1 = tcgen05 3xTF32 with 128-wide
  * tiles, 2 = tcgen05 3xTF32 with 144-wide tiles, 3 = tcgen05 3xTF32 on pre-split hi/lo operands
  * with the cp.async pipeline, 4 = the same through TMA tensor maps, 5 = the persistent
- * warp-specialised TMA kernel that splits A in shared memory -- the production path) on seeded
+ * warp-specialised TMA kernel that splits A in shared memory -- the production path, 6 = the
+ * same with A split into tensor memory and read by the MMA from there) on seeded
  * random A[M x K], B[K x N] and return
  * max_ij |C - C_fp64| / sum_k |A_ik B_kj| (host reference).  Test-only; allocates its own memory. */
 tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int32_t impl,

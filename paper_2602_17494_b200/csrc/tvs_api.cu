@@ -247,11 +247,11 @@ struct tvs_ctx {
   std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
   std::map<int, std::unique_ptr<Tables>> tables;
   bool profiling = false;
-  // projection contractions: TVS_GEMM = persistent (default: TMA + tcgen05 3xTF32, A split in
-  // shared memory, overlapped epilogue), tma (pre-split hi/lo operand planes), cpasync (cp.async +
-  // tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
-  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3 };
-  int gemm = G_PERSIST;
+  // projection contractions: TVS_GEMM = ts (default: persistent TMA + tcgen05 3xTF32 with A split
+  // into tensor memory), persistent (A split in shared memory), tma (pre-split hi/lo operand
+  // planes), cpasync (cp.async + tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
+  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3, G_TS = 4 };
+  int gemm = G_TS;
   bool presplit() const { return gemm == G_CPASYNC || gemm == G_TMA; }
   // partial x-DCTs: 0 = choose per batch by estimated time, 1 = dense GEMM, 2 = chirp-z (TVS_DCT)
   int dct_mode = 0;
@@ -830,6 +830,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
     switch (gm) {
       case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
+      case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       default: return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
@@ -852,6 +853,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
     switch (gm) {
       case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+      case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       default: return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
@@ -925,6 +927,11 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_g_row0(tau2, ldt, n1, P->g0, s); }));
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, s);
+    }));
+    // zero-mean g (reading A3): only the constant of f moves, so the dual energy D_IRV2 matches
+    // the oracle's convention (the iteration itself depends on grad f only)
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_irv2_zero_mean_g(P->f, ld, d0, n2, n1, alpha, P->d_part, P->d_energy + 1, s);
     }));
   }
   CK(cudaMemsetAsync(P->p, 0, 2 * pl * sizeof(float), s));
@@ -1123,11 +1130,12 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->rank = rank;
   c->world = world;
   const char *g = getenv("TVS_GEMM");
-  c->gemm = !g                          ? tvs_ctx::G_PERSIST
+  c->gemm = !g                          ? tvs_ctx::G_TS
             : strcmp(g, "simt") == 0    ? tvs_ctx::G_SIMT
             : strcmp(g, "cpasync") == 0 ? tvs_ctx::G_CPASYNC
             : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
-                                        : tvs_ctx::G_PERSIST;
+            : strcmp(g, "persistent") == 0 ? tvs_ctx::G_PERSIST
+                                        : tvs_ctx::G_TS;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {
@@ -1343,7 +1351,7 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
       {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
   TRY(upload(ctx, own, &dd, desc));
   cudaError_t e;
-  if (impl == 5) {   // persistent TMA kernel: A as one fp32 plane, split in shared memory
+  if (impl == 5 || impl == 6) {   // persistent TMA kernels: A as one fp32 plane, split on chip
     auto rna = [](float x) {
       uint32_t u;
       memcpy(&u, &x, 4);
@@ -1362,7 +1370,7 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
     CK(make_tma_desc(&d3[0], g2, 144));
     TmaGemmDesc *dd3;
     TRY(upload(ctx, own, &dd3, d3));
-    e = launch_gemm_tma_p(dd3, 1, M, N, 144, 0);
+    e = impl == 5 ? launch_gemm_tma_p(dd3, 1, M, N, 144, 0) : launch_gemm_tma_ts(dd3, 1, M, N, 144, 0);
   } else if (impl == 3 || impl == 4) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
     auto rna = [](float x) {
       uint32_t u;

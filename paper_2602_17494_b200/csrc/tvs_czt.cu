@@ -40,57 +40,144 @@ __device__ __forceinline__ float2 chirp(int v, int c, double n4, double inv_n4, 
   return make_float2(co, s);
 }
 
-// In-place radix-4 DIF on z[M] (natural order in, base-4 digit-reversed out); tw[n] = e^{-2 pi i n/M}.
-__device__ void fft_dif4(float2 *z, int M, int logM4, const float2 *__restrict__ tw) {
+// Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
+// makes every access pattern below at most 2-way bank-conflicted.
+__device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
+
+// Twiddle w^n = e^{-2 pi i n / M} from a two-level table in shared memory:
+// fine[n & 255] * coarse[n >> 8] (fine: 256 entries, coarse: M/256).
+struct Tw {
+  const float2 *fine, *coarse;
+  __device__ __forceinline__ float2 operator()(int n) const {
+    const float2 f = fine[n & 255];
+    return (n >> 8) ? cmul(f, coarse[n >> 8]) : f;
+  }
+};
+
+__device__ __forceinline__ void bfly4_dif(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+  const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
+  const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
+  x0 = make_float2(a0.x + a2.x, a0.y + a2.y);
+  x1 = make_float2(a1.x + a3.y, a1.y - a3.x);   // a1 - i a3
+  x2 = make_float2(a0.x - a2.x, a0.y - a2.y);
+  x3 = make_float2(a1.x - a3.y, a1.y + a3.x);   // a1 + i a3
+}
+__device__ __forceinline__ void bfly4_dit(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+  const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
+  const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
+  x0 = make_float2(a0.x + a2.x, a0.y + a2.y);
+  x1 = make_float2(a1.x - a3.y, a1.y + a3.x);   // a1 + i a3
+  x2 = make_float2(a0.x - a2.x, a0.y - a2.y);
+  x3 = make_float2(a1.x + a3.y, a1.y - a3.x);   // a1 - i a3
+}
+
+// In-place radix-4 DIF on z (natural order in, base-4 digit-reversed out).  Consecutive stage
+// pairs (spans L and L/4) are fused: a thread loads the 16 elements {base + m L/4} that the two
+// stages mix, runs both in registers and stores them back (one shared-memory round trip per
+// pair); an odd number of stages ends with one plain radix-4 stage (span 1).
+// e^{-2 pi i e / 16} for compile-time e (the fixed part of a fused pair's twiddles)
+__device__ __forceinline__ float2 w16(int e) {
+  constexpr float C[16] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                           0.f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                           -1.f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                           0.f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  return make_float2(C[e & 15], -C[(e + 12) & 15]);   // sin(x) = cos(x - pi/2)
+}
+
+__device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
   const int nth = blockDim.x, tid = threadIdx.x;
-  for (int lg = logM4 - 1; lg >= 0; --lg) {
-    const int L = 1 << (2 * lg), s = M >> (2 * lg + 2);
-    for (int b = tid; b < (M >> 2); b += nth) {
-      const int blk = b >> (2 * lg), k = b & (L - 1);
-      const int i0 = (blk << (2 * lg + 2)) + k;
-      const float2 x0 = z[i0], x1 = z[i0 + L], x2 = z[i0 + 2 * L], x3 = z[i0 + 3 * L];
-      const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
-      const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
-      z[i0] = make_float2(a0.x + a2.x, a0.y + a2.y);
-      const float2 y1 = make_float2(a1.x + a3.y, a1.y - a3.x);   // a1 - i a3
-      const float2 y2 = make_float2(a0.x - a2.x, a0.y - a2.y);
-      const float2 y3 = make_float2(a1.x - a3.y, a1.y + a3.x);   // a1 + i a3
-      if (k == 0) {
-        z[i0 + L] = y1;
-        z[i0 + 2 * L] = y2;
-        z[i0 + 3 * L] = y3;
-      } else {
-        z[i0 + L] = cmul(y1, __ldg(tw + k * s));
-        z[i0 + 2 * L] = cmul(y2, __ldg(tw + 2 * k * s));
-        z[i0 + 3 * L] = cmul(y3, __ldg(tw + 3 * k * s));
+  int lg = logM4 - 1;
+  for (; lg >= 1; lg -= 2) {
+    const int L = 1 << (2 * lg), Q = L >> 2, s1 = M >> (2 * lg + 2);
+    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+      const int blk = gidx >> (2 * lg - 2), kp = gidx & (Q - 1);
+      const int base = blk * 4 * L + kp;
+      float2 x[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m * Q)];
+      // twiddles of the pair from one lookup: stage 1 (span L, k = kp + r Q) uses
+      // w^{c k s1} = W^c * e^{-2 pi i c r / 16} with W = w^{kp s1}; stage 2 (span Q, k = kp,
+      // stride 4 s1) uses W^{4c}.
+      const float2 W1 = tw(kp * s1), W2 = cmul(W1, W1), W3 = cmul(W1, W2);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        bfly4_dif(x[r], x[r + 4], x[r + 8], x[r + 12]);
+        x[r + 4] = cmul(x[r + 4], r ? cmul(W1, w16(r)) : W1);
+        x[r + 8] = cmul(x[r + 8], r ? cmul(W2, w16(2 * r)) : W2);
+        x[r + 12] = cmul(x[r + 12], r ? cmul(W3, w16(3 * r)) : W3);
       }
+      const float2 V1 = cmul(W2, W2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        bfly4_dif(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
+        x[4 * t + 1] = cmul(x[4 * t + 1], V1);
+        x[4 * t + 2] = cmul(x[4 * t + 2], V2);
+        x[4 * t + 3] = cmul(x[4 * t + 3], V3);
+      }
+#pragma unroll
+      for (int m = 0; m < 16; ++m) z[pz(base + m * Q)] = x[m];
+    }
+    __syncthreads();
+  }
+  if (lg == 0) {   // span 1 (no twiddles)
+    for (int b = tid; b < (M >> 2); b += nth) {
+      float2 x0 = z[pz(4 * b)], x1 = z[pz(4 * b + 1)], x2 = z[pz(4 * b + 2)], x3 = z[pz(4 * b + 3)];
+      bfly4_dif(x0, x1, x2, x3);
+      z[pz(4 * b)] = x0;
+      z[pz(4 * b + 1)] = x1;
+      z[pz(4 * b + 2)] = x2;
+      z[pz(4 * b + 3)] = x3;
     }
     __syncthreads();
   }
 }
 
 // In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
-// transform times M.
-__device__ void fft_dit4_inv(float2 *z, int M, int logM4, const float2 *__restrict__ tw) {
+// transform times M.  Mirror image of fft_dif (span 1 first when the stage count is odd, then
+// fused pairs of spans L and 4L).
+__device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
   const int nth = blockDim.x, tid = threadIdx.x;
-  for (int lg = 0; lg < logM4; ++lg) {
-    const int L = 1 << (2 * lg), s = M >> (2 * lg + 2);
+  int lg = 0;
+  if (logM4 & 1) {
     for (int b = tid; b < (M >> 2); b += nth) {
-      const int blk = b >> (2 * lg), k = b & (L - 1);
-      const int i0 = (blk << (2 * lg + 2)) + k;
-      const float2 x0 = z[i0];
-      float2 x1 = z[i0 + L], x2 = z[i0 + 2 * L], x3 = z[i0 + 3 * L];
-      if (k != 0) {
-        x1 = cmulc(x1, __ldg(tw + k * s));
-        x2 = cmulc(x2, __ldg(tw + 2 * k * s));
-        x3 = cmulc(x3, __ldg(tw + 3 * k * s));
+      float2 x0 = z[pz(4 * b)], x1 = z[pz(4 * b + 1)], x2 = z[pz(4 * b + 2)], x3 = z[pz(4 * b + 3)];
+      bfly4_dit(x0, x1, x2, x3);
+      z[pz(4 * b)] = x0;
+      z[pz(4 * b + 1)] = x1;
+      z[pz(4 * b + 2)] = x2;
+      z[pz(4 * b + 3)] = x3;
+    }
+    __syncthreads();
+    lg = 1;
+  }
+  for (; lg < logM4; lg += 2) {
+    const int L = 1 << (2 * lg), s2 = M >> (2 * lg + 4);
+    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+      const int blk = gidx >> (2 * lg), kp = gidx & (L - 1);
+      const int base = blk * 16 * L + kp;
+      float2 x[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m * L)];
+      // stage 2 (span 4L, k = kp + r L, stride s2) uses U^c e^{-2 pi i c r/16}, U = w^{kp s2};
+      // stage 1 (span L, k = kp, stride 4 s2) uses U^{4c}
+      const float2 U1 = tw(kp * s2), U2 = cmul(U1, U1), U3 = cmul(U1, U2);
+      const float2 V1 = cmul(U2, U2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {   // span L, k = kp
+        x[4 * t + 1] = cmulc(x[4 * t + 1], V1);
+        x[4 * t + 2] = cmulc(x[4 * t + 2], V2);
+        x[4 * t + 3] = cmulc(x[4 * t + 3], V3);
+        bfly4_dit(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
       }
-      const float2 a0 = make_float2(x0.x + x2.x, x0.y + x2.y), a1 = make_float2(x0.x - x2.x, x0.y - x2.y);
-      const float2 a2 = make_float2(x1.x + x3.x, x1.y + x3.y), a3 = make_float2(x1.x - x3.x, x1.y - x3.y);
-      z[i0] = make_float2(a0.x + a2.x, a0.y + a2.y);
-      z[i0 + L] = make_float2(a1.x - a3.y, a1.y + a3.x);        // a1 + i a3
-      z[i0 + 2 * L] = make_float2(a0.x - a2.x, a0.y - a2.y);
-      z[i0 + 3 * L] = make_float2(a1.x + a3.y, a1.y - a3.x);    // a1 - i a3
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // span 4L, k = kp + r L
+        x[r + 4] = cmulc(x[r + 4], r ? cmul(U1, w16(r)) : U1);
+        x[r + 8] = cmulc(x[r + 8], r ? cmul(U2, w16(2 * r)) : U2);
+        x[r + 12] = cmulc(x[r + 12], r ? cmul(U3, w16(3 * r)) : U3);
+        bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
+      }
+#pragma unroll
+      for (int m = 0; m < 16; ++m) z[pz(base + m * L)] = x[m];
     }
     __syncthreads();
   }
@@ -105,7 +192,9 @@ __global__ void __launch_bounds__(CZT_THREADS)
 k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gtab,
       const float2 *__restrict__ tw) {
   extern __shared__ float2 zsm[];
-  float *acc = reinterpret_cast<float *>(zsm + G.M);
+  const int MP = G.M + (G.M >> 4);                     // padded FFT buffer
+  float2 *tfine = zsm + MP, *tcoarse = tfine + 256;      // twiddle tables
+  float *acc = reinterpret_cast<float *>(tcoarse + (G.M >> 8) + 1);
   const CztJob jb = jobs[blockIdx.y];
   const int row = blockIdx.x;
   if (row >= jb.rows) return;
@@ -118,6 +207,9 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   const int cpre = jb.kind == 0 ? 0 : 2 * jb.tx0 + jb.kind;   // kind 1: 2tx0+1, kind 2: 2tx0+2
   const int cpost = jb.kind == 0 ? 2 * jb.tx0 + 1 : 0;
   for (int i = tid; i < vcnt; i += nth) acc[i] = 0.f;
+  for (int i = tid; i < 256; i += nth) tfine[i] = i < G.M ? __ldg(tw + i) : make_float2(1.f, 0.f);
+  for (int i = tid; i <= (G.M >> 8); i += nth) tcoarse[i] = (i << 8) < G.M ? __ldg(tw + (i << 8)) : make_float2(1.f, 0.f);
+  const Tw twd{tfine, tcoarse};
   const float *__restrict__ in = jb.in + (size_t)row * jb.ldin;
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
   for (int uc = 0; uc < nuc; ++uc) {
@@ -129,16 +221,16 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
         const float2 c = chirp(u0 + i, cpre, n4, inv_n4, inv_2n);
         a = make_float2(x * c.x, x * c.y);
       }
-      zsm[i] = a;
+      zsm[pz(i)] = a;
     }
     __syncthreads();
-    fft_dif4(zsm, G.M, G.logM4, tw);
+    fft_dif(zsm, G.M, G.logM4, twd);
     const float2 *__restrict__ gk = gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M;
-    for (int i = tid; i < G.M; i += nth) zsm[i] = cmul(zsm[i], __ldg(gk + i));
+    for (int i = tid; i < G.M; i += nth) zsm[pz(i)] = cmul(zsm[pz(i)], __ldg(gk + i));
     __syncthreads();
-    fft_dit4_inv(zsm, G.M, G.logM4, tw);
+    fft_dit_inv(zsm, G.M, G.logM4, twd);
     for (int i = tid; i < vcnt; i += nth) {
-      const float2 c = cmul(chirp(v0 + i, cpost, n4, inv_n4, inv_2n), zsm[i]);
+      const float2 c = cmul(chirp(v0 + i, cpost, n4, inv_n4, inv_2n), zsm[pz(i)]);
       acc[i] += jb.kind == 2 ? c.y : c.x;
     }
     __syncthreads();
@@ -252,7 +344,8 @@ void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2>
 
 cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
                        const float2 *gtab, const float2 *tw, cudaStream_t s) {
-  const size_t smem = (size_t)g.M * sizeof(float2) + (size_t)g.Vp * sizeof(float);
+  const size_t smem = (size_t)(g.M + (g.M >> 4) + 256 + (g.M >> 8) + 1) * sizeof(float2) +
+                      (size_t)g.Vp * sizeof(float);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_czt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

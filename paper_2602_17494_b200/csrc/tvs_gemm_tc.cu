@@ -865,7 +865,263 @@ static cudaError_t launch_tma_p(const TmaGemmDesc *descs, int batch, int maxM, i
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// TS form (A in tensor memory): same persistent roles as k_gemm_tma_p, but the split warps write
+// A_hi / A_lo into TMEM with tcgen05.st and the MMAs read A from TMEM ([a-tmem] operand), so the
+// tensor core reads only B from shared memory and a shared-memory stage holds A raw + B hi/lo
+// (52 KB: four stages in flight instead of three).  TMEM: accumulators at columns 0 and 256
+// (BN = 144 each), A slots (hi 32 + lo 32 columns) at 144 and 400.
+constexpr int QSTAGES = 4;
+
+template <int BN>
+struct QSmem {
+  static constexpr int A_BYTES = BM * TBK * 4;                 // 16 KB (raw fp32 A)
+  static constexpr int B_BYTES = BN * TBK * 4;
+  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;          // A raw, B hi, B lo
+  static constexpr int TX = STAGE;
+  static constexpr int TOTAL = QSTAGES * STAGE + 256 + 1024;
+};
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accumulate) {
+  uint32_t z = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate), "r"(z), "r"(z), "r"(z), "r"(z)
+      : "memory");
+}
+
+#define TST32(addr, v)                                                                              \
+  asm volatile(                                                                                     \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),               \
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),       \
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), \
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),          \
+      "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),          \
+      "r"(v[30]), "r"(v[31])                                                                        \
+      : "memory")
+
+template <int BN>
+__global__ void __launch_bounds__(PNT, 1)
+k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int nblocks) {
+  static_assert(BN <= 144, "TMEM column plan assumes BN <= 144");
+  using SM = QSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + QSTAGES * SM::STAGE);
+  uint64_t *empty = full + QSTAGES;       // smem stage free (MMA done)
+  uint64_t *aful = empty + QSTAGES;       // [2] TMEM A slot written
+  uint64_t *aemp = aful + 2;              // [2] TMEM A slot free (MMA done)
+  uint64_t *accf = aemp + 2;              // [2]
+  uint64_t *acce = accf + 2;              // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int q = 0; q < QSTAGES; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&aful[b], 1);
+      mbar_init(&aemp[b], 1);
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t ACC[2] = {0u, 256u}, ASLOT[2] = {144u, 400u};
+  const int per = mblocks * nblocks, ntiles = batch * per;
+  auto decode = [&](int t, const TmaGemmDesc *&dp, int &m0, int &n0) {
+    const int z = t / per, r = t - z * per;
+    dp = descs + z;
+    m0 = (r / nblocks) * BM;
+    n0 = (r % nblocks) * BN;
+    return m0 < dp->M && n0 < dp->N;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TmaGemmDesc *dp;
+        int m0, n0;
+        if (!decode(t, dp, m0, n0)) continue;
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int q = it % QSTAGES;
+          if (it >= QSTAGES) mbar_wait(&empty[q], ((it / QSTAGES) - 1) & 1);
+          mbar_expect_tx(&full[q], SM::TX);
+          const uint32_t st = sbase + q * SM::STAGE;
+          tma_load_2d(st, &dp->a_hi, kt * TBK, m0, &full[q]);
+          tma_load_2d(st + SM::A_BYTES, &dp->b_hi, kt * TBK, n0, &full[q]);
+          tma_load_2d(st + SM::A_BYTES + SM::B_BYTES, &dp->b_lo, kt * TBK, n0, &full[q]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ------------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC = make_idesc(BM, BN);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TmaGemmDesc *dp;
+        int m0, n0;
+        if (!decode(t, dp, m0, n0)) continue;
+        const int b = tc & 1;
+        if (tc >= 2) mbar_wait(&acce[b], ((tc >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + ACC[b];
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int q = it % QSTAGES, a = it & 1;
+          mbar_wait(&full[q], (it / QSTAGES) & 1);   // B landed (TMA, async proxy)
+          mbar_wait(&aful[a], (it >> 1) & 1);        // A slot written to TMEM
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = sbase + q * SM::STAGE;
+          const uint32_t bhi = st + SM::A_BYTES, blo = bhi + SM::B_BYTES;
+          const uint32_t ahi = tmem + ASLOT[a], alo = ahi + 32;
+#pragma unroll
+          for (int ks = 0; ks < TBK / 8; ++ks) {
+            const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
+            mma_tf32_ts(acc, alo + 8 * ks, dbh, IDESC, (kt > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32_ts(acc, ahi + 8 * ks, dbl, IDESC, 1u);
+            mma_tf32_ts(acc, ahi + 8 * ks, dbh, IDESC, 1u);
+          }
+          mma_commit(&empty[q]);
+          mma_commit(&aemp[a]);
+        }
+        mma_commit(&accf[b]);
+        ++tc;
+      }
+    }
+  } else if (warp >= 6) {   // ----------------------------------------------- A split -> TMEM
+    const int q4 = warp & 3, row = q4 * 32 + lane;   // this thread's A row (TMEM lane)
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TmaGemmDesc *dp;
+      int m0, n0;
+      if (!decode(t, dp, m0, n0)) continue;
+      const int nk = (dp->K + TBK - 1) / TBK;
+      for (int kt = 0; kt < nk; ++kt, ++it) {
+        const int q = it % QSTAGES, a = it & 1;
+        mbar_wait(&full[q], (it / QSTAGES) & 1);
+        if (it >= 2) mbar_wait(&aemp[a], ((it >> 1) - 1) & 1);
+        // row `row` of the 128-B swizzled A tile: 16-B chunk c sits at chunk c ^ (row & 7)
+        const float4 *ar = reinterpret_cast<const float4 *>(smem + q * SM::STAGE + row * 128);
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = ar[c ^ (row & 7)];
+          float h, l;
+          split(x.x, h, l); hi[4 * c] = __float_as_uint(h); lo[4 * c] = __float_as_uint(l);
+          split(x.y, h, l); hi[4 * c + 1] = __float_as_uint(h); lo[4 * c + 1] = __float_as_uint(l);
+          split(x.z, h, l); hi[4 * c + 2] = __float_as_uint(h); lo[4 * c + 2] = __float_as_uint(l);
+          split(x.w, h, l); hi[4 * c + 3] = __float_as_uint(h); lo[4 * c + 3] = __float_as_uint(l);
+        }
+        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT[a];
+        TST32(ta, hi);
+        TST32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 6 * 32) mbar_arrive(&aful[a]);
+      }
+    }
+  } else {   // warps 2..5 ------------------------------------------------------ epilogue
+    const int q4 = warp & 3;
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TmaGemmDesc *dp;
+      int m0, n0;
+      if (!decode(t, dp, m0, n0)) continue;
+      const int b = tc & 1;
+      mbar_wait(&accf[b], (tc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int M = dp->M, N = dp->N, ldc = dp->ldc;
+      float *C = dp->C;
+      const int row = m0 + q4 * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC[b] + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+          float *out = C + (size_t)row * ldc + n0 + c0;
+          const int nvalid = N - (n0 + c0);
+          if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+              reinterpret_cast<float4 *>(out)[qq] =
+                  make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                              __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nvalid) out[j] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++tc;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int BN>
+static cudaError_t launch_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                                 cudaStream_t s) {
+  static int nsm = 0;
+  if (!nsm) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         QSmem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int mb = (maxM + BM - 1) / BM, nb = (maxN + BN - 1) / BN;
+  const int ntiles = batch * mb * nb;
+  const int grid = ntiles < nsm ? ntiles : nsm;
+  k_gemm_tma_ts<BN><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
+  return cudaGetLastError();
+}
+
 }  // namespace tc
+
+cudaError_t launch_gemm_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                               cudaStream_t s) {
+  return bn == 144 ? tc::launch_tma_ts<144>(descs, batch, maxM, maxN, s)
+                   : tc::launch_tma_ts<128>(descs, batch, maxM, maxN, s);
+}
 
 cudaError_t launch_gemm_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                               cudaStream_t s) {

@@ -118,6 +118,9 @@ cudaError_t launch_irv1_f(const float *tau1, const float *tau2, int ldt, const f
 cudaError_t launch_dual_energy2(const float *p1, const float *p2, const float *f, int ld, int n2,
                                 int n1, int row0, int row1, double *part, double *out,
                                 cudaStream_t s);
+// IRV2 f with the zero-mean g of the oracle (reading A3): f += alpha mean(g)  (part >= 592 doubles)
+cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, int n1,
+                                    float alpha, double *part, double *shift, cudaStream_t s);
 cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
                           double *part, double *out, cudaStream_t s);
 
@@ -154,6 +157,9 @@ cudaError_t launch_gemm_tc2(const GemmDesc2 *descs, int batch, int maxM, int max
 // persistent warp-specialised form: A given as ONE fp32 plane (a_hi map), split in shared memory
 cudaError_t launch_gemm_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                               cudaStream_t s);
+// TS form: A split into tensor memory (tcgen05.st), MMA with [a-tmem]; same descriptors as _p
+cudaError_t launch_gemm_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
+                               cudaStream_t s);
 cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
 cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,

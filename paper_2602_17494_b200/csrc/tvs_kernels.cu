@@ -632,6 +632,40 @@ k_sumsq2_partial(const float *__restrict__ r, size_t plane, int ld, int n1, int 
   }
   block_sum_store(acc, part + blockIdx.x);
 }
+// Zero-mean convention of g (reading A3): the integrated g of k_irv2_f has
+// g[0][0] = 0; with f = alpha (d0 - g), mean(g) = mean(d0) - mean(f)/alpha, so f + alpha mean(g)
+// is alpha (d0 - (g - mean g)).  Partials of (sum f, sum d0) per block.
+__global__ void __launch_bounds__(RED_T)
+k_sum_fd_partial(const float *__restrict__ f, int ldf, const float *__restrict__ d0, int n2, int n1,
+                 double *__restrict__ part) {
+  double sf = 0.0, sd = 0.0;
+  const long long total = (long long)n2 * n1;
+  for (long long e = (long long)blockIdx.x * RED_T + threadIdx.x; e < total;
+       e += (long long)gridDim.x * RED_T) {
+    const int i = (int)(e / n1), j = (int)(e % n1);
+    sf += f[(size_t)i * ldf + j];
+    sd += d0[e];
+  }
+  block_sum_store(sf, part + 2 * blockIdx.x);
+  __syncthreads();
+  block_sum_store(sd, part + 2 * blockIdx.x + 1);
+}
+__global__ void k_fd_shift(const double *__restrict__ part, int nb, double alpha, double npix,
+                           double *__restrict__ shift) {
+  if (threadIdx.x != 0) return;
+  double sf = 0.0, sd = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    sf += part[2 * b];
+    sd += part[2 * b + 1];
+  }
+  *shift = alpha * (sd / npix) - sf / npix;   // alpha mean(g)
+}
+__global__ void k_add_shift(float *__restrict__ f, int ldf, int n2, int n1,
+                            const double *__restrict__ shift) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n2 || j >= n1) return;
+  f[(size_t)i * ldf + j] = (float)((double)f[(size_t)i * ldf + j] + *shift);
+}
 __global__ void __launch_bounds__(RED_T) k_sum_partials(const double *__restrict__ part, int n,
                                                         double *__restrict__ out) {
   double acc = 0.0;
@@ -1258,7 +1292,7 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
               float *__restrict__ phy_lo, int AP) {
   __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
   __shared__ double sh_tot[SJB];
-  extern __shared__ float sbuf[];   // SMEM: [AT][SJB]
+  extern __shared__ __align__(16) float sbuf[];   // SMEM: [AT][SJB]
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
   const int j = blockIdx.x * SJB + tx;
   const int tix = blockIdx.y;
@@ -1277,47 +1311,60 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const float *bb = SMEM ? zb : b;   // second read of b
   const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;   // s_j^2 (Eq. form:DCTmat normalisation)
 
+  if constexpr (SMEM) {
+    // stage the CTA's [nt x 32] column block of qhat in shared memory with asynchronous 16-byte
+    // copies issued by every thread (all rows in flight at once), then every pass reads it there
+    const float *blk = qhat + (size_t)tix * AT * st + (size_t)blockIdx.x * SJB;
+    const int nthr = SJB * nseg, lt = sg * SJB + tx;
+    for (int e = lt; e < nt * (SJB / 4); e += nthr) {
+      const int k = e / (SJB / 4), c = e % (SJB / 4);
+      float *dst = sbuf + k * SJB + 4 * c;
+      if (blockIdx.x * SJB + 4 * c < ldn) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                     "l"(blk + (size_t)k * st + 4 * c) : "memory");
+      } else {
+        dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
+  const float *b1 = SMEM ? zb : b;   // first read of b
+  const size_t b1st = SMEM ? zst : st;
+
   // ---- forward, local pass from a zero carry: end value a and coefficient product g
   double a = 0.0, g = 1.0;
   if (valid) {
     if (j == 0) {
-      const float *bp = b + (size_t)k0 * st;
-      for (int k = k0; k < k1; ++k, bp += st) {
-        const float bk = *bp;
-        if constexpr (SMEM) zb[(size_t)k * zst] = bk;
-        a += (double)bk;
-      }
+      const float *bp = b1 + (size_t)k0 * b1st;
+      for (int k = k0; k < k1; ++k, bp += b1st) a += (double)*bp;
     } else {
       int k = k0;
       if (k == 0 && k < k1) {   // z_0 = b_0 (no coupling above row 0 of T)
-        const float b0 = b[0];
-        if constexpr (SMEM) zb[0] = b0;
-        a = (double)b0;
+        a = (double)b1[0];
         g = 0.0;
         k = 1;
       }
-      const float *bp = b + (size_t)k * st;
+      const float *bp = b1 + (size_t)k * b1st;
       const double *rp = ri + (size_t)(k - 1) * st;
-      for (; k + SU <= k1; k += SU, bp += SU * st, rp += SU * st) {
+      for (; k + SU <= k1; k += SU, bp += SU * b1st, rp += SU * st) {
         float bv[SU];
         double rv[SU];
 #pragma unroll
         for (int u = 0; u < SU; ++u) {   // the whole batch of loads first (latency-bound)
-          bv[u] = bp[u * st];
+          bv[u] = bp[u * b1st];
           rv[u] = rp[u * st];
         }
 #pragma unroll
         for (int u = 0; u < SU; ++u) {
-          if constexpr (SMEM) zb[(size_t)(k + u) * zst] = bv[u];
           a = fma(-rv[u], a, (double)bv[u]);
           g *= -rv[u];
         }
       }
-      for (; k < k1; ++k, bp += st, rp += st) {
+      for (; k < k1; ++k, bp += b1st, rp += st) {
         const double r = *rp;
-        const float bk = *bp;
-        if constexpr (SMEM) zb[(size_t)k * zst] = bk;
-        a = fma(-r, a, (double)bk);
+        a = fma(-r, a, (double)*bp);
         g *= -r;
       }
     }
@@ -1624,6 +1671,13 @@ cudaError_t launch_dual_energy2(const float *p1, const float *p2, const float *f
                                 cudaStream_t s) {
   k_dual2_partial<<<RED_BLOCKS, RED_T, 0, s>>>(p1, p2, f, ld, n2, n1, row0, row1, part);
   k_sum_partials<<<1, RED_T, 0, s>>>(part, RED_BLOCKS, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, int n1,
+                                    float alpha, double *part, double *shift, cudaStream_t s) {
+  k_sum_fd_partial<<<RED_BLOCKS / 2, RED_T, 0, s>>>(f, ldf, d0, n2, n1, part);
+  k_fd_shift<<<1, 32, 0, s>>>(part, RED_BLOCKS / 2, (double)alpha, (double)n2 * n1, shift);
+  k_add_shift<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(f, ldf, n2, n1, shift);
   return cudaGetLastError();
 }
 cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
