@@ -244,11 +244,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (fp64 y-solves)", "data": "synthetic",
-        "config": {"workload": f"{c.name}: {n}x{n} Voronoi-{c.cells}, {c.m2}x{c.m1} subdomains, "
-                               f"overlap {c.overlap}, {c.sweeps}x{c.inner} per step, delta {c.delta}, "
-                               f"lambda {c.lam}, t {c.t}",
-                   "pixel_updates_per_step": upd_step, "l2": "flushed (256 MB write) between steps",
-                   "parallelism": f"slab decomposition over {world} GPUs (NCCL)" if world > 1 else "1 GPU"},
+        "config": bench_config(c, world, upd_step),
         "gpu_launches": launches,
         "e2e": {"value": upd_step / (e2e_t / 1e3), "unit": "pixel-updates/s",
                 "h2d_bytes_per_step": int(img.nbytes), "d2h_bytes_per_step": int(img.nbytes),
@@ -404,6 +400,25 @@ def _cpu_model():
     return "unknown"
 
 
+def bench_config(c, world, upd_step):
+    """The `config` object of both arms (same workload description)."""
+    return {"workload": f"{c.name}: {c.n}x{c.n} Voronoi-{c.cells}, {c.m2}x{c.m1} subdomains, "
+                        f"overlap {c.overlap}, {c.sweeps}x{c.inner} per step, delta {c.delta}, "
+                        f"lambda {c.lam}, t {c.t}",
+            "pixel_updates_per_step": upd_step, "l2": "flushed (256 MB write) between steps",
+            "parallelism": f"slab decomposition over {world} GPUs (NCCL)" if world > 1 else "1 GPU"}
+
+
+def _oracle_updates(c):
+    """Dual pixel-updates per step counted with the oracle's layout (reference arm only)."""
+    from oracle.layout import ranges_1d
+    ys, xs = ranges_1d(c.n + 1, c.m2, c.overlap), ranges_1d(c.n + 1, c.m1, c.overlap)
+    tot = 0
+    for lim in (c.n, c.n - 1):   # Omega~ (step 1), Omega (step 2)
+        tot += sum(min(b, lim) - a + 1 for a, b in ys) * sum(min(b, lim) - a + 1 for a, b in xs)
+    return tot * c.sweeps * c.inner
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -416,13 +431,12 @@ def run_reference(args, rank, world):
         rates.append(r)
         secs += s
     value = statistics.median(rates)
-    c_name = c.name
     line = {
         "impl": "reference", "metric": "dual pixel-updates/s (step 1 + step 2, overlap counted per subdomain)",
         "value": value, "unit": "pixel-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c_name, "note": "fp64 CPU oracle on a bounded sample per step"},
+        "config": bench_config(c, world, _oracle_updates(c)),
         "cpu_baseline": {"value": value, "unit": "pixel-updates/s", "cores": _blas_threads(),
                          "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "pixel-updates/s", "h2d_bytes_per_step": 0,

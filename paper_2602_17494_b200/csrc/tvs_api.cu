@@ -176,7 +176,7 @@ struct ProjBatch {
   float *G = nullptr;       // output, [tile][2][AP][ldG]
   int ldG = 0;
   float *qhat = nullptr;
-  double *z = nullptr, *rinv = nullptr;
+  double *z = nullptr, *rinv = nullptr, *segprod = nullptr;
   float *phx = nullptr, *phy = nullptr, *phx_lo = nullptr, *phy_lo = nullptr;
   GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
   GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
@@ -419,17 +419,24 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(upload(ctx, P.bufs, &B.d_tiles, B.tiles));
   TRY(upload(ctx, P.bufs, &B.d_first, first));
   TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * B.ldn));
-  TRY(dalloc(ctx, P.bufs, &B.z, (size_t)B.ntiles * B.AT * B.ldn));
+  // z scratch: fp64 for the serial solve, fp32 for the segmented solve when its column block does
+  // not fit in shared memory, none otherwise
+  const size_t nz = (size_t)B.ntiles * B.AT * B.ldn;
+  const bool smem_z = (size_t)B.AT * 32 * sizeof(float) <= 160 * 1024;
+  if (ctx->solve_impl == 1) TRY(dalloc(ctx, P.bufs, &B.z, nz));
+  else if (ctx->solve_impl != 2 && !smem_z) TRY(dalloc(ctx, P.bufs, &B.z, nz / 2 + 1));
   TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
-  TRY(dalloc(ctx, P.bufs, &B.phx_lo, (size_t)B.ntiles * B.AP * B.ldn));
-  TRY(dalloc(ctx, P.bufs, &B.phy_lo, (size_t)B.ntiles * B.AP * B.ldn));
+  if (ctx->presplit()) {   // hi/lo operand planes of the pre-split GEMM variants
+    TRY(dalloc(ctx, P.bufs, &B.phx_lo, (size_t)B.ntiles * B.AP * B.ldn));
+    TRY(dalloc(ctx, P.bufs, &B.phy_lo, (size_t)B.ntiles * B.AP * B.ldn));
+  }
   std::vector<GemmDesc> fwd, inv, fwd_tc, inv_tc;
   std::vector<GemmDesc2> fwd2, inv2;
   // ∇φ output is plane-major: G[c][tile][AP][ldG]
   const size_t gplane = gplane_arg ? gplane_arg : (size_t)B.ntiles * B.AP * ldG;
-  for (int i = 0; i < B.ntiles;) {
+  for (int i = 0; T && i < B.ntiles;) {
     // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
     int j = i + 1;
     while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
@@ -469,7 +476,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.tcM_inv = std::max(B.tcM_inv, Mi);
     i = j;
   }
-  for (int i = 0; i < B.ntiles; ++i) {
+  for (int i = 0; T && i < B.ntiles; ++i) {
     const ProjTile &t = B.tiles[i];
     int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
     int no = t.py1 - t.ty0 + 1 - t.po, bo = t.px1 - t.tx0 + 1;
@@ -489,11 +496,6 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.fwdN = std::max(B.fwdN, n1t);
     B.invM = std::max(B.invM, no);
     B.invN = std::max(B.invN, bo);
-    B.fwd_flops += 2.0 * nt * bt * n1t;
-    B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
-    // solve, algorithmic bytes per (row, frequency): qhat 4 + pivots 8 + two fp32 grad planes 8
-    // (the z scratch stays on chip in the default segmented kernel)
-    B.solve_bytes += (double)nt * n1t * 20.0;
   }
   // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
   {
@@ -509,6 +511,11 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
       const int no = t.py1 - t.ty0 + 1 - t.po;
       const size_t goff = (size_t)t.po * ldG;
+      // algorithmic work: the dense-equivalent contraction flops, and for the solve per (row,
+      // frequency) Q-hat 4 + pivots 8 + two fp32 gradient planes 8 bytes
+      B.fwd_flops += 2.0 * nt * bt * n1t;
+      B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
+      B.solve_bytes += (double)nt * n1t * 20.0;
       fj.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3),
                     B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, ldq, B.ldn, t.tx0, bt, n1t, 0});
       ij.push_back({B.phx + (size_t)i * B.AP * B.ldn, G + (size_t)i * B.AP * ldG + goff, no, B.ldn,
@@ -537,7 +544,8 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
     const bool long_axis = n1t > 4096;
     B.czt = okf && oki && !ctx->presplit() && ctx->gemm != tvs_ctx::G_SIMT &&
-            (ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
+            (!T || ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
+    if (!T && !B.czt) return fail(ctx, TVS_EINVAL, "projection batch without DCT tables needs chirp-z");
     if (B.czt) {
       std::vector<float2> gt, tw;
       czt_tables(B.gf, gt, tw);
@@ -570,6 +578,10 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(upload(ctx, P.bufs, &B.d_fwd4, fwd3));
   TRY(upload(ctx, P.bufs, &B.d_inv4, inv3));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
+  if (solve4_fits(B.AT)) {
+    TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
+    CK(launch_segprod(B.d_tiles, B.d_first, B.nchains, B.rinv, B.ldn, B.AT, n1t, B.segprod, 0));
+  }
   CK(cudaDeviceSynchronize());
   return TVS_OK;
 }
@@ -695,12 +707,16 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->f, (size_t)G2 * P->ld));
     TRY(dalloc(ctx, P->bufs, &P->g0, (size_t)G1));
   } else {
+    // the dense DCT tables (10 planes of N x N floats) only when a batch may take the GEMM form:
+    // long axes always run the chirp-z form
+    const bool czt_only = G1 > 4096 && ctx->dct_mode != 1 && !ctx->presplit() &&
+                          ctx->gemm != tvs_ctx::G_SIMT;
     Tables *T = nullptr;
-    TRY(get_tables(ctx, G1, &T));
+    if (!czt_only) TRY(get_tables(ctx, G1, &T));
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * 2 * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->vtmp, vsz));
     TRY(dalloc(ctx, P->bufs, &P->q, (size_t)g.M * g.AT * g.ldT));
-    TRY(dalloc(ctx, P->bufs, &P->qlo, (size_t)g.M * g.AT * g.ldT));
+    if (ctx->presplit()) TRY(dalloc(ctx, P->bufs, &P->qlo, (size_t)g.M * g.AT * g.ldT));
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)g.M * 2 * g.AP * g.ldP));
     size_t pl = (size_t)G2 * P->ld;
     TRY(dalloc(ctx, P->bufs, &P->f, 2 * pl));
@@ -708,7 +724,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->w, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->r, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->qg, pl));
-    TRY(dalloc(ctx, P->bufs, &P->qglo, pl));
+    if (ctx->presplit()) TRY(dalloc(ctx, P->bufs, &P->qglo, pl));
     TRY(dalloc(ctx, P->bufs, &P->Gg, 2 * pl));
     std::vector<ProjTile> lt;
     for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
@@ -819,9 +835,11 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     }));
     if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
     TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-      return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
-                                reinterpret_cast<float *>(B.z), B.phx, B.phy, nullptr, nullptr,
-                                B.AP, s);
+      return B.segprod ? launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
+                                            B.rinv, B.segprod, B.phx, B.phy, B.AP, s)
+                       : launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
+                                            B.rinv, reinterpret_cast<float *>(B.z), B.phx, B.phy,
+                                            nullptr, nullptr, B.AP, s);
     }));
     return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
       return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
@@ -838,7 +856,10 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    if (ctx->solve_impl == 3)
+    if (ctx->solve_impl == 3 && !tc && B.segprod)
+      return launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
+                                B.segprod, B.phx, B.phy, B.AP, s);
+    if (ctx->solve_impl >= 3)
       return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
                                 reinterpret_cast<float *>(B.z), B.phx, B.phy,
                                 tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
@@ -1143,7 +1164,11 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
     if (v >= 16 && v <= 16384 && (v & (v - 1)) == 0 && (__builtin_ctz(v) % 2) == 0) c->czt_max_m = v;
   }
   const char *sv = getenv("TVS_SOLVE");
-  c->solve_impl = sv && strcmp(sv, "chunked") == 0 ? 2 : sv && strcmp(sv, "serial") == 0 ? 1 : 3;
+  c->solve_impl = !sv                          ? 3
+                  : strcmp(sv, "chunked") == 0 ? 2
+                  : strcmp(sv, "serial") == 0  ? 1
+                  : strcmp(sv, "seg3") == 0    ? 4
+                                               : 3;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;

@@ -165,7 +165,17 @@ cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int m
 cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *phx,
                                float *phy, float *phx_lo, float *phy_lo, int AP, cudaStream_t s);
-// segmented y-solve (default): fp32 z scratch [tile][AT][ldn]
+// segmented y-solve, shared-memory form (default when solve4_fits(AT)); segprod from
+// launch_segprod ([chain][2][solve_nseg(AT)][ldn] doubles), outputs plain fp32
+int solve_nseg(int AT);
+bool solve4_fits(int AT);
+cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
+                           int ldn, int AT, int n1, double *segprod, cudaStream_t s);
+cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1,
+                               const float *qhat, int AT, int ldn, const double *rinv,
+                               const double *segprod, float *phx, float *phy, int AP,
+                               cudaStream_t s);
+// segmented y-solve: fp32 z scratch [tile][AT][ldn]
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,

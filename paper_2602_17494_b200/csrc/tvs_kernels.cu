@@ -1504,6 +1504,233 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   for (; k >= k0; --k, zp -= zst, rp -= st) emit(k, *rp * ((double)*zp - un));
 }
 
+// Products of the recurrence coefficients over each solve segment (data-independent, computed
+// once per plan): forward GF_s = prod_{k in seg} (-r_{k-1}) (r_{-1} = 0), backward GB_s =
+// prod_{k in seg} (-r_k); segments of LS = ceil(nt / nseg) rows as in k_proj_solve4.
+// segprod layout: [chain][2][nseg][ldn].
+__global__ void k_segprod(const ProjTile *__restrict__ tiles, const int *__restrict__ first,
+                          int nchains, const double *__restrict__ rinv, int ldn, int AT, int n1,
+                          int nseg, double *__restrict__ segprod) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (j >= n1 || c >= nchains) return;
+  const ProjTile tl = tiles[first[c]];
+  const int nt = tl.ty1 - tl.ty0 + 1, LS = (nt + nseg - 1) / nseg;
+  const double *r = rinv + (size_t)c * AT * ldn + j;
+  double *gf = segprod + (size_t)c * 2 * nseg * ldn + j, *gb = gf + (size_t)nseg * ldn;
+  for (int sg = 0; sg < nseg; ++sg) {
+    const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
+    double pf = 1.0, pb = 1.0;
+    for (int k = k0; k < k1; ++k) {
+      pf *= k > 0 ? -r[(size_t)(k - 1) * ldn] : 0.0;
+      pb *= -r[(size_t)k * ldn];
+    }
+    gf[(size_t)sg * ldn] = pf;
+    gb[(size_t)sg * ldn] = pb;
+  }
+}
+
+// Segmented y-solve, shared-memory form (default when a tile's column block fits): the same four
+// passes as k_proj_solve3<true> with 32-bit shared indices and precomputed segment products.  The
+// CTA's [nt x 32] blocks of Q-hat (fp32) and of the pivots (fp64) are staged in shared memory with
+// cp.async, so the pivots are read from L2 once instead of four times and every pass runs on
+// shared-memory data.  Outputs are plain fp32.
+__global__ void __launch_bounds__(SJB *SSEG_MAX)
+k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
+              int AT, int ldn, const double *__restrict__ rinv, const double *__restrict__ segprod,
+              float *__restrict__ phx, float *__restrict__ phy, int AP) {
+  __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
+  __shared__ double sh_tot[SJB];
+  extern __shared__ __align__(16) double sr4[];   // [AT][SJB] pivots, then [AT][SJB] floats
+  float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)AT * SJB);   // Q-hat, overwritten by z
+  const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
+  const int j = blockIdx.x * SJB + tx;
+  const int tix = blockIdx.y;
+  const bool valid = j < n1;
+  const ProjTile tl = tiles[tix];
+  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
+  const int LS = (nt + nseg - 1) / nseg;
+  const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
+  const int jj = valid ? j : 0;
+  {   // stage the column blocks (16-byte asynchronous copies, all rows in flight)
+    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)blockIdx.x * SJB;
+    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)blockIdx.x * SJB;
+    const int nthr = SJB * nseg, lt = sg * SJB + tx;
+    for (int e = lt; e < nt * (SJB / 4); e += nthr) {
+      const int k = e / (SJB / 4), c = e % (SJB / 4);
+      float *dst = sb4 + k * SJB + 4 * c;
+      if (blockIdx.x * SJB + 4 * c < ldn) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                     "l"(blk + (size_t)k * ldn + 4 * c) : "memory");
+      } else {
+        dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
+      }
+    }
+    for (int e = lt; e < nt * (SJB / 2); e += nthr) {
+      const int k = e / (SJB / 2), c = e % (SJB / 2);
+      double *dst = sr4 + k * SJB + 2 * c;
+      if (blockIdx.x * SJB + 2 * c < ldn) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                     "l"(rblk + (size_t)k * ldn + 2 * c) : "memory");
+      } else {
+        dst[0] = dst[1] = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
+  const double *ri = sr4 + tx;   // pivot of row k at ri[k * SJB]
+  const double *__restrict__ gp = segprod + (size_t)tl.chain * 2 * nseg * ldn + jj;
+  float *sbt = sb4 + tx;                                                     // row k at sbt[k*SJB]
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
+
+  // ---- forward, local pass (zero carry): end value
+  double a = 0.0;
+  if (valid) {
+    if (j == 0) {
+      for (int k = k0; k < k1; ++k) a += (double)sbt[k * SJB];
+    } else {
+      int k = k0;
+      if (k == 0 && k < k1) {
+        a = (double)sbt[0];
+        k = 1;
+      }
+      for (; k + SU <= k1; k += SU) {
+        float bv[SU];
+        double rv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          bv[u] = sbt[(k + u) * SJB];
+          rv[u] = ri[(k + u - 1) * SJB];
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) a = fma(-rv[u], a, (double)bv[u]);
+      }
+      for (; k < k1; ++k) a = fma(-ri[(k - 1) * SJB], a, (double)sbt[k * SJB]);
+    }
+  }
+  sh_a[sg][tx] = a;
+  sh_c[sg][tx] = (valid && j > 0) ? gp[sg * ldn] : 1.0;
+  __syncthreads();
+  if (sg == 0) {
+    double Z = 0.0;
+    for (int s = 0; s < nseg; ++s) {
+      const double as = sh_a[s][tx], gs = sh_c[s][tx];
+      sh_c[s][tx] = Z;
+      Z = fma(gs, Z, as);
+    }
+    sh_tot[tx] = Z;
+  }
+  __syncthreads();
+  const double fcarry = sh_c[sg][tx];
+
+  // ---- forward, final pass: z overwrites b in shared memory
+  if (valid && j > 0 && k0 < k1) {
+    double zc = fcarry;
+    int k = k0;
+    if (k == 0) {
+      zc = (double)sbt[0];
+      k = 1;
+    }
+    for (; k + SU <= k1; k += SU) {
+      float bv[SU];
+      double rv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        bv[u] = sbt[(k + u) * SJB];
+        rv[u] = ri[(k + u - 1) * SJB];
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        zc = fma(-rv[u], zc, (double)bv[u]);
+        sbt[(k + u) * SJB] = (float)zc;
+      }
+    }
+    for (; k < k1; ++k) {
+      zc = fma(-ri[(k - 1) * SJB], zc, (double)sbt[k * SJB]);
+      sbt[k * SJB] = (float)zc;
+    }
+  }
+  // ---- backward, local pass (u_{k1} = 0)
+  a = 0.0;
+  if (valid && j > 0 && k0 < k1) {
+    int k = k1 - 1;
+    for (; k - SU + 1 >= k0; k -= SU) {
+      float zv[SU];
+      double rv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        zv[u] = sbt[(k - u) * SJB];
+        rv[u] = ri[(k - u) * SJB];
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) a = rv[u] * ((double)zv[u] - a);
+    }
+    for (; k >= k0; --k) a = ri[k * SJB] * ((double)sbt[k * SJB] - a);
+  }
+  __syncthreads();
+  sh_a[sg][tx] = a;
+  sh_c[sg][tx] = (valid && j > 0) ? gp[(nseg + sg) * ldn] : 1.0;
+  __syncthreads();
+  if (sg == 0) {
+    double U = 0.0;
+    for (int s = nseg - 1; s >= 0; --s) {
+      const double as = sh_a[s][tx], gs = sh_c[s][tx];
+      sh_c[s][tx] = U;
+      U = fma(gs, U, as);
+    }
+  }
+  __syncthreads();
+  if (!valid || k0 >= k1) return;
+  float *__restrict__ ox = phx + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
+  float *__restrict__ oy = phy + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
+  if (j == 0) {
+    const double mu = sh_tot[tx] / (double)n2;
+    double pre = fcarry;
+    for (int k = k0; k < min(k1, nout); ++k) {
+      pre += (double)sbt[k * SJB];
+      const int y = tl.ty0 + k;
+      const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
+      if (k >= po) {
+        ox[(size_t)k * ldn] = 0.f;
+        oy[(size_t)k * ldn] = (float)(s2 * w);
+      }
+    }
+    return;
+  }
+  const double sg_j = 2.0 * sinpi((double)j / (2.0 * n1));
+  const double cx = -s2 * sg_j;
+  double un = sh_c[sg][tx];
+  const int klo = max(k0, po), khi = min(k1, nout);   // output rows of this segment
+  int k = k1 - 1;
+  // rows above nout (T rows below S+) only carry the recurrence
+  for (; k >= khi && k >= k0; --k) un = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+  for (; k - SU + 1 >= klo; k -= SU) {
+    float zv[SU];
+    double rv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      zv[u] = sbt[(k - u) * SJB];
+      rv[u] = ri[(k - u) * SJB];
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const double uk = rv[u] * ((double)zv[u] - un);
+      ox[(size_t)(k - u) * ldn] = (float)(cx * uk);
+      // D+_y u = u_{k+1} - u_k; 0 on the global last row (T = S+ in y there)
+      oy[(size_t)(k - u) * ldn] = (k - u == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+      un = uk;
+    }
+  }
+  for (; k >= klo; --k) {
+    const double uk = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+    ox[(size_t)k * ldn] = (float)(cx * uk);
+    oy[(size_t)k * ldn] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+    un = uk;
+  }
+}
+
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
 constexpr int GBM = 128, GBN = 128, GBK = 8;
@@ -1777,6 +2004,31 @@ cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1
   }
   k_proj_solve2<<<dim3((n1 + nth - 1) / nth, ntiles), nth, smem, s>>>(
       tiles, n2, n1, qhat, AT, ldn, rinv, phx, phy, phx_lo, phy_lo, AP, nch);
+  return cudaGetLastError();
+}
+int solve_nseg(int AT) { return std::min(SSEG_MAX, std::max(1, (AT + 31) / 32)); }
+bool solve4_fits(int AT) { return (size_t)AT * SJB * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
+cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
+                           int ldn, int AT, int n1, double *segprod, cudaStream_t s) {
+  k_segprod<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, rinv, ldn, AT,
+                                                            n1, solve_nseg(AT), segprod);
+  return cudaGetLastError();
+}
+cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1,
+                               const float *qhat, int AT, int ldn, const double *rinv,
+                               const double *segprod, float *phx, float *phy, int AP,
+                               cudaStream_t s) {
+  const int nseg = solve_nseg(AT);
+  const size_t smem = (size_t)AT * SJB * (sizeof(float) + sizeof(double));
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_proj_solve4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k_proj_solve4<<<dim3((n1 + SJB - 1) / SJB, ntiles), dim3(SJB, nseg), smem, s>>>(
+      tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,

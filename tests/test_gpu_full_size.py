@@ -202,3 +202,42 @@ def test_config5_step2_sampled_and_properties(ctx):
         d_chk = img[r0:r0 + 256, c0:c0 + 256].astype(np.float64) - ops.div(pw) / alpha
         err = np.abs(d_g[r0:r0 + 256, c0:c0 + 256].cpu().numpy() - d_chk)[1:-1, 1:-1].max()
         assert err <= 1e-5, ((r0, c0), err)
+
+
+# ----------------------------------------------------------------------------- config 5, 1-GPU size
+
+def test_config5_weak1_step1_sampled(ctx):
+    """Config 5 at its one-GPU weak-scaling size (11585^2, 16 x 16 subdomains of ~745^2, s = 32;
+    reading A16): the 11586^2 global projection P tau_0 element-wise, one sweep of two Alg. 5
+    updates on three subdomains (corner, edge, interior), div tau = 0.  N = 11586 > 4096, so every
+    projection batch runs the chirp-z x-DCTs."""
+    c = CONFIGS["c5w1"]
+    img = _image("c5w1")
+    d0 = img.astype(np.float64)
+    n = c.n
+    nt = n + 1
+    lay = olayout.Layout(n, n, *_layout(c))
+    d0_dev = torch.from_numpy(img).cuda()
+    tau_p, _, _ = ctx.tv_stokes_step1(d0_dev, c.delta, _layout(c), (1, 0, c.t))
+    f = spectral.project(S.tau0(d0)) / c.delta
+    e_P = np.abs(tau_p.cpu().numpy().astype(np.float64) - c.delta * f).max()
+    _log("c5w1_global_P", err=e_P)
+    assert e_P <= TOL, e_P
+    del tau_p
+    tau_g, p_g, _ = ctx.tv_stokes_step1(d0_dev, c.delta, _layout(c), (1, 2, c.t), want_p=True)
+    p0 = np.zeros((2, 2, nt, nt))
+    for m in ((0, 0), (0, 7), (9, 6)):
+        s = lay.rect(m, extended=True)
+        v = S._tfs_inner_local(m, lay, p0, f, np.zeros((2, 2) + S.rect_shape(s)), 2, c.t)
+        ylo, yhi = _core(lay.ry, m[0], nt)
+        xlo, xhi = _core(lay.rx, m[1], nt)
+        (y0, _), (x0, _) = s
+        p_ref = lay.alpha_hat * v[:, :, ylo - y0:yhi - y0 + 1, xlo - x0:xhi - x0 + 1]
+        p_gpu = (p_g.reshape(2, 2, nt, nt)[:, :, ylo:yhi + 1, xlo:xhi + 1]
+                 .cpu().numpy().astype(np.float64))
+        e_p = np.abs(p_gpu - p_ref).max()
+        _log("c5w1_step1_sweep1", m=list(m), p_err=e_p)
+        assert e_p <= TOL, (m, e_p)
+    e_div = np.abs(ops.div(tau_g.cpu().numpy().astype(np.float64))).max()
+    _log("c5w1_step1_div_tau", div=e_div)
+    assert e_div <= TOL, e_div

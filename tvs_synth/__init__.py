@@ -209,6 +209,10 @@ CONFIGS = {
     "c3": Config("c3", 2048, 8, 8, 16, 50, 10, 1003, cells=64),
     "c4": Config("c4", 8192, 8, 1, 32, 30, 20, 1004, cells=1024),
     "c5": Config("c5", 32768, 16, 16, 32, 20, 10, 1005, cells=16384),
+    # config-5 weak-scaling sizes at 1 / 2 / 4 GPUs (16 x 16 subdomains at every size, reading A16)
+    "c5w1": Config("c5w1", 11585, 16, 16, 32, 20, 10, 1006, cells=16384),
+    "c5w2": Config("c5w2", 16384, 16, 16, 32, 20, 10, 1007, cells=16384),
+    "c5w4": Config("c5w4", 23170, 16, 16, 32, 20, 10, 1008, cells=16384),
 }
 
 
