@@ -95,9 +95,9 @@ __device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
       float2 x[16];
 #pragma unroll
       for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m * Q)];
-      // twiddles of the pair from one lookup: stage 1 (span L, k = kp + r Q) uses
+      // twiddles of the pair from two lookups: stage 1 (span L, k = kp + r Q) uses
       // w^{c k s1} = W^c * e^{-2 pi i c r / 16} with W = w^{kp s1}; stage 2 (span Q, k = kp,
-      // stride 4 s1) uses W^{4c}.
+      // stride 4 s1) uses V^c with V = w^{4 kp s1} (looked up, not W^4: keeps the error flat).
       const float2 W1 = tw(kp * s1), W2 = cmul(W1, W1), W3 = cmul(W1, W2);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -106,7 +106,7 @@ __device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
         x[r + 8] = cmul(x[r + 8], r ? cmul(W2, w16(2 * r)) : W2);
         x[r + 12] = cmul(x[r + 12], r ? cmul(W3, w16(3 * r)) : W3);
       }
-      const float2 V1 = cmul(W2, W2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+      const float2 V1 = tw(4 * kp * s1), V2 = cmul(V1, V1), V3 = cmul(V1, V2);   // direct lookup
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         bfly4_dif(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
@@ -161,7 +161,7 @@ __device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
       // stage 2 (span 4L, k = kp + r L, stride s2) uses U^c e^{-2 pi i c r/16}, U = w^{kp s2};
       // stage 1 (span L, k = kp, stride 4 s2) uses U^{4c}
       const float2 U1 = tw(kp * s2), U2 = cmul(U1, U1), U3 = cmul(U1, U2);
-      const float2 V1 = cmul(U2, U2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+      const float2 V1 = tw(4 * kp * s2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);   // direct lookup
 #pragma unroll
       for (int t = 0; t < 4; ++t) {   // span L, k = kp
         x[4 * t + 1] = cmulc(x[4 * t + 1], V1);

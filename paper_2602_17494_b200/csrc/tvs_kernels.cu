@@ -303,20 +303,20 @@ k_sweep2s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
 // (c0 - 2 + 2l, c0 - 1 + 2l) -> 8-byte loads/stores; a warp produces 60 output columns
 // (lanes 1..30), lane 0 supplies the left halo column and lane 31 the right one.  Two rows of
 // loads are kept in flight ahead of the arithmetic (bytes in flight per SM ~ 3x the scalar form).
-constexpr int SV_OUT = 60, SV_RB = 32, SV_WARPS = 4;
+constexpr int SV_OUT = 60, SV_WARPS = 4;
 __global__ void __launch_bounds__(32 * SV_WARPS)
 k_sweep2v(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
           const float *__restrict__ thx, const float *__restrict__ vin,
-          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t, int rb) {
   const SubDesc sd = subs[blockIdx.z];
   const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
   const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
   const int lane = threadIdx.x, strip = blockIdx.x * SV_WARPS + threadIdx.y;
   const int c0 = strip * SV_OUT;
   if (c0 >= b) return;
-  const int r0 = blockIdx.y * SV_RB;
+  const int r0 = blockIdx.y * rb;
   if (r0 >= a) return;
-  const int r1 = min(a, r0 + SV_RB);
+  const int r1 = min(a, r0 + rb);
   const int jA = c0 - 2 + 2 * lane, jB = jA + 1;          // local columns of this lane
   // a column pair is loaded as one float2 when both columns lie inside the plane's extent
   const bool SA = jA >= 0 && jA < b, SB = jB >= 0 && jB < b;
@@ -820,7 +820,7 @@ __global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *_
 // (c0 - 2 + 2l, c0 - 1 + 2l) of the subdomain-local grid, lanes 1..30 produce 60 output
 // columns, lane 0 / lane 31 are halo columns, and each warp walks RB rows with the next rows'
 // loads in flight (same scheme as k_sweep2v).
-constexpr int S1_OUT = 60, S1_RB = 32, S1_WARPS = 4;
+constexpr int S1_OUT = 60, S1_WARPS = 4;
 
 struct PairCtx {
   int jA, jB;
@@ -851,16 +851,16 @@ __device__ __forceinline__ float2 div_pair(const PairCtx &pc, int gi, int n2, fl
 // q = div_T E_{S+} multidiv E_S v on T (Alg. 5 pre-div)
 __global__ void __launch_bounds__(32 * S1_WARPS)
 k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v, int n2, int n1,
-           float *__restrict__ q, float *__restrict__ qlo) {
+           float *__restrict__ q, float *__restrict__ qlo, int rb) {
   const SubDesc sd = subs[blockIdx.z];
   const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
   const int at = sd.ty1 - sd.y0 + 1, bt = sd.tx1 - sd.x0 + 1;
   const int lane = threadIdx.x, strip = blockIdx.x * S1_WARPS + threadIdx.y;
   const int c0 = strip * S1_OUT;
   if (c0 >= bt) return;
-  const int r0 = blockIdx.y * S1_RB;
+  const int r0 = blockIdx.y * rb;
   if (r0 >= at) return;
-  const int r1 = min(at, r0 + S1_RB);
+  const int r1 = min(at, r0 + rb);
   PairCtx pc;
   pc.jA = c0 - 2 + 2 * lane;
   pc.jB = pc.jA + 1;
@@ -913,16 +913,16 @@ __global__ void __launch_bounds__(32 * S1_WARPS)
 k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
           const float *__restrict__ thx, const float *__restrict__ vin,
           const float *__restrict__ gphi, int ldg, const float *__restrict__ om,
-          float *__restrict__ vout, int n2, int n1, float t) {
+          float *__restrict__ vout, int n2, int n1, float t, int rb) {
   const SubDesc sd = subs[blockIdx.z];
   const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
   const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
   const int lane = threadIdx.x, strip = blockIdx.x * S1_WARPS + threadIdx.y;
   const int c0 = strip * S1_OUT;
   if (c0 >= b) return;
-  const int r0 = blockIdx.y * S1_RB;
+  const int r0 = blockIdx.y * rb;
   if (r0 >= a) return;
-  const int r1 = min(a, r0 + S1_RB);
+  const int r1 = min(a, r0 + rb);
   PairCtx pc;
   pc.jA = c0 - 2 + 2 * lane;
   pc.jB = pc.jA + 1;
@@ -1839,6 +1839,13 @@ cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const 
                                                                    ld, n2, n1, om);
   return cudaGetLastError();
 }
+// Rows per warp of the streaming stencil kernels (TVS_RB overrides; default 32).
+static int stencil_rb(int rows, int nsub) {
+  static const int env = getenv("TVS_RB") ? atoi(getenv("TVS_RB")) : 0;
+  (void)rows;
+  (void)nsub;
+  return env >= 4 ? env : 32;
+}
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s) {
@@ -1853,9 +1860,9 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
   } else if ((getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "pair") == 0) ||
              (!getenv("TVS_SWEEP2") && g.B < 512)) {
     // narrow subdomains (L2-resident regime): the 2-column form keeps more warps in flight
-    const int strips = (g.B + SV_OUT - 1) / SV_OUT;
-    dim3 grid((strips + SV_WARPS - 1) / SV_WARPS, (g.A + SV_RB - 1) / SV_RB, g.M);
-    k_sweep2v<<<grid, dim3(32, SV_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+    const int strips = (g.B + SV_OUT - 1) / SV_OUT, rb = stencil_rb(g.A, g.M);
+    dim3 grid((strips + SV_WARPS - 1) / SV_WARPS, (g.A + rb - 1) / rb, g.M);
+    k_sweep2v<<<grid, dim3(32, SV_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t, rb);
   } else {
     const int strips = (g.B + SQ_OUT - 1) / SQ_OUT;
     dim3 grid((strips + SQ_WARPS - 1) / SQ_WARPS, (g.A + SQ_RB - 1) / SQ_RB, g.M);
@@ -1946,9 +1953,9 @@ cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, i
   if (naive) {
     k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
   } else {
-    const int strips = (g.BT + S1_OUT - 1) / S1_OUT;
-    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + S1_RB - 1) / S1_RB, g.M);
-    k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo);
+    const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M);
+    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + rb - 1) / rb, g.M);
+    k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo, rb);
   }
   return cudaGetLastError();
 }
@@ -1967,10 +1974,10 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
     k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
                                                                  ldg, om, vout, n2, n1, t);
   } else {
-    const int strips = (g.B + S1_OUT - 1) / S1_OUT;
-    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + S1_RB - 1) / S1_RB, g.M);
+    const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M);
+    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + rb - 1) / rb, g.M);
     k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
-                                                  n2, n1, t);
+                                                  n2, n1, t, rb);
   }
   return cudaGetLastError();
 }
@@ -2021,7 +2028,8 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   const int nseg = solve_nseg(AT);
   const size_t smem = (size_t)AT * SJB * (sizeof(float) + sizeof(double));
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  // (the kernel also has ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
+  if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_proj_solve4, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -2041,7 +2049,7 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
   const size_t smem = (size_t)AT * SJB * sizeof(float);
   if (smem <= 160 * 1024) {
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
       cudaError_t e = cudaFuncSetAttribute(k_proj_solve3<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
