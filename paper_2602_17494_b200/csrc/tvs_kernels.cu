@@ -519,34 +519,55 @@ __device__ __forceinline__ float ky_part(const float *__restrict__ q, const Geo 
 // is grouped as sum_ky (sum_kx qhat) in ascending ky, where the parts of layout rows owned by the
 // slab neighbours (ky < k0: `up`, ky >= k1: `dn`, rows [*_r0, *_r1)) arrive as partial sums over
 // NCCL -- so overlaps are bitwise identical for every GPU count.  Flags non-finite values.
-__global__ void k_combine(const SubDesc *__restrict__ subs, Geo g, int planes,
+template <int C>
+__global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
                           const int2 *__restrict__ covy, const int2 *__restrict__ covx,
                           const int *__restrict__ loy, const int *__restrict__ lox, int m2loc,
                           int k0, int k1, const float *__restrict__ q, float *__restrict__ p,
                           int ld, int n2, int row0, int row1, int n1, float ahat, int *bad,
                           const float *__restrict__ up, int up_r0, int up_r1,
                           const float *__restrict__ dn, int dn_r0, int dn_r1) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= row1 || j >= n1) return;
-  int2 cy = covy[i], cx = covx[j];
-  for (int c = 0; c < planes; ++c) {
-    float acc = 0.f;
-    for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
-      float part;
-      if (ky < k0)
-        part = (i >= up_r0 && i < up_r1) ? up[((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + j] : 0.f;
-      else if (ky >= k1)
-        part = (i >= dn_r0 && i < dn_r1) ? dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j] : 0.f;
-      else
-        part = ky_part(q, g, planes, c, ky, k0, m2loc, i, j, cx, loy, lox);
-      acc += part;
+  const int2 cy = covy[i], cx = covx[j];
+  const size_t qpl = (size_t)g.A * g.ldS;   // plane stride inside one subdomain's block
+  float acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.f;
+  for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
+    float part[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) part[c] = 0.f;
+    if (ky < k0) {
+      if (i >= up_r0 && i < up_r1)
+#pragma unroll
+        for (int c = 0; c < C; ++c) part[c] = up[((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + j];
+    } else if (ky >= k1) {
+      if (i >= dn_r0 && i < dn_r1)
+#pragma unroll
+        for (int c = 0; c < C; ++c) part[c] = dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j];
+    } else {   // sum over kx of this layout row (same grouping as k_partial)
+      const int li = i - loy[ky];
+      for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
+        const int m = kx * m2loc + (ky - k0);
+        const float *qb = q + ((size_t)m * C * g.A + li) * g.ldS + (j - lox[kx]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) part[c] += qb[c * qpl];
+      }
     }
-    size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
-    float v = (1.f - ahat) * p[idx] + ahat * acc;
-    if (!isfinite(v)) atomicOr(bad, 1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] += part[c];
+  }
+  bool finite = true;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
+    const float v = (1.f - ahat) * p[idx] + ahat * acc[c];
+    finite = finite && isfinite(v);
     p[idx] = v;
   }
+  if (!finite) atomicOr(bad, 1);
 }
 
 // Partial sums of the local subdomains on rows [ra, rb) for a slab neighbour:
@@ -1839,12 +1860,16 @@ cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const 
                                                                    ld, n2, n1, om);
   return cudaGetLastError();
 }
-// Rows per warp of the streaming stencil kernels (TVS_RB overrides; default 32).
-static int stencil_rb(int rows, int nsub) {
+// Rows per warp of the streaming stencil kernels: the longest of 32 / 16 / 8 that still gives
+// >= 8192 warps (~55 per SM) -- short row blocks cost 2-3 halo rows each, but small subdomains
+// (config 3: 64 x 274 x 274) need the extra warps to keep loads in flight (measured: kernel (a)
+// 46 -> 34 us, (a') 95 -> 76 us from 32 to 8 rows).  TVS_RB overrides.
+static int stencil_rb(int rows, int nsub, int strips) {
   static const int env = getenv("TVS_RB") ? atoi(getenv("TVS_RB")) : 0;
-  (void)rows;
-  (void)nsub;
-  return env >= 4 ? env : 32;
+  if (env >= 4) return env;
+  for (int rb : {32, 16})
+    if ((long long)strips * nsub * ((rows + rb - 1) / rb) >= 8192) return rb;
+  return 8;
 }
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
@@ -1860,7 +1885,7 @@ cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const fl
   } else if ((getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "pair") == 0) ||
              (!getenv("TVS_SWEEP2") && g.B < 512)) {
     // narrow subdomains (L2-resident regime): the 2-column form keeps more warps in flight
-    const int strips = (g.B + SV_OUT - 1) / SV_OUT, rb = stencil_rb(g.A, g.M);
+    const int strips = (g.B + SV_OUT - 1) / SV_OUT, rb = stencil_rb(g.A, g.M, strips);
     dim3 grid((strips + SV_WARPS - 1) / SV_WARPS, (g.A + rb - 1) / rb, g.M);
     k_sweep2v<<<grid, dim3(32, SV_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t, rb);
   } else {
@@ -1876,9 +1901,14 @@ cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *c
                            int n1, float ahat, int *bad, const float *up, int up_r0, int up_r1,
                            const float *dn, int dn_r0, int dn_r1, cudaStream_t s) {
   if (row1 <= row0) return cudaSuccess;
-  k_combine<<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
-      subs, g, planes, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat,
-      bad, up, up_r0, up_r1, dn, dn_r0, dn_r1);
+  if (planes == 4)
+    k_combine<4><<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
+        subs, g, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat, bad, up,
+        up_r0, up_r1, dn, dn_r0, dn_r1);
+  else
+    k_combine<2><<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
+        subs, g, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat, bad, up,
+        up_r0, up_r1, dn, dn_r0, dn_r1);
   return cudaGetLastError();
 }
 cudaError_t launch_partial(const SubDesc *subs, Geo g, int planes, const int2 *covy,
@@ -1953,7 +1983,7 @@ cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, i
   if (naive) {
     k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
   } else {
-    const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M);
+    const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M, strips);
     dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + rb - 1) / rb, g.M);
     k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo, rb);
   }
@@ -1974,7 +2004,7 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
     k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
                                                                  ldg, om, vout, n2, n1, t);
   } else {
-    const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M);
+    const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M, strips);
     dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + rb - 1) / rb, g.M);
     k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
                                                   n2, n1, t, rb);
