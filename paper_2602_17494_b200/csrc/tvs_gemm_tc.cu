@@ -19,6 +19,7 @@
 #include "tvs_internal.h"
 
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 namespace tvs {
@@ -905,7 +906,7 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "r"(v[30]), "r"(v[31])                                                                        \
       : "memory")
 
-template <int BN>
+template <int BN, int NS>
 __global__ void __launch_bounds__(PNT, 1)
 k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int nblocks) {
   static_assert(BN <= 144, "TMEM column plan assumes BN <= 144");
@@ -916,9 +917,9 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + QSTAGES * SM::STAGE);
   uint64_t *empty = full + QSTAGES;       // smem stage free (MMA done)
-  uint64_t *aful = empty + QSTAGES;       // [2] TMEM A slot written
-  uint64_t *aemp = aful + 2;              // [2] TMEM A slot free (MMA done)
-  uint64_t *accf = aemp + 2;              // [2]
+  uint64_t *aful = empty + QSTAGES;       // [NS] TMEM A slot written
+  uint64_t *aemp = aful + 3;              // [NS] TMEM A slot free (MMA done)
+  uint64_t *accf = aemp + 3;              // [2]
   uint64_t *acce = accf + 2;              // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
   if (warp == 2) {
@@ -932,9 +933,11 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&aful[b], 1);
       mbar_init(&aemp[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], 4);
     }
@@ -945,7 +948,10 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t ACC[2] = {0u, 256u}, ASLOT[2] = {144u, 400u};
+  // TMEM columns: NS = 2: accumulators 0 / 256, A slots 144 / 400; NS = 3: accumulators 0 / 144,
+  // A slots 288 / 352 / 416 (each slot: hi 32 + lo 32 columns)
+  const uint32_t ACC[2] = {0u, NS == 2 ? 256u : 144u};
+  const uint32_t ASLOT[3] = {NS == 2 ? 144u : 288u, NS == 2 ? 400u : 352u, 416u};
   const int per = mblocks * nblocks, ntiles = batch * per;
   auto decode = [&](int t, const TmaGemmDesc *&dp, int &m0, int &n0) {
     const int z = t / per, r = t - z * per;
@@ -988,9 +994,9 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
         const uint32_t acc = tmem + ACC[b];
         const int nk = (dp->K + TBK - 1) / TBK;
         for (int kt = 0; kt < nk; ++kt, ++it) {
-          const int q = it % QSTAGES, a = it & 1;
+          const int q = it % QSTAGES, a = it % NS;
           mbar_wait(&full[q], (it / QSTAGES) & 1);   // B landed (TMA, async proxy)
-          mbar_wait(&aful[a], (it >> 1) & 1);        // A slot written to TMEM
+          mbar_wait(&aful[a], (it / NS) & 1);        // A slot written to TMEM
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = sbase + q * SM::STAGE;
           const uint32_t bhi = st + SM::A_BYTES, blo = bhi + SM::B_BYTES;
@@ -1018,9 +1024,9 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
       if (!decode(t, dp, m0, n0)) continue;
       const int nk = (dp->K + TBK - 1) / TBK;
       for (int kt = 0; kt < nk; ++kt, ++it) {
-        const int q = it % QSTAGES, a = it & 1;
+        const int q = it % QSTAGES, a = it % NS;
         mbar_wait(&full[q], (it / QSTAGES) & 1);
-        if (it >= 2) mbar_wait(&aemp[a], ((it >> 1) - 1) & 1);
+        if (it >= NS) mbar_wait(&aemp[a], ((it / NS) - 1) & 1);
         // row `row` of the 128-B swizzled A tile: 16-B chunk c sits at chunk c ^ (row & 7)
         const float4 *ar = reinterpret_cast<const float4 *>(smem + q * SM::STAGE + row * 128);
         uint32_t hi[32], lo[32];
@@ -1098,10 +1104,14 @@ template <int BN>
 static cudaError_t launch_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
                                  cudaStream_t s) {
   static int nsm = 0;
+  static const int slots = getenv("TVS_TS_SLOTS") && atoi(getenv("TVS_TS_SLOTS")) == 3 ? 3 : 2;
   if (!nsm) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts<BN>,
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts<BN, 2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          QSmem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tma_ts<BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             QSmem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1111,7 +1121,10 @@ static cudaError_t launch_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, 
   const int mb = (maxM + BM - 1) / BM, nb = (maxN + BN - 1) / BN;
   const int ntiles = batch * mb * nb;
   const int grid = ntiles < nsm ? ntiles : nsm;
-  k_gemm_tma_ts<BN><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
+  if (slots == 3)
+    k_gemm_tma_ts<BN, 3><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
+  else
+    k_gemm_tma_ts<BN, 2><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
   return cudaGetLastError();
 }
 
