@@ -257,6 +257,7 @@ struct tvs_ctx {
   int dct_mode = 0;
   int czt_max_m = 16384;
   double *h_energy = nullptr;   // pinned slot for dual energies
+  bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
   int stop_crit = 0;       // tvs_set_stopping
   double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
   // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
@@ -976,12 +977,19 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       return launch_omega0_2(P->d_subs, g, P->d_thy, P->d_thx, P->f, P->p, P->p + pl, ld, n2, n1,
                              P->om, s);
     }));
-    for (int k = 0; k < it.inner; ++k) {
+    for (int k = 0; k < it.inner;) {
+      // two updates per pass where possible (temporal blocking, bitwise identical): the
+      // algorithmic traffic of the pass is still 20 B per point, now for two updates
+      // (only for wide subdomains: narrow ones keep the 2-column kernel with short row blocks)
+      const bool two = ctx->sweep2x2 && k + 1 < it.inner && g.B >= 512;
       TRY(run(ctx, s, F_SWEEP2, sweep_bytes, 0, [&] {
-        return launch_sweep2(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->om, P->v[cur ^ 1],
-                             n2, n1, it.t, s);
+        return two ? launch_sweep2x2(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->om,
+                                     P->v[cur ^ 1], n2, n1, it.t, s)
+                   : launch_sweep2(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->om,
+                                   P->v[cur ^ 1], n2, n1, it.t, s);
       }));
       cur ^= 1;
+      k += two ? 2 : 1;
     }
     TRY(combine_step(ctx, *P, P->v[cur], s));
     if (stopping) {
@@ -1157,6 +1165,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
             : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
             : strcmp(g, "persistent") == 0 ? tvs_ctx::G_PERSIST
                                         : tvs_ctx::G_TS;
+  if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {

@@ -94,6 +94,10 @@ cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, cons
 cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                             const float *f, const float *p1, const float *p2, int ld, int n2,
                             int n1, float *om, cudaStream_t s);
+// two inner iterations of kernel (a) in one pass (temporal blocking; bitwise = two launch_sweep2)
+cudaError_t launch_sweep2x2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                            const float *vin, const float *om, float *vout, int n2, int n1,
+                            float t, cudaStream_t s);
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s);

@@ -500,6 +500,131 @@ k_sweep2q(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   }
 }
 
+// Kernel (a) with two inner iterations per pass (temporal blocking of Alg. 3's inner loop,
+// P:1346-1352; omega0 is fixed within a sweep): the same 4-columns-per-lane streaming layout as
+// k_sweep2q; the column halo of lanes 0 / 31 is 4 wide and a level-k result is wrong only k columns
+// from a halo edge, so lanes 1..30 stay exact for two levels.  Rows: level 1 is computed on rows
+// r0-1 .. r1 and level 2 on r0 .. r1-1 from a register ring (raw rows up to r1+2 in flight).  Each
+// element goes through exactly the operations of two k_sweep2q launches (bitwise identical);
+// HBM traffic per update is about half.
+template <int MINB>
+__global__ void __launch_bounds__(32 * SQ_WARPS, MINB)
+k_sweep2q2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
+           const float *__restrict__ thx, const float *__restrict__ vin,
+           const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
+  const SubDesc sd = subs[blockIdx.z];
+  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
+  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
+  const int lane = threadIdx.x, strip = blockIdx.x * SQ_WARPS + threadIdx.y;
+  const int c0 = strip * SQ_OUT;
+  if (c0 >= b) return;
+  const int r0 = blockIdx.y * SQ_RB;
+  if (r0 >= a) return;
+  const int r1 = min(a, r0 + SQ_RB);
+  const int j0 = c0 - 4 + 4 * lane;
+  float mS[4], mP[4], xk[4], thc[4];
+  bool fullS = true, fullP = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = j0 + q;
+    const bool s_ = j >= 0 && j < b, p_ = j >= 0 && j < bp;
+    mS[q] = s_ ? 1.f : 0.f;
+    mP[q] = p_ ? 1.f : 0.f;
+    fullS &= s_;
+    fullP &= p_;
+    xk[q] = (sd.x0 + j < n1 - 1) ? 1.f : 0.f;
+    thc[q] = s_ ? thx[sd.ix * g.B + j] : 0.f;
+  }
+  const bool out_lane = lane >= 1 && lane <= 30;
+  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  const float *v2 = v1 + (size_t)g.A * g.ldS;
+  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
+  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
+  float *o2 = o1 + (size_t)g.A * g.ldS;
+  auto ld4 = [&](const float *base, int ld, int li, int rows, bool full, const float *m) {
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (li < 0 || li >= rows) return r;
+    const float *p = base + (size_t)li * ld + j0;
+    if (full) return __ldg(reinterpret_cast<const float4 *>(p));
+    if (m[0] != 0.f) r.x = __ldg(p);
+    if (m[1] != 0.f) r.y = __ldg(p + 1);
+    if (m[2] != 0.f) r.z = __ldg(p + 2);
+    if (m[3] != 0.f) r.w = __ldg(p + 3);
+    return r;
+  };
+  struct Raw { float4 w1, w2, o; };
+  struct V2 { float4 w1, w2; };
+  auto ldraw = [&](int li) {
+    Raw r;
+    r.w1 = ld4(v1, g.ldS, li, a, fullS, mS);
+    r.w2 = ld4(v2, g.ldS, li, a, fullS, mS);
+    r.o = ld4(omm, g.ldP, li, ap, fullP, mP);
+    return r;
+  };
+  // u = div_{S+} E v - omega0 at row li (global D- rules), given v at li and v_2 at li - 1
+  auto ucalc = [&](int li, float4 w1, float4 w2, float4 w2m, float4 o) {
+    const float left = __shfl_up_sync(0xffffffffu, w1.w, 1);
+    const float gy = (sd.y0 + li < n2 - 1) ? 1.f : 0.f;
+    const float rowok = (li >= 0 && li < ap) ? 1.f : 0.f;
+    float4 u;
+    u.x = rowok * mP[0] * (xk[0] * w1.x - left + gy * w2.x - w2m.x - o.x);
+    u.y = rowok * mP[1] * (xk[1] * w1.y - w1.x + gy * w2.y - w2m.y - o.y);
+    u.z = rowok * mP[2] * (xk[2] * w1.z - w1.y + gy * w2.z - w2m.z - o.z);
+    u.w = rowok * mP[3] * (xk[3] * w1.w - w1.z + gy * w2.w - w2m.w - o.w);
+    return u;
+  };
+  const bool lastx[4] = {j0 + 1 >= bp, j0 + 2 >= bp, j0 + 3 >= bp, j0 + 4 >= bp};
+  // one Chambolle update of row li from u at li and li + 1 (theta = 0 outside S)
+  auto upd = [&](int li, V2 w, float4 u_c, float4 u_n) {
+    const float ur = __shfl_down_sync(0xffffffffu, u_c.x, 1);
+    const float ydiff = (li + 1 < ap) ? 1.f : 0.f;
+    const float psx0 = lastx[0] ? 0.f : u_c.y - u_c.x, psy0 = ydiff * (u_n.x - u_c.x);
+    const float psx1 = lastx[1] ? 0.f : u_c.z - u_c.y, psy1 = ydiff * (u_n.y - u_c.y);
+    const float psx2 = lastx[2] ? 0.f : u_c.w - u_c.z, psy2 = ydiff * (u_n.z - u_c.z);
+    const float psx3 = lastx[3] ? 0.f : ur - u_c.w, psy3 = ydiff * (u_n.w - u_c.w);
+    const float ty = (li >= 0 && li < a) ? thy[sd.iy * g.A + li] : 0.f;
+    ball_update_fast(ty * thc[0], t, psx0, psy0, w.w1.x, w.w2.x);
+    ball_update_fast(ty * thc[1], t, psx1, psy1, w.w1.y, w.w2.y);
+    ball_update_fast(ty * thc[2], t, psx2, psy2, w.w1.z, w.w2.z);
+    ball_update_fast(ty * thc[3], t, psx3, psy3, w.w1.w, w.w2.w);
+    return w;
+  };
+  // ---- warm-up: raw rows r0-2 .. r0+2, level 1 on r0-1 and r0, level-2 u' on r0
+  const Raw Rm2 = ldraw(r0 - 2), Rm1 = ldraw(r0 - 1), R0 = ldraw(r0);
+  Raw Rn = ldraw(r0 + 1), Rm = ldraw(r0 + 2);
+  const float4 u_m1 = ucalc(r0 - 1, Rm1.w1, Rm1.w2, Rm2.w2, Rm1.o);
+  const float4 u_0 = ucalc(r0, R0.w1, R0.w2, Rm1.w2, R0.o);
+  float4 u_n = ucalc(r0 + 1, Rn.w1, Rn.w2, R0.w2, Rn.o);
+  const V2 vp_m1 = upd(r0 - 1, V2{Rm1.w1, Rm1.w2}, u_m1, u_0);
+  V2 vp_c = upd(r0, V2{R0.w1, R0.w2}, u_0, u_n);
+  float4 up_c = ucalc(r0, vp_c.w1, vp_c.w2, vp_m1.w2, R0.o);
+  for (int li = r0; li < r1; ++li) {
+    const Raw Rq = ldraw(li + 3);
+    const float4 u_m = ucalc(li + 2, Rm.w1, Rm.w2, Rn.w2, Rm.o);           // level 1, row li+2
+    const V2 vp_n = upd(li + 1, V2{Rn.w1, Rn.w2}, u_n, u_m);               // level 1, row li+1
+    const float4 up_n = ucalc(li + 1, vp_n.w1, vp_n.w2, vp_c.w2, Rn.o);    // level 2 u, row li+1
+    const V2 vo = upd(li, vp_c, up_c, up_n);                               // level 2, row li
+    if (out_lane) {
+      float *q1 = o1 + (size_t)li * g.ldS + j0, *q2 = o2 + (size_t)li * g.ldS + j0;
+      if (fullS) {
+        *reinterpret_cast<float4 *>(q1) = vo.w1;
+        *reinterpret_cast<float4 *>(q2) = vo.w2;
+      } else {
+        if (mS[0] != 0.f) { q1[0] = vo.w1.x; q2[0] = vo.w2.x; }
+        if (mS[1] != 0.f) { q1[1] = vo.w1.y; q2[1] = vo.w2.y; }
+        if (mS[2] != 0.f) { q1[2] = vo.w1.z; q2[2] = vo.w2.z; }
+        if (mS[3] != 0.f) { q1[3] = vo.w1.w; q2[3] = vo.w2.w; }
+      }
+    }
+    Rn = Rm;
+    Rm = Rq;
+    u_n = u_m;
+    vp_c = vp_n;
+    up_c = up_n;
+  }
+}
+
+
 // Sum over the local layout-row ky of sum_kx qhat (subdomains stored column-major per rank:
 // m = kx * m2loc + (ky - k0)).
 __device__ __forceinline__ float ky_part(const float *__restrict__ q, const Geo &g, int planes,
@@ -1870,6 +1995,20 @@ static int stencil_rb(int rows, int nsub, int strips) {
   for (int rb : {32, 16})
     if ((long long)strips * nsub * ((rows + rb - 1) / rb) >= 8192) return rb;
   return 8;
+}
+cudaError_t launch_sweep2x2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
+                            const float *vin, const float *om, float *vout, int n2, int n1,
+                            float t, cudaStream_t s) {
+  const int strips = (g.B + SQ_OUT - 1) / SQ_OUT;
+  dim3 grid((strips + SQ_WARPS - 1) / SQ_WARPS, (g.A + SQ_RB - 1) / SQ_RB, g.M);
+  static const int minb = getenv("TVS_X2_MINB") ? atoi(getenv("TVS_X2_MINB")) : 4;
+  if (minb >= 8)
+    k_sweep2q2<8><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  else if (minb >= 6)
+    k_sweep2q2<6><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  else
+    k_sweep2q2<4><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  return cudaGetLastError();
 }
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,

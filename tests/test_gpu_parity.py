@@ -297,3 +297,31 @@ def test_gemm_selftest(ctx, impl, mnk):
     """Projection GEMMs (SIMT fp32 and tcgen05 3xTF32) vs an fp64 host product."""
     err = ctx.selftest_gemm(*mnk, impl, seed=7)
     assert err < (4e-6 if impl else 1e-6), err
+
+
+def test_sweep2_two_updates_per_pass_bitwise(ctx):
+    """Kernel (a) temporal blocking (two inner updates per pass, the default) performs exactly the
+    operations of two single-update passes: outputs are bitwise identical to TVS_SWEEP2X2=0, on
+    ragged layouts, odd inner counts and the global-boundary rows/columns."""
+    import os
+    import paper_2602_17494_b200 as pkg
+    old = os.environ.get("TVS_SWEEP2X2")
+    os.environ["TVS_SWEEP2X2"] = "0"
+    try:
+        single = pkg.Context(0)
+    finally:
+        if old is None:
+            del os.environ["TVS_SWEEP2X2"]
+        else:
+            os.environ["TVS_SWEEP2X2"] = old
+    try:
+        for shape, L, inner in (((37, 53), (3, 2, 3, 5), 5), ((130, 260), (2, 1, 8, 0), 4),
+                                ((300, 300), (1, 1, 0, 0), 3)):
+            img = random_image(*shape, seed=shape[0] + shape[1])
+            tau, _ = S.chambolle_tfs(img.astype(np.float64), 0.05, 10)
+            args = (_dev(tau), _dev(img), 0.1, L, (3, inner, 0.125))
+            d1, p1, _ = ctx.tv_stokes_step2(*args, want_p=True)
+            d0, p0, _ = single.tv_stokes_step2(*args, want_p=True)
+            assert torch.equal(d0, d1) and torch.equal(p0, p1), shape
+    finally:
+        single.close()
