@@ -281,33 +281,48 @@ def ncu_traffic(workload, family):
 def aux_kernel_a(ctx, pkg, img, peaks, peak_src, flush):
     """Kernel (a) in the HBM-bound regime the north-star's >=70 % target refers to: config-4
     step 2 (8192^2, 8 horizontal strips, overlap 32, 30 x 20), tau = 0 (the sweep's work and
-    traffic are data-independent).  Reports the fused sweep's algorithmic GB/s: 20 B per point
-    per pass (v read 8, omega0 4, v write 8); a pass does two inner updates when the temporal
-    blocking is on (bytes_per_update = 10)."""
+    traffic are data-independent).  Algorithmic traffic: 20 B per point per pass (v read 8,
+    omega0 4, v write 8).  Reported twice: the default two-updates-per-pass kernel (temporal
+    blocking, 10 B per update) and the single-update kernel (TVS_SWEEP2X2=0, 20 B per update)."""
     import torch
     c4 = CONFIGS["c4"]
     L4, it4 = (c4.m2, c4.m1, c4.overlap, c4.overlap), (c4.sweeps, c4.inner, c4.t)
     d0 = torch.from_numpy(img).cuda()
     tau = torch.zeros((2, c4.n + 1, c4.n + 1), device="cuda", dtype=torch.float32)
-    ctx.tv_stokes_step2(tau, d0, c4.lam, L4, it4)          # warm-up (plan build)
-    flush_l2(flush)
-    torch.cuda.synchronize()
-    ctx.reset_kernel_times()
-    ctx.set_profiling(True)
-    _, _, st = ctx.tv_stokes_step2(tau, d0, c4.lam, L4, it4)
-    ctx.set_profiling(False)
-    kt = ctx.kernel_times()
-    i = pkg.KERNEL_FAMILIES.index("sweep2")
-    gbs = kt.bytes[i] / (kt.ms[i] / 1e3) / 1e9
-    per_pass = st.pixel_updates / max(1, kt.counts[i] * sum_sub(c4.n, L4, False))   # 1 or 2
-    return {"workload": "c4 step 2: 8192x8192, 8 strips, overlap 32, 30x20, tau = 0",
-            "kernel": "sweep2 (kernel a)", "bound": "hbm", "achieved": round(gbs, 1),
-            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
-            "frac_of_8TBs": round(gbs / 8000.0, 4), "avg_us": round(kt.ms[i] / kt.counts[i] * 1e3, 2),
-            "launches": kt.counts[i], "updates_per_pass": round(per_pass, 3),
-            "bytes_per_update": round(20 / per_pass, 2),
-            "step2_pixel_updates_per_s": st.pixel_updates / st.seconds,
-            "peak_source": f"hbm_gbs ({peak_src})"}
+
+    def measure(cx):
+        cx.tv_stokes_step2(tau, d0, c4.lam, L4, it4)          # warm-up (plan build)
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        cx.reset_kernel_times()
+        cx.set_profiling(True)
+        _, _, st = cx.tv_stokes_step2(tau, d0, c4.lam, L4, it4)
+        cx.set_profiling(False)
+        kt = cx.kernel_times()
+        i = pkg.KERNEL_FAMILIES.index("sweep2")
+        gbs = kt.bytes[i] / (kt.ms[i] / 1e3) / 1e9
+        per_pass = st.pixel_updates / max(1, kt.counts[i] * sum_sub(c4.n, L4, False))   # 1 or 2
+        return {"achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / peaks["hbm_gbs"], 4), "frac_of_8TBs": round(gbs / 8000.0, 4),
+                "avg_us": round(kt.ms[i] / kt.counts[i] * 1e3, 2), "launches": kt.counts[i],
+                "updates_per_pass": round(per_pass, 3), "bytes_per_update": round(20 / per_pass, 2),
+                "step2_pixel_updates_per_s": st.pixel_updates / st.seconds}
+
+    out = {"workload": "c4 step 2: 8192x8192, 8 strips, overlap 32, 30x20, tau = 0",
+           "kernel": "sweep2 (kernel a)", "bound": "hbm", "peak_source": f"hbm_gbs ({peak_src})"}
+    out.update(measure(ctx))
+    old = os.environ.get("TVS_SWEEP2X2")
+    os.environ["TVS_SWEEP2X2"] = "0"
+    try:
+        single = pkg.Context(torch.cuda.current_device())
+    finally:
+        if old is None:
+            del os.environ["TVS_SWEEP2X2"]
+        else:
+            os.environ["TVS_SWEEP2X2"] = old
+    out["single_update_per_pass"] = measure(single)
+    single.close()
+    return out
 
 
 def aux_step1_c4(ctx, pkg, img, flush):

@@ -182,6 +182,7 @@ struct ProjBatch {
   GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
   TmaGemmDesc *d_fwd3 = nullptr, *d_inv3 = nullptr;   // same, TMA tensor maps
   TmaGemmDesc *d_fwd4 = nullptr, *d_inv4 = nullptr;   // persistent: A as one fp32 plane
+  TmaGemmDesc *d_fwd5 = nullptr, *d_inv5 = nullptr;   // CTA pairs: B maps with 72-row boxes
   GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
   int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
   // chirp-z form of the two contractions (used when its estimated time is lower, TVS_DCT)
@@ -250,7 +251,7 @@ struct tvs_ctx {
   // projection contractions: TVS_GEMM = ts (default: persistent TMA + tcgen05 3xTF32 with A split
   // into tensor memory), persistent (A split in shared memory), tma (pre-split hi/lo operand
   // planes), cpasync (cp.async + tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
-  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3, G_TS = 4 };
+  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3, G_TS = 4, G_TS2 = 5 };
   int gemm = G_TS;
   bool presplit() const { return gemm == G_CPASYNC || gemm == G_TMA; }
   // partial x-DCTs: 0 = choose per batch by estimated time, 1 = dense GEMM, 2 = chirp-z (TVS_DCT)
@@ -578,6 +579,10 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
   TRY(upload(ctx, P.bufs, &B.d_fwd4, fwd3));
   TRY(upload(ctx, P.bufs, &B.d_inv4, inv3));
+  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 72));
+  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 72));
+  TRY(upload(ctx, P.bufs, &B.d_fwd5, fwd3));
+  TRY(upload(ctx, P.bufs, &B.d_inv5, inv3));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
@@ -850,6 +855,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     switch (gm) {
       case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
+      case tvs_ctx::G_TS2: return launch_gemm_tma_ts2(B.d_fwd5, B.nstack, B.tcM_fwd, B.fwdN, s);
       case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
       default: return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
@@ -876,6 +882,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     switch (gm) {
       case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+      case tvs_ctx::G_TS2: return launch_gemm_tma_ts2(B.d_inv5, 2 * B.nstack, B.tcM_inv, B.invN, s);
       case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
       default: return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
@@ -1164,6 +1171,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
             : strcmp(g, "cpasync") == 0 ? tvs_ctx::G_CPASYNC
             : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
             : strcmp(g, "persistent") == 0 ? tvs_ctx::G_PERSIST
+            : strcmp(g, "ts2") == 0     ? tvs_ctx::G_TS2
                                         : tvs_ctx::G_TS;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
   const char *dm = getenv("TVS_DCT");
@@ -1385,7 +1393,7 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
       {dA, impl == 0 ? dBk : dB, dC, M, N, K, lda, impl == 0 ? N : lda, N}};
   TRY(upload(ctx, own, &dd, desc));
   cudaError_t e;
-  if (impl == 5 || impl == 6) {   // persistent TMA kernels: A as one fp32 plane, split on chip
+  if (impl == 5 || impl == 6 || impl == 7) {   // persistent TMA kernels: A as one fp32 plane
     auto rna = [](float x) {
       uint32_t u;
       memcpy(&u, &x, 4);
@@ -1401,10 +1409,12 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
     TRY(upload(ctx, own, &dBl, Bl));
     GemmDesc2 g2 = {dA, nullptr, dBh, dBl, dC, M, N, K, lda, lda, N};
     std::vector<TmaGemmDesc> d3(1);
-    CK(make_tma_desc(&d3[0], g2, 144));
+    CK(make_tma_desc(&d3[0], g2, impl == 7 ? 72 : 144));
     TmaGemmDesc *dd3;
     TRY(upload(ctx, own, &dd3, d3));
-    e = impl == 5 ? launch_gemm_tma_p(dd3, 1, M, N, 144, 0) : launch_gemm_tma_ts(dd3, 1, M, N, 144, 0);
+    e = impl == 5   ? launch_gemm_tma_p(dd3, 1, M, N, 144, 0)
+        : impl == 6 ? launch_gemm_tma_ts(dd3, 1, M, N, 144, 0)
+                    : launch_gemm_tma_ts2(dd3, 1, M, N, 0);
   } else if (impl == 3 || impl == 4) {   // pre-split operands: hi = tf32 round-to-nearest-away, lo = x - hi
     auto rna = [](float x) {
       uint32_t u;

@@ -1128,7 +1128,300 @@ static cudaError_t launch_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair form of the TS kernel (cta_group::2, M = 256 per MMA): a cluster of two CTAs on one
+// TPC computes a 256 x 144 tile.  Each CTA stages its own 128 A rows (raw fp32 -> split into its
+// TMEM) and HALF of the pre-split B tile (72 of the 144 rows, hi + lo); the leader CTA issues the
+// MMAs, which read A from both CTAs' TMEM and B from both CTAs' shared memory.  Per SM this halves
+// the B bytes from L2 and the B reads from shared memory, and a stage shrinks to 34 KB (6 stages).
+// Barriers: A landed -> local fullA; B halves of both CTAs -> the leader's fullB (2-SM TMA);
+// A split written -> the leader's aful (remote arrive, count 2); MMA commits multicast to both
+// CTAs (empty, aemp, accf); epilogue done -> the leader's acce (remote arrive, count 8).
+constexpr int RSTAGES = 6;
+
+template <int BN>
+struct RSmem {
+  static constexpr int A_BYTES = BM * TBK * 4;                 // 16 KB
+  static constexpr int BH_BYTES = (BN / 2) * TBK * 4;          // 9 KB (72 rows)
+  static constexpr int STAGE = A_BYTES + 2 * BH_BYTES;         // 34 KB
+  static constexpr int TOTAL = RSTAGES * STAGE + 512 + 1024;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                                uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  uint32_t z = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8, %9, %10, %11, %12}, p;\n\t}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate), "r"(z), "r"(z), "r"(z), "r"(z), "r"(z),
+      "r"(z), "r"(z), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PNT, 1)
+k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int nblocks) {
+  using SM = RSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(smem + RSTAGES * SM::STAGE);
+  uint64_t *fullB = fullA + RSTAGES;     // leader only
+  uint64_t *empty = fullB + RSTAGES;
+  uint64_t *aful = empty + RSTAGES;      // [2] leader only
+  uint64_t *aemp = aful + 2;             // [2]
+  uint64_t *accf = aemp + 2;             // [2]
+  uint64_t *acce = accf + 2;             // [2] leader only
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  if (tid == 0) {
+    for (int q = 0; q < RSTAGES; ++q) {
+      mbar_init(&fullA[q], 1);
+      mbar_init(&fullB[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&aful[b], 2);
+      mbar_init(&aemp[b], 1);
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t ACC[2] = {0u, 256u}, ASLOT[2] = {144u, 400u};
+  const int per = mpairs * nblocks, ntiles = batch * per;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  auto decode = [&](int t, const TmaGemmDesc *&dp, int &mp0, int &n0) {
+    const int z = t / per, r = t - z * per;
+    dp = descs + z;
+    mp0 = (r / nblocks) * (2 * BM);
+    n0 = (r % nblocks) * BN;
+    return mp0 < dp->M && n0 < dp->N;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ TMA producer (both)
+      int it = 0;
+      const uint32_t fullB0 = map_to_rank0(smem_u32(fullB));
+      for (int t = cid; t < ntiles; t += ncl) {
+        const TmaGemmDesc *dp;
+        int mp0, n0;
+        if (!decode(t, dp, mp0, n0)) continue;
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int q = it % RSTAGES;
+          if (it >= RSTAGES) mbar_wait(&empty[q], ((it / RSTAGES) - 1) & 1);
+          const uint32_t st = sbase + q * SM::STAGE;
+          mbar_expect_tx(&fullA[q], SM::A_BYTES);
+          tma_load_2d(st, &dp->a_hi, kt * TBK, mp0 + (int)rank * BM, &fullA[q]);
+          if (leader) mbar_expect_tx(&fullB[q], 4 * SM::BH_BYTES);   // both CTAs' hi + lo halves
+          const uint32_t fb = fullB0 + q * 8;
+          tma_load_2d_2sm(st + SM::A_BYTES, &dp->b_hi, kt * TBK, n0 + (int)rank * (BN / 2), fb);
+          tma_load_2d_2sm(st + SM::A_BYTES + SM::BH_BYTES, &dp->b_lo, kt * TBK,
+                          n0 + (int)rank * (BN / 2), fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {   // ---------------------------------- MMA issuer (leader only)
+      constexpr uint32_t IDESC = make_idesc(2 * BM, BN);
+      int it = 0, tc = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        const TmaGemmDesc *dp;
+        int mp0, n0;
+        if (!decode(t, dp, mp0, n0)) continue;
+        const int b = tc & 1;
+        if (tc >= 2) mbar_wait(&acce[b], ((tc >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + ACC[b];
+        const int nk = (dp->K + TBK - 1) / TBK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int q = it % RSTAGES, a = it & 1;
+          mbar_wait(&fullB[q], (it / RSTAGES) & 1);
+          mbar_wait(&aful[a], (it >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = sbase + q * SM::STAGE;
+          const uint32_t bhi = st + SM::A_BYTES, blo = bhi + SM::BH_BYTES;
+          const uint32_t ahi = tmem + ASLOT[a], alo = ahi + 32;
+#pragma unroll
+          for (int ks = 0; ks < TBK / 8; ++ks) {
+            const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
+            mma_tf32_ts_pair(acc, alo + 8 * ks, dbh, IDESC, (kt > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32_ts_pair(acc, ahi + 8 * ks, dbl, IDESC, 1u);
+            mma_tf32_ts_pair(acc, ahi + 8 * ks, dbh, IDESC, 1u);
+          }
+          mma_commit_pair(&empty[q]);
+          mma_commit_pair(&aemp[a]);
+        }
+        mma_commit_pair(&accf[b]);
+        ++tc;
+      }
+    }
+  } else if (warp >= 6) {   // ----------------------------------------------- A split -> TMEM
+    const int q4 = warp & 3, row = q4 * 32 + lane;
+    const uint32_t aful0 = map_to_rank0(smem_u32(aful));
+    int it = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const TmaGemmDesc *dp;
+      int mp0, n0;
+      if (!decode(t, dp, mp0, n0)) continue;
+      const int nk = (dp->K + TBK - 1) / TBK;
+      for (int kt = 0; kt < nk; ++kt, ++it) {
+        const int q = it % RSTAGES, a = it & 1;
+        mbar_wait(&fullA[q], (it / RSTAGES) & 1);
+        if (it >= 2) mbar_wait(&aemp[a], ((it >> 1) - 1) & 1);
+        const float4 *ar = reinterpret_cast<const float4 *>(smem + q * SM::STAGE + row * 128);
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = ar[c ^ (row & 7)];
+          float h, l;
+          split(x.x, h, l); hi[4 * c] = __float_as_uint(h); lo[4 * c] = __float_as_uint(l);
+          split(x.y, h, l); hi[4 * c + 1] = __float_as_uint(h); lo[4 * c + 1] = __float_as_uint(l);
+          split(x.z, h, l); hi[4 * c + 2] = __float_as_uint(h); lo[4 * c + 2] = __float_as_uint(l);
+          split(x.w, h, l); hi[4 * c + 3] = __float_as_uint(h); lo[4 * c + 3] = __float_as_uint(l);
+        }
+        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT[a];
+        TST32(ta, hi);
+        TST32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 6 * 32) mbar_arrive_remote(aful0 + a * 8);
+      }
+    }
+  } else {   // warps 2..5 ------------------------------------------------------ epilogue
+    const int q4 = warp & 3;
+    const uint32_t acce0 = map_to_rank0(smem_u32(acce));
+    int tc = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const TmaGemmDesc *dp;
+      int mp0, n0;
+      if (!decode(t, dp, mp0, n0)) continue;
+      const int b = tc & 1;
+      mbar_wait(&accf[b], (tc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int M = dp->M, N = dp->N, ldc = dp->ldc;
+      float *C = dp->C;
+      const int row = mp0 + (int)rank * BM + q4 * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC[b] + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+          float *out = C + (size_t)row * ldc + n0 + c0;
+          const int nvalid = N - (n0 + c0);
+          if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+              reinterpret_cast<float4 *>(out)[qq] =
+                  make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                              __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nvalid) out[j] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(acce0 + b * 8);
+      ++tc;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int BN>
+static cudaError_t launch_tma_ts2(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                                  cudaStream_t s) {
+  static int nsm = 0;
+  if (!nsm) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts2<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         RSmem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int mp = (maxM + 2 * BM - 1) / (2 * BM), nb = (maxN + BN - 1) / BN;
+  const int ntiles = batch * mp * nb;
+  const int clusters = ntiles < nsm / 2 ? ntiles : nsm / 2;
+  k_gemm_tma_ts2<BN><<<2 * clusters, PNT, RSmem<BN>::TOTAL, s>>>(descs, batch, mp, nb);
+  return cudaGetLastError();
+}
+
 }  // namespace tc
+
+cudaError_t launch_gemm_tma_ts2(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                                cudaStream_t s) {
+  return tc::launch_tma_ts2<144>(descs, batch, maxM, maxN, s);
+}
 
 cudaError_t launch_gemm_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                                cudaStream_t s) {

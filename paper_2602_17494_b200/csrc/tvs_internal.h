@@ -164,6 +164,9 @@ cudaError_t launch_gemm_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int
 // TS form: A split into tensor memory (tcgen05.st), MMA with [a-tmem]; same descriptors as _p
 cudaError_t launch_gemm_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                                cudaStream_t s);
+// CTA-pair TS form (cta_group::2, 256 x 144 tiles); descriptors whose B maps have 72-row boxes
+cudaError_t launch_gemm_tma_ts2(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
+                                cudaStream_t s);
 cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
 cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,

@@ -290,7 +290,7 @@ def test_config3_full_size_short_schedule(ctx):
     check_step2(ctx, img, tau_ref, c.lam, L, 3, c.inner)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("mnk", [(128, 128, 16), (276, 2049, 276), (275, 275, 2049), (1, 7, 3),
                                  (130, 145, 35), (513, 513, 513)])
 def test_gemm_selftest(ctx, impl, mnk):
