@@ -177,6 +177,10 @@ struct ProjBatch {
   int ldG = 0;
   float *qhat = nullptr;
   double *z = nullptr, *rinv = nullptr, *segprod = nullptr;
+  SolveMaps *d_smaps = nullptr;   // TMA maps of the solve's staged blocks (solve4)
+  int smem_rows = 0;
+  int *d_order = nullptr;         // solve4 launch order: tiles grouped by chain [nchains][per_chain]
+  int per_chain = 0;
   float *phx = nullptr, *phy = nullptr, *phx_lo = nullptr, *phy_lo = nullptr;
   GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
   GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
@@ -259,6 +263,7 @@ struct tvs_ctx {
   int czt_max_m = 16384;
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
+  bool solve_tma = true;         // y-solve blocks staged by TMA (TVS_SOLVE_TMA=0: cp.async)
   int stop_crit = 0;       // tvs_set_stopping
   double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
   // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
@@ -587,6 +592,24 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
     CK(launch_segprod(B.d_tiles, B.d_first, B.nchains, B.rinv, B.ldn, B.AT, n1t, B.segprod, 0));
+    {   // tiles grouped by chain (layout row) for the solve's launch order
+      std::vector<std::vector<int>> byc(B.nchains);
+      for (int i = 0; i < B.ntiles; ++i) byc[B.tiles[i].chain].push_back(i);
+      for (auto &v : byc) B.per_chain = std::max(B.per_chain, (int)v.size());
+      std::vector<int> order((size_t)B.nchains * B.per_chain, -1);
+      for (int c = 0; c < B.nchains; ++c)
+        for (size_t k = 0; k < byc[c].size(); ++k) order[(size_t)c * B.per_chain + k] = byc[c][k];
+      TRY(upload(ctx, P.bufs, &B.d_order, order));
+    }
+    if (ctx->solve_tma) {   // TMA boxes of {32 columns, <= 256 rows} for the staged blocks
+      SolveMaps m{};
+      m.nbox = (B.AT + 255) / 256;
+      m.box_rows = (B.AT + m.nbox - 1) / m.nbox;
+      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, 32, m.box_rows));
+      CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, 32, m.box_rows));
+      B.smem_rows = m.nbox * m.box_rows;
+      TRY(upload(ctx, P.bufs, &B.d_smaps, std::vector<SolveMaps>{m}));
+    }
   }
   CK(cudaDeviceSynchronize());
   return TVS_OK;
@@ -842,7 +865,8 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
     TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
       return B.segprod ? launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
-                                            B.rinv, B.segprod, B.phx, B.phy, B.AP, s)
+                                            B.rinv, B.segprod, B.phx, B.phy, B.AP, B.d_smaps,
+                                            B.smem_rows, B.d_order, B.nchains, B.per_chain, s)
                        : launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
                                             B.rinv, reinterpret_cast<float *>(B.z), B.phx, B.phy,
                                             nullptr, nullptr, B.AP, s);
@@ -865,7 +889,8 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
     if (ctx->solve_impl == 3 && !tc && B.segprod)
       return launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
-                                B.segprod, B.phx, B.phy, B.AP, s);
+                                B.segprod, B.phx, B.phy, B.AP, B.d_smaps, B.smem_rows,
+                                B.d_order, B.nchains, B.per_chain, s);
     if (ctx->solve_impl >= 3)
       return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
                                 reinterpret_cast<float *>(B.z), B.phx, B.phy,
@@ -1174,6 +1199,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
             : strcmp(g, "ts2") == 0     ? tvs_ctx::G_TS2
                                         : tvs_ctx::G_TS;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
+  if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {

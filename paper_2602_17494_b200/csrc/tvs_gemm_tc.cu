@@ -1466,6 +1466,29 @@ static cudaError_t encode_2d(CUtensorMap *map, const float *base, int cols, int 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Plain (unswizzled) 2D tensor map for the y-solve's staged blocks: fp32 or fp64 elements.
+cudaError_t encode_plain_2d(CUtensorMap *map, const void *base, bool fp64, int cols, int rows,
+                            int ld_elems, int box_cols, int box_rows) {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !p) return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+    fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  const size_t es = fp64 ? 8 : 4;
+  const cuuint64_t dims[2] = {(cuuint64_t)(cols > 0 ? cols : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld_elems * es};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, fp64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn) {
   memset(out, 0, sizeof *out);
   cudaError_t e;

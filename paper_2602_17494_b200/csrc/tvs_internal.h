@@ -52,6 +52,14 @@ struct alignas(64) TmaGemmDesc {
   float *C;
   int M, N, K, ldc;
 };
+// Tensor maps of the y-solve's staged column blocks (Q-hat fp32 and pivots fp64), boxes of
+// {32 columns, box_rows rows}, nbox boxes per CTA.
+struct alignas(64) SolveMaps {
+  CUtensorMap q, r;
+  int box_rows, nbox;
+};
+cudaError_t encode_plain_2d(CUtensorMap *map, const void *base, bool fp64, int cols, int rows,
+                            int ld_elems, int box_cols, int box_rows);
 // host: encode the four tensor maps of d for a tile of width bn
 cudaError_t make_tma_desc(TmaGemmDesc *out, const GemmDesc2 &d, int bn);
 
@@ -181,7 +189,8 @@ cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains,
 cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv,
                                const double *segprod, float *phx, float *phy, int AP,
-                               cudaStream_t s);
+                               const SolveMaps *maps, int smem_rows, const int *order,
+                               int nchains, int per_chain, cudaStream_t s);
 // segmented y-solve: fp32 z scratch [tile][AT][ldn]
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,

@@ -1683,28 +1683,65 @@ __global__ void k_segprod(const ProjTile *__restrict__ tiles, const int *__restr
 __global__ void __launch_bounds__(SJB *SSEG_MAX)
 k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
               int AT, int ldn, const double *__restrict__ rinv, const double *__restrict__ segprod,
-              float *__restrict__ phx, float *__restrict__ phy, int AP) {
+              float *__restrict__ phx, float *__restrict__ phy, int AP,
+              const SolveMaps *__restrict__ maps, int srows, const int *__restrict__ order,
+              int per_chain) {
   __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
   __shared__ double sh_tot[SJB];
-  extern __shared__ __align__(16) double sr4[];   // [AT][SJB] pivots, then [AT][SJB] floats
-  float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)AT * SJB);   // Q-hat, overwritten by z
+  __shared__ uint64_t sbar;
+  extern __shared__ __align__(128) double sr4[];   // [srows][SJB] pivots, then [srows][SJB] floats
+  float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)srows * SJB);   // Q-hat, overwritten by z
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
-  const int j = blockIdx.x * SJB + tx;
-  const int tix = blockIdx.y;
+  // grid (tile within its chain, frequency block, chain): the tiles sharing a pivot block (one
+  // layout row) run back to back, so their pivot reads hit L2
+  const int jb = blockIdx.y;
+  const int tix = order[blockIdx.z * per_chain + blockIdx.x];
+  if (tix < 0) return;
+  const int j = jb * SJB + tx;
   const bool valid = j < n1;
   const ProjTile tl = tiles[tix];
   const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
   const int LS = (nt + nseg - 1) / nseg;
   const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
   const int jj = valid ? j : 0;
-  {   // stage the column blocks (16-byte asynchronous copies, all rows in flight)
-    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)blockIdx.x * SJB;
-    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)blockIdx.x * SJB;
+  if (maps) {   // stage both column blocks with TMA (nbox boxes of {32 columns, box_rows rows})
+    const int lt = sg * SJB + tx;
+    if (lt == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sbar)));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sbar);
+    if (lt == 0) {
+      const int br = maps->box_rows, nb = maps->nbox;
+      const uint32_t bytes = (uint32_t)(nb * br * SJB * (sizeof(float) + sizeof(double)));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      const int col = jb * SJB;
+      for (int bi = 0; bi < nb; ++bi) {
+        const uint32_t dq = (uint32_t)__cvta_generic_to_shared(sb4 + (size_t)bi * br * SJB);
+        const uint32_t dr = (uint32_t)__cvta_generic_to_shared(sr4 + (size_t)bi * br * SJB);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dq),
+            "l"(reinterpret_cast<uint64_t>(&maps->q)), "r"(col), "r"(tix * AT + bi * br), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dr),
+            "l"(reinterpret_cast<uint64_t>(&maps->r)), "r"(col), "r"(tl.chain * AT + bi * br), "r"(bar)
+            : "memory");
+      }
+    }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+        "@!P1 bra W_%=;\n\t}" ::"r"(bar) : "memory");
+  } else {   // stage the column blocks (16-byte asynchronous copies, all rows in flight)
+    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)jb * SJB;
+    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)jb * SJB;
     const int nthr = SJB * nseg, lt = sg * SJB + tx;
     for (int e = lt; e < nt * (SJB / 4); e += nthr) {
       const int k = e / (SJB / 4), c = e % (SJB / 4);
       float *dst = sb4 + k * SJB + 4 * c;
-      if (blockIdx.x * SJB + 4 * c < ldn) {
+      if (jb * SJB + 4 * c < ldn) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
                      "l"(blk + (size_t)k * ldn + 4 * c) : "memory");
@@ -1715,7 +1752,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     for (int e = lt; e < nt * (SJB / 2); e += nthr) {
       const int k = e / (SJB / 2), c = e % (SJB / 2);
       double *dst = sr4 + k * SJB + 2 * c;
-      if (blockIdx.x * SJB + 2 * c < ldn) {
+      if (jb * SJB + 2 * c < ldn) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
                      "l"(rblk + (size_t)k * ldn + 2 * c) : "memory");
@@ -2183,7 +2220,7 @@ cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1
   return cudaGetLastError();
 }
 int solve_nseg(int AT) { return std::min(SSEG_MAX, std::max(1, (AT + 31) / 32)); }
-bool solve4_fits(int AT) { return (size_t)AT * SJB * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
+bool solve4_fits(int AT) { return (size_t)(AT + 1) * SJB * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
 cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
                            int ldn, int AT, int n1, double *segprod, cudaStream_t s) {
   k_segprod<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, rinv, ldn, AT,
@@ -2193,9 +2230,11 @@ cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains,
 cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv,
                                const double *segprod, float *phx, float *phy, int AP,
-                               cudaStream_t s) {
+                               const SolveMaps *maps, int smem_rows, const int *order,
+                               int nchains, int per_chain, cudaStream_t s) {
   const int nseg = solve_nseg(AT);
-  const size_t smem = (size_t)AT * SJB * (sizeof(float) + sizeof(double));
+  const int srows = maps ? smem_rows : AT;
+  const size_t smem = (size_t)srows * SJB * (sizeof(float) + sizeof(double));
   static size_t configured = 0;
   // (the kernel also has ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
   if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
@@ -2204,8 +2243,9 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k_proj_solve4<<<dim3((n1 + SJB - 1) / SJB, ntiles), dim3(SJB, nseg), smem, s>>>(
-      tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP);
+  (void)ntiles;
+  k_proj_solve4<<<dim3(per_chain, (n1 + SJB - 1) / SJB, nchains), dim3(SJB, nseg), smem, s>>>(
+      tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
