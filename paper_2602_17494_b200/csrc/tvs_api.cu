@@ -864,6 +864,9 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     }));
     if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
     TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
+      if (ctx->solve_impl == 5 && B.segprod && B.d_smaps && solve5_fits(B.AT))
+        return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
+                                  B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
       return B.segprod ? launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
                                             B.rinv, B.segprod, B.phx, B.phy, B.AP, B.d_smaps,
                                             B.smem_rows, B.d_order, B.nchains, B.per_chain, s)
@@ -887,7 +890,10 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    if (ctx->solve_impl == 3 && !tc && B.segprod)
+    if (ctx->solve_impl == 5 && !tc && B.segprod && B.d_smaps && solve5_fits(B.AT))
+      return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
+                                B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
+    if ((ctx->solve_impl == 3 || ctx->solve_impl == 5) && !tc && B.segprod)
       return launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
                                 B.segprod, B.phx, B.phy, B.AP, B.d_smaps, B.smem_rows,
                                 B.d_order, B.nchains, B.per_chain, s);
@@ -1211,6 +1217,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
                   : strcmp(sv, "chunked") == 0 ? 2
                   : strcmp(sv, "serial") == 0  ? 1
                   : strcmp(sv, "seg3") == 0    ? 4
+                  : strcmp(sv, "chain") == 0   ? 5
                                                : 3;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {

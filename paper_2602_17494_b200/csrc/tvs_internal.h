@@ -191,6 +191,12 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
                                const double *segprod, float *phx, float *phy, int AP,
                                const SolveMaps *maps, int smem_rows, const int *order,
                                int nchains, int per_chain, cudaStream_t s);
+// chain-shared y-solve (one pivot block per CTA for the tiles of a layout row); needs the TMA maps
+bool solve5_fits(int AT);
+cudaError_t launch_proj_solve5(const ProjTile *tiles, int n2, int n1, int AT, int ldn,
+                               const double *segprod, float *phx, float *phy, int AP,
+                               const SolveMaps *maps, int smem_rows, const int *order, int nchains,
+                               int per_chain, cudaStream_t s);
 // segmented y-solve: fp32 z scratch [tile][AT][ldn]
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,

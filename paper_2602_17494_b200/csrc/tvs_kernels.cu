@@ -1914,6 +1914,240 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   }
 }
 
+// y-solve, chain-shared form: one CTA per (layout row = pivot chain, frequency block) runs the
+// chain's tiles two at a time (two groups of nseg warps, group-local named barriers) against ONE
+// staged pivot block, so the pivots cross L2 -> SM once per chain instead of once per tile.  Same
+// passes and arithmetic as k_proj_solve4.
+__device__ __forceinline__ void group_sync(int g, int nthr) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthr) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                      uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra W_%=;\n\t}" ::"r"(bar), "r"(ph) : "memory");
+}
+
+__global__ void __launch_bounds__(SJB * 2 * SSEG_MAX)
+k_proj_solve5(const ProjTile *__restrict__ tiles, int n2, int n1, int AT, int ldn,
+              const double *__restrict__ segprod, float *__restrict__ phx, float *__restrict__ phy,
+              int AP, const SolveMaps *__restrict__ maps, int srows, const int *__restrict__ order,
+              int per_chain) {
+  __shared__ double sh_a[2][SSEG_MAX][SJB], sh_c[2][SSEG_MAX][SJB];
+  __shared__ double sh_tot[2][SJB];
+  __shared__ uint64_t sbar[2];
+  extern __shared__ __align__(128) double sr5[];   // [srows][SJB] pivots, then 2 x [srows][SJB] floats
+  const int nseg = blockDim.y / 2;
+  const int tx = threadIdx.x, gq = threadIdx.y / nseg, sg = threadIdx.y % nseg;
+  const int gthr = SJB * nseg;
+  const int jb = blockIdx.x, chain = blockIdx.y;
+  const int j = jb * SJB + tx;
+  const bool valid = j < n1;
+  const int jj = valid ? j : 0;
+  const int lt = threadIdx.y * SJB + tx;
+  const int br = maps->box_rows, nb = maps->nbox;
+  float *sbq = reinterpret_cast<float *>(sr5 + (size_t)srows * SJB) + (size_t)gq * srows * SJB;
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+  const uint32_t bar1 = (uint32_t)__cvta_generic_to_shared(&sbar[1]);
+  if (lt == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const int col = jb * SJB;
+  if (lt == 0) {   // the chain's pivot block, once
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar0),
+                 "r"((uint32_t)(nb * br * SJB * sizeof(double))) : "memory");
+    for (int bi = 0; bi < nb; ++bi)
+      tma2d((uint32_t)__cvta_generic_to_shared(sr5 + (size_t)bi * br * SJB), &maps->r, col,
+            chain * AT + bi * br, bar0);
+  }
+  const double *ri = sr5 + tx;
+  float *sbt = sbq + tx;
+  const double *__restrict__ gp = segprod + (size_t)chain * 2 * nseg * ldn + jj;
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
+  const int npairs = (per_chain + 1) / 2;
+  for (int pr = 0; pr < npairs; ++pr) {
+    // Q-hat blocks of this pair's two tiles (group 0: tile 2 pr, group 1: tile 2 pr + 1)
+    if (lt == 0) {
+      uint32_t bytes = 0;
+      for (int g = 0; g < 2; ++g)
+        if (2 * pr + g < per_chain && order[chain * per_chain + 2 * pr + g] >= 0)
+          bytes += (uint32_t)(nb * br * SJB * sizeof(float));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar1), "r"(bytes) : "memory");
+      for (int g = 0; g < 2; ++g) {
+        if (2 * pr + g >= per_chain) continue;
+        const int t = order[chain * per_chain + 2 * pr + g];
+        if (t < 0) continue;
+        float *dstb = reinterpret_cast<float *>(sr5 + (size_t)srows * SJB) + (size_t)g * srows * SJB;
+        for (int bi = 0; bi < nb; ++bi)
+          tma2d((uint32_t)__cvta_generic_to_shared(dstb + (size_t)bi * br * SJB), &maps->q, col,
+                t * AT + bi * br, bar1);
+      }
+    }
+    if (pr == 0) mbar_wait_parity(bar0, 0);
+    mbar_wait_parity(bar1, pr & 1);
+    const int slot = 2 * pr + gq;
+    const int tix = slot < per_chain ? order[chain * per_chain + slot] : -1;
+    if (tix >= 0) {
+      const ProjTile tl = tiles[tix];
+      const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
+      const int LS = (nt + nseg - 1) / nseg;
+      const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
+      // ---- forward, local pass
+      double a = 0.0;
+      if (valid) {
+        if (j == 0) {
+          for (int k = k0; k < k1; ++k) a += (double)sbt[k * SJB];
+        } else {
+          int k = k0;
+          if (k == 0 && k < k1) {
+            a = (double)sbt[0];
+            k = 1;
+          }
+          for (; k + SU <= k1; k += SU) {
+            float bv[SU];
+            double rv[SU];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+              bv[u] = sbt[(k + u) * SJB];
+              rv[u] = ri[(k + u - 1) * SJB];
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u) a = fma(-rv[u], a, (double)bv[u]);
+          }
+          for (; k < k1; ++k) a = fma(-ri[(k - 1) * SJB], a, (double)sbt[k * SJB]);
+        }
+      }
+      sh_a[gq][sg][tx] = a;
+      sh_c[gq][sg][tx] = (valid && j > 0) ? gp[sg * ldn] : 1.0;
+      group_sync(gq, gthr);
+      if (sg == 0) {
+        double Z = 0.0;
+        for (int q = 0; q < nseg; ++q) {
+          const double as = sh_a[gq][q][tx], gs = sh_c[gq][q][tx];
+          sh_c[gq][q][tx] = Z;
+          Z = fma(gs, Z, as);
+        }
+        sh_tot[gq][tx] = Z;
+      }
+      group_sync(gq, gthr);
+      const double fcarry = sh_c[gq][sg][tx];
+      // ---- forward, final pass (z overwrites b)
+      if (valid && j > 0 && k0 < k1) {
+        double zc = fcarry;
+        int k = k0;
+        if (k == 0) {
+          zc = (double)sbt[0];
+          k = 1;
+        }
+        for (; k + SU <= k1; k += SU) {
+          float bv[SU];
+          double rv[SU];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            bv[u] = sbt[(k + u) * SJB];
+            rv[u] = ri[(k + u - 1) * SJB];
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            zc = fma(-rv[u], zc, (double)bv[u]);
+            sbt[(k + u) * SJB] = (float)zc;
+          }
+        }
+        for (; k < k1; ++k) {
+          zc = fma(-ri[(k - 1) * SJB], zc, (double)sbt[k * SJB]);
+          sbt[k * SJB] = (float)zc;
+        }
+      }
+      // ---- backward, local pass
+      a = 0.0;
+      if (valid && j > 0 && k0 < k1) {
+        int k = k1 - 1;
+        for (; k - SU + 1 >= k0; k -= SU) {
+          float zv[SU];
+          double rv[SU];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            zv[u] = sbt[(k - u) * SJB];
+            rv[u] = ri[(k - u) * SJB];
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u) a = rv[u] * ((double)zv[u] - a);
+        }
+        for (; k >= k0; --k) a = ri[k * SJB] * ((double)sbt[k * SJB] - a);
+      }
+      group_sync(gq, gthr);
+      sh_a[gq][sg][tx] = a;
+      sh_c[gq][sg][tx] = (valid && j > 0) ? gp[(nseg + sg) * ldn] : 1.0;
+      group_sync(gq, gthr);
+      if (sg == 0) {
+        double U = 0.0;
+        for (int q = nseg - 1; q >= 0; --q) {
+          const double as = sh_a[gq][q][tx], gs = sh_c[gq][q][tx];
+          sh_c[gq][q][tx] = U;
+          U = fma(gs, U, as);
+        }
+      }
+      group_sync(gq, gthr);
+      if (valid && k0 < k1) {
+        float *__restrict__ ox = phx + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
+        float *__restrict__ oy = phy + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
+        if (j == 0) {
+          const double mu = sh_tot[gq][tx] / (double)n2;
+          double pre = fcarry;
+          for (int k = k0; k < min(k1, nout); ++k) {
+            pre += (double)sbt[k * SJB];
+            const int y = tl.ty0 + k;
+            const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
+            if (k >= po) {
+              ox[(size_t)k * ldn] = 0.f;
+              oy[(size_t)k * ldn] = (float)(s2 * w);
+            }
+          }
+        } else {
+          const double cx = -s2 * 2.0 * sinpi((double)j / (2.0 * n1));
+          double un = sh_c[gq][sg][tx];
+          const int klo = max(k0, po), khi = min(k1, nout);
+          int k = k1 - 1;
+          for (; k >= khi && k >= k0; --k) un = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+          for (; k - SU + 1 >= klo; k -= SU) {
+            float zv[SU];
+            double rv[SU];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+              zv[u] = sbt[(k - u) * SJB];
+              rv[u] = ri[(k - u) * SJB];
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+              const double uk = rv[u] * ((double)zv[u] - un);
+              ox[(size_t)(k - u) * ldn] = (float)(cx * uk);
+              oy[(size_t)(k - u) * ldn] = (k - u == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+              un = uk;
+            }
+          }
+          for (; k >= klo; --k) {
+            const double uk = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+            ox[(size_t)k * ldn] = (float)(cx * uk);
+            oy[(size_t)k * ldn] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+            un = uk;
+          }
+        }
+      }
+    }
+    __syncthreads();   // both groups done with their Q-hat buffers before the next pair lands
+  }
+}
+
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
 constexpr int GBM = 128, GBN = 128, GBK = 8;
@@ -2246,6 +2480,27 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   (void)ntiles;
   k_proj_solve4<<<dim3(per_chain, (n1 + SJB - 1) / SJB, nchains), dim3(SJB, nseg), smem, s>>>(
       tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
+  return cudaGetLastError();
+}
+bool solve5_fits(int AT) {
+  return (size_t)(AT + 1) * SJB * (sizeof(double) + 2 * sizeof(float)) <= 180 * 1024 &&
+         2 * solve_nseg(AT) <= 2 * SSEG_MAX;
+}
+cudaError_t launch_proj_solve5(const ProjTile *tiles, int n2, int n1, int AT, int ldn,
+                               const double *segprod, float *phx, float *phy, int AP,
+                               const SolveMaps *maps, int smem_rows, const int *order, int nchains,
+                               int per_chain, cudaStream_t s) {
+  const int nseg = solve_nseg(AT);
+  const size_t smem = (size_t)smem_rows * SJB * (sizeof(double) + 2 * sizeof(float));
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_proj_solve5, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k_proj_solve5<<<dim3((n1 + SJB - 1) / SJB, nchains), dim3(SJB, 2 * nseg), smem, s>>>(
+      tiles, n2, n1, AT, ldn, segprod, phx, phy, AP, maps, smem_rows, order, per_chain);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
