@@ -116,6 +116,7 @@ def run_ours(args, rank, world, local_rank):
     c, L, it = workload(args.workload)
     img = c.image()
     aux_img = CONFIGS["c4"].image() if (not args.no_aux and world == 1) else None   # before CUDA init
+    aux5_img = CONFIGS["c5w1"].image() if (not args.no_aux and world == 1) else None
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -259,6 +260,8 @@ def run_ours(args, rank, world, local_rank):
     if aux_img is not None:
         line["aux_kernel_a_c4"] = aux_kernel_a(ctx, pkg, aux_img, peaks, peak_src, flush)
         line["aux_step1_c4"] = aux_step1_c4(ctx, pkg, aux_img, flush)
+    if aux5_img is not None:
+        line["aux_c5w1"] = aux_c5w1(ctx, pkg, aux5_img, flush)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c, L, it, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
@@ -346,6 +349,29 @@ def aux_step1_c4(ctx, pkg, img, flush):
             "seconds": round(st.seconds, 3), "pixel_updates": st.pixel_updates,
             "pixel_updates_per_s": st.pixel_updates / st.seconds, "avg_us": fams,
             "dct": "chirp-z (N = 8193 > 4096)"}
+
+
+def aux_c5w1(ctx, pkg, img, flush):
+    """Config 5 at its one-GPU weak-scaling size (11585^2, 16 x 16 subdomains, s = 32): step 2
+    over the full 20 x 10 schedule and one outer sweep of step 1 (10 Alg. 5 updates, chirp-z
+    x-DCTs), each after a warm-up call; rates in dual pixel-updates/s."""
+    import torch
+    c = CONFIGS["c5w1"]
+    L = (c.m2, c.m1, c.overlap, c.overlap)
+    d0 = torch.from_numpy(img).cuda()
+    tau = torch.zeros((2, c.n + 1, c.n + 1), device="cuda", dtype=torch.float32)
+    ctx.tv_stokes_step2(tau, d0, c.lam, L, (1, 2, c.t))
+    flush_l2(flush)
+    _, _, s2 = ctx.tv_stokes_step2(tau, d0, c.lam, L, (c.sweeps, c.inner, c.t))
+    ctx.tv_stokes_step1(d0, c.delta, L, (1, 1, c.t))
+    flush_l2(flush)
+    _, _, s1 = ctx.tv_stokes_step1(d0, c.delta, L, (1, c.inner, c.t))
+    return {"workload": "c5 weak-scaling base: 11585x11585, 16x16 subdomains, overlap 32",
+            "step2_20x10": {"seconds": round(s2.seconds, 3), "pixel_updates": s2.pixel_updates,
+                            "pixel_updates_per_s": s2.pixel_updates / s2.seconds},
+            "step1_1x10": {"seconds": round(s1.seconds, 3), "pixel_updates": s1.pixel_updates,
+                           "pixel_updates_per_s": s1.pixel_updates / s1.seconds},
+            "dct": "chirp-z (N = 11586 > 4096)"}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU)
