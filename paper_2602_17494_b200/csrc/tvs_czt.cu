@@ -84,10 +84,12 @@ __device__ __forceinline__ float2 w16(int e) {
   return make_float2(C[e & 15], -C[(e + 12) & 15]);   // sin(x) = cos(x - pi/2)
 }
 
+// The last DIF pass (span 1, or the pair of spans 4 and 1) is left to czt_middle, which fuses it
+// with the pointwise kernel multiply and the first DIT pass: both touch the same 4 (or 16)
+// consecutive elements, so the three run in registers.
 __device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
   const int nth = blockDim.x, tid = threadIdx.x;
-  int lg = logM4 - 1;
-  for (; lg >= 1; lg -= 2) {
+  for (int lg = logM4 - 1; lg >= 2; lg -= 2) {
     const int L = 1 << (2 * lg), Q = L >> 2, s1 = M >> (2 * lg + 2);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
       const int blk = gidx >> (2 * lg - 2), kp = gidx & (Q - 1);
@@ -119,38 +121,78 @@ __device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
     }
     __syncthreads();
   }
-  if (lg == 0) {   // span 1 (no twiddles)
-    for (int b = tid; b < (M >> 2); b += nth) {
-      float2 x0 = z[pz(4 * b)], x1 = z[pz(4 * b + 1)], x2 = z[pz(4 * b + 2)], x3 = z[pz(4 * b + 3)];
-      bfly4_dif(x0, x1, x2, x3);
-      z[pz(4 * b)] = x0;
-      z[pz(4 * b + 1)] = x1;
-      z[pz(4 * b + 2)] = x2;
-      z[pz(4 * b + 3)] = x3;
-    }
-    __syncthreads();
-  }
 }
 
-// In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
-// transform times M.  Mirror image of fft_dif (span 1 first when the stage count is odd, then
-// fused pairs of spans L and 4L).
-__device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
+// Last DIF pass, pointwise multiply by the transformed kernel gk (digit-reversed order, as the
+// DIF output), first DIT pass.  logM4 odd: span-1 stages on 4 consecutive elements (no twiddles);
+// even: the span-4/span-1 pairs on 16 consecutive elements (kp = 0: twiddles e^{-2 pi i c r/16}).
+__device__ void czt_middle(float2 *z, int M, int logM4, const float2 *__restrict__ gk) {
   const int nth = blockDim.x, tid = threadIdx.x;
-  int lg = 0;
   if (logM4 & 1) {
     for (int b = tid; b < (M >> 2); b += nth) {
+      const float4 g01 = __ldg(reinterpret_cast<const float4 *>(gk + 4 * b));
+      const float4 g23 = __ldg(reinterpret_cast<const float4 *>(gk + 4 * b + 2));
       float2 x0 = z[pz(4 * b)], x1 = z[pz(4 * b + 1)], x2 = z[pz(4 * b + 2)], x3 = z[pz(4 * b + 3)];
+      bfly4_dif(x0, x1, x2, x3);
+      x0 = cmul(x0, make_float2(g01.x, g01.y));
+      x1 = cmul(x1, make_float2(g01.z, g01.w));
+      x2 = cmul(x2, make_float2(g23.x, g23.y));
+      x3 = cmul(x3, make_float2(g23.z, g23.w));
       bfly4_dit(x0, x1, x2, x3);
       z[pz(4 * b)] = x0;
       z[pz(4 * b + 1)] = x1;
       z[pz(4 * b + 2)] = x2;
       z[pz(4 * b + 3)] = x3;
     }
-    __syncthreads();
-    lg = 1;
+  } else {
+    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+      const int base = gidx * 16;
+      float4 g[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) g[m] = __ldg(reinterpret_cast<const float4 *>(gk + base) + m);
+      float2 x[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m)];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // DIF span 4, k = r
+        bfly4_dif(x[r], x[r + 4], x[r + 8], x[r + 12]);
+        if (r) {
+          x[r + 4] = cmul(x[r + 4], w16(r));
+          x[r + 8] = cmul(x[r + 8], w16(2 * r));
+          x[r + 12] = cmul(x[r + 12], w16(3 * r));
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bfly4_dif(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        x[2 * m] = cmul(x[2 * m], make_float2(g[m].x, g[m].y));
+        x[2 * m + 1] = cmul(x[2 * m + 1], make_float2(g[m].z, g[m].w));
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bfly4_dit(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // DIT span 4, k = r
+        if (r) {
+          x[r + 4] = cmulc(x[r + 4], w16(r));
+          x[r + 8] = cmulc(x[r + 8], w16(2 * r));
+          x[r + 12] = cmulc(x[r + 12], w16(3 * r));
+        }
+        bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
+      }
+#pragma unroll
+      for (int m = 0; m < 16; ++m) z[pz(base + m)] = x[m];
+    }
   }
-  for (; lg < logM4; lg += 2) {
+  __syncthreads();
+}
+
+// In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
+// transform times M.  Mirror image of fft_dif: after czt_middle's first pass, fused pairs of
+// spans L and 4L.
+__device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
+  const int nth = blockDim.x, tid = threadIdx.x;
+  for (int lg = (logM4 & 1) ? 1 : 2; lg < logM4; lg += 2) {   // first pass done by czt_middle
     const int L = 1 << (2 * lg), s2 = M >> (2 * lg + 4);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
       const int blk = gidx >> (2 * lg), kp = gidx & (L - 1);
@@ -225,9 +267,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
     }
     __syncthreads();
     fft_dif(zsm, G.M, G.logM4, twd);
-    const float2 *__restrict__ gk = gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M;
-    for (int i = tid; i < G.M; i += nth) zsm[pz(i)] = cmul(zsm[pz(i)], __ldg(gk + i));
-    __syncthreads();
+    czt_middle(zsm, G.M, G.logM4, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M);
     fft_dit_inv(zsm, G.M, G.logM4, twd);
     for (int i = tid; i < vcnt; i += nth) {
       const float2 c = cmul(chirp(v0 + i, cpost, n4, inv_n4, inv_2n), zsm[pz(i)]);
