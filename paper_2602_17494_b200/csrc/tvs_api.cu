@@ -263,6 +263,7 @@ struct tvs_ctx {
   int czt_max_m = 16384;
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
+  int x2_minw = 512;             // ... on subdomains at least this wide (TVS_X2_MINW)
   bool solve_tma = true;         // y-solve blocks staged by TMA (TVS_SOLVE_TMA=0: cp.async)
   int stop_crit = 0;       // tvs_set_stopping
   double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
@@ -1019,7 +1020,7 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       // two updates per pass where possible (temporal blocking, bitwise identical): the
       // algorithmic traffic of the pass is still 20 B per point, now for two updates
       // (only for wide subdomains: narrow ones keep the 2-column kernel with short row blocks)
-      const bool two = ctx->sweep2x2 && k + 1 < it.inner && g.B >= 512;
+      const bool two = ctx->sweep2x2 && k + 1 < it.inner && g.B >= ctx->x2_minw;
       TRY(run(ctx, s, F_SWEEP2, sweep_bytes, 0, [&] {
         return two ? launch_sweep2x2(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->om,
                                      P->v[cur ^ 1], n2, n1, it.t, s)
@@ -1205,6 +1206,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
             : strcmp(g, "ts2") == 0     ? tvs_ctx::G_TS2
                                         : tvs_ctx::G_TS;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
+  if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;

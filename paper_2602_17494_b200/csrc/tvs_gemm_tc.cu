@@ -950,8 +950,9 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
   const uint32_t sbase = smem_u32(smem);
   // TMEM columns: NS = 2: accumulators 0 / 256, A slots 144 / 400; NS = 3: accumulators 0 / 144,
   // A slots 288 / 352 / 416 (each slot: hi 32 + lo 32 columns)
-  const uint32_t ACC[2] = {0u, NS == 2 ? 256u : 144u};
-  const uint32_t ASLOT[3] = {NS == 2 ? 144u : 288u, NS == 2 ? 400u : 352u, 416u};
+  // (computed, not tables: an indexed array lands in local memory, an LDL on the MMA issue path)
+  auto ACC = [](int b) { return (uint32_t)b * (NS == 2 ? 256u : 144u); };
+  auto ASLOT = [](int a) { return NS == 2 ? 144u + 256u * (uint32_t)a : 288u + 64u * (uint32_t)a; };
   const int per = mblocks * nblocks, ntiles = batch * per;
   auto decode = [&](int t, const TmaGemmDesc *&dp, int &m0, int &n0) {
     const int z = t / per, r = t - z * per;
@@ -991,7 +992,7 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
         const int b = tc & 1;
         if (tc >= 2) mbar_wait(&acce[b], ((tc >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + ACC[b];
+        const uint32_t acc = tmem + ACC(b);
         const int nk = (dp->K + TBK - 1) / TBK;
         for (int kt = 0; kt < nk; ++kt, ++it) {
           const int q = it % QSTAGES, a = it % NS;
@@ -1000,7 +1001,7 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = sbase + q * SM::STAGE;
           const uint32_t bhi = st + SM::A_BYTES, blo = bhi + SM::B_BYTES;
-          const uint32_t ahi = tmem + ASLOT[a], alo = ahi + 32;
+          const uint32_t ahi = tmem + ASLOT(a), alo = ahi + 32;
 #pragma unroll
           for (int ks = 0; ks < TBK / 8; ++ks) {
             const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
@@ -1039,7 +1040,7 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
           split(x.z, h, l); hi[4 * c + 2] = __float_as_uint(h); lo[4 * c + 2] = __float_as_uint(l);
           split(x.w, h, l); hi[4 * c + 3] = __float_as_uint(h); lo[4 * c + 3] = __float_as_uint(l);
         }
-        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT[a];
+        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT(a);
         TST32(ta, hi);
         TST32(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1064,7 +1065,7 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC[b] + (uint32_t)c0;
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC(b) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
@@ -1239,7 +1240,8 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t ACC[2] = {0u, 256u}, ASLOT[2] = {144u, 400u};
+  auto ACC = [](int b) { return 256u * (uint32_t)b; };
+  auto ASLOT = [](int a) { return 144u + 256u * (uint32_t)a; };
   const int per = mpairs * nblocks, ntiles = batch * per;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   auto decode = [&](int t, const TmaGemmDesc *&dp, int &mp0, int &n0) {
@@ -1284,7 +1286,7 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
         const int b = tc & 1;
         if (tc >= 2) mbar_wait(&acce[b], ((tc >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + ACC[b];
+        const uint32_t acc = tmem + ACC(b);
         const int nk = (dp->K + TBK - 1) / TBK;
         for (int kt = 0; kt < nk; ++kt, ++it) {
           const int q = it % RSTAGES, a = it & 1;
@@ -1293,7 +1295,7 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = sbase + q * SM::STAGE;
           const uint32_t bhi = st + SM::A_BYTES, blo = bhi + SM::BH_BYTES;
-          const uint32_t ahi = tmem + ASLOT[a], alo = ahi + 32;
+          const uint32_t ahi = tmem + ASLOT(a), alo = ahi + 32;
 #pragma unroll
           for (int ks = 0; ks < TBK / 8; ++ks) {
             const uint64_t dbh = make_desc_sw128(bhi + 32 * ks), dbl = make_desc_sw128(blo + 32 * ks);
@@ -1332,7 +1334,7 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
           split(x.z, h, l); hi[4 * c + 2] = __float_as_uint(h); lo[4 * c + 2] = __float_as_uint(l);
           split(x.w, h, l); hi[4 * c + 3] = __float_as_uint(h); lo[4 * c + 3] = __float_as_uint(l);
         }
-        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT[a];
+        const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + ASLOT(a);
         TST32(ta, hi);
         TST32(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1358,7 +1360,7 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC[b] + (uint32_t)c0;
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC(b) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
