@@ -657,10 +657,18 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
   if (i >= row1 || j >= n1) return;
   const int2 cy = covy[i], cx = covx[j];
   const size_t qpl = (size_t)g.A * g.ldS;   // plane stride inside one subdomain's block
+  // every load is issued before the sums: p first, then the (at most 2 x 2, layout check) covering
+  // subdomains' values, so a thread has all its reads in flight at once
+  float pv[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) pv[c] = p[(size_t)c * n2 * ld + (size_t)i * ld + j];
   float acc[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) acc[c] = 0.f;
-  for (int ky = cy.x; ky < cy.x + cy.y; ++ky) {
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    if (t >= cy.y) break;
+    const int ky = cy.x + t;
     float part[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) part[c] = 0.f;
@@ -674,11 +682,20 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
         for (int c = 0; c < C; ++c) part[c] = dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j];
     } else {   // sum over kx of this layout row (same grouping as k_partial)
       const int li = i - loy[ky];
-      for (int kx = cx.x; kx < cx.x + cx.y; ++kx) {
-        const int m = kx * m2loc + (ky - k0);
-        const float *qb = q + ((size_t)m * C * g.A + li) * g.ldS + (j - lox[kx]);
+      const float *qa = q + ((size_t)(cx.x * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[cx.x]);
+      float a[C], b[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) part[c] += qb[c * qpl];
+      for (int c = 0; c < C; ++c) a[c] = __ldg(qa + c * qpl);
+      if (cx.y > 1) {
+        const int kx = cx.x + 1;
+        const float *qb = q + ((size_t)(kx * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[kx]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) b[c] = __ldg(qb + c * qpl);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        part[c] += a[c];
+        if (cx.y > 1) part[c] += b[c];
       }
     }
 #pragma unroll
@@ -688,7 +705,7 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
-    const float v = (1.f - ahat) * p[idx] + ahat * acc[c];
+    const float v = (1.f - ahat) * pv[c] + ahat * acc[c];
     finite = finite && isfinite(v);
     p[idx] = v;
   }
