@@ -256,14 +256,25 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
   for (int uc = 0; uc < nuc; ++uc) {
     const int u0 = uc * G.Uc, ucnt = min(G.Uc, jb.ulen - u0);
-    for (int i = tid; i < G.M; i += nth) {
-      float2 a = make_float2(0.f, 0.f);
-      if (i < ucnt) {
-        const float x = in[u0 + i];
-        const float2 c = chirp(u0 + i, cpre, n4, inv_n4, inv_2n);
-        a = make_float2(x * c.x, x * c.y);
+    // input row chunk times the pre-chirp: eight loads in flight per thread before any use
+    for (int i0 = tid; i0 < G.M; i0 += 8 * nth) {
+      float xv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r * nth;
+        xv[r] = i < ucnt ? __ldg(in + u0 + i) : 0.f;
       }
-      zsm[pz(i)] = a;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r * nth;
+        if (i >= G.M) break;
+        float2 a = make_float2(0.f, 0.f);
+        if (i < ucnt) {
+          const float2 c = chirp(u0 + i, cpre, n4, inv_n4, inv_2n);
+          a = make_float2(xv[r] * c.x, xv[r] * c.y);
+        }
+        zsm[pz(i)] = a;
+      }
     }
     __syncthreads();
     fft_dif(zsm, G.M, G.logM4, twd);
