@@ -2470,7 +2470,10 @@ cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1
       tiles, n2, n1, qhat, AT, ldn, rinv, phx, phy, phx_lo, phy_lo, AP, nch);
   return cudaGetLastError();
 }
-int solve_nseg(int AT) { return std::min(SSEG_MAX, std::max(1, (AT + 31) / 32)); }
+int solve_nseg(int AT) {
+  static const int ls = getenv("TVS_SOLVE_LS") ? std::max(4, atoi(getenv("TVS_SOLVE_LS"))) : 32;
+  return std::min(SSEG_MAX, std::max(1, (AT + ls - 1) / ls));
+}
 bool solve4_fits(int AT) { return (size_t)(AT + 1) * SJB * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
 cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
                            int ldn, int AT, int n1, double *segprod, cudaStream_t s) {
