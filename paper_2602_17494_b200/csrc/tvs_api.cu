@@ -562,6 +562,23 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       czt_tables(B.gi, gt, tw);
       TRY(upload(ctx, P.bufs, &B.gtab_i, gt));
       TRY(upload(ctx, P.bufs, &B.tw_i, tw));
+      {   // chirp tables: one device buffer for both job lists
+        std::vector<size_t> pf, qf, pi, qi;
+        std::vector<float2> tf = czt_chirp_tables(B.gf.N, fj, pf, qf);
+        std::vector<float2> ti = czt_chirp_tables(B.gi.N, ij, pi, qi);
+        const size_t nf = tf.size();
+        tf.insert(tf.end(), ti.begin(), ti.end());
+        float2 *dch = nullptr;
+        TRY(upload(ctx, P.bufs, &dch, tf));
+        for (size_t k = 0; k < fj.size(); ++k) {
+          fj[k].pre = dch + pf[k];
+          fj[k].post = dch + qf[k];
+        }
+        for (size_t k = 0; k < ij.size(); ++k) {
+          ij[k].pre = dch + nf + pi[k];
+          ij[k].post = dch + nf + qi[k];
+        }
+      }
       TRY(upload(ctx, P.bufs, &B.d_fj, fj));
       TRY(upload(ctx, P.bufs, &B.d_ij, ij));
     }

@@ -19,6 +19,7 @@
 
 #include <cmath>
 #include <complex>
+#include <map>
 #include <vector>
 
 namespace tvs {
@@ -29,17 +30,6 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
   return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
-// e^{i theta m}, m = v^2 + c v reduced exactly mod 4N (v^2 + c v < 2^53)
-__device__ __forceinline__ float2 chirp(int v, int c, double n4, double inv_n4, float inv_2n) {
-  const double x = (double)v * (double)v + (double)c * (double)v;
-  double r = x - floor(x * inv_n4) * n4;
-  if (r < 0.0) r += n4;
-  if (r >= n4) r -= n4;
-  float s, co;
-  sincospif((float)r * inv_2n, &s, &co);
-  return make_float2(co, s);
-}
-
 // Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
 // makes every access pattern below at most 2-way bank-conflicted.
 __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
@@ -244,10 +234,6 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   if (v0 >= jb.vlen) return;
   const int vcnt = min(G.Vp, jb.vlen - v0);
   const int tid = threadIdx.x, nth = blockDim.x;
-  const double n4 = 4.0 * G.N, inv_n4 = 1.0 / n4;
-  const float inv_2n = 1.0f / (2.0f * (float)G.N);
-  const int cpre = jb.kind == 0 ? 0 : 2 * jb.tx0 + jb.kind;   // kind 1: 2tx0+1, kind 2: 2tx0+2
-  const int cpost = jb.kind == 0 ? 2 * jb.tx0 + 1 : 0;
   for (int i = tid; i < vcnt; i += nth) acc[i] = 0.f;
   for (int i = tid; i < 256; i += nth) tfine[i] = i < G.M ? __ldg(tw + i) : make_float2(1.f, 0.f);
   for (int i = tid; i <= (G.M >> 8); i += nth) tcoarse[i] = (i << 8) < G.M ? __ldg(tw + (i << 8)) : make_float2(1.f, 0.f);
@@ -256,33 +242,42 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
   for (int uc = 0; uc < nuc; ++uc) {
     const int u0 = uc * G.Uc, ucnt = min(G.Uc, jb.ulen - u0);
-    // input row chunk times the pre-chirp: eight loads in flight per thread before any use
+    // input row chunk times the pre-chirp: the row values and chirps of eight elements are in
+    // flight per thread before any use
     for (int i0 = tid; i0 < G.M; i0 += 8 * nth) {
       float xv[8];
+      float2 cv[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int i = i0 + r * nth;
         xv[r] = i < ucnt ? __ldg(in + u0 + i) : 0.f;
+        cv[r] = i < ucnt ? __ldg(jb.pre + u0 + i) : make_float2(0.f, 0.f);
       }
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int i = i0 + r * nth;
         if (i >= G.M) break;
-        float2 a = make_float2(0.f, 0.f);
-        if (i < ucnt) {
-          const float2 c = chirp(u0 + i, cpre, n4, inv_n4, inv_2n);
-          a = make_float2(xv[r] * c.x, xv[r] * c.y);
-        }
-        zsm[pz(i)] = a;
+        zsm[pz(i)] = make_float2(xv[r] * cv[r].x, xv[r] * cv[r].y);
       }
     }
     __syncthreads();
     fft_dif(zsm, G.M, G.logM4, twd);
     czt_middle(zsm, G.M, G.logM4, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M);
     fft_dit_inv(zsm, G.M, G.logM4, twd);
-    for (int i = tid; i < vcnt; i += nth) {
-      const float2 c = cmul(chirp(v0 + i, cpost, n4, inv_n4, inv_2n), zsm[pz(i)]);
-      acc[i] += jb.kind == 2 ? c.y : c.x;
+    for (int i0 = tid; i0 < vcnt; i0 += 4 * nth) {
+      float2 pv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + r * nth;
+        pv[r] = i < vcnt ? __ldg(jb.post + v0 + i) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + r * nth;
+        if (i >= vcnt) break;
+        const float2 c = cmul(pv[r], zsm[pz(i)]);
+        acc[i] += jb.kind == 2 ? c.y : c.x;
+      }
     }
     __syncthreads();
   }
@@ -363,6 +358,40 @@ bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g) {
 
 // Kernel tables: for output pass p and input chunk c the digit-reversed FFT of the circular window
 // g[n] = h[(p Vp - c Uc) + n], n in [-(M - Vp), Vp - 1], scaled by 1/M (fp64 on the host).
+// Chirp tables of the jobs: pre-chirp offset c = 0 (forward) or 2 tx0 + kind (inverse cos / sin),
+// post-chirp offset 2 tx0 + 1 (forward) or 0 (inverse); phases m = v^2 + c v reduced exactly mod 4N
+// in integers, angles in fp64, one rounding to fp32.  Tables shared by equal (c, length).
+std::vector<float2> czt_chirp_tables(int N, std::vector<CztJob> &jobs, std::vector<size_t> &pre_off,
+                                     std::vector<size_t> &post_off) {
+  std::map<std::pair<long long, int>, size_t> at;
+  std::vector<float2> tab;
+  const long long n4 = 4LL * N;
+  auto get = [&](long long c, int len) {
+    const auto key = std::make_pair(c, len);
+    const auto it = at.find(key);
+    if (it != at.end()) return it->second;
+    const size_t off = tab.size();
+    at[key] = off;
+    for (long long v = 0; v < len; ++v) {
+      long long m = (v * v + c * v) % n4;
+      if (m < 0) m += n4;
+      const double ang = M_PI * (double)m / (2.0 * (double)N);
+      tab.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+    }
+    return off;
+  };
+  pre_off.assign(jobs.size(), 0);
+  post_off.assign(jobs.size(), 0);
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const CztJob &j = jobs[i];
+    const long long cpre = j.kind == 0 ? 0 : 2LL * j.tx0 + j.kind;
+    const long long cpost = j.kind == 0 ? 2LL * j.tx0 + 1 : 0;
+    pre_off[i] = get(cpre, j.ulen);
+    post_off[i] = get(cpost, j.vlen);
+  }
+  return tab;
+}
+
 void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw) {
   const int M = g.M;
   gtab.assign((size_t)g.nvp * g.nuc * M, make_float2(0.f, 0.f));

@@ -71,7 +71,13 @@ struct CztJob {
   float *out;
   int rows, ldin, ldout;
   int tx0, ulen, vlen, kind;
+  // chirp tables (fp64-accurate, rounded once): pre[u] = e^{i theta (u^2 + cpre u)} for
+  // u in [0, ulen), post[v] = e^{i theta (v^2 + cpost v)} for v in [0, vlen)
+  const float2 *pre = nullptr, *post = nullptr;
 };
+// host: fill the chirp tables of every job (deduplicated by (c, length)); returns the table
+std::vector<float2> czt_chirp_tables(int N, std::vector<CztJob> &jobs, std::vector<size_t> &pre_off,
+                                     std::vector<size_t> &post_off);
 struct CztGeom {
   int N;          // axis length (theta = pi / (2N))
   int M, logM4;   // FFT size (power of 4) and log4 M
