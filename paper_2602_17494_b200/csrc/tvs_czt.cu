@@ -14,7 +14,8 @@
 // and M = 2N - 2 one pass suffices (h even: the one colliding index holds the same value).
 // Cost per row O(M log M) instead of O(width * N): the dense GEMM stays faster for narrow tiles
 // (config 3), the chirp-z for full-width strips and large N (configs 4, 5).  fp32 FFT arithmetic;
-// chirp phases by exact integer reduction mod 4N (in double), kernel FFTs in fp64 on the host.
+// pre/post chirps from per-job tables built on the host (phases reduced exactly mod 4N in
+// integers, angles in fp64, one rounding), kernel FFTs in fp64 on the host.
 #include "tvs_internal.h"
 
 #include <cmath>
