@@ -159,8 +159,9 @@ tvs_status tv_stokes_denoise_host(tvs_ctx *ctx, const float *d0, int32_t n2, int
  * the library's kernels is bracketed by events; tvs_kernel_times reports, per kernel family,
  * the number of launches and the summed device milliseconds since the last reset.
  * Families: 0 sweep2 (kernel a), 1 sweep1 (kernel a'), 2 prediv, 3 proj_fwd_gemm, 4 proj_solve,
- * 5 proj_inv_gemm, 6 omega0/combine/other stencils. */
-#define TVS_NUM_KERNEL_FAMILIES 7
+ * 5 proj_inv_gemm, 6 omega0/combine/other stencils, 7 proj_fwd_czt, 8 proj_inv_czt (the chirp-z
+ * form of the two partial x-DCTs; flops are the dense-equivalent 2MNK of the contraction). */
+#define TVS_NUM_KERNEL_FAMILIES 9
 tvs_status tvs_set_profiling(tvs_ctx *ctx, int enable);
 tvs_status tvs_kernel_times(tvs_ctx *ctx, int64_t counts[TVS_NUM_KERNEL_FAMILIES],
                             double ms[TVS_NUM_KERNEL_FAMILIES],

@@ -29,7 +29,7 @@ ABI_SYMBOLS = [
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
           6: "TVS_ENCCL", 7: "TVS_ENOMEM"}
 KERNEL_FAMILIES = ["sweep2", "sweep1", "prediv", "proj_fwd_gemm", "proj_solve", "proj_inv_gemm",
-                   "other"]
+                   "other", "proj_fwd_czt", "proj_inv_czt"]
 
 
 class TvsError(RuntimeError):
@@ -93,8 +93,8 @@ def load_library(path: str = LIB_PATH):
     lib.tv_stokes_denoise_host.argtypes = lib.tv_stokes_denoise.argtypes
     lib.tvs_set_profiling.argtypes = [P, ctypes.c_int]
     lib.tvs_set_stopping.argtypes = [P, i32, ctypes.c_double]
-    arr7i = ctypes.c_int64 * 7
-    arr7d = ctypes.c_double * 7
+    arr7i = ctypes.c_int64 * len(KERNEL_FAMILIES)
+    arr7d = ctypes.c_double * len(KERNEL_FAMILIES)
     lib.tvs_kernel_times.argtypes = [P, arr7i, arr7d, arr7d, arr7d]
     lib.tvs_reset_kernel_times.argtypes = [P]
     lib.tvs_selftest_gemm.argtypes = [P, i32, i32, i32, i32, ctypes.c_uint64,
@@ -318,8 +318,9 @@ class Context:
         self._check(self.lib.tvs_reset_kernel_times(self.h), "tvs_reset_kernel_times")
 
     def kernel_times(self) -> KernelTimes:
-        c = (ctypes.c_int64 * 7)()
-        ms, by, fl = (ctypes.c_double * 7)(), (ctypes.c_double * 7)(), (ctypes.c_double * 7)()
+        n = len(KERNEL_FAMILIES)
+        c = (ctypes.c_int64 * n)()
+        ms, by, fl = (ctypes.c_double * n)(), (ctypes.c_double * n)(), (ctypes.c_double * n)()
         self._check(self.lib.tvs_kernel_times(self.h, c, ms, by, fl), "tvs_kernel_times")
         return KernelTimes(list(c), list(ms), list(by), list(fl))
 

@@ -284,7 +284,7 @@ struct tvs_ctx {
 
 namespace {
 
-enum Fam { F_SWEEP2 = 0, F_SWEEP1, F_PREDIV, F_FWD, F_SOLVE, F_INV, F_OTHER };
+enum Fam { F_SWEEP2 = 0, F_SWEEP1, F_PREDIV, F_FWD, F_SOLVE, F_INV, F_OTHER, F_CZT_FWD, F_CZT_INV };
 
 tvs_status fail(tvs_ctx *c, tvs_status st, const char *fmt, ...) {
   char buf[512];
@@ -539,14 +539,14 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.nij = (int)ij.size();
     const bool okf = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
     const bool oki = czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
-    // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~3.5 TF/s
+    // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~12 TF/s (5 M log2 M flops per FFT; config-4 forward launch: 14 TF/s)
     double t_gemm = 0, t_czt = 0;
     for (int i = 0; i < B.ntiles; ++i) {
       t_gemm += 3.0 * (2.0 * fj[i].rows * fj[i].ulen * fj[i].vlen +
                        2.0 * 2.0 * ij[2 * i].rows * ij[2 * i].ulen * ij[2 * i].vlen) / 400e12;
       const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)B.gf.M);
       const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)B.gi.M);
-      t_czt += (fj[i].rows * B.gf.nvp * B.gf.nuc * f1 + 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2) / 3.5e12;
+      t_czt += (fj[i].rows * B.gf.nvp * B.gf.nuc * f1 + 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2) / 12e12;
     }
     // accuracy: the tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193
     // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
@@ -877,7 +877,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   const bool tc = ctx->presplit();   // solve writes hi/lo planes
   const int gm = ctx->gemm;
   if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
-    TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
+    TRY(run(ctx, s, F_CZT_FWD, 0, B.fwd_flops, [&] {
       return launch_czt(B.d_fj, B.nfj, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
     }));
     if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
@@ -892,7 +892,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
                                             B.rinv, reinterpret_cast<float *>(B.z), B.phx, B.phy,
                                             nullptr, nullptr, B.AP, s);
     }));
-    return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
+    return run(ctx, s, F_CZT_INV, 0, B.inv_flops, [&] {
       return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
     });
   }
