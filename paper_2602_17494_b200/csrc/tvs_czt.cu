@@ -31,6 +31,8 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
   return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
+constexpr int CZT_THREADS = 512;   // threads per chirp-z CTA (the FFT passes assume it)
+
 // Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
 // makes every access pattern below at most 2-way bank-conflicted.
 __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
@@ -78,8 +80,11 @@ __device__ __forceinline__ float2 w16(int e) {
 // The last DIF pass (span 1, or the pair of spans 4 and 1) is left to czt_middle, which fuses it
 // with the pointwise kernel multiply and the first DIT pass: both touch the same 4 (or 16)
 // consecutive elements, so the three run in registers.
-__device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
-  const int nth = blockDim.x, tid = threadIdx.x;
+template <int logM4>
+__device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw) {
+  constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
+  const int tid = threadIdx.x;
+#pragma unroll
   for (int lg = logM4 - 1; lg >= 2; lg -= 2) {
     const int L = 1 << (2 * lg), Q = L >> 2, s1 = M >> (2 * lg + 2);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
@@ -117,9 +122,11 @@ __device__ void fft_dif(float2 *z, int M, int logM4, const Tw &tw) {
 // Last DIF pass, pointwise multiply by the transformed kernel gk (digit-reversed order, as the
 // DIF output), first DIT pass.  logM4 odd: span-1 stages on 4 consecutive elements (no twiddles);
 // even: the span-4/span-1 pairs on 16 consecutive elements (kp = 0: twiddles e^{-2 pi i c r/16}).
-__device__ void czt_middle(float2 *z, int M, int logM4, const float2 *__restrict__ gk) {
-  const int nth = blockDim.x, tid = threadIdx.x;
-  if (logM4 & 1) {
+template <int logM4>
+__device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__ gk) {
+  constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
+  const int tid = threadIdx.x;
+  if constexpr (logM4 & 1) {
     for (int b = tid; b < (M >> 2); b += nth) {
       const float4 g01 = __ldg(reinterpret_cast<const float4 *>(gk + 4 * b));
       const float4 g23 = __ldg(reinterpret_cast<const float4 *>(gk + 4 * b + 2));
@@ -181,8 +188,11 @@ __device__ void czt_middle(float2 *z, int M, int logM4, const float2 *__restrict
 // In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
 // transform times M.  Mirror image of fft_dif: after czt_middle's first pass, fused pairs of
 // spans L and 4L.
-__device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
-  const int nth = blockDim.x, tid = threadIdx.x;
+template <int logM4>
+__device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw) {
+  constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
+  const int tid = threadIdx.x;
+#pragma unroll
   for (int lg = (logM4 & 1) ? 1 : 2; lg < logM4; lg += 2) {   // first pass done by czt_middle
     const int L = 1 << (2 * lg), s2 = M >> (2 * lg + 4);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
@@ -216,7 +226,27 @@ __device__ void fft_dit_inv(float2 *z, int M, int logM4, const Tw &tw) {
   }
 }
 
-constexpr int CZT_THREADS = 512;
+
+// FFT -> kernel multiply -> inverse FFT of one chunk, with the size a compile-time constant so
+// every shared-memory offset inside a pass folds to an immediate.
+template <int logM4>
+__device__ __forceinline__ void czt_fft_pair_t(float2 *z, const Tw &tw, const float2 *__restrict__ gk) {
+  fft_dif<logM4>(z, tw);
+  czt_middle<logM4>(z, gk);
+  fft_dit_inv<logM4>(z, tw);
+}
+__device__ __forceinline__ void czt_fft_pair(float2 *z, int logM4, const Tw &tw,
+                                             const float2 *__restrict__ gk) {
+  switch (logM4) {
+    case 1: czt_fft_pair_t<1>(z, tw, gk); break;
+    case 2: czt_fft_pair_t<2>(z, tw, gk); break;
+    case 3: czt_fft_pair_t<3>(z, tw, gk); break;
+    case 4: czt_fft_pair_t<4>(z, tw, gk); break;
+    case 5: czt_fft_pair_t<5>(z, tw, gk); break;
+    case 6: czt_fft_pair_t<6>(z, tw, gk); break;
+    default: czt_fft_pair_t<7>(z, tw, gk); break;
+  }
+}
 
 // One CTA per (row, job, output pass).  kind 0: forward cos (pre u^2, post v^2 + v(2tx0+1), Re);
 // kind 1: inverse cos (pre u^2 + u(2tx0+1), post v^2, Re); kind 2: inverse sin (pre u^2 +
@@ -262,9 +292,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
       }
     }
     __syncthreads();
-    fft_dif(zsm, G.M, G.logM4, twd);
-    czt_middle(zsm, G.M, G.logM4, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M);
-    fft_dit_inv(zsm, G.M, G.logM4, twd);
+    czt_fft_pair(zsm, G.logM4, twd, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M);
     for (int i0 = tid; i0 < vcnt; i0 += 4 * nth) {
       float2 pv[4];
 #pragma unroll
@@ -354,7 +382,7 @@ bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g) {
   while ((1 << (2 * g->logM4)) < g->M) ++g->logM4;
   g->nuc = (ulen_max + g->Uc - 1) / g->Uc;
   g->nvp = (vlen_max + g->Vp - 1) / g->Vp;
-  return (1 << (2 * g->logM4)) == g->M;
+  return (1 << (2 * g->logM4)) == g->M && g->logM4 >= 1 && g->logM4 <= 7;   // k_czt instantiates M = 4 .. 16384
 }
 
 // Kernel tables: for output pass p and input chunk c the digit-reversed FFT of the circular window
