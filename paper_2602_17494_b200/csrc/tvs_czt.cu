@@ -271,6 +271,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   const Tw twd{tfine, tcoarse};
   const float *__restrict__ in = jb.in + (size_t)row * jb.ldin;
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
+  float *__restrict__ out = jb.out + (size_t)row * jb.ldout + v0;
   for (int uc = 0; uc < nuc; ++uc) {
     const int u0 = uc * G.Uc, ucnt = min(G.Uc, jb.ulen - u0);
     // input row chunk times the pre-chirp: the row values and chirps of eight elements are in
@@ -305,13 +306,15 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
         const int i = i0 + r * nth;
         if (i >= vcnt) break;
         const float2 c = cmul(pv[r], zsm[pz(i)]);
-        acc[i] += jb.kind == 2 ? c.y : c.x;
+        const float val = jb.kind == 2 ? c.y : c.x;
+        if (nuc == 1) out[i] = val;   // one input chunk: straight to global memory
+        else acc[i] += val;
       }
     }
     __syncthreads();
   }
-  float *__restrict__ out = jb.out + (size_t)row * jb.ldout + v0;
-  for (int i = tid; i < vcnt; i += nth) out[i] = acc[i];
+  if (nuc > 1)
+    for (int i = tid; i < vcnt; i += nth) out[i] = acc[i];
 }
 
 // ------------------------------------------------------------------------------------ host side
