@@ -880,8 +880,80 @@ struct QSmem {
   static constexpr int B_BYTES = BN * TBK * 4;
   static constexpr int STAGE = A_BYTES + 2 * B_BYTES;          // A raw, B hi, B lo
   static constexpr int TX = STAGE;
-  static constexpr int TOTAL = QSTAGES * STAGE + 256 + 1024;
+  static constexpr int STG = QSTAGES * STAGE + 256;            // epilogue staging: 4 KB per warp
+  static constexpr int TOTAL = STG + 4 * 4096 + 1024;
 };
+
+// Coalesced epilogue of one 32-row TMEM lane quarter: columns are read from TMEM 32 at a time,
+// transposed through a 4 KB shared-memory block (16-byte chunk j of row r at chunk j ^ (r & 7):
+// conflict-free both ways), and written as whole 128-byte row segments (8 lanes per row), so every
+// global store instruction covers four full lines instead of 32 partial ones.
+template <int BN>
+__device__ __forceinline__ void epilogue_quarter(uint32_t tacc, float *stg, float *C, int ldc, int M,
+                                                 int N, int row0, int n0, int lane) {
+  const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  const int cj = lane & 7, rq = lane >> 3;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    const int w = BN - c0 < 32 ? BN - c0 : 32;   // 32, or 16 for the last chunk of BN = 144
+    uint32_t v[32];
+    if (w == 32) {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(tacc + (uint32_t)c0));
+    } else {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(tacc + (uint32_t)c0));
+#pragma unroll
+      for (int j = 16; j < 32; ++j) v[j] = 0u;
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (!vec) {   // unaligned output rows: per-thread row stores
+      const int row = row0 + lane;
+      if (row < M) {
+        float *out = C + (size_t)row * ldc + n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < w && n0 + c0 + j < N) out[j] = __uint_as_float(v[j]);
+      }
+      continue;
+    }
+    __syncwarp();   // the previous chunk's reads of the staging block are done
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (4 * j < w)
+        reinterpret_cast<float4 *>(stg + lane * 32)[j ^ (lane & 7)] =
+            make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                        __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+    __syncwarp();
+    const int col = n0 + c0 + 4 * cj;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 4 * i + rq, row = row0 + r;
+      if (4 * cj < w && row < M && col < N) {
+        const float4 x = reinterpret_cast<const float4 *>(stg + r * 32)[cj ^ (r & 7)];
+        float *out = C + (size_t)row * ldc + col;
+        if (col + 3 < N) {
+          *reinterpret_cast<float4 *>(out) = x;
+        } else {
+          out[0] = x.x;
+          if (col + 1 < N) out[1] = x.y;
+          if (col + 2 < N) out[2] = x.z;
+        }
+      }
+    }
+  }
+}
 
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -1059,36 +1131,9 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
       const int b = tc & 1;
       mbar_wait(&accf[b], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int M = dp->M, N = dp->N, ldc = dp->ldc;
-      float *C = dp->C;
-      const int row = m0 + q4 * 32 + lane;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + ACC(b) + (uint32_t)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < M) {
-          float *out = C + (size_t)row * ldc + n0 + c0;
-          const int nvalid = N - (n0 + c0);
-          if (nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-              reinterpret_cast<float4 *>(out)[qq] =
-                  make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
-                              __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nvalid) out[j] = __uint_as_float(v[j]);
-          }
-        }
-      }
+      epilogue_quarter<BN>(tmem + ((uint32_t)(q4 * 32) << 16) + ACC(b),
+                           reinterpret_cast<float *>(smem + SM::STG) + q4 * 1024, dp->C, dp->ldc,
+                           dp->M, dp->N, m0 + q4 * 32, n0, lane);
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[b]);
