@@ -292,7 +292,10 @@ def test_config3_full_size_short_schedule(ctx):
 
 @pytest.mark.parametrize("impl", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("mnk", [(128, 128, 16), (276, 2049, 276), (275, 275, 2049), (1, 7, 3),
-                                 (130, 145, 35), (513, 513, 513)])
+                                 (130, 145, 35), (513, 513, 513),
+                                 # output pitch a multiple of 4: the staged (coalesced) epilogue,
+                                 # with ragged row / column tails
+                                 (300, 2048, 276), (257, 292, 100)])
 def test_gemm_selftest(ctx, impl, mnk):
     """Projection GEMMs (SIMT fp32 and tcgen05 3xTF32) vs an fp64 host product."""
     err = ctx.selftest_gemm(*mnk, impl, seed=7)
