@@ -33,6 +33,17 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
 }
 constexpr int CZT_THREADS = 512;   // threads per chirp-z CTA (the FFT passes assume it)
 
+// Row pointers of one chunk for the pruned first / last FFT passes.
+struct CztIo {
+  const float *in;
+  const float2 *pre;
+  int ucnt;
+  float *out;
+  const float2 *post;
+  int vcnt, kind;
+  bool pin, pout;
+};
+
 // Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
 // makes every access pattern below at most 2-way bank-conflicted.
 __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
@@ -80,12 +91,39 @@ __device__ __forceinline__ float2 w16(int e) {
 // The last DIF pass (span 1, or the pair of spans 4 and 1) is left to czt_middle, which fuses it
 // with the pointwise kernel multiply and the first DIT pass: both touch the same 4 (or 16)
 // consecutive elements, so the three run in registers.
-template <int logM4>
-__device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw) {
+// PIN (narrow input, ucnt <= M/16): the first pair (spans M/4, M/16) sees one nonzero element per
+// group, element kp = in[kp] pre[kp] (kp < M/16), so its 16 outputs are that value times W^t V^c;
+// it reads the input row straight from global memory (no staging pass) and performs exactly the
+// products of the full pass (the butterflies only add zeros), so the result is bitwise the same.
+template <int logM4, bool PIN>
+__device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__restrict__ in,
+                                        const float2 *__restrict__ pre, int ucnt) {
   constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
   const int tid = threadIdx.x;
+  if constexpr (PIN) {
+    constexpr int Q = M >> 4;   // s1 = 1 on the first pair
+    for (int kp = tid; kp < Q; kp += nth) {
+      float2 a = make_float2(0.f, 0.f);
+      if (kp < ucnt) {
+        const float x = __ldg(in + kp);
+        const float2 c = __ldg(pre + kp);
+        a = make_float2(x * c.x, x * c.y);
+      }
+      const float2 W1 = tw(kp), W2 = cmul(W1, W1), W3 = cmul(W1, W2);
+      const float2 V1 = tw(4 * kp), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+      const float2 aw[4] = {a, cmul(a, W1), cmul(a, W2), cmul(a, W3)};
 #pragma unroll
-  for (int lg = logM4 - 1; lg >= 2; lg -= 2) {
+      for (int t = 0; t < 4; ++t) {
+        z[pz(kp + (4 * t) * Q)] = aw[t];
+        z[pz(kp + (4 * t + 1) * Q)] = cmul(aw[t], V1);
+        z[pz(kp + (4 * t + 2) * Q)] = cmul(aw[t], V2);
+        z[pz(kp + (4 * t + 3) * Q)] = cmul(aw[t], V3);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int lg = PIN ? logM4 - 3 : logM4 - 1; lg >= 2; lg -= 2) {
     const int L = 1 << (2 * lg), Q = L >> 2, s1 = M >> (2 * lg + 2);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
       const int blk = gidx >> (2 * lg - 2), kp = gidx & (Q - 1);
@@ -188,12 +226,16 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
 // In-place radix-4 DIT with conjugate twiddles (digit-reversed in, natural out): the inverse
 // transform times M.  Mirror image of fft_dif: after czt_middle's first pass, fused pairs of
 // spans L and 4L.
-template <int logM4>
-__device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw) {
+// POUT (narrow output, vcnt <= M/16): the last pair (spans M/16, M/4) is evaluated only for its
+// output element 0 of each group, kp < vcnt, in the full pass's operation order, and the result
+// goes through the post-chirp straight to global memory (kind 2: imaginary part).
+template <int logM4, bool POUT>
+__device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__restrict__ out,
+                                            const float2 *__restrict__ post, int vcnt, int kind) {
   constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
   const int tid = threadIdx.x;
 #pragma unroll
-  for (int lg = (logM4 & 1) ? 1 : 2; lg < logM4; lg += 2) {   // first pass done by czt_middle
+  for (int lg = (logM4 & 1) ? 1 : 2; lg < (POUT ? logM4 - 2 : logM4); lg += 2) {   // first pass: czt_middle
     const int L = 1 << (2 * lg), s2 = M >> (2 * lg + 4);
     for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
       const int blk = gidx >> (2 * lg), kp = gidx & (L - 1);
@@ -224,27 +266,63 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw) {
     }
     __syncthreads();
   }
+  if constexpr (POUT) {
+    constexpr int L = M >> 4;   // s2 = 1 on the last pair
+    for (int kp = tid; kp < vcnt; kp += nth) {
+      float2 x[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = z[pz(kp + m * L)];
+      const float2 U1 = tw(kp), U2 = cmul(U1, U1), U3 = cmul(U1, U2);
+      const float2 V1 = tw(4 * kp), V2 = cmul(V1, V1), V3 = cmul(V1, V2);
+      float2 y[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {   // span L, k = kp: first butterfly output = plain sum
+        const float2 b1 = cmulc(x[4 * t + 1], V1), b2 = cmulc(x[4 * t + 2], V2),
+                     b3 = cmulc(x[4 * t + 3], V3);
+        const float2 a0 = make_float2(x[4 * t].x + b2.x, x[4 * t].y + b2.y);
+        const float2 a2 = make_float2(b1.x + b3.x, b1.y + b3.y);
+        y[t] = make_float2(a0.x + a2.x, a0.y + a2.y);
+      }
+      // span 4L, r = 0: twiddles U^c, first output
+      const float2 c1 = cmulc(y[1], U1), c2 = cmulc(y[2], U2), c3 = cmulc(y[3], U3);
+      const float2 a0 = make_float2(y[0].x + c2.x, y[0].y + c2.y);
+      const float2 a2 = make_float2(c1.x + c3.x, c1.y + c3.y);
+      const float2 o = cmul(__ldg(post + kp), make_float2(a0.x + a2.x, a0.y + a2.y));
+      out[kp] = kind == 2 ? o.y : o.x;
+    }
+  }
 }
 
 
 // FFT -> kernel multiply -> inverse FFT of one chunk, with the size a compile-time constant so
 // every shared-memory offset inside a pass folds to an immediate.
-template <int logM4>
-__device__ __forceinline__ void czt_fft_pair_t(float2 *z, const Tw &tw, const float2 *__restrict__ gk) {
-  fft_dif<logM4>(z, tw);
+template <int logM4, bool PIN, bool POUT>
+__device__ __forceinline__ void czt_fft_pair_t(float2 *z, const Tw &tw, const float2 *__restrict__ gk,
+                                               const CztIo &io) {
+  fft_dif<logM4, PIN>(z, tw, io.in, io.pre, io.ucnt);
   czt_middle<logM4>(z, gk);
-  fft_dit_inv<logM4>(z, tw);
+  fft_dit_inv<logM4, POUT>(z, tw, io.out, io.post, io.vcnt, io.kind);
+}
+template <int logM4>
+__device__ __forceinline__ void czt_fft_pair_p(float2 *z, const Tw &tw, const float2 *__restrict__ gk,
+                                               const CztIo &io) {
+  if constexpr (logM4 >= 3) {
+    if (io.pin && io.pout) return czt_fft_pair_t<logM4, true, true>(z, tw, gk, io);
+    if (io.pin) return czt_fft_pair_t<logM4, true, false>(z, tw, gk, io);
+    if (io.pout) return czt_fft_pair_t<logM4, false, true>(z, tw, gk, io);
+  }
+  czt_fft_pair_t<logM4, false, false>(z, tw, gk, io);
 }
 __device__ __forceinline__ void czt_fft_pair(float2 *z, int logM4, const Tw &tw,
-                                             const float2 *__restrict__ gk) {
+                                             const float2 *__restrict__ gk, const CztIo &io) {
   switch (logM4) {
-    case 1: czt_fft_pair_t<1>(z, tw, gk); break;
-    case 2: czt_fft_pair_t<2>(z, tw, gk); break;
-    case 3: czt_fft_pair_t<3>(z, tw, gk); break;
-    case 4: czt_fft_pair_t<4>(z, tw, gk); break;
-    case 5: czt_fft_pair_t<5>(z, tw, gk); break;
-    case 6: czt_fft_pair_t<6>(z, tw, gk); break;
-    default: czt_fft_pair_t<7>(z, tw, gk); break;
+    case 1: czt_fft_pair_p<1>(z, tw, gk, io); break;
+    case 2: czt_fft_pair_p<2>(z, tw, gk, io); break;
+    case 3: czt_fft_pair_p<3>(z, tw, gk, io); break;
+    case 4: czt_fft_pair_p<4>(z, tw, gk, io); break;
+    case 5: czt_fft_pair_p<5>(z, tw, gk, io); break;
+    case 6: czt_fft_pair_p<6>(z, tw, gk, io); break;
+    default: czt_fft_pair_p<7>(z, tw, gk, io); break;
   }
 }
 
@@ -272,11 +350,14 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   const float *__restrict__ in = jb.in + (size_t)row * jb.ldin;
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
   float *__restrict__ out = jb.out + (size_t)row * jb.ldout + v0;
+  // pruned first / last passes for narrow inputs / outputs (tiles of a wide layout)
+  const bool pin = G.prune && G.logM4 >= 3 && jb.ulen <= (G.M >> 4);
+  const bool pout = G.prune && G.logM4 >= 3 && nuc == 1 && vcnt <= (G.M >> 4);
   for (int uc = 0; uc < nuc; ++uc) {
     const int u0 = uc * G.Uc, ucnt = min(G.Uc, jb.ulen - u0);
     // input row chunk times the pre-chirp: the row values and chirps of eight elements are in
     // flight per thread before any use
-    for (int i0 = tid; i0 < G.M; i0 += 8 * nth) {
+    for (int i0 = tid; i0 < (pin ? 0 : G.M); i0 += 8 * nth) {
       float xv[8];
       float2 cv[8];
 #pragma unroll
@@ -293,8 +374,9 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
       }
     }
     __syncthreads();
-    czt_fft_pair(zsm, G.logM4, twd, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M);
-    for (int i0 = tid; i0 < vcnt; i0 += 4 * nth) {
+    const CztIo io{in + u0, jb.pre + u0, ucnt, out, jb.post + v0, vcnt, jb.kind, pin, pout};
+    czt_fft_pair(zsm, G.logM4, twd, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M, io);
+    for (int i0 = tid; i0 < (pout ? 0 : vcnt); i0 += 4 * nth) {
       float2 pv[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -465,7 +547,10 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
     configured = smem;
   }
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
-  k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, g, gtab, tw);
+  static const int prune = getenv("TVS_CZT_PRUNE") ? atoi(getenv("TVS_CZT_PRUNE")) : 1;
+  CztGeom gg = g;
+  gg.prune = prune;
+  k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
   return cudaGetLastError();
 }
 

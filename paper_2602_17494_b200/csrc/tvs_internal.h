@@ -83,6 +83,7 @@ struct CztGeom {
   int M, logM4;   // FFT size (power of 4) and log4 M
   int Uc, Vp;     // input chunk and output pass lengths (Uc + Vp - 1 <= M, or the M = 2N-2 case)
   int nuc, nvp;   // numbers of chunks / passes for the largest job
+  int prune = 1;  // pruned first / last FFT passes for narrow jobs (TVS_CZT_PRUNE=0: off)
 };
 bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g);
 void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw);

@@ -58,6 +58,16 @@ def test_step1_czt_small(ctx, ctx_chunked, shape, L):
     check_step1(ctx_chunked, img, 0.05, L, 3, 4)
 
 
+@pytest.mark.parametrize("shape,L", [((20, 150), (1, 16, 0, 2)), ((20, 300), (1, 24, 0, 2)),
+                                     ((24, 600), (2, 24, 2, 2))])
+def test_step1_czt_narrow_tiles(ctx, shape, L):
+    """Tiles at most M/16 wide (M = 256, 1024): the forward transform takes the pruned first FFT
+    pass (input read straight from global memory) and the inverse the pruned last pass (outputs
+    written straight through the post-chirp), as config 5's 16 x 16 layout does at full size."""
+    img = random_image(*shape, seed=shape[0] * 5 + shape[1])
+    check_step1(ctx, img, 0.05, L, 3, 4)
+
+
 def test_config2_czt(ctx):
     c = CONFIGS["c2"]
     img = c.image()
