@@ -1721,6 +1721,10 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const int LS = (nt + nseg - 1) / nseg;
   const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
   const int jj = valid ? j : 0;
+  // segment products of the two carry scans: loaded now so their latency overlaps the staging
+  const double *__restrict__ gp = segprod + (size_t)tl.chain * 2 * nseg * ldn + jj;
+  const double gpf = (valid && j > 0) ? __ldg(gp + (size_t)sg * ldn) : 1.0;
+  const double gpb = (valid && j > 0) ? __ldg(gp + (size_t)(nseg + sg) * ldn) : 1.0;
   if (maps) {   // stage both column blocks with TMA (nbox boxes of {32 columns, box_rows rows})
     const int lt = sg * SJB + tx;
     if (lt == 0) {
@@ -1781,7 +1785,6 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     __syncthreads();
   }
   const double *ri = sr4 + tx;   // pivot of row k at ri[k * SJB]
-  const double *__restrict__ gp = segprod + (size_t)tl.chain * 2 * nseg * ldn + jj;
   float *sbt = sb4 + tx;                                                     // row k at sbt[k*SJB]
   const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
 
@@ -1811,7 +1814,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     }
   }
   sh_a[sg][tx] = a;
-  sh_c[sg][tx] = (valid && j > 0) ? gp[sg * ldn] : 1.0;
+  sh_c[sg][tx] = gpf;
   __syncthreads();
   if (sg == 0) {
     double Z = 0.0;
@@ -1871,7 +1874,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   }
   __syncthreads();
   sh_a[sg][tx] = a;
-  sh_c[sg][tx] = (valid && j > 0) ? gp[(nseg + sg) * ldn] : 1.0;
+  sh_c[sg][tx] = gpb;
   __syncthreads();
   if (sg == 0) {
     double U = 0.0;
