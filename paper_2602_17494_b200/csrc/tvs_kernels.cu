@@ -1697,24 +1697,25 @@ __global__ void k_segprod(const ProjTile *__restrict__ tiles, const int *__restr
 // CTA's [nt x 32] blocks of Q-hat (fp32) and of the pivots (fp64) are staged in shared memory with
 // cp.async, so the pivots are read from L2 once instead of four times and every pass runs on
 // shared-memory data.  Outputs are plain fp32.
-__global__ void __launch_bounds__(SJB *SSEG_MAX)
+template <int J>
+__global__ void __launch_bounds__(J *SSEG_MAX)
 k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
               int AT, int ldn, const double *__restrict__ rinv, const double *__restrict__ segprod,
               float *__restrict__ phx, float *__restrict__ phy, int AP,
               const SolveMaps *__restrict__ maps, int srows, const int *__restrict__ order,
               int per_chain) {
-  __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
-  __shared__ double sh_tot[SJB];
+  __shared__ double sh_a[SSEG_MAX][J], sh_c[SSEG_MAX][J];
+  __shared__ double sh_tot[J];
   __shared__ uint64_t sbar;
-  extern __shared__ __align__(128) double sr4[];   // [srows][SJB] pivots, then [srows][SJB] floats
-  float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)srows * SJB);   // Q-hat, overwritten by z
+  extern __shared__ __align__(128) double sr4[];   // [srows][J] pivots, then [srows][J] floats
+  float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)srows * J);   // Q-hat, overwritten by z
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
   // grid (tile within its chain, frequency block, chain): the tiles sharing a pivot block (one
   // layout row) run back to back, so their pivot reads hit L2
   const int jb = blockIdx.y;
   const int tix = order[blockIdx.z * per_chain + blockIdx.x];
   if (tix < 0) return;
-  const int j = jb * SJB + tx;
+  const int j = jb * J + tx;
   const bool valid = j < n1;
   const ProjTile tl = tiles[tix];
   const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
@@ -1726,7 +1727,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const double gpf = (valid && j > 0) ? __ldg(gp + (size_t)sg * ldn) : 1.0;
   const double gpb = (valid && j > 0) ? __ldg(gp + (size_t)(nseg + sg) * ldn) : 1.0;
   if (maps) {   // stage both column blocks with TMA (nbox boxes of {32 columns, box_rows rows})
-    const int lt = sg * SJB + tx;
+    const int lt = sg * J + tx;
     if (lt == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sbar)));
       asm volatile("fence.mbarrier_init.release.cluster;");
@@ -1735,12 +1736,12 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sbar);
     if (lt == 0) {
       const int br = maps->box_rows, nb = maps->nbox;
-      const uint32_t bytes = (uint32_t)(nb * br * SJB * (sizeof(float) + sizeof(double)));
+      const uint32_t bytes = (uint32_t)(nb * br * J * (sizeof(float) + sizeof(double)));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-      const int col = jb * SJB;
+      const int col = jb * J;
       for (int bi = 0; bi < nb; ++bi) {
-        const uint32_t dq = (uint32_t)__cvta_generic_to_shared(sb4 + (size_t)bi * br * SJB);
-        const uint32_t dr = (uint32_t)__cvta_generic_to_shared(sr4 + (size_t)bi * br * SJB);
+        const uint32_t dq = (uint32_t)__cvta_generic_to_shared(sb4 + (size_t)bi * br * J);
+        const uint32_t dr = (uint32_t)__cvta_generic_to_shared(sr4 + (size_t)bi * br * J);
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dq),
             "l"(reinterpret_cast<uint64_t>(&maps->q)), "r"(col), "r"(tix * AT + bi * br), "r"(bar)
@@ -1756,13 +1757,13 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
         "@!P1 bra W_%=;\n\t}" ::"r"(bar) : "memory");
   } else {   // stage the column blocks (16-byte asynchronous copies, all rows in flight)
-    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)jb * SJB;
-    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)jb * SJB;
-    const int nthr = SJB * nseg, lt = sg * SJB + tx;
-    for (int e = lt; e < nt * (SJB / 4); e += nthr) {
-      const int k = e / (SJB / 4), c = e % (SJB / 4);
-      float *dst = sb4 + k * SJB + 4 * c;
-      if (jb * SJB + 4 * c < ldn) {
+    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)jb * J;
+    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)jb * J;
+    const int nthr = J * nseg, lt = sg * J + tx;
+    for (int e = lt; e < nt * (J / 4); e += nthr) {
+      const int k = e / (J / 4), c = e % (J / 4);
+      float *dst = sb4 + k * J + 4 * c;
+      if (jb * J + 4 * c < ldn) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
                      "l"(blk + (size_t)k * ldn + 4 * c) : "memory");
@@ -1770,10 +1771,10 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
       }
     }
-    for (int e = lt; e < nt * (SJB / 2); e += nthr) {
-      const int k = e / (SJB / 2), c = e % (SJB / 2);
-      double *dst = sr4 + k * SJB + 2 * c;
-      if (jb * SJB + 2 * c < ldn) {
+    for (int e = lt; e < nt * (J / 2); e += nthr) {
+      const int k = e / (J / 2), c = e % (J / 2);
+      double *dst = sr4 + k * J + 2 * c;
+      if (jb * J + 2 * c < ldn) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
                      "l"(rblk + (size_t)k * ldn + 2 * c) : "memory");
@@ -1784,15 +1785,15 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncthreads();
   }
-  const double *ri = sr4 + tx;   // pivot of row k at ri[k * SJB]
-  float *sbt = sb4 + tx;                                                     // row k at sbt[k*SJB]
+  const double *ri = sr4 + tx;   // pivot of row k at ri[k * J]
+  float *sbt = sb4 + tx;                                                     // row k at sbt[k*J]
   const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
 
   // ---- forward, local pass (zero carry): end value
   double a = 0.0;
   if (valid) {
     if (j == 0) {
-      for (int k = k0; k < k1; ++k) a += (double)sbt[k * SJB];
+      for (int k = k0; k < k1; ++k) a += (double)sbt[k * J];
     } else {
       int k = k0;
       if (k == 0 && k < k1) {
@@ -1804,13 +1805,13 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         double rv[SU];
 #pragma unroll
         for (int u = 0; u < SU; ++u) {
-          bv[u] = sbt[(k + u) * SJB];
-          rv[u] = ri[(k + u - 1) * SJB];
+          bv[u] = sbt[(k + u) * J];
+          rv[u] = ri[(k + u - 1) * J];
         }
 #pragma unroll
         for (int u = 0; u < SU; ++u) a = fma(-rv[u], a, (double)bv[u]);
       }
-      for (; k < k1; ++k) a = fma(-ri[(k - 1) * SJB], a, (double)sbt[k * SJB]);
+      for (; k < k1; ++k) a = fma(-ri[(k - 1) * J], a, (double)sbt[k * J]);
     }
   }
   sh_a[sg][tx] = a;
@@ -1841,18 +1842,18 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
       double rv[SU];
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
-        bv[u] = sbt[(k + u) * SJB];
-        rv[u] = ri[(k + u - 1) * SJB];
+        bv[u] = sbt[(k + u) * J];
+        rv[u] = ri[(k + u - 1) * J];
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         zc = fma(-rv[u], zc, (double)bv[u]);
-        sbt[(k + u) * SJB] = (float)zc;
+        sbt[(k + u) * J] = (float)zc;
       }
     }
     for (; k < k1; ++k) {
-      zc = fma(-ri[(k - 1) * SJB], zc, (double)sbt[k * SJB]);
-      sbt[k * SJB] = (float)zc;
+      zc = fma(-ri[(k - 1) * J], zc, (double)sbt[k * J]);
+      sbt[k * J] = (float)zc;
     }
   }
   // ---- backward, local pass (u_{k1} = 0)
@@ -1864,13 +1865,13 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
       double rv[SU];
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
-        zv[u] = sbt[(k - u) * SJB];
-        rv[u] = ri[(k - u) * SJB];
+        zv[u] = sbt[(k - u) * J];
+        rv[u] = ri[(k - u) * J];
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) a = rv[u] * ((double)zv[u] - a);
     }
-    for (; k >= k0; --k) a = ri[k * SJB] * ((double)sbt[k * SJB] - a);
+    for (; k >= k0; --k) a = ri[k * J] * ((double)sbt[k * J] - a);
   }
   __syncthreads();
   sh_a[sg][tx] = a;
@@ -1892,7 +1893,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     const double mu = sh_tot[tx] / (double)n2;
     double pre = fcarry;
     for (int k = k0; k < min(k1, nout); ++k) {
-      pre += (double)sbt[k * SJB];
+      pre += (double)sbt[k * J];
       const int y = tl.ty0 + k;
       const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
       if (k >= po) {
@@ -1908,14 +1909,14 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const int klo = max(k0, po), khi = min(k1, nout);   // output rows of this segment
   int k = k1 - 1;
   // rows above nout (T rows below S+) only carry the recurrence
-  for (; k >= khi && k >= k0; --k) un = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+  for (; k >= khi && k >= k0; --k) un = ri[k * J] * ((double)sbt[k * J] - un);
   for (; k - SU + 1 >= klo; k -= SU) {
     float zv[SU];
     double rv[SU];
 #pragma unroll
     for (int u = 0; u < SU; ++u) {
-      zv[u] = sbt[(k - u) * SJB];
-      rv[u] = ri[(k - u) * SJB];
+      zv[u] = sbt[(k - u) * J];
+      rv[u] = ri[(k - u) * J];
     }
 #pragma unroll
     for (int u = 0; u < SU; ++u) {
@@ -1927,7 +1928,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     }
   }
   for (; k >= klo; --k) {
-    const double uk = ri[k * SJB] * ((double)sbt[k * SJB] - un);
+    const double uk = ri[k * J] * ((double)sbt[k * J] - un);
     ox[(size_t)k * ldn] = (float)(cx * uk);
     oy[(size_t)k * ldn] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
     un = uk;
@@ -2477,7 +2478,12 @@ int solve_nseg(int AT) {
   static const int ls = getenv("TVS_SOLVE_LS") ? std::max(4, atoi(getenv("TVS_SOLVE_LS"))) : 32;
   return std::min(SSEG_MAX, std::max(1, (AT + ls - 1) / ls));
 }
-bool solve4_fits(int AT) { return (size_t)(AT + 1) * SJB * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
+static int solve_j() {   // column block width of solve4 (TVS_SOLVE_J=16|32)
+  static const int j = getenv("TVS_SOLVE_J") && atoi(getenv("TVS_SOLVE_J")) == 16 ? 16 : 32;
+  return j;
+}
+int solve4_width() { return solve_j(); }
+bool solve4_fits(int AT) { return (size_t)(AT + 1) * solve_j() * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
 cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
                            int ldn, int AT, int n1, double *segprod, cudaStream_t s) {
   k_segprod<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, rinv, ldn, AT,
@@ -2489,20 +2495,24 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
                                const double *segprod, float *phx, float *phy, int AP,
                                const SolveMaps *maps, int smem_rows, const int *order,
                                int nchains, int per_chain, cudaStream_t s) {
-  const int nseg = solve_nseg(AT);
+  const int nseg = solve_nseg(AT), J = solve_j();
   const int srows = maps ? smem_rows : AT;
-  const size_t smem = (size_t)srows * SJB * (sizeof(float) + sizeof(double));
+  const size_t smem = (size_t)srows * J * (sizeof(float) + sizeof(double));
   static size_t configured = 0;
-  // (the kernel also has ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
+  // (the kernel also has up to ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
   if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_proj_solve4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = J == 16 ? cudaFuncSetAttribute(k_proj_solve4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                            : cudaFuncSetAttribute(k_proj_solve4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   (void)ntiles;
-  k_proj_solve4<<<dim3(per_chain, (n1 + SJB - 1) / SJB, nchains), dim3(SJB, nseg), smem, s>>>(
-      tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
+  if (J == 16)
+    k_proj_solve4<16><<<dim3(per_chain, (n1 + 15) / 16, nchains), dim3(16, nseg), smem, s>>>(
+        tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
+  else
+    k_proj_solve4<32><<<dim3(per_chain, (n1 + 31) / 32, nchains), dim3(32, nseg), smem, s>>>(
+        tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
   return cudaGetLastError();
 }
 bool solve5_fits(int AT) {
