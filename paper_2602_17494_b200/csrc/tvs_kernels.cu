@@ -385,10 +385,12 @@ k_sweep2v(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   }
 }
 
-// ball update with a fast reciprocal (MUFU.RCP, <= 2 ulp): v <- (th v + t th psi) / (th + t|psi|)
+// ball update with fast MUFU square root and reciprocal (each within ~2 ulp; no slow-path
+// branches): v <- (th v + t th psi) / (th + t|psi|)
 __device__ __forceinline__ void ball_update_fast(float th, float t, float psx, float psy,
                                                  float &vx, float &vy) {
-  const float nrm = __fsqrt_rn(psx * psx + psy * psy);
+  float nrm;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(psx * psx + psy * psy));
   const float inv = __fdividef(th, th + t * nrm);
   const float nx = (vx + t * psx) * inv, ny = (vy + t * psy) * inv;
   vx = th > 0.f ? nx : 0.f;
