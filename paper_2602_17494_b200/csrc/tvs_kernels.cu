@@ -51,6 +51,18 @@ __device__ __forceinline__ float div_S(const float *vx, const float *vy, int li,
   return dx + dy;
 }
 
+// ball update with fast MUFU square root and reciprocal (each within ~2 ulp; no slow-path
+// branches): v <- (th v + t th psi) / (th + t|psi|)
+__device__ __forceinline__ void ball_update_fast(float th, float t, float psx, float psy,
+                                                 float &vx, float &vy) {
+  float nrm;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(psx * psx + psy * psy));
+  const float inv = __fdividef(th, th + t * nrm);
+  const float nx = (vx + t * psx) * inv, ny = (vy + t * psy) * inv;
+  vx = th > 0.f ? nx : 0.f;
+  vy = th > 0.f ? ny : 0.f;
+}
+
 // Row-wise projection of Alg. 3/5:
 // v <- (theta v + t theta psi) / (theta + t |psi|); theta = 0 -> 0 (reading A13).
 __device__ __forceinline__ void ball_update(float th, float t, float psx, float psy, float &vx,
@@ -369,8 +381,8 @@ k_sweep2v(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
     const float psyB = (li + 1 < ap) ? u_n.y - u_c.y : 0.f;
     const float ty = thy[sd.iy * g.A + li];
     float2 nv1 = c.w1, nv2 = c.w2;
-    ball_update(ty * thA, t, psxA, psyA, nv1.x, nv2.x);
-    ball_update(ty * thB, t, psxB, psyB, nv1.y, nv2.y);
+    ball_update_fast(ty * thA, t, psxA, psyA, nv1.x, nv2.x);
+    ball_update_fast(ty * thB, t, psxB, psyB, nv1.y, nv2.y);
     float *q1 = o1 + (size_t)li * g.ldS + jA, *q2 = o2 + (size_t)li * g.ldS + jA;
     if (outA && outB) {
       *reinterpret_cast<float2 *>(q1) = nv1;
@@ -385,17 +397,6 @@ k_sweep2v(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   }
 }
 
-// ball update with fast MUFU square root and reciprocal (each within ~2 ulp; no slow-path
-// branches): v <- (th v + t th psi) / (th + t|psi|)
-__device__ __forceinline__ void ball_update_fast(float th, float t, float psx, float psy,
-                                                 float &vx, float &vy) {
-  float nrm;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(psx * psx + psy * psy));
-  const float inv = __fdividef(th, th + t * nrm);
-  const float nx = (vx + t * psx) * inv, ny = (vy + t * psy) * inv;
-  vx = th > 0.f ? nx : 0.f;
-  vy = th > 0.f ? ny : 0.f;
-}
 
 // Kernel (a), 4 columns per lane (default): lane l owns columns c0-4+4l .. c0-1+4l (16-byte loads
 // and stores); lanes 1..30 produce 120 output columns, lane 0 / lane 31 are the halo columns.
