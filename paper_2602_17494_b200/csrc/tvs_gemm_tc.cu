@@ -1101,11 +1101,15 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
         mbar_wait(&full[q], (it / QSTAGES) & 1);
         if (it >= NS) mbar_wait(&aemp[a], ((it / NS) - 1) & 1);
         // row `row` of the 128-B swizzled A tile: 16-B chunk c sits at chunk c ^ (row & 7)
-        const float4 *ar = reinterpret_cast<const float4 *>(smem + q * SM::STAGE + row * 128);
+        const uint32_t ar = sbase + (uint32_t)(q * SM::STAGE + row * 128);   // shared window
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 x = ar[c ^ (row & 7)];
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(ar + 16u * (uint32_t)(c ^ (row & 7)))
+                       : "memory");
           float h, l;
           split(x.x, h, l); hi[4 * c] = __float_as_uint(h); lo[4 * c] = __float_as_uint(l);
           split(x.y, h, l); hi[4 * c + 1] = __float_as_uint(h); lo[4 * c + 1] = __float_as_uint(l);
@@ -1368,11 +1372,15 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
         const int q = it % RSTAGES, a = it & 1;
         mbar_wait(&fullA[q], (it / RSTAGES) & 1);
         if (it >= 2) mbar_wait(&aemp[a], ((it >> 1) - 1) & 1);
-        const float4 *ar = reinterpret_cast<const float4 *>(smem + q * SM::STAGE + row * 128);
+        const uint32_t ar = sbase + (uint32_t)(q * SM::STAGE + row * 128);   // shared window
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 x = ar[c ^ (row & 7)];
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(ar + 16u * (uint32_t)(c ^ (row & 7)))
+                       : "memory");
           float h, l;
           split(x.x, h, l); hi[4 * c] = __float_as_uint(h); lo[4 * c] = __float_as_uint(l);
           split(x.y, h, l); hi[4 * c + 1] = __float_as_uint(h); lo[4 * c + 1] = __float_as_uint(l);
