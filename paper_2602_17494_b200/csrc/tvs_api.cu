@@ -624,8 +624,8 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       m.nbox = (B.AT + 255) / 256;
       // even row counts: every box of the fp32 block then starts 128-byte aligned (J = 16 columns)
       m.box_rows = round_up((B.AT + m.nbox - 1) / m.nbox, 2);
-      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(), m.box_rows));
-      CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, solve4_width(), m.box_rows));
+      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
+      CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       B.smem_rows = m.nbox * m.box_rows;
       TRY(upload(ctx, P.bufs, &B.d_smaps, std::vector<SolveMaps>{m}));
     }
@@ -883,7 +883,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     }));
     if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
     TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-      if (ctx->solve_impl == 5 && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width() == 32)
+      if (ctx->solve_impl == 5 && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width(B.AT) == 32)
         return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
                                   B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
       return B.segprod ? launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
@@ -909,7 +909,7 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
   }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    if (ctx->solve_impl == 5 && !tc && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width() == 32)
+    if (ctx->solve_impl == 5 && !tc && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width(B.AT) == 32)
       return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
                                 B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
     if ((ctx->solve_impl == 3 || ctx->solve_impl == 5) && !tc && B.segprod)

@@ -191,7 +191,7 @@ cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1
 // launch_segprod ([chain][2][solve_nseg(AT)][ldn] doubles), outputs plain fp32
 int solve_nseg(int AT);
 bool solve4_fits(int AT);
-int solve4_width();   // column block width of k_proj_solve4 (16 or 32)
+int solve4_width(int AT);   // column block width of k_proj_solve4 (16 or 32)
 cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
                            int ldn, int AT, int n1, double *segprod, cudaStream_t s);
 cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1,

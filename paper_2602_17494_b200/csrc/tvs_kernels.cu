@@ -2481,12 +2481,15 @@ int solve_nseg(int AT) {
   static const int ls = getenv("TVS_SOLVE_LS") ? std::max(4, atoi(getenv("TVS_SOLVE_LS"))) : 32;
   return std::min(SSEG_MAX, std::max(1, (AT + ls - 1) / ls));
 }
-static int solve_j() {   // column block width of solve4 (TVS_SOLVE_J=16|32)
-  static const int j = getenv("TVS_SOLVE_J") && atoi(getenv("TVS_SOLVE_J")) == 16 ? 16 : 32;
-  return j;
+// column block width of solve4: 16 for tiles up to 512 rows (four CTAs per SM instead of two:
+// config 3 -3 %), else 32; TVS_SOLVE_J=16|32 forces one
+static int solve_j(int AT) {
+  static const int forced = getenv("TVS_SOLVE_J") ? atoi(getenv("TVS_SOLVE_J")) : 0;
+  if (forced == 16 || forced == 32) return forced;
+  return AT <= 512 ? 16 : 32;
 }
-int solve4_width() { return solve_j(); }
-bool solve4_fits(int AT) { return (size_t)(AT + 1) * solve_j() * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
+int solve4_width(int AT) { return solve_j(AT); }
+bool solve4_fits(int AT) { return (size_t)(AT + 1) * solve_j(AT) * (sizeof(float) + sizeof(double)) <= 200 * 1024; }
 cudaError_t launch_segprod(const ProjTile *tiles, const int *first, int nchains, const double *rinv,
                            int ldn, int AT, int n1, double *segprod, cudaStream_t s) {
   k_segprod<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, rinv, ldn, AT,
@@ -2498,16 +2501,17 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
                                const double *segprod, float *phx, float *phy, int AP,
                                const SolveMaps *maps, int smem_rows, const int *order,
                                int nchains, int per_chain, cudaStream_t s) {
-  const int nseg = solve_nseg(AT), J = solve_j();
+  const int nseg = solve_nseg(AT), J = solve_j(AT);
   const int srows = maps ? smem_rows : AT;
   const size_t smem = (size_t)srows * J * (sizeof(float) + sizeof(double));
-  static size_t configured = 0;
+  static size_t configured[2] = {0, 0};   // per instantiation
+  size_t &cfg = configured[J == 16 ? 0 : 1];
   // (the kernel also has up to ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
-  if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
+  if (smem + 9 * 1024 > 48 * 1024 && smem > cfg) {
     cudaError_t e = J == 16 ? cudaFuncSetAttribute(k_proj_solve4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                             : cudaFuncSetAttribute(k_proj_solve4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    cfg = smem;
   }
   (void)ntiles;
   if (J == 16)
