@@ -280,6 +280,11 @@ struct tvs_ctx {
   // scratch for denoise / host variants
   std::unique_ptr<DevBuf> tau_scratch, h_d0, h_d, h_tau;
   ncclComm_t nccl = nullptr;   // world > 1 only
+  // side stream: step 1 runs the global residual projection of a sweep on it, concurrently with
+  // the omega0 local projection chain (independent until omega0 reads both; TVS_OVERLAP=0: off)
+  bool overlap = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -1118,15 +1123,15 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   CK(cudaMemsetAsync(P->v[0], 0, (size_t)g.M * 4 * g.A * g.ldS * sizeof(float), s));
   // r = f - P multidiv p = f - w + grad phi, phi = Delta^dagger div w (global, once per sweep)
   // rows: w on [E0, V1) (needs p on [V0, V1)); q on the core rows; r on [E0, V1)
-  auto residual = [&](float *out, float scale) -> tvs_status {
-    TRY(run(ctx, s, F_OTHER, 0, 0,
-            [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, D.E0, D.V1, s); }));
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, s);
+  auto residual = [&](float *out, float scale, cudaStream_t rs) -> tvs_status {
+    TRY(run(ctx, rs, F_OTHER, 0, 0,
+            [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, D.E0, D.V1, rs); }));
+    TRY(run(ctx, rs, F_OTHER, 0, 0, [&] {
+      return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, rs);
     }));
-    TRY(project_batch(ctx, *P, P->global, s, gather));
-    return run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, D.E0, D.V1, s);
+    TRY(project_batch(ctx, *P, P->global, rs, gather));
+    return run(ctx, rs, F_OTHER, 0, 0, [&] {
+      return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, D.E0, D.V1, rs);
     });
   };
   int cur = 0;
@@ -1142,8 +1147,23 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   const bool stopping = ctx->stop_crit != 0;
   double e_prev = 0.0;
   int sweeps_run = it.sweeps;
+  // overlap the global residual with the omega0 chain: one GPU, no stopping test (which needs r^n
+  // first); the chains write disjoint buffers and join before omega0 reads r^n and grad phi
+  const bool overlap = ctx->overlap && D.world == 1 && !stopping;
+  if (overlap && !ctx->side) {
+    CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
   for (int n = 0; n < it.sweeps; ++n) {
-    TRY(residual(P->r, 1.f));
+    if (overlap) {
+      CK(cudaEventRecord(ctx->ev_fork, s));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      TRY(residual(P->r, 1.f, ctx->side));
+      CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    } else {
+      TRY(residual(P->r, 1.f, s));
+    }
     if (stopping) {   // r^n is D(p^n)'s residual: test the previous sweep before starting this one
       double e = 0.0;
       TRY(energy1(&e, true));
@@ -1159,6 +1179,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
             [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, tc ? P->qlo : nullptr, s); }));
     TRY(project_batch(ctx, *P, P->local, s));
+    if (overlap) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
       return launch_omega0_1(P->d_subs, g, P->r, ld, P->vtmp, P->gphi, g.ldP, G2, G1, P->om, s);
     }));
@@ -1175,7 +1196,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     TRY(combine_step(ctx, *P, P->v[cur], s));
   }
   // tau = P tau_0 - delta P multidiv p = delta r^S; every rank ends with the full field
-  TRY(residual(P->r, delta));
+  TRY(residual(P->r, delta, s));
   double e_final = 0.0;
   TRY(energy1(&e_final, false));   // ||delta r^S||^2, read after the final synchronisation
   TRY(allgather_rows(ctx, D, P->r, 2, pl, ld, s));
@@ -1225,6 +1246,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
                                         : tvs_ctx::G_TS;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
   if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
+  if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
@@ -1262,6 +1284,9 @@ tvs_status tvs_destroy(tvs_ctx *ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->nccl) ncclCommDestroy(ctx->nccl);
   delete ctx;
   return TVS_OK;
