@@ -216,7 +216,7 @@ struct Plan {
   float *v[2] = {nullptr, nullptr};
   float *om = nullptr, *p = nullptr, *f = nullptr;
   float *dxi = nullptr;   // IRV1: div xi (allocated on first use)
-  double *g0 = nullptr;
+  double *g0 = nullptr, *gsum = nullptr;
   int *d_bad = nullptr;
   double *d_part = nullptr, *d_energy = nullptr;   // dual-energy reduction scratch
   // step 1 only
@@ -759,6 +759,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->f, (size_t)G2 * P->ld));
     TRY(dalloc(ctx, P->bufs, &P->g0, (size_t)G1));
+    TRY(dalloc(ctx, P->bufs, &P->gsum, (size_t)((G2 + 63) / 64) * G1));   // k_irv2_f chunk sums
   } else {
     // the dense DCT tables (10 planes of N x N floats) only when a batch may take the GEMM form:
     // long axes always run the chirp-z form
@@ -1010,7 +1011,7 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
   } else {              // IRV2: f = alpha (d0 - g)
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_g_row0(tau2, ldt, n1, P->g0, s); }));
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, s);
+      return launch_irv2_f(tau1, ldt, P->g0, d0, n2, n1, alpha, P->f, ld, P->gsum, s);
     }));
     // zero-mean g (reading A3): only the constant of f moves, so the dual energy D_IRV2 matches
     // the oracle's convention (the iteration itself depends on grad f only)

@@ -104,7 +104,8 @@ struct Geo {
 cudaError_t launch_tau0(const float *d0, int n2, int n1, float *tau, int ldt, cudaStream_t s);
 cudaError_t launch_g_row0(const float *tau2, int ldt, int n1, double *g_row0, cudaStream_t s);
 cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, const float *d0,
-                          int n2, int n1, float alpha, float *f, int ldf, cudaStream_t s);
+                          int n2, int n1, float alpha, float *f, int ldf, double *csum,
+                          cudaStream_t s);
 
 cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                             const float *f, const float *p1, const float *p2, int ld, int n2,

@@ -139,6 +139,34 @@ __global__ void k_irv2_f(const float *__restrict__ tau1, int ldt, const double *
   }
 }
 
+// Column-parallel form of k_irv2_f: the column integration runs in chunks of IRV2_ROWS rows (one
+// thread per (chunk, column)); chunk sums of tau_1 first, then each chunk starts from g0 minus the
+// sums of the chunks above (fp64 throughout; the same integral in a chunked summation order).
+constexpr int IRV2_ROWS = 64;
+__global__ void k_irv2_chunk_sums(const float *__restrict__ tau1, int ldt, int n2, int n1,
+                                  double *__restrict__ csum) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (j >= n1) return;
+  const int i0 = max(1, c * IRV2_ROWS), i1 = min(n2, (c + 1) * IRV2_ROWS);
+  double acc = 0.0;
+  for (int i = i0; i < i1; ++i) acc += (double)tau1[(size_t)i * ldt + j];
+  csum[(size_t)c * n1 + j] = acc;
+}
+__global__ void k_irv2_f_chunked(const float *__restrict__ tau1, int ldt,
+                                 const double *__restrict__ g0, const float *__restrict__ d0, int n2,
+                                 int n1, float alpha, float *__restrict__ f, int ldf,
+                                 const double *__restrict__ csum) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (j >= n1) return;
+  double acc = g0[j];
+  for (int k = 0; k < c; ++k) acc -= csum[(size_t)k * n1 + j];
+  const int i0 = c * IRV2_ROWS, i1 = min(n2, (c + 1) * IRV2_ROWS);
+  for (int i = i0; i < i1; ++i) {
+    if (i >= 1) acc -= (double)tau1[(size_t)i * ldt + j];
+    f[(size_t)i * ldf + j] = (float)((double)alpha * ((double)d0[(size_t)i * n1 + j] - acc));
+  }
+}
+
 // IRV1 data (Eq. ir1dualdis): f = alpha d0 - div xi, xi = tau_perp / sqrt(|tau_perp|^2 + eps)
 // with tau_perp = R_Omega(tau_2, -tau_1) (Eq. defXi2:discrete); div with the three-case
 // D- (P:560-571).  Also stores div xi for the recovery d = d0 - (div p + div xi)/alpha.
@@ -2273,8 +2301,16 @@ cudaError_t launch_g_row0(const float *tau2, int ldt, int n1, double *g_row0, cu
   return cudaGetLastError();
 }
 cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, const float *d0,
-                          int n2, int n1, float alpha, float *f, int ldf, cudaStream_t s) {
-  k_irv2_f<<<(n1 + 127) / 128, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf);
+                          int n2, int n1, float alpha, float *f, int ldf, double *csum,
+                          cudaStream_t s) {
+  if (!csum) {   // one thread per column, sequential down the column
+    k_irv2_f<<<(n1 + 127) / 128, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf);
+    return cudaGetLastError();
+  }
+  const int nch = (n2 + IRV2_ROWS - 1) / IRV2_ROWS;
+  const dim3 grid((n1 + 127) / 128, nch);
+  k_irv2_chunk_sums<<<grid, 128, 0, s>>>(tau1, ldt, n2, n1, csum);
+  k_irv2_f_chunked<<<grid, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf, csum);
   return cudaGetLastError();
 }
 cudaError_t launch_irv1_f(const float *tau1, const float *tau2, int ldt, const float *d0, int n2,
