@@ -1150,7 +1150,8 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   int sweeps_run = it.sweeps;
   // overlap the global residual with the omega0 chain: one GPU, no stopping test (which needs r^n
   // first); the chains write disjoint buffers and join before omega0 reads r^n and grad phi
-  const bool overlap = ctx->overlap && D.world == 1 && !stopping;
+  // (not while profiling: concurrent kernels would stretch each other's per-launch event times)
+  const bool overlap = ctx->overlap && D.world == 1 && !stopping && !ctx->profiling;
   if (overlap && !ctx->side) {
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
