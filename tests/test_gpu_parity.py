@@ -328,3 +328,29 @@ def test_sweep2_two_updates_per_pass_bitwise(ctx):
             assert torch.equal(d0, d1) and torch.equal(p0, p1), shape
     finally:
         single.close()
+
+
+def test_step1_side_stream_overlap_bitwise(ctx):
+    """The global residual projection of each step-1 sweep runs on a side stream, concurrently with
+    the omega0 local-projection chain (default on one GPU): tau and p are bitwise identical to the
+    serial schedule (TVS_OVERLAP=0), so the two chains share no buffer."""
+    import os
+    import paper_2602_17494_b200 as pkg
+    old = os.environ.get("TVS_OVERLAP")
+    os.environ["TVS_OVERLAP"] = "0"
+    try:
+        serial = pkg.Context(0)
+    finally:
+        if old is None:
+            del os.environ["TVS_OVERLAP"]
+        else:
+            os.environ["TVS_OVERLAP"] = old
+    try:
+        for shape, L in (((37, 53), (3, 2, 3, 5)), ((130, 260), (2, 4, 8, 8))):
+            img = random_image(*shape, seed=shape[0] * 3 + shape[1])
+            t1, p1, _ = ctx.tv_stokes_step1(_dev(img), 0.05, L, (4, 3, 0.125), want_p=True)
+            t0, p0, _ = serial.tv_stokes_step1(_dev(img), 0.05, L, (4, 3, 0.125), want_p=True)
+            torch.cuda.synchronize()
+            assert torch.equal(t0, t1) and torch.equal(p0, p1), shape
+    finally:
+        serial.close()
