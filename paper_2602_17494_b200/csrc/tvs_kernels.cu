@@ -1752,10 +1752,11 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   extern __shared__ __align__(128) double sr4[];   // [srows][J] pivots, then [srows][J] floats
   float *sb4 = reinterpret_cast<float *>(sr4 + (size_t)srows * J);   // Q-hat, overwritten by z
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
-  // grid (tile within its chain, frequency block, chain): the tiles sharing a pivot block (one
-  // layout row) run back to back, so their pivot reads hit L2
-  const int jb = blockIdx.y;
-  const int tix = order[blockIdx.z * per_chain + blockIdx.x];
+  // grid (frequency block, tile within its chain, chain): adjacent CTAs stage adjacent 128-byte
+  // row segments (DRAM locality: -4 % against tile-fastest), and the tiles sharing a pivot block
+  // (one layout row) still run within one wave, so their pivot reads hit L2
+  const int jb = blockIdx.x;
+  const int tix = order[blockIdx.z * per_chain + blockIdx.y];
   if (tix < 0) return;
   const int j = jb * J + tx;
   const bool valid = j < n1;
@@ -2562,10 +2563,10 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   }
   (void)ntiles;
   if (J == 16)
-    k_proj_solve4<16><<<dim3(per_chain, (n1 + 15) / 16, nchains), dim3(16, nseg), smem, s>>>(
+    k_proj_solve4<16><<<dim3((n1 + 15) / 16, per_chain, nchains), dim3(16, nseg), smem, s>>>(
         tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
   else
-    k_proj_solve4<32><<<dim3(per_chain, (n1 + 31) / 32, nchains), dim3(32, nseg), smem, s>>>(
+    k_proj_solve4<32><<<dim3((n1 + 31) / 32, per_chain, nchains), dim3(32, nseg), smem, s>>>(
         tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
   return cudaGetLastError();
 }
