@@ -1493,6 +1493,19 @@ tvs_status tvs_selftest_gemm(tvs_ctx *ctx, int32_t M, int32_t N, int32_t K, int3
     GemmDesc2 g2 = {dA, nullptr, dBh, dBl, dC, M, N, K, lda, lda, ldcC};
     std::vector<TmaGemmDesc> d3(1);
     CK(make_tma_desc(&d3[0], g2, impl == 7 ? 72 : 144));
+    if (impl == 6 && getenv("TVS_SELFTEST_BLOCKA")) {   // A re-laid out column-block-major
+      const int nkt = (K + 31) / 32;
+      std::vector<float> Ab((size_t)nkt * M * 32, 0.f);
+      for (int i = 0; i < M; ++i)
+        for (int k = 0; k < K; ++k) Ab[((size_t)(k / 32) * M + i) * 32 + (k % 32)] = A[(size_t)i * lda + k];
+      float *dAb;
+      TRY(upload(ctx, own, &dAb, Ab));
+      GemmDesc2 gb = {dAb, nullptr, dBh, dBl, dC, nkt * M, N, 32, 32, lda, ldcC};
+      TmaGemmDesc tb;
+      CK(make_tma_desc(&tb, gb, 144));
+      d3[0].a_hi = tb.a_hi;
+      d3[0].a_blk_rows = M;
+    }
     TmaGemmDesc *dd3;
     TRY(upload(ctx, own, &dd3, d3));
     auto go = [&]() {

@@ -1047,7 +1047,10 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
           if (it >= QSTAGES) mbar_wait(&empty[q], ((it / QSTAGES) - 1) & 1);
           mbar_expect_tx(&full[q], SM::TX);
           const uint32_t st = sbase + q * SM::STAGE;
-          tma_load_2d(st, &dp->a_hi, kt * TBK, m0, &full[q]);
+          if (dp->a_blk_rows > 0)
+            tma_load_2d(st, &dp->a_hi, 0, kt * dp->a_blk_rows + m0, &full[q]);
+          else
+            tma_load_2d(st, &dp->a_hi, kt * TBK, m0, &full[q]);
           tma_load_2d(st + SM::A_BYTES, &dp->b_hi, kt * TBK, n0, &full[q]);
           tma_load_2d(st + SM::A_BYTES + SM::B_BYTES, &dp->b_lo, kt * TBK, n0, &full[q]);
         }

@@ -51,6 +51,9 @@ struct alignas(64) TmaGemmDesc {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
   float *C;
   int M, N, K, ldc;
+  // > 0: A is stored column-block-major, [K/32][a_blk_rows][32] (k-step kt of rows m0.. is the
+  // contiguous box at row kt * a_blk_rows + m0 of a 32-wide map); 0: row-major [M][lda]
+  int a_blk_rows = 0;
 };
 // Tensor maps of the y-solve's staged column blocks (Q-hat fp32 and pivots fp64), boxes of
 // {32 columns, box_rows rows}, nbox boxes per CTA.
