@@ -196,6 +196,7 @@ struct ProjBatch {
   int nfj = 0, nij = 0, fj_rows = 0, ij_rows = 0;
   float2 *gtab_f = nullptr, *gtab_i = nullptr, *tw_f = nullptr, *tw_i = nullptr;
   int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
+  bool qblk = false;   // Q-hat column-block-major (see build_proj)
   double fwd_flops = 0, inv_flops = 0, solve_bytes = 0;
 };
 
@@ -283,6 +284,8 @@ struct tvs_ctx {
   // side stream: step 1 runs the global residual projection of a sweep on it, concurrently with
   // the omega0 local projection chain (independent until omega0 reads both; TVS_OVERLAP=0: off)
   bool overlap = true;
+  bool qblk = false;  // column-block-major Q-hat for the staged y-solve (TVS_QBLK=1: on; measured
+                      // net negative at config 3: solve -1.6 %, forward GEMM epilogue +8 %)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -431,7 +434,8 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   B.ldG = ldG;
   TRY(upload(ctx, P.bufs, &B.d_tiles, B.tiles));
   TRY(upload(ctx, P.bufs, &B.d_first, first));
-  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * B.ldn));
+  // (room for the column-block-major layout too: blocks of up to 32 columns)
+  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * round_up(n1t, 32)));
   // z scratch: fp64 for the serial solve, fp32 for the segmented solve when its column block does
   // not fit in shared memory, none otherwise
   const size_t nz = (size_t)B.ntiles * B.AT * B.ldn;
@@ -605,6 +609,26 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   for (auto &d : inv2) d.Alo = nullptr;
   for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
   for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
+  // column-block-major Q-hat between the forward GEMM and the staged y-solve (local batch, ts GEMM,
+  // TMA-staged solve4): each solve CTA then stages one contiguous block (TVS_QBLK=1; off by default)
+  B.qblk = T && !B.czt && fr0 < 0 && ctx->qblk && ctx->gemm == tvs_ctx::G_TS &&
+           ctx->solve_impl == 3 && ctx->solve_tma && solve4_fits(B.AT);
+  if (B.qblk) {
+    const int J = solve4_width(B.AT);
+    const long long plane = (long long)B.ntiles * B.AT * J;
+    size_t st = 0;
+    for (int i = 0; i < B.ntiles;) {   // same stacking as fwd2 above
+      int j = i + 1;
+      while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
+             B.tiles[j].px1 == B.tiles[i].px1)
+        ++j;
+      fwd3[st].C = B.qhat + (size_t)i * B.AT * J;
+      fwd3[st].c_blk = J;
+      fwd3[st].c_plane = plane;
+      ++st;
+      i = j;
+    }
+  }
   TRY(upload(ctx, P.bufs, &B.d_fwd4, fwd3));
   TRY(upload(ctx, P.bufs, &B.d_inv4, inv3));
   for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 72));
@@ -629,7 +653,13 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       m.nbox = (B.AT + 255) / 256;
       // even row counts: every box of the fp32 block then starts 128-byte aligned (J = 16 columns)
       m.box_rows = round_up((B.AT + m.nbox - 1) / m.nbox, 2);
-      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
+      if (B.qblk) {   // [block][ntiles * AT rows][J]
+        const int J = solve4_width(B.AT), nj = (n1t + J - 1) / J;
+        m.q_blk_rows = B.ntiles * B.AT;
+        CK(encode_plain_2d(&m.q, B.qhat, false, J, nj * B.ntiles * B.AT, J, J, m.box_rows));
+      } else {
+        CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
+      }
       CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       B.smem_rows = m.nbox * m.box_rows;
       TRY(upload(ctx, P.bufs, &B.d_smaps, std::vector<SolveMaps>{m}));
@@ -1249,6 +1279,7 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
   if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
+  if (const char *qb = getenv("TVS_QBLK")) c->qblk = atoi(qb) != 0;
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;

@@ -890,8 +890,10 @@ struct QSmem {
 // global store instruction covers four full lines instead of 32 partial ones.
 template <int BN>
 __device__ __forceinline__ void epilogue_quarter(uint32_t tacc, float *stg, float *C, int ldc, int M,
-                                                 int N, int row0, int n0, int lane) {
-  const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+                                                 int N, int row0, int n0, int lane, int c_blk = 0,
+                                                 long long c_plane = 0) {
+  // column-block-major C (c_blk = 16 or 32): a 4-column group never straddles a block
+  const bool vec = (c_blk > 0 || (ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   const int cj = lane & 7, rq = lane >> 3;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -942,7 +944,8 @@ __device__ __forceinline__ void epilogue_quarter(uint32_t tacc, float *stg, floa
       const int r = 4 * i + rq, row = row0 + r;
       if (4 * cj < w && row < M && col < N) {
         const float4 x = reinterpret_cast<const float4 *>(stg + r * 32)[cj ^ (r & 7)];
-        float *out = C + (size_t)row * ldc + col;
+        float *out = c_blk > 0 ? C + (size_t)(col / c_blk) * c_plane + (size_t)row * c_blk + col % c_blk
+                               : C + (size_t)row * ldc + col;
         if (col + 3 < N) {
           *reinterpret_cast<float4 *>(out) = x;
         } else {
@@ -1140,7 +1143,7 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
       asm volatile("tcgen05.fence::after_thread_sync;");
       epilogue_quarter<BN>(tmem + ((uint32_t)(q4 * 32) << 16) + ACC(b),
                            reinterpret_cast<float *>(smem + SM::STG) + q4 * 1024, dp->C, dp->ldc,
-                           dp->M, dp->N, m0 + q4 * 32, n0, lane);
+                           dp->M, dp->N, m0 + q4 * 32, n0, lane, dp->c_blk, dp->c_plane);
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[b]);

@@ -54,12 +54,18 @@ struct alignas(64) TmaGemmDesc {
   // > 0: A is stored column-block-major, [K/32][a_blk_rows][32] (k-step kt of rows m0.. is the
   // contiguous box at row kt * a_blk_rows + m0 of a 32-wide map); 0: row-major [M][lda]
   int a_blk_rows = 0;
+  // > 0: C is stored column-block-major, element (row, col) at
+  // C + (col / c_blk) * c_plane + row * c_blk + col % c_blk (ldc unused); 0: row-major, pitch ldc
+  int c_blk = 0;
+  long long c_plane = 0;
 };
 // Tensor maps of the y-solve's staged column blocks (Q-hat fp32 and pivots fp64), boxes of
 // {32 columns, box_rows rows}, nbox boxes per CTA.
 struct alignas(64) SolveMaps {
   CUtensorMap q, r;
   int box_rows, nbox;
+  // > 0: Q-hat is column-block-major ([J-column block][q_blk_rows rows][J]); the map is J wide
+  int q_blk_rows = 0;
 };
 cudaError_t encode_plain_2d(CUtensorMap *map, const void *base, bool fp64, int cols, int rows,
                             int ld_elems, int box_cols, int box_rows);

@@ -1782,12 +1782,15 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
       const uint32_t bytes = (uint32_t)(nb * br * J * (sizeof(float) + sizeof(double)));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       const int col = jb * J;
+      // Q-hat: row-major (column jb J, row tix AT) or column-block-major (block jb, same rows)
+      const int qcol = maps->q_blk_rows > 0 ? 0 : col;
+      const int qrow0 = (maps->q_blk_rows > 0 ? jb * maps->q_blk_rows : 0) + tix * AT;
       for (int bi = 0; bi < nb; ++bi) {
         const uint32_t dq = (uint32_t)__cvta_generic_to_shared(sb4 + (size_t)bi * br * J);
         const uint32_t dr = (uint32_t)__cvta_generic_to_shared(sr4 + (size_t)bi * br * J);
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dq),
-            "l"(reinterpret_cast<uint64_t>(&maps->q)), "r"(col), "r"(tix * AT + bi * br), "r"(bar)
+            "l"(reinterpret_cast<uint64_t>(&maps->q)), "r"(qcol), "r"(qrow0 + bi * br), "r"(bar)
             : "memory");
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dr),
