@@ -77,14 +77,26 @@ typedef struct {
   double dual_energy;       /* D(p) of the returned dual (Eq. opt_dual_discrete),
                                fp64 reduction over the whole grid (all ranks)                   */
   int64_t sweeps_run;       /* outer sweeps performed (< sweeps when a stopping rule fired)     */
+  double primal_energy;     /* primal energy of the returned solution, fp64 reduction over the
+                               whole grid (all ranks): step 1 E_1 = TV(tau) + ||tau - P tau_0||^2
+                               / (2 delta) (Cor. tfsdual; channel-wise TV, reading
+                               A15); step 2 E_2 = TV(d - g) + alpha/2 ||d - d_0||^2 (Eq.
+                               modifiedStep2), IRV1 E = TV(d) + <d, div xi> + alpha/2
+                               ||d - d_0||^2 (Eq. IRPXi)                            */
+  double gap;               /* duality gap sum_k sum_px (|grad u_k| + p_k . grad u_k) >= 0 with
+                               u = tau (step 1), d - g (IRV2) or d (IRV1): equals E(u(p)) - G(p),
+                               G the dual objective; 0 iff p is optimal      */
 } tvs_stats;
 
 typedef struct tvs_ctx tvs_ctx;   /* opaque: device, plans, scratch, profiling, communicator */
 
-/* Create a context on CUDA device `device`.  Single process / single GPU: rank = 0, world = 1,
- * nccl_id = NULL.  Multi-GPU (one process per GPU): every rank passes the same 128-byte
- * ncclUniqueId obtained from tvs_nccl_unique_id on rank 0. */
-tvs_status tvs_create(tvs_ctx **ctx, int device, int rank, int world, const uint8_t *nccl_id);
+/* Create a context on CUDA device `device` (argument order of SURVEY 8(b)).  Single process /
+ * single GPU: rank = 0, world = 1, nccl_id = NULL.  Multi-GPU (one process per GPU): every rank
+ * passes the same 128-byte ncclUniqueId obtained from tvs_nccl_unique_id on rank 0; the context
+ * owns its NCCL communicator (band send/recv per sweep, all-gathers, all-reduces).
+ * Errors: TVS_EINVAL (ctx NULL, rank/world out of range, world > 1 without an id), TVS_ECUDA
+ * (bad device), TVS_ENCCL (communicator init).  *ctx is NULL on failure. */
+tvs_status tvs_create(tvs_ctx **ctx, int rank, int world, const uint8_t *nccl_id, int device);
 tvs_status tvs_destroy(tvs_ctx *ctx);
 const char *tvs_last_error(const tvs_ctx *ctx);
 tvs_status tvs_nccl_unique_id(uint8_t id_out[128]);

@@ -424,6 +424,23 @@ def primal_energy_irv1(d, d0, dxi, alpha):
     return tv(d) + ops.inner(d, dxi) + 0.5 * alpha * ops.inner(dd, dd)
 
 
+def dual_value_tfs(p, ptau0, delta):
+    """Dual objective of Cor. tfsdual in the projected-data form: with
+    D_TFS(p) = ||P multidiv p - delta^{-1} P tau_0||^2 (Eq. tfsdualdis),
+    G_1(p) = ||P tau_0||^2 / (2 delta) - (delta / 2) D_TFS(p) <= min E_1 (weak duality); at the
+    recovered tau = P tau_0 - delta P multidiv p, E_1(tau) - G_1(p) equals the C-15 gap."""
+    f = np.asarray(ptau0, np.float64) / delta
+    return ops.inner(ptau0, ptau0) / (2.0 * delta) - 0.5 * delta * dual_energy_tfs(p, f)
+
+
+def dual_value_irv2(p, d0, g, alpha):
+    """Dual objective of the ROF problem of Eq. modifiedStep2 (dual P:504-510): with
+    D_IRV2(p) = ||div p - alpha (d_0 - g)||^2 (Eq. ir2dualdis),
+    G_2(p) = alpha/2 ||d_0 - g||^2 - D_IRV2(p) / (2 alpha) <= min E_2 (weak duality)."""
+    h = np.asarray(d0, np.float64) - g
+    return 0.5 * alpha * ops.inner(h, h) - dual_energy_irv2(p, alpha * h) / (2.0 * alpha)
+
+
 def dual_value_irv1(p, d0, f, alpha):
     """The dual function whose maximiser Cor. irdual characterises:
     G(p) = alpha/2 ||d_0||^2 - ||div p - f||^2 / (2 alpha) <= min E (weak duality)."""

@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("seconds", ctypes.c_double), ("pixel_updates", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("flops_proj", ctypes.c_double),
                 ("bytes_sweep", ctypes.c_double), ("dual_energy", ctypes.c_double),
-                ("sweeps_run", ctypes.c_int64)]
+                ("sweeps_run", ctypes.c_int64), ("primal_energy", ctypes.c_double),
+                ("gap", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -72,7 +73,7 @@ def load_library(path: str = LIB_PATH):
     P = ctypes.c_void_p
     i32, f32 = ctypes.c_int32, ctypes.c_float
     LP, IP = ctypes.POINTER(Layout), ctypes.POINTER(Iters)
-    lib.tvs_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
+    lib.tvs_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
     lib.tvs_destroy.argtypes = [P]
     lib.tvs_last_error.argtypes = [P]
     lib.tvs_last_error.restype = ctypes.c_char_p
@@ -195,7 +196,7 @@ class Context:
         self.device = device
         h = ctypes.c_void_p()
         idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
-        st = self.lib.tvs_create(ctypes.byref(h), device, rank, world, idbuf)
+        st = self.lib.tvs_create(ctypes.byref(h), rank, world, idbuf, device)
         if st:
             raise TvsError(st, "tvs_create")
         self.h = h
@@ -219,10 +220,9 @@ class Context:
     def _ptr(t):
         return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
-    @staticmethod
-    def _stream(stream):
+    def _stream(self, stream):
         import torch
-        s = stream if stream is not None else torch.cuda.current_stream()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
         return ctypes.c_void_p(s.cuda_stream)
 
     def _dev(self, x, shape):

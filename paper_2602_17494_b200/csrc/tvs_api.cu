@@ -170,34 +170,29 @@ struct ProjBatch {
   std::vector<ProjTile> tiles;
   ProjTile *d_tiles = nullptr;
   int *d_first = nullptr;
-  float *q = nullptr;       // input, [tile][AT][ldq] (hi plane in 3xTF32 mode)
-  float *qlo = nullptr;     // lo plane (3xTF32 mode)
+  float *q = nullptr;       // input, [tile][AT][ldq]
   int ldq = 0;
   float *G = nullptr;       // output, [tile][2][AP][ldG]
   int ldG = 0;
   float *qhat = nullptr;
-  double *z = nullptr, *rinv = nullptr, *segprod = nullptr;
+  float *z = nullptr;       // fp32 z scratch of solve3 when its column block exceeds shared memory
+  double *rinv = nullptr, *segprod = nullptr;
   SolveMaps *d_smaps = nullptr;   // TMA maps of the solve's staged blocks (solve4)
   int smem_rows = 0;
   int *d_order = nullptr;         // solve4 launch order: tiles grouped by chain [nchains][per_chain]
   int per_chain = 0;
-  float *phx = nullptr, *phy = nullptr, *phx_lo = nullptr, *phy_lo = nullptr;
-  GemmDesc *d_fwd = nullptr, *d_inv = nullptr;        // SIMT: B as [K][N]
-  GemmDesc2 *d_fwd2 = nullptr, *d_inv2 = nullptr;     // tcgen05 3xTF32, pre-split operands
-  TmaGemmDesc *d_fwd3 = nullptr, *d_inv3 = nullptr;   // same, TMA tensor maps
-  TmaGemmDesc *d_fwd4 = nullptr, *d_inv4 = nullptr;   // persistent: A as one fp32 plane
-  TmaGemmDesc *d_fwd5 = nullptr, *d_inv5 = nullptr;   // CTA pairs: B maps with 72-row boxes
-  GemmDesc *d_fwd_tc = nullptr, *d_inv_tc = nullptr;  // tcgen05: B as Bt [N][K]
-  int fwdM = 0, fwdN = 0, invM = 0, invN = 0;
-  // chirp-z form of the two contractions (used when its estimated time is lower, TVS_DCT)
+  float *phx = nullptr, *phy = nullptr;
+  TmaGemmDesc *d_fwd = nullptr, *d_inv = nullptr;   // persistent tcgen05 3xTF32 (TS form)
+  int nstack = 0, tcM_fwd = 0, tcM_inv = 0, fwdN = 0, invN = 0;
+  // chirp-z form of the two contractions (long axes, or when its estimated time is lower)
   bool czt = false;
   CztGeom gf{}, gi{};
   CztJob *d_fj = nullptr, *d_ij = nullptr;
   int nfj = 0, nij = 0, fj_rows = 0, ij_rows = 0;
   float2 *gtab_f = nullptr, *gtab_i = nullptr, *tw_f = nullptr, *tw_i = nullptr;
-  int tcM_fwd = 0, tcM_inv = 0, nstack = 0;
-  bool qblk = false;   // Q-hat column-block-major (see build_proj)
-  double fwd_flops = 0, inv_flops = 0, solve_bytes = 0;
+  // algorithmic work per launch: contraction flops (dense 2MNK), FFT flops of the chirp-z form
+  // (2 x 5 M log2 M per FFT pair and row chunk), and the y-solve's HBM bytes
+  double fwd_flops = 0, inv_flops = 0, fwd_fft_flops = 0, inv_fft_flops = 0, solve_bytes = 0;
 };
 
 struct Plan {
@@ -221,7 +216,7 @@ struct Plan {
   int *d_bad = nullptr;
   double *d_part = nullptr, *d_energy = nullptr;   // dual-energy reduction scratch
   // step 1 only
-  float *vtmp = nullptr, *q = nullptr, *qlo = nullptr, *gphi = nullptr, *qglo = nullptr;
+  float *vtmp = nullptr, *q = nullptr, *gphi = nullptr;
   float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
   ProjBatch local, global;
   int64_t sum_S = 0, sum_T = 0;
@@ -253,12 +248,6 @@ struct tvs_ctx {
   std::map<std::tuple<int, int, int, int, int, int, int>, std::unique_ptr<Plan>> plans;
   std::map<int, std::unique_ptr<Tables>> tables;
   bool profiling = false;
-  // projection contractions: TVS_GEMM = ts (default: persistent TMA + tcgen05 3xTF32 with A split
-  // into tensor memory), persistent (A split in shared memory), tma (pre-split hi/lo operand
-  // planes), cpasync (cp.async + tcgen05 3xTF32) or simt (fp32 FMA baseline, A/B comparisons)
-  enum { G_SIMT = 0, G_CPASYNC = 1, G_TMA = 2, G_PERSIST = 3, G_TS = 4, G_TS2 = 5 };
-  int gemm = G_TS;
-  bool presplit() const { return gemm == G_CPASYNC || gemm == G_TMA; }
   // partial x-DCTs: 0 = choose per batch by estimated time, 1 = dense GEMM, 2 = chirp-z (TVS_DCT)
   int dct_mode = 0;
   int czt_max_m = 16384;
@@ -268,9 +257,6 @@ struct tvs_ctx {
   bool solve_tma = true;         // y-solve blocks staged by TMA (TVS_SOLVE_TMA=0: cp.async)
   int stop_crit = 0;       // tvs_set_stopping
   double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
-  // y-solve variant: segmented recurrences with an fp32 z scratch (default), TVS_SOLVE=serial (one
-  // thread per frequency, fp64 z scratch) or TVS_SOLVE=chunked (z checkpoints in shared memory)
-  int solve_impl = 3;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<PendingEv> pending;
@@ -284,8 +270,6 @@ struct tvs_ctx {
   // side stream: step 1 runs the global residual projection of a sweep on it, concurrently with
   // the omega0 local projection chain (independent until omega0 reads both; TVS_OVERLAP=0: off)
   bool overlap = true;
-  bool qblk = false;  // column-block-major Q-hat for the staged y-solve (TVS_QBLK=1: on; measured
-                      // net negative at config 3: solve -1.6 %, forward GEMM epilogue +8 %)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -356,9 +340,10 @@ tvs_status run(tvs_ctx *ctx, cudaStream_t s, int fam, double bytes, double flops
     b = ctx->ev_pool[ctx->ev_used++];
     CK(cudaEventRecord(a, s));
   }
+  g_extra_launches = 0;
   cudaError_t e = launch();
   if (e != cudaSuccess) return fail(ctx, TVS_ECUDA, "kernel launch (family %d): %s", fam, cudaGetErrorString(e));
-  ctx->launches++;
+  ctx->launches += 1 + g_extra_launches;
   if (ctx->profiling) {
     CK(cudaEventRecord(b, s));
     ctx->pending.push_back({fam, a, b, bytes, flops});
@@ -408,8 +393,8 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
 // fr0/fr1 (global batch only): rows whose partial x-DCT this rank computes (its core rows; the
 // rest of qhat arrives by all-gather); gplane: plane stride of G (0 = ntiles * AP * ldG).
 tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
-                      int n2t, int n1t, float *q, float *qlo, int ldq, float *G, int ldG,
-                      const Tables *T, int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0) {
+                      int n2t, int n1t, float *q, int ldq, float *G, int ldG, const Tables *T,
+                      int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0) {
   B.tiles = tiles_in;
   B.ntiles = (int)tiles_in.size();
   std::map<std::pair<int, int>, int> chain_of;
@@ -428,31 +413,21 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   B.nchains = (int)first.size();
   B.ldn = round_up(n1t, 4);
   B.q = q;
-  B.qlo = qlo;
   B.ldq = ldq;
   B.G = G;
   B.ldG = ldG;
   TRY(upload(ctx, P.bufs, &B.d_tiles, B.tiles));
   TRY(upload(ctx, P.bufs, &B.d_first, first));
-  // (room for the column-block-major layout too: blocks of up to 32 columns)
-  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * round_up(n1t, 32)));
-  // z scratch: fp64 for the serial solve, fp32 for the segmented solve when its column block does
-  // not fit in shared memory, none otherwise
+  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * B.ldn));
+  // fp32 z scratch for the segmented solve only when its column block does not fit in shared memory
   const size_t nz = (size_t)B.ntiles * B.AT * B.ldn;
-  const bool smem_z = (size_t)B.AT * 32 * sizeof(float) <= 160 * 1024;
-  if (ctx->solve_impl == 1) TRY(dalloc(ctx, P.bufs, &B.z, nz));
-  else if (ctx->solve_impl != 2 && !smem_z) TRY(dalloc(ctx, P.bufs, &B.z, nz / 2 + 1));
+  if ((size_t)B.AT * 32 * sizeof(float) > 160 * 1024) TRY(dalloc(ctx, P.bufs, &B.z, nz));
   TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
-  if (ctx->presplit()) {   // hi/lo operand planes of the pre-split GEMM variants
-    TRY(dalloc(ctx, P.bufs, &B.phx_lo, (size_t)B.ntiles * B.AP * B.ldn));
-    TRY(dalloc(ctx, P.bufs, &B.phy_lo, (size_t)B.ntiles * B.AP * B.ldn));
-  }
-  std::vector<GemmDesc> fwd, inv, fwd_tc, inv_tc;
-  std::vector<GemmDesc2> fwd2, inv2;
   // ∇φ output is plane-major: G[c][tile][AP][ldG]
   const size_t gplane = gplane_arg ? gplane_arg : (size_t)B.ntiles * B.AP * ldG;
+  std::vector<GemmDesc2> fwd2, inv2;
   for (int i = 0; T && i < B.ntiles;) {
     // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
     int j = i + 1;
@@ -464,177 +439,121 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
     int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
     const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1 - B.tiles[j - 1].po);
-    // forward rows [f0, f0 + Mf) of the stacked operand; inverse output rows start at po
-    int f0 = 0;
+    int f0 = 0;   // forward rows [f0, f0 + Mf) of the stacked operand; inverse output rows from po
     if (fr0 >= 0) {
       f0 = fr0;
       Mf = fr1 - fr0;
     }
     const size_t goff = (size_t)t.po * ldG;
-    fwd_tc.push_back({q + ((size_t)i * B.AT + f0) * ldq, T->cn + t.tx0,
-                      B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t, bt, ldq, T->ld, B.ldn});
-    inv_tc.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->snT + (size_t)t.tx0 * T->ld,
-                      G + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
-    inv_tc.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cf + (size_t)t.tx0 * T->ld,
-                      G + gplane + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
-    // 3xTF32 pre-split forms; q carries a leading zero offset of (tx0 & 3) columns so the table
-    // rows start 16-byte aligned: K = bt + off, tables from column tx0 - off
+    // 3xTF32: A (q, Phi) is one fp32 plane split in the kernel, B = the pre-split DCT tables; q
+    // carries a leading zero offset of (tx0 & 3) columns so the table rows start 16-byte aligned:
+    // K = bt + off, tables from column tx0 - off
     const int off = t.tx0 & 3;
-    fwd2.push_back({q + ((size_t)i * B.AT + f0) * ldq, qlo + ((size_t)i * B.AT + f0) * ldq,
-                    T->part(2) + (t.tx0 - off), T->part(3) + (t.tx0 - off),
-                    B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t, bt + off, ldq, T->ld, B.ldn});
-    inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, B.phx_lo + (size_t)i * B.AP * B.ldn,
-                    T->part(4) + (size_t)t.tx0 * T->ld, T->part(5) + (size_t)t.tx0 * T->ld,
-                    G + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
-    inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, B.phy_lo + (size_t)i * B.AP * B.ldn,
-                    T->part(0) + (size_t)t.tx0 * T->ld, T->part(1) + (size_t)t.tx0 * T->ld,
-                    G + gplane + (size_t)i * B.AP * ldG + goff, Mi, bo, n1t, B.ldn, T->ld, ldG});
+    fwd2.push_back({q + ((size_t)i * B.AT + f0) * ldq, nullptr, T->part(2) + (t.tx0 - off),
+                    T->part(3) + (t.tx0 - off), B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t,
+                    bt + off, ldq, T->ld, B.ldn});
+    inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, nullptr, T->part(4) + (size_t)t.tx0 * T->ld,
+                    T->part(5) + (size_t)t.tx0 * T->ld, G + (size_t)i * B.AP * ldG + goff, Mi, bo,
+                    n1t, B.ldn, T->ld, ldG});
+    inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, nullptr, T->part(0) + (size_t)t.tx0 * T->ld,
+                    T->part(1) + (size_t)t.tx0 * T->ld, G + gplane + (size_t)i * B.AP * ldG + goff,
+                    Mi, bo, n1t, B.ldn, T->ld, ldG});
     B.tcM_fwd = std::max(B.tcM_fwd, Mf);
     B.tcM_inv = std::max(B.tcM_inv, Mi);
+    B.fwdN = std::max(B.fwdN, n1t);
+    B.invN = std::max(B.invN, bo);
     i = j;
   }
-  for (int i = 0; T && i < B.ntiles; ++i) {
+  // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
+  std::vector<CztJob> fj, ij;
+  int bt_max = 0, bo_max = 0;
+  for (int i = 0; i < B.ntiles; ++i) {
     const ProjTile &t = B.tiles[i];
-    int nt = t.ty1 - t.ty0 + 1, bt = t.tx1 - t.tx0 + 1;
-    int no = t.py1 - t.ty0 + 1 - t.po, bo = t.px1 - t.tx0 + 1;
-    int f0 = 0;
+    int nt = t.ty1 - t.ty0 + 1, f0 = 0;
     if (fr0 >= 0) {
       f0 = fr0;
       nt = fr1 - fr0;
     }
+    const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
+    const int no = t.py1 - t.ty0 + 1 - t.po;
     const size_t goff = (size_t)t.po * ldG;
-    fwd.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3), T->cf + (size_t)t.tx0 * T->ld,
-                   B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, n1t, bt, ldq, T->ld, B.ldn});
-    inv.push_back({B.phx + (size_t)i * B.AP * B.ldn, T->sn + t.tx0,
-                   G + (size_t)i * B.AP * ldG + goff, no, bo, n1t, B.ldn, T->ld, ldG});
-    inv.push_back({B.phy + (size_t)i * B.AP * B.ldn, T->cn + t.tx0,
-                   G + gplane + (size_t)i * B.AP * ldG + goff, no, bo, n1t, B.ldn, T->ld, ldG});
-    B.fwdM = std::max(B.fwdM, nt);
-    B.fwdN = std::max(B.fwdN, n1t);
-    B.invM = std::max(B.invM, no);
-    B.invN = std::max(B.invN, bo);
+    // algorithmic work: the contraction flops (2MNK of each partial x-DCT) and, for the y-solve,
+    // Q-hat read (4 B) per (T row, frequency) plus the two fp32 gradient planes written (8 B)
+    // per (output row, frequency); the fp64 pivots are added once per chain below
+    B.fwd_flops += 2.0 * nt * bt * n1t;
+    B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
+    B.solve_bytes += (double)nt * n1t * 4.0 + (double)no * n1t * 8.0;
+    fj.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3),
+                  B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, ldq, B.ldn, t.tx0, bt, n1t, 0});
+    ij.push_back({B.phx + (size_t)i * B.AP * B.ldn, G + (size_t)i * B.AP * ldG + goff, no, B.ldn,
+                  ldG, t.tx0, n1t, bo, 2});
+    ij.push_back({B.phy + (size_t)i * B.AP * B.ldn, G + gplane + (size_t)i * B.AP * ldG + goff, no,
+                  B.ldn, ldG, t.tx0, n1t, bo, 1});
+    bt_max = std::max(bt_max, bt);
+    bo_max = std::max(bo_max, bo);
+    B.fj_rows = std::max(B.fj_rows, nt);
+    B.ij_rows = std::max(B.ij_rows, no);
   }
-  // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
-  {
-    std::vector<CztJob> fj, ij;
-    int bt_max = 0, bo_max = 0;
-    for (int i = 0; i < B.ntiles; ++i) {
-      const ProjTile &t = B.tiles[i];
-      int nt = t.ty1 - t.ty0 + 1, f0 = 0;
-      if (fr0 >= 0) {
-        f0 = fr0;
-        nt = fr1 - fr0;
+  for (int c = 0; c < B.nchains; ++c) {
+    const ProjTile &t = B.tiles[first[c]];
+    B.solve_bytes += (double)(t.ty1 - t.ty0 + 1) * n1t * 8.0;
+  }
+  B.nfj = (int)fj.size();
+  B.nij = (int)ij.size();
+  const bool okf = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
+  const bool oki = czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
+  // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~12 TF/s
+  // (5 M log2 M flops per FFT; config-4 forward launch: 14 TF/s)
+  double t_gemm = 0, t_czt = 0;
+  const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)std::max(2, B.gf.M));
+  const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)std::max(2, B.gi.M));
+  for (int i = 0; i < B.ntiles; ++i) {
+    t_gemm += 3.0 * (2.0 * fj[i].rows * fj[i].ulen * fj[i].vlen +
+                     2.0 * 2.0 * ij[2 * i].rows * ij[2 * i].ulen * ij[2 * i].vlen) / 400e12;
+    B.fwd_fft_flops += (double)fj[i].rows * B.gf.nvp * B.gf.nuc * f1;
+    B.inv_fft_flops += 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2;
+  }
+  t_czt = (B.fwd_fft_flops + B.inv_fft_flops) / 12e12;
+  // accuracy: the tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193
+  // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
+  const bool long_axis = n1t > 4096;
+  B.czt = okf && oki && (!T || ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
+  if (!T && !B.czt) return fail(ctx, TVS_EINVAL, "projection batch without DCT tables needs chirp-z");
+  if (B.czt) {
+    std::vector<float2> gt, tw;
+    czt_tables(B.gf, gt, tw);
+    TRY(upload(ctx, P.bufs, &B.gtab_f, gt));
+    TRY(upload(ctx, P.bufs, &B.tw_f, tw));
+    czt_tables(B.gi, gt, tw);
+    TRY(upload(ctx, P.bufs, &B.gtab_i, gt));
+    TRY(upload(ctx, P.bufs, &B.tw_i, tw));
+    {   // chirp tables: one device buffer for both job lists
+      std::vector<size_t> pf, qf, pi, qi;
+      std::vector<float2> tf = czt_chirp_tables(B.gf.N, fj, pf, qf);
+      std::vector<float2> ti = czt_chirp_tables(B.gi.N, ij, pi, qi);
+      const size_t nf = tf.size();
+      tf.insert(tf.end(), ti.begin(), ti.end());
+      float2 *dch = nullptr;
+      TRY(upload(ctx, P.bufs, &dch, tf));
+      for (size_t k = 0; k < fj.size(); ++k) {
+        fj[k].pre = dch + pf[k];
+        fj[k].post = dch + qf[k];
       }
-      const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
-      const int no = t.py1 - t.ty0 + 1 - t.po;
-      const size_t goff = (size_t)t.po * ldG;
-      // algorithmic work: the dense-equivalent contraction flops, and for the solve per (row,
-      // frequency) Q-hat 4 + pivots 8 + two fp32 gradient planes 8 bytes
-      B.fwd_flops += 2.0 * nt * bt * n1t;
-      B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
-      B.solve_bytes += (double)nt * n1t * 20.0;
-      fj.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3),
-                    B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, ldq, B.ldn, t.tx0, bt, n1t, 0});
-      ij.push_back({B.phx + (size_t)i * B.AP * B.ldn, G + (size_t)i * B.AP * ldG + goff, no, B.ldn,
-                    ldG, t.tx0, n1t, bo, 2});
-      ij.push_back({B.phy + (size_t)i * B.AP * B.ldn, G + gplane + (size_t)i * B.AP * ldG + goff, no,
-                    B.ldn, ldG, t.tx0, n1t, bo, 1});
-      bt_max = std::max(bt_max, bt);
-      bo_max = std::max(bo_max, bo);
-      B.fj_rows = std::max(B.fj_rows, nt);
-      B.ij_rows = std::max(B.ij_rows, no);
-    }
-    B.nfj = (int)fj.size();
-    B.nij = (int)ij.size();
-    const bool okf = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
-    const bool oki = czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
-    // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~12 TF/s (5 M log2 M flops per FFT; config-4 forward launch: 14 TF/s)
-    double t_gemm = 0, t_czt = 0;
-    for (int i = 0; i < B.ntiles; ++i) {
-      t_gemm += 3.0 * (2.0 * fj[i].rows * fj[i].ulen * fj[i].vlen +
-                       2.0 * 2.0 * ij[2 * i].rows * ij[2 * i].ulen * ij[2 * i].vlen) / 400e12;
-      const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)B.gf.M);
-      const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)B.gi.M);
-      t_czt += (fj[i].rows * B.gf.nvp * B.gf.nuc * f1 + 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2) / 12e12;
-    }
-    // accuracy: the tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193
-    // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
-    const bool long_axis = n1t > 4096;
-    B.czt = okf && oki && !ctx->presplit() && ctx->gemm != tvs_ctx::G_SIMT &&
-            (!T || ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
-    if (!T && !B.czt) return fail(ctx, TVS_EINVAL, "projection batch without DCT tables needs chirp-z");
-    if (B.czt) {
-      std::vector<float2> gt, tw;
-      czt_tables(B.gf, gt, tw);
-      TRY(upload(ctx, P.bufs, &B.gtab_f, gt));
-      TRY(upload(ctx, P.bufs, &B.tw_f, tw));
-      czt_tables(B.gi, gt, tw);
-      TRY(upload(ctx, P.bufs, &B.gtab_i, gt));
-      TRY(upload(ctx, P.bufs, &B.tw_i, tw));
-      {   // chirp tables: one device buffer for both job lists
-        std::vector<size_t> pf, qf, pi, qi;
-        std::vector<float2> tf = czt_chirp_tables(B.gf.N, fj, pf, qf);
-        std::vector<float2> ti = czt_chirp_tables(B.gi.N, ij, pi, qi);
-        const size_t nf = tf.size();
-        tf.insert(tf.end(), ti.begin(), ti.end());
-        float2 *dch = nullptr;
-        TRY(upload(ctx, P.bufs, &dch, tf));
-        for (size_t k = 0; k < fj.size(); ++k) {
-          fj[k].pre = dch + pf[k];
-          fj[k].post = dch + qf[k];
-        }
-        for (size_t k = 0; k < ij.size(); ++k) {
-          ij[k].pre = dch + nf + pi[k];
-          ij[k].post = dch + nf + qi[k];
-        }
+      for (size_t k = 0; k < ij.size(); ++k) {
+        ij[k].pre = dch + nf + pi[k];
+        ij[k].post = dch + nf + qi[k];
       }
-      TRY(upload(ctx, P.bufs, &B.d_fj, fj));
-      TRY(upload(ctx, P.bufs, &B.d_ij, ij));
     }
+    TRY(upload(ctx, P.bufs, &B.d_fj, fj));
+    TRY(upload(ctx, P.bufs, &B.d_ij, ij));
+  } else {
+    B.nstack = (int)fwd2.size();
+    std::vector<TmaGemmDesc> fwd3(fwd2.size()), inv3(inv2.size());
+    for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
+    for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
+    TRY(upload(ctx, P.bufs, &B.d_fwd, fwd3));
+    TRY(upload(ctx, P.bufs, &B.d_inv, inv3));
   }
-  TRY(upload(ctx, P.bufs, &B.d_fwd, fwd));
-  TRY(upload(ctx, P.bufs, &B.d_inv, inv));
-  B.nstack = (int)fwd_tc.size();
-  TRY(upload(ctx, P.bufs, &B.d_fwd_tc, fwd_tc));
-  TRY(upload(ctx, P.bufs, &B.d_inv_tc, inv_tc));
-  TRY(upload(ctx, P.bufs, &B.d_fwd2, fwd2));
-  TRY(upload(ctx, P.bufs, &B.d_inv2, inv2));
-  std::vector<TmaGemmDesc> fwd3(fwd2.size()), inv3(inv2.size());
-  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
-  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
-  TRY(upload(ctx, P.bufs, &B.d_fwd3, fwd3));
-  TRY(upload(ctx, P.bufs, &B.d_inv3, inv3));
-  // persistent kernel: the A operand is the single fp32 plane (split in shared memory)
-  for (auto &d : fwd2) d.Alo = nullptr;
-  for (auto &d : inv2) d.Alo = nullptr;
-  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
-  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
-  // column-block-major Q-hat between the forward GEMM and the staged y-solve (local batch, ts GEMM,
-  // TMA-staged solve4): each solve CTA then stages one contiguous block (TVS_QBLK=1; off by default)
-  B.qblk = T && !B.czt && fr0 < 0 && ctx->qblk && ctx->gemm == tvs_ctx::G_TS &&
-           ctx->solve_impl == 3 && ctx->solve_tma && solve4_fits(B.AT);
-  if (B.qblk) {
-    const int J = solve4_width(B.AT);
-    const long long plane = (long long)B.ntiles * B.AT * J;
-    size_t st = 0;
-    for (int i = 0; i < B.ntiles;) {   // same stacking as fwd2 above
-      int j = i + 1;
-      while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
-             B.tiles[j].px1 == B.tiles[i].px1)
-        ++j;
-      fwd3[st].C = B.qhat + (size_t)i * B.AT * J;
-      fwd3[st].c_blk = J;
-      fwd3[st].c_plane = plane;
-      ++st;
-      i = j;
-    }
-  }
-  TRY(upload(ctx, P.bufs, &B.d_fwd4, fwd3));
-  TRY(upload(ctx, P.bufs, &B.d_inv4, inv3));
-  for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 72));
-  for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 72));
-  TRY(upload(ctx, P.bufs, &B.d_fwd5, fwd3));
-  TRY(upload(ctx, P.bufs, &B.d_inv5, inv3));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
@@ -648,18 +567,12 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
         for (size_t k = 0; k < byc[c].size(); ++k) order[(size_t)c * B.per_chain + k] = byc[c][k];
       TRY(upload(ctx, P.bufs, &B.d_order, order));
     }
-    if (ctx->solve_tma) {   // TMA boxes of {32 columns, <= 256 rows} for the staged blocks
+    if (ctx->solve_tma) {   // TMA boxes of {J columns, <= 256 rows} for the staged blocks
       SolveMaps m{};
       m.nbox = (B.AT + 255) / 256;
       // even row counts: every box of the fp32 block then starts 128-byte aligned (J = 16 columns)
       m.box_rows = round_up((B.AT + m.nbox - 1) / m.nbox, 2);
-      if (B.qblk) {   // [block][ntiles * AT rows][J]
-        const int J = solve4_width(B.AT), nj = (n1t + J - 1) / J;
-        m.q_blk_rows = B.ntiles * B.AT;
-        CK(encode_plain_2d(&m.q, B.qhat, false, J, nj * B.ntiles * B.AT, J, J, m.box_rows));
-      } else {
-        CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
-      }
+      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       B.smem_rows = m.nbox * m.box_rows;
       TRY(upload(ctx, P.bufs, &B.d_smaps, std::vector<SolveMaps>{m}));
@@ -777,8 +690,8 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   TRY(dalloc(ctx, P->bufs, &P->v[1], vsz));
   TRY(dalloc(ctx, P->bufs, &P->p, (size_t)C * G2 * P->ld));
   TRY(dalloc(ctx, P->bufs, &P->d_bad, 1));
-  TRY(dalloc(ctx, P->bufs, &P->d_part, 1024));
-  TRY(dalloc(ctx, P->bufs, &P->d_energy, 4));
+  TRY(dalloc(ctx, P->bufs, &P->d_part, 4 * 1024));
+  TRY(dalloc(ctx, P->bufs, &P->d_energy, 16));
   if (D.world > 1) {   // partial-sum band buffers [planes][rows][ld]
     TRY(dalloc(ctx, P->bufs, &P->send_up, (size_t)C * std::max(1, D.us1 - D.us0) * P->ld));
     TRY(dalloc(ctx, P->bufs, &P->recv_up, (size_t)C * std::max(1, D.ur1 - D.ur0) * P->ld));
@@ -793,14 +706,12 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   } else {
     // the dense DCT tables (10 planes of N x N floats) only when a batch may take the GEMM form:
     // long axes always run the chirp-z form
-    const bool czt_only = G1 > 4096 && ctx->dct_mode != 1 && !ctx->presplit() &&
-                          ctx->gemm != tvs_ctx::G_SIMT;
+    const bool czt_only = G1 > 4096 && ctx->dct_mode != 1;
     Tables *T = nullptr;
     if (!czt_only) TRY(get_tables(ctx, G1, &T));
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * 2 * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->vtmp, vsz));
     TRY(dalloc(ctx, P->bufs, &P->q, (size_t)g.M * g.AT * g.ldT));
-    if (ctx->presplit()) TRY(dalloc(ctx, P->bufs, &P->qlo, (size_t)g.M * g.AT * g.ldT));
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)g.M * 2 * g.AP * g.ldP));
     size_t pl = (size_t)G2 * P->ld;
     TRY(dalloc(ctx, P->bufs, &P->f, 2 * pl));
@@ -808,15 +719,14 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->w, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->r, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->qg, pl));
-    if (ctx->presplit()) TRY(dalloc(ctx, P->bufs, &P->qglo, pl));
     TRY(dalloc(ctx, P->bufs, &P->Gg, 2 * pl));
     std::vector<ProjTile> lt;
     for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
-    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, P->qlo, g.ldT, P->gphi, g.ldP, T));
+    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T));
     // global projection: the y-solves span every row; this rank transforms its core rows
     // (qhat of the others arrives by all-gather) and needs grad phi only on its valid rows V
     std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, D.V1 - 1, G1 - 1, 0, D.V0}};
-    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->qglo, P->ld, P->Gg, P->ld, T, D.R0,
+    TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->ld, P->Gg, P->ld, T, D.R0,
                    D.R1, pl));
   }
   *out = P.get();
@@ -882,17 +792,20 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
   });
 }
 
-// Sum the device scalar over ranks (NCCL) and copy it to the pinned host slot; sync = read it now
-// (otherwise the value is valid after the call's final stream synchronisation).
-tvs_status fetch_energy(tvs_ctx *ctx, Plan &P, cudaStream_t s, double *out, bool sync = true) {
+// Sum the device scalars d_energy[off, off + n) over ranks (NCCL) and copy them to the same slots
+// of the pinned host array; sync = read slot `off` into *out now (otherwise the values are valid
+// after the call's final stream synchronisation).
+tvs_status fetch_energy(tvs_ctx *ctx, Plan &P, cudaStream_t s, double *out, bool sync = true,
+                        int off = 0, int n = 1) {
   if (P.dist.world > 1)
-    TRY(nccl_ck(ctx, ncclAllReduce(P.d_energy, P.d_energy, 1, ncclDouble, ncclSum, ctx->nccl, s),
-                "ncclAllReduce"));
-  if (!ctx->h_energy) CK(cudaMallocHost(&ctx->h_energy, 8 * sizeof(double)));
-  CK(cudaMemcpyAsync(ctx->h_energy, P.d_energy, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TRY(nccl_ck(ctx, ncclAllReduce(P.d_energy + off, P.d_energy + off, n, ncclDouble, ncclSum,
+                                   ctx->nccl, s), "ncclAllReduce"));
+  if (!ctx->h_energy) CK(cudaMallocHost(&ctx->h_energy, 16 * sizeof(double)));
+  CK(cudaMemcpyAsync(ctx->h_energy + off, P.d_energy + off, n * sizeof(double),
+                     cudaMemcpyDeviceToHost, s));
   if (sync) {
     CK(cudaStreamSynchronize(s));
-    *out = ctx->h_energy[0];
+    if (out) *out = ctx->h_energy[off];
   }
   return TVS_OK;
 }
@@ -911,70 +824,33 @@ bool stop_now(const tvs_ctx *ctx, double d_prev, double d_next, double npts, dou
 // global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
 tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
-  const bool tc = ctx->presplit();   // solve writes hi/lo planes
-  const int gm = ctx->gemm;
   if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
-    TRY(run(ctx, s, F_CZT_FWD, 0, B.fwd_flops, [&] {
+    TRY(run(ctx, s, F_CZT_FWD, 0, B.fwd_fft_flops, [&] {
       return launch_czt(B.d_fj, B.nfj, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
     }));
-    if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
-    TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-      if (ctx->solve_impl == 5 && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width(B.AT) == 32)
-        return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
-                                  B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
-      return B.segprod ? launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
-                                            B.rinv, B.segprod, B.phx, B.phy, B.AP, B.d_smaps,
-                                            B.smem_rows, B.d_order, B.nchains, B.per_chain, s)
-                       : launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn,
-                                            B.rinv, reinterpret_cast<float *>(B.z), B.phx, B.phy,
-                                            nullptr, nullptr, B.AP, s);
+  } else {       // dense 3xTF32 tcgen05 contraction (persistent, A in tensor memory)
+    TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
+      return launch_gemm_tma_ts(B.d_fwd, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
     }));
-    return run(ctx, s, F_CZT_INV, 0, B.inv_flops, [&] {
-      return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
-    });
   }
-  TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
-    switch (gm) {
-      case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
-      case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_fwd4, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
-      case tvs_ctx::G_TS2: return launch_gemm_tma_ts2(B.d_fwd5, B.nstack, B.tcM_fwd, B.fwdN, s);
-      case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_fwd3, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
-      case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_fwd2, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
-      default: return launch_gemm(B.d_fwd, B.ntiles, B.fwdM, B.fwdN, s);
-    }
-  }));
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
-    if (ctx->solve_impl == 5 && !tc && B.segprod && B.d_smaps && solve5_fits(B.AT) && solve4_width(B.AT) == 32)
-      return launch_proj_solve5(B.d_tiles, G2, G1, B.AT, B.ldn, B.segprod, B.phx, B.phy, B.AP,
-                                B.d_smaps, B.smem_rows, B.d_order, B.nchains, B.per_chain, s);
-    if ((ctx->solve_impl == 3 || ctx->solve_impl == 5) && !tc && B.segprod)
+    // segmented fp64 y-solve: staged in shared memory (solve4) when the tile height allows,
+    // else solve3 (shared-memory z up to 160 KB per column block, fp32 global scratch beyond)
+    if (B.segprod)
       return launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
                                 B.segprod, B.phx, B.phy, B.AP, B.d_smaps, B.smem_rows,
                                 B.d_order, B.nchains, B.per_chain, s);
-    if (ctx->solve_impl >= 3)
-      return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
-                                reinterpret_cast<float *>(B.z), B.phx, B.phy,
-                                tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr, B.AP, s);
-    return ctx->solve_impl == 1
-               ? launch_proj_solve(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
-                                   B.phx, B.phy, tc ? B.phx_lo : nullptr, tc ? B.phy_lo : nullptr,
-                                   B.AP, s)
-               : launch_proj_solve2(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
-                                    B.phx, B.phy, tc ? B.phx_lo : nullptr,
-                                    tc ? B.phy_lo : nullptr, B.AP, s);
+    return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
+                              B.phx, B.phy, nullptr, nullptr, B.AP, s);
   }));
-  TRY(run(ctx, s, F_INV, 0, B.inv_flops, [&] {
-    switch (gm) {
-      case tvs_ctx::G_PERSIST: return launch_gemm_tma_p(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
-      case tvs_ctx::G_TS: return launch_gemm_tma_ts(B.d_inv4, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
-      case tvs_ctx::G_TS2: return launch_gemm_tma_ts2(B.d_inv5, 2 * B.nstack, B.tcM_inv, B.invN, s);
-      case tvs_ctx::G_TMA: return launch_gemm_tma(B.d_inv3, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
-      case tvs_ctx::G_CPASYNC: return launch_gemm_tc2(B.d_inv2, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
-      default: return launch_gemm(B.d_inv, 2 * B.ntiles, B.invM, B.invN, s);
-    }
-  }));
-  return TVS_OK;
+  if (B.czt)
+    return run(ctx, s, F_CZT_INV, 0, B.inv_fft_flops, [&] {
+      return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
+    });
+  return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
+    return launch_gemm_tma_ts(B.d_inv, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
+  });
 }
 
 tvs_status check_common(tvs_ctx *ctx, int32_t n2, int32_t n1, tvs_layout L, tvs_iters it) {
@@ -1095,14 +971,23 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       e_prev = e;
     }
   }
-  double e_final = 0.0;
-  TRY(energy2(&e_final, false));   // read after the final synchronisation
   const Dist &D = P->dist;
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
     return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha,
                            variant == 1 ? P->dxi : nullptr, d, D.R0, D.R1, s);
   }));
   TRY(allgather_rows(ctx, D, d, 1, 0, n1, s));
+  // final dual energy D(p^S) into slot 4, primal-energy / gap sums into slots 5..8 (read after the
+  // final synchronisation)
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_dual_energy2(P->p, P->p + pl, P->f, ld, n2, n1, D2.R0, D2.R1, P->d_part,
+                               P->d_energy + 4, s);
+  }));
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_primal2(d, d0, P->f, variant == 1 ? P->dxi : nullptr, P->p, P->p + pl, ld, n2,
+                          n1, D.R0, D.R1, 1.f / alpha, P->d_part, P->d_energy + 5, s);
+  }));
+  TRY(fetch_energy(ctx, *P, s, nullptr, false, 4, 5));
   if (p_out) TRY(allgather_rows(ctx, D, P->p, 2, pl, ld, s));
   if (p_out)
     for (int c = 0; c < 2; ++c)
@@ -1115,8 +1000,12 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
     st->sweeps_run = sweeps_run;
   }
   TRY(finish_call(ctx, *P, s, tm, st, l0));
-  (void)e_final;
-  if (st) st->dual_energy = ctx->h_energy[0];
+  if (st) {
+    const double *h = ctx->h_energy;   // D, TV(u), ||d - d0||^2, gap, <d, div xi>
+    st->dual_energy = h[4];
+    st->primal_energy = h[5] + 0.5 * (double)alpha * h[6] + (variant == 1 ? h[8] : 0.0);
+    st->gap = h[7];
+  }
   return TVS_OK;
 }
 
@@ -1136,14 +1025,13 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   const Geo g = P->geo;
   const int G2 = P->G2, G1 = P->G1, ld = P->ld;
   const size_t pl = (size_t)G2 * ld;
-  const bool tc = ctx->presplit();   // operand planes pre-split into hi/lo
   CK(cudaMemsetAsync(P->d_bad, 0, sizeof(int), s));
   // f = delta^{-1} P tau_0 (tau_0 pre-projected, reading A1)
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] { return launch_tau0(d0, n2, n1, P->t0, ld, s); }));
   const Dist &D = P->dist;
   const bool gather = D.world > 1;
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-    return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, s);
+    return launch_div(P->t0, P->t0 + pl, ld, G2, G1, P->qg, nullptr, D.R0, D.R1, s);
   }));
   TRY(project_batch(ctx, *P, P->global, s, gather));
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
@@ -1158,7 +1046,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     TRY(run(ctx, rs, F_OTHER, 0, 0,
             [&] { return launch_multidiv(P->p, ld, G2, G1, P->w, D.E0, D.V1, rs); }));
     TRY(run(ctx, rs, F_OTHER, 0, 0, [&] {
-      return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, tc ? P->qglo : nullptr, D.R0, D.R1, rs);
+      return launch_div(P->w, P->w + pl, ld, G2, G1, P->qg, nullptr, D.R0, D.R1, rs);
     }));
     TRY(project_batch(ctx, *P, P->global, rs, gather));
     return run(ctx, rs, F_OTHER, 0, 0, [&] {
@@ -1209,7 +1097,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       return launch_load_tp(P->d_subs, g, P->d_thy, P->d_thx, P->p, ld, G2, G1, P->vtmp, s);
     }));
     TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, tc ? P->qlo : nullptr, s); }));
+            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, nullptr, s); }));
     TRY(project_batch(ctx, *P, P->local, s));
     if (overlap) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
@@ -1217,7 +1105,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     }));
     for (int k = 0; k < it.inner; ++k) {
       TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, tc ? P->qlo : nullptr, s); }));
+              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, nullptr, s); }));
       TRY(project_batch(ctx, *P, P->local, s));
       TRY(run(ctx, s, F_SWEEP1, sweep_bytes, 0, [&] {
         return launch_sweep1(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->gphi, g.ldP, P->om,
@@ -1229,9 +1117,17 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   }
   // tau = P tau_0 - delta P multidiv p = delta r^S; every rank ends with the full field
   TRY(residual(P->r, delta, s));
-  double e_final = 0.0;
-  TRY(energy1(&e_final, false));   // ||delta r^S||^2, read after the final synchronisation
   TRY(allgather_rows(ctx, D, P->r, 2, pl, ld, s));
+  // ||delta r^S||^2 into slot 4, primal-energy / gap sums into slots 5..7 (read after the final
+  // synchronisation)
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_sumsq2(P->r, pl, ld, G1, D.R0, D.R1, P->d_part, P->d_energy + 4, s);
+  }));
+  TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+    return launch_primal1(P->r, pl, ld, P->f, P->p, G2, G1, D.R0, D.R1, delta, P->d_part,
+                          P->d_energy + 5, s);
+  }));
+  TRY(fetch_energy(ctx, *P, s, nullptr, false, 4, 4));
   if (p_out) TRY(allgather_rows(ctx, D, P->p, 4, pl, ld, s));
   for (int c = 0; c < 2; ++c)
     CK(cudaMemcpy2DAsync(tau_out + (size_t)c * G2 * G1, G1 * sizeof(float), P->r + c * pl,
@@ -1249,8 +1145,12 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     st->sweeps_run = sweeps_run;
   }
   TRY(finish_call(ctx, *P, s, tm, st, l0));
-  (void)e_final;
-  if (st) st->dual_energy = ctx->h_energy[0] / ((double)delta * (double)delta);
+  if (st) {
+    const double *h = ctx->h_energy;   // ||tau||^2, TV(tau), ||tau - P tau_0||^2, gap
+    st->dual_energy = h[4] / ((double)delta * (double)delta);
+    st->primal_energy = h[5] + h[6] / (2.0 * (double)delta);
+    st->gap = h[7];
+  }
   return TVS_OK;
 }
 
@@ -1260,7 +1160,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
 
 extern "C" {
 
-tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint8_t *nccl_id) {
+tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id, int device) {
   if (!out) return TVS_EINVAL;
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) return TVS_EINVAL;
@@ -1268,18 +1168,9 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
   c->device = device;
   c->rank = rank;
   c->world = world;
-  const char *g = getenv("TVS_GEMM");
-  c->gemm = !g                          ? tvs_ctx::G_TS
-            : strcmp(g, "simt") == 0    ? tvs_ctx::G_SIMT
-            : strcmp(g, "cpasync") == 0 ? tvs_ctx::G_CPASYNC
-            : strcmp(g, "tma") == 0     ? tvs_ctx::G_TMA
-            : strcmp(g, "persistent") == 0 ? tvs_ctx::G_PERSIST
-            : strcmp(g, "ts2") == 0     ? tvs_ctx::G_TS2
-                                        : tvs_ctx::G_TS;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
   if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
-  if (const char *qb = getenv("TVS_QBLK")) c->qblk = atoi(qb) != 0;
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
@@ -1287,13 +1178,6 @@ tvs_status tvs_create(tvs_ctx **out, int device, int rank, int world, const uint
     const int v = atoi(mm);
     if (v >= 16 && v <= 16384 && (v & (v - 1)) == 0 && (__builtin_ctz(v) % 2) == 0) c->czt_max_m = v;
   }
-  const char *sv = getenv("TVS_SOLVE");
-  c->solve_impl = !sv                          ? 3
-                  : strcmp(sv, "chunked") == 0 ? 2
-                  : strcmp(sv, "serial") == 0  ? 1
-                  : strcmp(sv, "seg3") == 0    ? 4
-                  : strcmp(sv, "chain") == 0   ? 5
-                                               : 3;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;

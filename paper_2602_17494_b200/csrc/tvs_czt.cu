@@ -540,11 +540,9 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
                        const float2 *gtab, const float2 *tw, cudaStream_t s) {
   const size_t smem = (size_t)(g.M + (g.M >> 4) + 256 + (g.M >> 8) + 1) * sizeof(float2) +
                       (size_t)g.Vp * sizeof(float);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_czt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {
+    cudaError_t e = smem_optin((const void *)k_czt, smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
   static const int prune = getenv("TVS_CZT_PRUNE") ? atoi(getenv("TVS_CZT_PRUNE")) : 1;

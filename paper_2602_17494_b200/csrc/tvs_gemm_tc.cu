@@ -436,13 +436,9 @@ __global__ void __launch_bounds__(NT) k_gemm_tc2(const GemmDesc2 *__restrict__ d
 template <int BN>
 static cudaError_t launch_two(const GemmDesc2 *descs, int batch, int maxM, int maxN,
                               cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc2<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tc2<BN>, Smem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   dim3 grid((maxN + BN - 1) / BN, (maxM + BM - 1) / BM, batch);
   k_gemm_tc2<BN><<<grid, NT, Smem<BN>::TOTAL, s>>>(descs);
@@ -452,13 +448,9 @@ static cudaError_t launch_two(const GemmDesc2 *descs, int batch, int maxM, int m
 template <int BN, bool AL>
 static cudaError_t launch_one(const GemmDesc *descs, int batch, int maxM, int maxN,
                               cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, AL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tc<BN, AL>, Smem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   dim3 grid((maxN + BN - 1) / BN, (maxM + BM - 1) / BM, batch);
   k_gemm_tc<BN, AL><<<grid, NT, Smem<BN>::TOTAL, s>>>(descs);
@@ -623,13 +615,9 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_tma(const TmaGemmDesc *__restric
 template <int BN>
 static cudaError_t launch_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
                               cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         TSmem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tma<BN>, TSmem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   dim3 grid((maxN + BN - 1) / BN, (maxM + BM - 1) / BM, batch);
   k_gemm_tma<BN><<<grid, NT, TSmem<BN>::TOTAL, s>>>(descs);
@@ -848,17 +836,11 @@ k_gemm_tma_p(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int 
 template <int BN>
 static cudaError_t launch_tma_p(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
                                 cudaStream_t s) {
-  static int nsm = 0;
-  if (!nsm) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_p<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PSmem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tma_p<BN>, PSmem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
   }
+  const int nsm = sm_count();
   const int mb = (maxM + BM - 1) / BM, nb = (maxN + BN - 1) / BN;
   const int ntiles = batch * mb * nb;
   const int grid = ntiles < nsm ? ntiles : nsm;
@@ -1159,28 +1141,15 @@ k_gemm_tma_ts(const TmaGemmDesc *__restrict__ descs, int batch, int mblocks, int
 template <int BN>
 static cudaError_t launch_tma_ts(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
                                  cudaStream_t s) {
-  static int nsm = 0;
-  static const int slots = getenv("TVS_TS_SLOTS") && atoi(getenv("TVS_TS_SLOTS")) == 3 ? 3 : 2;
-  if (!nsm) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts<BN, 2>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         QSmem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tma_ts<BN, 2>, QSmem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gemm_tma_ts<BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             QSmem<BN>::TOTAL);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
   }
+  const int nsm = sm_count();
   const int mb = (maxM + BM - 1) / BM, nb = (maxN + BN - 1) / BN;
   const int ntiles = batch * mb * nb;
   const int grid = ntiles < nsm ? ntiles : nsm;
-  if (slots == 3)
-    k_gemm_tma_ts<BN, 3><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
-  else
-    k_gemm_tma_ts<BN, 2><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
+  k_gemm_tma_ts<BN, 2><<<grid, PNT, QSmem<BN>::TOTAL, s>>>(descs, batch, mb, nb);
   return cudaGetLastError();
 }
 
@@ -1459,17 +1428,11 @@ k_gemm_tma_ts2(const TmaGemmDesc *__restrict__ descs, int batch, int mpairs, int
 template <int BN>
 static cudaError_t launch_tma_ts2(const TmaGemmDesc *descs, int batch, int maxM, int maxN,
                                   cudaStream_t s) {
-  static int nsm = 0;
-  if (!nsm) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_ts2<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         RSmem<BN>::TOTAL);
+  {
+    cudaError_t e = smem_optin((const void *)k_gemm_tma_ts2<BN>, RSmem<BN>::TOTAL);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
   }
+  const int nsm = sm_count();
   const int mp = (maxM + 2 * BM - 1) / (2 * BM), nb = (maxN + BN - 1) / BN;
   const int ntiles = batch * mp * nb;
   const int clusters = ntiles < nsm / 2 ? ntiles : nsm / 2;

@@ -9,6 +9,16 @@
 
 namespace tvs {
 
+// Dynamic shared-memory opt-in of kernel `func` for `bytes` on the CURRENT device.  The attribute
+// belongs to a device context, so the (device, func) pairs already opted in are kept in a
+// mutex-guarded table: thread-safe, and a context on a second device opts in again.
+cudaError_t smem_optin(const void *func, size_t bytes);
+// Multiprocessor count of the current device (cached per device).
+int sm_count();
+// Kernels a launcher started beyond its first (launchers that start several add k - 1 here; the
+// host driver resets it before and reads it after every launcher call to count launches exactly).
+extern thread_local int g_extra_launches;
+
 // One overlapping subdomain Gamma_m of the step grid (Omega~ for step 1, Omega for step 2).
 // S = [y0, y1] x [x0, x1]; S+ = [y0, py1] x [x0, px1] (one more row/col, clipped, reading A12);
 // T = [y0, ty1] x [x0, tx1] (S+ plus one more row/col, clipped: support of div E_{S+}).
@@ -150,6 +160,14 @@ cudaError_t launch_dual_energy2(const float *p1, const float *p2, const float *f
 // IRV2 f with the zero-mean g of the oracle (reading A3): f += alpha mean(g)  (part >= 592 doubles)
 cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, int n1,
                                     float alpha, double *part, double *shift, cudaStream_t s);
+// Primal-energy / duality-gap raw sums (see k_primal1_partial / k_primal2_partial): part needs
+// 3 (step 1) or 4 (step 2) x 592 doubles; out receives 3 or 4 doubles.
+cudaError_t launch_primal1(const float *tau, size_t plane, int ld, const float *f, const float *p,
+                           int n2, int n1, int row0, int row1, float delta, double *part,
+                           double *out, cudaStream_t s);
+cudaError_t launch_primal2(const float *d, const float *d0, const float *f, const float *dxi,
+                           const float *p1, const float *p2, int ldf, int n2, int n1, int row0,
+                           int row1, float inv_alpha, double *part, double *out, cudaStream_t s);
 cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
                           double *part, double *out, cudaStream_t s);
 
@@ -194,9 +212,6 @@ cudaError_t launch_gemm_tma_ts2(const TmaGemmDesc *descs, int batch, int maxM, i
                                 cudaStream_t s);
 cudaError_t launch_gemm_tma(const TmaGemmDesc *descs, int batch, int maxM, int maxN, int bn,
                             cudaStream_t s);
-cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,
-                               const float *qhat, int AT, int ldn, const double *rinv, float *phx,
-                               float *phy, float *phx_lo, float *phy_lo, int AP, cudaStream_t s);
 // segmented y-solve, shared-memory form (default when solve4_fits(AT)); segprod from
 // launch_segprod ([chain][2][solve_nseg(AT)][ldn] doubles), outputs plain fp32
 int solve_nseg(int AT);
@@ -210,19 +225,10 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
                                const SolveMaps *maps, int smem_rows, const int *order,
                                int nchains, int per_chain, cudaStream_t s);
 // chain-shared y-solve (one pivot block per CTA for the tiles of a layout row); needs the TMA maps
-bool solve5_fits(int AT);
-cudaError_t launch_proj_solve5(const ProjTile *tiles, int n2, int n1, int AT, int ldn,
-                               const double *segprod, float *phx, float *phy, int AP,
-                               const SolveMaps *maps, int smem_rows, const int *order, int nchains,
-                               int per_chain, cudaStream_t s);
 // segmented y-solve: fp32 z scratch [tile][AT][ldn]
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
                                cudaStream_t s);
-cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
-                              const float *qhat, int AT, int ldn, const double *rinv,
-                              double *z, float *phx, float *phy, float *phx_lo, float *phy_lo,
-                              int AP, cudaStream_t s);
 
 }  // namespace tvs

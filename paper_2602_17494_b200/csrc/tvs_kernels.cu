@@ -5,6 +5,8 @@
 #include "tvs_internal.h"
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -52,30 +54,21 @@ __device__ __forceinline__ float div_S(const float *vx, const float *vy, int li,
 }
 
 // ball update with fast MUFU square root and reciprocal (each within ~2 ulp; no slow-path
-// branches): v <- (th v + t th psi) / (th + t|psi|)
+// branches): v <- (th v + t th psi) / (th + t|psi|).  __fdividef(a, b) returns 0 for b in
+// (2^126, 2^128); with th <= 1 and t <= 1/8 that range needs |psi| > 2^129, i.e. only |psi| = inf
+// (overflow of psx^2 + psy^2) reaches it -- where IEEE division gives 0 as well.  A dual that has
+// blown up that far is written as NaN instead, so the combine's non-finite flag reports
+// TVS_ENUMERIC rather than silently resetting v to 0.
 __device__ __forceinline__ void ball_update_fast(float th, float t, float psx, float psy,
                                                  float &vx, float &vy) {
   float nrm;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(psx * psx + psy * psy));
   const float inv = __fdividef(th, th + t * nrm);
+  const bool finite = nrm <= 3.402823466e38f;   // false for inf and NaN
+  const float bad = __int_as_float(0x7fc00000);
   const float nx = (vx + t * psx) * inv, ny = (vy + t * psy) * inv;
-  vx = th > 0.f ? nx : 0.f;
-  vy = th > 0.f ? ny : 0.f;
-}
-
-// Row-wise projection of Alg. 3/5:
-// v <- (theta v + t theta psi) / (theta + t |psi|); theta = 0 -> 0 (reading A13).
-__device__ __forceinline__ void ball_update(float th, float t, float psx, float psy, float &vx,
-                                            float &vy) {
-  if (th > 0.f) {
-    float nrm = sqrtf(psx * psx + psy * psy);
-    float inv = 1.f / (th + t * nrm);
-    vx = (th * vx + t * th * psx) * inv;
-    vy = (th * vy + t * th * psy) * inv;
-  } else {
-    vx = 0.f;
-    vy = 0.f;
-  }
+  vx = th > 0.f ? (finite ? nx : bad) : 0.f;
+  vy = th > 0.f ? (finite ? ny : bad) : 0.f;
 }
 
 // ----------------------------------------------------------------------------- step data
@@ -221,123 +214,7 @@ __global__ void k_omega0_2(const SubDesc *__restrict__ subs, Geo g, const float 
   om[((size_t)blockIdx.z * g.AP + li) * g.ldP + lj] = f[(size_t)gi * ld + gj] - divp + divu;
 }
 
-// Kernel (a): one fused IRV2 dual sweep of Alg. 3 for every subdomain:
-//   u = div_{S+}(E_S v) - omega0 on S+;  psi = R_S grad_{S+} u;  v <- ball_update.
-// CTA = 32 x 8 tile of S; v (2 planes, 1-px halo) and omega0 staged through shared memory.
-constexpr int SW_TX = 32, SW_TY = 8;
-__global__ void __launch_bounds__(SW_TX *SW_TY)
-k_sweep2(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
-         const float *__restrict__ thx, const float *__restrict__ vin,
-         const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
-  __shared__ float sv1[SW_TY + 2][SW_TX + 2];
-  __shared__ float sv2[SW_TY + 2][SW_TX + 2];
-  __shared__ float su[SW_TY + 1][SW_TX + 1];
-  const SubDesc sd = subs[blockIdx.z];
-  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
-  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
-  const int r0 = blockIdx.y * SW_TY, c0 = blockIdx.x * SW_TX;
-  if (r0 >= a || c0 >= b) return;
-  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
-  const float *v2 = v1 + (size_t)g.A * g.ldS;
-  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
-  const int tid = threadIdx.y * SW_TX + threadIdx.x;
-  for (int e = tid; e < (SW_TY + 2) * (SW_TX + 2); e += SW_TX * SW_TY) {
-    int rr = e / (SW_TX + 2), cc = e % (SW_TX + 2);
-    int li = r0 - 1 + rr, lj = c0 - 1 + cc;
-    sv1[rr][cc] = vS(v1, li, lj, a, b, g.ldS);
-    sv2[rr][cc] = vS(v2, li, lj, a, b, g.ldS);
-  }
-  __syncthreads();
-  for (int e = tid; e < (SW_TY + 1) * (SW_TX + 1); e += SW_TX * SW_TY) {
-    int rr = e / (SW_TX + 1), cc = e % (SW_TX + 1);
-    int li = r0 + rr, lj = c0 + cc;
-    float u = 0.f;
-    if (li < ap && lj < bp) {
-      int gi = sd.y0 + li, gj = sd.x0 + lj;
-      float dx = (gj < n1 - 1 ? sv1[rr + 1][cc + 1] : 0.f) - sv1[rr + 1][cc];
-      float dy = (gi < n2 - 1 ? sv2[rr + 1][cc + 1] : 0.f) - sv2[rr][cc + 1];
-      u = dx + dy - __ldg(omm + (size_t)li * g.ldP + lj);
-    }
-    su[rr][cc] = u;
-  }
-  __syncthreads();
-  const int li = r0 + threadIdx.y, lj = c0 + threadIdx.x;
-  if (li >= a || lj >= b) return;
-  const int rr = threadIdx.y, cc = threadIdx.x;
-  float psx = (lj + 1 < bp) ? su[rr][cc + 1] - su[rr][cc] : 0.f;
-  float psy = (li + 1 < ap) ? su[rr + 1][cc] - su[rr][cc] : 0.f;
-  float vx = sv1[rr + 1][cc + 1], vy = sv2[rr + 1][cc + 1];
-  ball_update(theta_at(thy, thx, sd, g, li, lj), t, psx, psy, vx, vy);
-  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
-  o1[(size_t)li * g.ldS + lj] = vx;
-  o1[(size_t)g.A * g.ldS + (size_t)li * g.ldS + lj] = vy;
-}
 
-// Kernel (a), streaming form (default): each warp owns 30 output columns of S (lane 0 and lane 31
-// are halo lanes) and walks down RB rows, keeping the previous row of v_2 and the next row of u
-// in registers; x-neighbours come from warp shuffles.  Traffic per update ~= (32/30)*12 B loaded
-// (v_1, v_2, omega0) + 8 B stored, i.e. the algorithmic 20 B plus 6.7 % halo.
-constexpr int SS_OUT = 30, SS_RB = 32, SS_WARPS = 4;
-__global__ void __launch_bounds__(32 * SS_WARPS)
-k_sweep2s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
-          const float *__restrict__ thx, const float *__restrict__ vin,
-          const float *__restrict__ om, float *__restrict__ vout, int n2, int n1, float t) {
-  const SubDesc sd = subs[blockIdx.z];
-  const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
-  const int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
-  const int lane = threadIdx.x, strip = blockIdx.x * SS_WARPS + threadIdx.y;
-  const int c0 = strip * SS_OUT;
-  if (c0 >= b) return;
-  const int r0 = blockIdx.y * SS_RB;
-  if (r0 >= a) return;
-  const int r1 = min(a, r0 + SS_RB);              // output rows [r0, r1)
-  const int lj = c0 - 1 + lane;                   // local column of this lane
-  const bool inS = lj >= 0 && lj < b;
-  const bool inSp = lj >= 0 && lj < bp;
-  const bool out_lane = lane >= 1 && lane <= SS_OUT && lj < b;
-  const int gj = sd.x0 + lj;
-  const float xkeep = (gj < n1 - 1) ? 1.f : 0.f;  // global rule of D-_x at the last column
-  const float *v1 = vin + (size_t)blockIdx.z * 2 * g.A * g.ldS;
-  const float *v2 = v1 + (size_t)g.A * g.ldS;
-  const float *omm = om + (size_t)blockIdx.z * g.AP * g.ldP;
-  float *o1 = vout + (size_t)blockIdx.z * 2 * g.A * g.ldS;
-  float *o2 = o1 + (size_t)g.A * g.ldS;
-  const float thx_l = (lj >= 0 && lj < b) ? thx[sd.ix * g.B + lj] : 0.f;
-  auto ld1 = [&](int li) { return (inS && li >= 0 && li < a) ? __ldg(v1 + (size_t)li * g.ldS + lj) : 0.f; };
-  auto ld2 = [&](int li) { return (inS && li >= 0 && li < a) ? __ldg(v2 + (size_t)li * g.ldS + lj) : 0.f; };
-  auto ldo = [&](int li) { return (inSp && li < ap) ? __ldg(omm + (size_t)li * g.ldP + lj) : 0.f; };
-  // u(li) for this lane's column, given v1(li), v2(li), v2(li-1), omega0(li)
-  auto ucalc = [&](int li, float a1, float a2, float a2m, float o) {
-    const float left = __shfl_up_sync(0xffffffffu, a1, 1);
-    const float gy = (sd.y0 + li < n2 - 1) ? a2 : 0.f;
-    return (inSp && li < ap) ? (xkeep * a1 - left + gy - a2m - o) : 0.f;
-  };
-  // register ring: row li (c*), row li+1 (n*, loaded one iteration ahead), row li+2 issued at the
-  // top of each iteration so a row of loads is always in flight behind the arithmetic
-  float c1 = ld1(r0), c2 = ld2(r0);
-  const float p2 = ld2(r0 - 1), co = ldo(r0);
-  float n1v = ld1(r0 + 1), n2v = ld2(r0 + 1), no = ldo(r0 + 1);
-  float u_c = ucalc(r0, c1, c2, p2, co);
-  for (int li = r0; li < r1; ++li) {
-    const float m1 = ld1(li + 2), m2 = ld2(li + 2), mo = ldo(li + 2);
-    const float u_n = ucalc(li + 1, n1v, n2v, c2, no);
-    const float u_r = __shfl_down_sync(0xffffffffu, u_c, 1);
-    const float psx = (lj + 1 < bp) ? u_r - u_c : 0.f;
-    const float psy = (li + 1 < ap) ? u_n - u_c : 0.f;
-    if (out_lane) {
-      float vx = c1, vy = c2;
-      ball_update(thy[sd.iy * g.A + li] * thx_l, t, psx, psy, vx, vy);
-      o1[(size_t)li * g.ldS + lj] = vx;
-      o2[(size_t)li * g.ldS + lj] = vy;
-    }
-    c1 = n1v;
-    c2 = n2v;
-    u_c = u_n;
-    n1v = m1;
-    n2v = m2;
-    no = mo;
-  }
-}
 
 // Kernel (a), vectorised streaming form (default): lane l owns the column pair
 // (c0 - 2 + 2l, c0 - 1 + 2l) -> 8-byte loads/stores; a warp produces 60 output columns
@@ -867,6 +744,94 @@ __global__ void __launch_bounds__(RED_T) k_sum_partials(const double *__restrict
   block_sum_store(acc, out);
 }
 
+// Primal energies and duality gaps (SURVEY C-13, C-15), fp64 terms per pixel, fixed-order block
+// partials.  For a scalar field u with dual row q = (q_x, q_y) at pixel (i, j): grad u = (D+_x u,
+// D+_y u) with the forward difference zero at the last index (Eq. defGradDis),
+// TV term |grad u| (channel-wise TV, reading A15) and gap term |grad u| + q . grad u >= 0
+// (TV(u) = sup_{|q| <= 1} -<grad u, q>, so the gap vanishes iff q attains the sup).
+__device__ __forceinline__ void tv_gap_terms(double u, double ur, double ud, double qx, double qy,
+                                             double &tv, double &gap) {
+  const double gx = ur - u, gy = ud - u;
+  const double nrm = sqrt(gx * gx + gy * gy);
+  tv += nrm;
+  gap += nrm + qx * gx + qy * gy;
+}
+__device__ __forceinline__ void block_sum_store3(double a, double b, double c, double *out,
+                                                 int stride) {
+  block_sum_store(a, out);
+  __syncthreads();
+  block_sum_store(b, out + stride);
+  __syncthreads();
+  block_sum_store(c, out + 2 * stride);
+}
+// Step 1 (Cor. tfsdual P:245-249): over rows [row0, row1) of Omega~, per block
+//   part[0][b] = sum_k TV-terms of tau_k,  part[1][b] = sum (tau - P tau_0)^2 with P tau_0 = delta f,
+//   part[2][b] = sum_k gap-terms of (tau_k, p_k);
+// E_1 = part0 + part1 / (2 delta) is formed by the host after the sums (and the ranks' all-reduce).
+__global__ void __launch_bounds__(RED_T)
+k_primal1_partial(const float *__restrict__ tau, size_t plane, int ld, const float *__restrict__ f,
+                  const float *__restrict__ p, int n2, int n1, int row0, int row1, float delta,
+                  double *__restrict__ part) {
+  double tv = 0.0, fit = 0.0, gap = 0.0;
+  const long long total = (long long)(row1 - row0) * n1;
+  for (long long e = (long long)blockIdx.x * RED_T + threadIdx.x; e < total;
+       e += (long long)gridDim.x * RED_T) {
+    const int i = row0 + (int)(e / n1), j = (int)(e % n1);
+    const size_t o = (size_t)i * ld + j;
+    for (int k = 0; k < 2; ++k) {
+      const float *t = tau + k * plane;
+      const double u = t[o];
+      const double ur = j < n1 - 1 ? (double)t[o + 1] : u;
+      const double ud = i < n2 - 1 ? (double)t[o + ld] : u;
+      tv_gap_terms(u, ur, ud, p[2 * k * plane + o], p[(2 * k + 1) * plane + o], tv, gap);
+      const double r = u - (double)delta * (double)f[k * plane + o];
+      fit += r * r;
+    }
+  }
+  block_sum_store3(tv, fit, gap, part + blockIdx.x, gridDim.x);
+}
+// Step 2 over rows [row0, row1) of Omega: u = d - g (IRV2, Eq. modifiedStep2; with
+// f = alpha (d_0 - g): g = d_0 - f / alpha) or u = d (IRV1, Eq. IRPXi, dxi != null);
+//   part[0][b] = TV-terms of u, part[1][b] = sum (d - d_0)^2, part[2][b] = gap-terms of (u, p),
+//   part[3][b] = sum d * div xi (IRV1; 0 for IRV2).
+// E_2 = part0 + alpha/2 part1 (+ part3 for IRV1), formed by the host.
+__global__ void __launch_bounds__(RED_T)
+k_primal2_partial(const float *__restrict__ d, const float *__restrict__ d0,
+                  const float *__restrict__ f, const float *__restrict__ dxi,
+                  const float *__restrict__ p1, const float *__restrict__ p2, int ldf, int n2,
+                  int n1, int row0, int row1, float inv_alpha, double *__restrict__ part) {
+  double tv = 0.0, fit = 0.0, gap = 0.0, cross = 0.0;
+  const long long total = (long long)(row1 - row0) * n1;
+  auto U = [&](int i, int j) -> double {
+    const size_t e = (size_t)i * n1 + j;
+    if (dxi) return (double)d[e];
+    return (double)d[e] - (double)d0[e] + (double)f[(size_t)i * ldf + j] * (double)inv_alpha;
+  };
+  for (long long e = (long long)blockIdx.x * RED_T + threadIdx.x; e < total;
+       e += (long long)gridDim.x * RED_T) {
+    const int i = row0 + (int)(e / n1), j = (int)(e % n1);
+    const size_t o = (size_t)i * ldf + j, od = (size_t)i * n1 + j;
+    const double u = U(i, j);
+    const double ur = j < n1 - 1 ? U(i, j + 1) : u;
+    const double ud = i < n2 - 1 ? U(i + 1, j) : u;
+    tv_gap_terms(u, ur, ud, p1[o], p2[o], tv, gap);
+    const double r = (double)d[od] - (double)d0[od];
+    fit += r * r;
+    if (dxi) cross += (double)d[od] * (double)dxi[o];
+  }
+  block_sum_store3(tv, fit, gap, part + blockIdx.x, gridDim.x);
+  __syncthreads();
+  block_sum_store(cross, part + 3 * gridDim.x + blockIdx.x);
+}
+// out[q] = sum of part[q][0..n) in a fixed order, one block per quantity q.
+__global__ void __launch_bounds__(RED_T) k_sum_partials_multi(const double *__restrict__ part, int n,
+                                                              double *__restrict__ out) {
+  const double *pq = part + (size_t)blockIdx.x * n;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += RED_T) acc += pq[i];
+  block_sum_store(acc, out + blockIdx.x);
+}
+
 // ----------------------------------------------------------------------------- step 1 (TFS)
 
 // w = multidiv p: w_k = div(p_k1, p_k2); p has 4 planes [p11 p12 p21 p22].
@@ -937,23 +902,6 @@ __device__ __forceinline__ float w_S(const float *vb, int k, int li, int lj, int
   return div_S(vx, vy, li, lj, gi, gj, a, b, g.ldS, n2, n1);
 }
 
-__global__ void k_prediv1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
-                          int n2, int n1, float *__restrict__ q, float *__restrict__ qlo) {
-  const SubDesc sd = subs[blockIdx.z];
-  int lj = blockIdx.x * blockDim.x + threadIdx.x;
-  int li = blockIdx.y * blockDim.y + threadIdx.y;
-  int gi = sd.y0 + li, gj = sd.x0 + lj;
-  if (gi > sd.ty1 || gj > sd.tx1) return;
-  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
-  const float *vb = v + (size_t)blockIdx.z * 4 * g.A * g.ldS;
-  float dv = (gj < n1 - 1 ? w_S(vb, 0, li, lj, gi, gj, a, b, g, n2, n1) : 0.f) -
-             (gj > 0 ? w_S(vb, 0, li, lj - 1, gi, gj - 1, a, b, g, n2, n1) : 0.f) +
-             (gi < n2 - 1 ? w_S(vb, 1, li, lj, gi, gj, a, b, g, n2, n1) : 0.f) -
-             (gi > 0 ? w_S(vb, 1, li - 1, lj, gi - 1, gj, a, b, g, n2, n1) : 0.f);
-  // column offset x0 & 3 keeps the forward GEMM's DCT-table rows 16-byte aligned (the leading
-  // columns stay zero)
-  store_split(q, qlo, ((size_t)blockIdx.z * g.AT + li) * g.ldT + lj + (sd.x0 & 3), dv);
-}
 
 // omega0_loc = R_{S+} r^n + (R_{S+} P E_{S+}) multidiv_{S+} E_S (theta_m p^n)  (Alg. 5, P:1740;
 // r^n = f - P multidiv p^n is the global part, reading A11), with P w = w - grad phi.
@@ -976,39 +924,6 @@ __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float 
   }
 }
 
-// Kernel (a'): fused TFS dual sweep of Alg. 5:
-//   rho_k = (w_k - grad phi_k) - omega0_k on S+ with w = multidiv E_S v (recomputed),
-//   psi_k = R_S grad_{S+} rho_k,  v_k <- ball_update (row-wise, k = 1, 2).
-__global__ void k_sweep1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
-                         const float *__restrict__ thx, const float *__restrict__ vin,
-                         const float *__restrict__ gphi, int ldg, const float *__restrict__ om,
-                         float *__restrict__ vout, int n2, int n1, float t) {
-  const SubDesc sd = subs[blockIdx.z];
-  int lj = blockIdx.x * blockDim.x + threadIdx.x;
-  int li = blockIdx.y * blockDim.y + threadIdx.y;
-  int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
-  if (li >= a || lj >= b) return;
-  int ap = sd.py1 - sd.y0 + 1, bp = sd.px1 - sd.x0 + 1;
-  const float *vb = vin + (size_t)blockIdx.z * 4 * g.A * g.ldS;
-  float *ob = vout + (size_t)blockIdx.z * 4 * g.A * g.ldS;
-  float th = theta_at(thy, thx, sd, g, li, lj);
-  for (int k = 0; k < 2; ++k) {
-    const float *gk = gphi + ((size_t)k * g.M + blockIdx.z) * g.AP * ldg;
-    const float *ok = om + ((size_t)blockIdx.z * 2 + k) * g.AP * g.ldP;
-    auto rho = [&](int i, int j) {
-      return w_S(vb, k, i, j, sd.y0 + i, sd.x0 + j, a, b, g, n2, n1) -
-             __ldg(gk + (size_t)i * ldg + j) - __ldg(ok + (size_t)i * g.ldP + j);
-    };
-    float r0 = rho(li, lj);
-    float psx = (lj + 1 < bp) ? rho(li, lj + 1) - r0 : 0.f;
-    float psy = (li + 1 < ap) ? rho(li + 1, lj) - r0 : 0.f;
-    float vx = vb[(size_t)(2 * k) * g.A * g.ldS + (size_t)li * g.ldS + lj];
-    float vy = vb[(size_t)(2 * k + 1) * g.A * g.ldS + (size_t)li * g.ldS + lj];
-    ball_update(th, t, psx, psy, vx, vy);
-    ob[(size_t)(2 * k) * g.A * g.ldS + (size_t)li * g.ldS + lj] = vx;
-    ob[(size_t)(2 * k + 1) * g.A * g.ldS + (size_t)li * g.ldS + lj] = vy;
-  }
-}
 
 // Streaming forms of the step-1 stencils (default): lane l owns the column pair
 // (c0 - 2 + 2l, c0 - 1 + 2l) of the subdomain-local grid, lanes 1..30 produce 60 output
@@ -1275,203 +1190,7 @@ __global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restri
   }
 }
 
-// Per-frequency y-solves (fp64), one thread per (tile, j).  Input: raw partial x-DCT
-// qhat[k][j] = sum_x q[k][x] cos(pi j (2x+1)/(2 n1)).  Output on the rows of S+:
-//   phx[k][j] = -s_j^2 sigma_j u_k,  phy[k][j] = s_j^2 (u_{k+1} - u_k)  (0 on the global last
-// row), with s_j = sqrt(2/n1) w_j the DCT normalisation (Eq. form:DCTmat).
-__global__ void __launch_bounds__(128, 8)
-k_proj_solve(const ProjTile *__restrict__ tiles, int n2, int n1,
-                             const float *__restrict__ qhat, int AT, int ldn,
-                             const double *__restrict__ rinv, double *__restrict__ z,
-                             float *__restrict__ phx, float *__restrict__ phy,
-                             float *__restrict__ phx_lo, float *__restrict__ phy_lo, int AP) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int tix = blockIdx.y;
-  if (j >= n1) return;
-  const ProjTile tl = tiles[tix];
-  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1;
-  const int po = tl.po;   // output rows are [po, nout) relative to ty0, stored from row 0
-  const float *__restrict__ b = qhat + (size_t)tix * AT * ldn + j;
-  const size_t obase = (size_t)tix * AP * ldn + j - (size_t)po * ldn;
-  float *__restrict__ ox = phx + obase;
-  float *__restrict__ oy = phy + obase;
-  float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
-  float *__restrict__ oyl = phy_lo ? phy_lo + obase : nullptr;
-  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;          // s_j^2
-  if (j == 0) {
-    // L_y^dagger b: D+_y u = w, w_y = sum_{l<=y} b_l - mu (y+1), mu = mean of b over n2 rows.
-    double tot = 0.0;
-    for (int k = 0; k < nt; ++k) tot += (double)b[(size_t)k * ldn];
-    double mu = tot / (double)n2, pre = 0.0;
-    for (int k = 0; k < nout; ++k) {
-      pre += (double)b[(size_t)k * ldn];
-      int y = tl.ty0 + k;
-      double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
-      if (k >= po) {
-        store_split(ox, oxl, (size_t)k * ldn, 0.0);
-        store_split(oy, oyl, (size_t)k * ldn, s2 * w);
-      }
-    }
-    return;
-  }
-  const double sg = 2.0 * sinpi((double)j / (2.0 * n1));
-  const double cx = -s2 * sg;
-  const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * ldn + j;
-  double *__restrict__ zz = z + (size_t)tix * AT * ldn + j;
-  const float *__restrict__ bb = b;
-  // forward substitution z_k = b_k - z_{k-1} r_{k-1}; loads batched U rows ahead so the only
-  // serial dependence is one DFMA per row (pointers are __restrict__, so they can be hoisted)
-  constexpr int U = 4;
-  double zp = (double)bb[0];
-  zz[0] = zp;
-  int k = 1;
-  for (; k + U <= nt; k += U) {
-    float bv[U];
-    double rv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      bv[u] = bb[(size_t)(k + u) * ldn];
-      rv[u] = ri[(size_t)(k + u - 1) * ldn];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      zp = fma(-zp, rv[u], (double)bv[u]);
-      zz[(size_t)(k + u) * ldn] = zp;
-    }
-  }
-  for (; k < nt; ++k) {
-    zp = fma(-zp, ri[(size_t)(k - 1) * ldn], (double)bb[(size_t)k * ldn]);
-    zz[(size_t)k * ldn] = zp;
-  }
-  double u = zp * ri[(size_t)(nt - 1) * ldn];
-  if (nt - 1 < nout && nt - 1 >= po) {       // T = S+ in y: global last row, D+_y = 0
-    store_split(ox, oxl, (size_t)(nt - 1) * ldn, cx * u);
-    store_split(oy, oyl, (size_t)(nt - 1) * ldn, 0.0);
-  }
-  // back substitution u_k = (z_k - u_{k+1}) r_k, k = nt-2 .. 0, batched the same way
-  k = nt - 2;
-  for (; k - U + 1 >= 0; k -= U) {
-    double zv[U], rv[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      zv[q] = zz[(size_t)(k - q) * ldn];
-      rv[q] = ri[(size_t)(k - q) * ldn];
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const double uk = (zv[q] - u) * rv[q];
-      if (k - q < nout && k - q >= po) {
-        store_split(ox, oxl, (size_t)(k - q) * ldn, cx * uk);
-        store_split(oy, oyl, (size_t)(k - q) * ldn, s2 * (u - uk));
-      }
-      u = uk;
-    }
-  }
-  for (; k >= 0; --k) {
-    const double uk = (zz[(size_t)k * ldn] - u) * ri[(size_t)k * ldn];
-    if (k < nout && k >= po) {
-      store_split(ox, oxl, (size_t)k * ldn, cx * uk);
-      store_split(oy, oyl, (size_t)k * ldn, s2 * (u - uk));
-    }
-    u = uk;
-  }
-}
 
-// Chunked form of the per-frequency y-solve (default): no global fp64 scratch.  The forward
-// substitution keeps z only at chunk boundaries (every SC rows, in shared memory); the backward
-// substitution recomputes each chunk's z (and caches its pivots) in shared memory from the
-// checkpoint, then back-substitutes it.  Global traffic per (row, frequency): qhat 2 x 4 B,
-// pivots 2 x 8 B (L2-resident, shared by the tiles of a layout row), outputs 16 B.
-constexpr int SC = 32;
-__global__ void k_proj_solve2(const ProjTile *__restrict__ tiles, int n2, int n1,
-                              const float *__restrict__ qhat, int AT, int ldn,
-                              const double *__restrict__ rinv, float *__restrict__ phx,
-                              float *__restrict__ phy, float *__restrict__ phx_lo,
-                              float *__restrict__ phy_lo, int AP, int nch) {
-  extern __shared__ double sm_solve[];
-  const int nth = blockDim.x, tid = threadIdx.x;
-  double *ck = sm_solve;                       // [nch][nth]: z_{cSC-1}
-  double *zc = ck + (size_t)nch * nth;         // [SC][nth]
-  double *rc = zc + (size_t)SC * nth;          // [SC][nth]
-  const int j = blockIdx.x * nth + tid;
-  const int tix = blockIdx.y;
-  if (j >= n1) return;
-  const ProjTile tl = tiles[tix];
-  const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
-  const float *__restrict__ b = qhat + (size_t)tix * AT * ldn + j;
-  const size_t obase = (size_t)tix * AP * ldn + j - (size_t)po * ldn;
-  float *__restrict__ ox = phx + obase;
-  float *__restrict__ oy = phy + obase;
-  float *__restrict__ oxl = phx_lo ? phx_lo + obase : nullptr;
-  float *__restrict__ oyl = phy_lo ? phy_lo + obase : nullptr;
-  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
-  if (j == 0) {   // L_y^dagger: D+_y u = prefix(b) - mu (y + 1)
-    double tot = 0.0;
-    for (int k = 0; k < nt; ++k) tot += (double)b[(size_t)k * ldn];
-    double mu = tot / (double)n2, pre = 0.0;
-    for (int k = 0; k < nout; ++k) {
-      pre += (double)b[(size_t)k * ldn];
-      const int y = tl.ty0 + k;
-      const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
-      if (k >= po) {
-        store_split(ox, oxl, (size_t)k * ldn, 0.0);
-        store_split(oy, oyl, (size_t)k * ldn, s2 * w);
-      }
-    }
-    return;
-  }
-  const double sg = 2.0 * sinpi((double)j / (2.0 * n1));
-  const double cx = -s2 * sg;
-  const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * ldn + j;
-  // forward sweep: checkpoints ck[c] = z_{c*SC - 1}
-  constexpr int U = 8;
-  double zp = (double)b[0];
-  int k = 1;
-  for (; k + U <= nt; k += U) {
-    float bv[U];
-    double rv[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      bv[q] = b[(size_t)(k + q) * ldn];
-      rv[q] = ri[(size_t)(k + q - 1) * ldn];
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      if ((k + q) % SC == 0) ck[(size_t)((k + q) / SC) * nth + tid] = zp;
-      zp = fma(-zp, rv[q], (double)bv[q]);
-    }
-  }
-  for (; k < nt; ++k) {
-    if (k % SC == 0) ck[(size_t)(k / SC) * nth + tid] = zp;
-    zp = fma(-zp, ri[(size_t)(k - 1) * ldn], (double)b[(size_t)k * ldn]);
-  }
-  // backward sweep, chunk by chunk from the bottom
-  double u_next = 0.0;
-  for (int c = (nt - 1) / SC; c >= 0; --c) {
-    const int k0 = c * SC, k1 = min(nt, k0 + SC);
-    double zprev = (c == 0) ? 0.0 : ck[(size_t)c * nth + tid];
-    double rprev = (c == 0) ? 0.0 : ri[(size_t)(k0 - 1) * ldn];
-#pragma unroll 8
-    for (int kk = k0; kk < k1; ++kk) {
-      const double r = ri[(size_t)kk * ldn];
-      const double z = fma(-zprev, rprev, (double)b[(size_t)kk * ldn]);
-      zc[(size_t)(kk - k0) * nth + tid] = z;
-      rc[(size_t)(kk - k0) * nth + tid] = r;
-      zprev = z;
-      rprev = r;
-    }
-    for (int kk = k1 - 1; kk >= k0; --kk) {
-      const double z = zc[(size_t)(kk - k0) * nth + tid], r = rc[(size_t)(kk - k0) * nth + tid];
-      const double u = (kk == nt - 1) ? z * r : (z - u_next) * r;
-      if (kk >= po && kk < nout) {
-        store_split(ox, oxl, (size_t)kk * ldn, cx * u);
-        // D+_y u = u_{k+1} - u_k; 0 on the global last row (T = S+ in y there)
-        store_split(oy, oyl, (size_t)kk * ldn, (kk == nt - 1) ? 0.0 : s2 * (u_next - u));
-      }
-      u_next = u;
-    }
-  }
-}
 
 // Segmented form of the per-frequency y-solve (default).  Both Thomas sweeps are first-order
 // linear recurrences in the precomputed pivots r_k = 1/e_k:
@@ -2002,218 +1721,6 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t ph) {
       "@!P1 bra W_%=;\n\t}" ::"r"(bar), "r"(ph) : "memory");
 }
 
-__global__ void __launch_bounds__(SJB * 2 * SSEG_MAX)
-k_proj_solve5(const ProjTile *__restrict__ tiles, int n2, int n1, int AT, int ldn,
-              const double *__restrict__ segprod, float *__restrict__ phx, float *__restrict__ phy,
-              int AP, const SolveMaps *__restrict__ maps, int srows, const int *__restrict__ order,
-              int per_chain) {
-  __shared__ double sh_a[2][SSEG_MAX][SJB], sh_c[2][SSEG_MAX][SJB];
-  __shared__ double sh_tot[2][SJB];
-  __shared__ uint64_t sbar[2];
-  extern __shared__ __align__(128) double sr5[];   // [srows][SJB] pivots, then 2 x [srows][SJB] floats
-  const int nseg = blockDim.y / 2;
-  const int tx = threadIdx.x, gq = threadIdx.y / nseg, sg = threadIdx.y % nseg;
-  const int gthr = SJB * nseg;
-  const int jb = blockIdx.x, chain = blockIdx.y;
-  const int j = jb * SJB + tx;
-  const bool valid = j < n1;
-  const int jj = valid ? j : 0;
-  const int lt = threadIdx.y * SJB + tx;
-  const int br = maps->box_rows, nb = maps->nbox;
-  float *sbq = reinterpret_cast<float *>(sr5 + (size_t)srows * SJB) + (size_t)gq * srows * SJB;
-  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
-  const uint32_t bar1 = (uint32_t)__cvta_generic_to_shared(&sbar[1]);
-  if (lt == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  __syncthreads();
-  const int col = jb * SJB;
-  if (lt == 0) {   // the chain's pivot block, once
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar0),
-                 "r"((uint32_t)(nb * br * SJB * sizeof(double))) : "memory");
-    for (int bi = 0; bi < nb; ++bi)
-      tma2d((uint32_t)__cvta_generic_to_shared(sr5 + (size_t)bi * br * SJB), &maps->r, col,
-            chain * AT + bi * br, bar0);
-  }
-  const double *ri = sr5 + tx;
-  float *sbt = sbq + tx;
-  const double *__restrict__ gp = segprod + (size_t)chain * 2 * nseg * ldn + jj;
-  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;
-  const int npairs = (per_chain + 1) / 2;
-  for (int pr = 0; pr < npairs; ++pr) {
-    // Q-hat blocks of this pair's two tiles (group 0: tile 2 pr, group 1: tile 2 pr + 1)
-    if (lt == 0) {
-      uint32_t bytes = 0;
-      for (int g = 0; g < 2; ++g)
-        if (2 * pr + g < per_chain && order[chain * per_chain + 2 * pr + g] >= 0)
-          bytes += (uint32_t)(nb * br * SJB * sizeof(float));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar1), "r"(bytes) : "memory");
-      for (int g = 0; g < 2; ++g) {
-        if (2 * pr + g >= per_chain) continue;
-        const int t = order[chain * per_chain + 2 * pr + g];
-        if (t < 0) continue;
-        float *dstb = reinterpret_cast<float *>(sr5 + (size_t)srows * SJB) + (size_t)g * srows * SJB;
-        for (int bi = 0; bi < nb; ++bi)
-          tma2d((uint32_t)__cvta_generic_to_shared(dstb + (size_t)bi * br * SJB), &maps->q, col,
-                t * AT + bi * br, bar1);
-      }
-    }
-    if (pr == 0) mbar_wait_parity(bar0, 0);
-    mbar_wait_parity(bar1, pr & 1);
-    const int slot = 2 * pr + gq;
-    const int tix = slot < per_chain ? order[chain * per_chain + slot] : -1;
-    if (tix >= 0) {
-      const ProjTile tl = tiles[tix];
-      const int nt = tl.ty1 - tl.ty0 + 1, nout = tl.py1 - tl.ty0 + 1, po = tl.po;
-      const int LS = (nt + nseg - 1) / nseg;
-      const int k0 = min(nt, sg * LS), k1 = min(nt, k0 + LS);
-      // ---- forward, local pass
-      double a = 0.0;
-      if (valid) {
-        if (j == 0) {
-          for (int k = k0; k < k1; ++k) a += (double)sbt[k * SJB];
-        } else {
-          int k = k0;
-          if (k == 0 && k < k1) {
-            a = (double)sbt[0];
-            k = 1;
-          }
-          for (; k + SU <= k1; k += SU) {
-            float bv[SU];
-            double rv[SU];
-#pragma unroll
-            for (int u = 0; u < SU; ++u) {
-              bv[u] = sbt[(k + u) * SJB];
-              rv[u] = ri[(k + u - 1) * SJB];
-            }
-#pragma unroll
-            for (int u = 0; u < SU; ++u) a = fma(-rv[u], a, (double)bv[u]);
-          }
-          for (; k < k1; ++k) a = fma(-ri[(k - 1) * SJB], a, (double)sbt[k * SJB]);
-        }
-      }
-      sh_a[gq][sg][tx] = a;
-      sh_c[gq][sg][tx] = (valid && j > 0) ? gp[sg * ldn] : 1.0;
-      group_sync(gq, gthr);
-      if (sg == 0) {
-        double Z = 0.0;
-        for (int q = 0; q < nseg; ++q) {
-          const double as = sh_a[gq][q][tx], gs = sh_c[gq][q][tx];
-          sh_c[gq][q][tx] = Z;
-          Z = fma(gs, Z, as);
-        }
-        sh_tot[gq][tx] = Z;
-      }
-      group_sync(gq, gthr);
-      const double fcarry = sh_c[gq][sg][tx];
-      // ---- forward, final pass (z overwrites b)
-      if (valid && j > 0 && k0 < k1) {
-        double zc = fcarry;
-        int k = k0;
-        if (k == 0) {
-          zc = (double)sbt[0];
-          k = 1;
-        }
-        for (; k + SU <= k1; k += SU) {
-          float bv[SU];
-          double rv[SU];
-#pragma unroll
-          for (int u = 0; u < SU; ++u) {
-            bv[u] = sbt[(k + u) * SJB];
-            rv[u] = ri[(k + u - 1) * SJB];
-          }
-#pragma unroll
-          for (int u = 0; u < SU; ++u) {
-            zc = fma(-rv[u], zc, (double)bv[u]);
-            sbt[(k + u) * SJB] = (float)zc;
-          }
-        }
-        for (; k < k1; ++k) {
-          zc = fma(-ri[(k - 1) * SJB], zc, (double)sbt[k * SJB]);
-          sbt[k * SJB] = (float)zc;
-        }
-      }
-      // ---- backward, local pass
-      a = 0.0;
-      if (valid && j > 0 && k0 < k1) {
-        int k = k1 - 1;
-        for (; k - SU + 1 >= k0; k -= SU) {
-          float zv[SU];
-          double rv[SU];
-#pragma unroll
-          for (int u = 0; u < SU; ++u) {
-            zv[u] = sbt[(k - u) * SJB];
-            rv[u] = ri[(k - u) * SJB];
-          }
-#pragma unroll
-          for (int u = 0; u < SU; ++u) a = rv[u] * ((double)zv[u] - a);
-        }
-        for (; k >= k0; --k) a = ri[k * SJB] * ((double)sbt[k * SJB] - a);
-      }
-      group_sync(gq, gthr);
-      sh_a[gq][sg][tx] = a;
-      sh_c[gq][sg][tx] = (valid && j > 0) ? gp[(nseg + sg) * ldn] : 1.0;
-      group_sync(gq, gthr);
-      if (sg == 0) {
-        double U = 0.0;
-        for (int q = nseg - 1; q >= 0; --q) {
-          const double as = sh_a[gq][q][tx], gs = sh_c[gq][q][tx];
-          sh_c[gq][q][tx] = U;
-          U = fma(gs, U, as);
-        }
-      }
-      group_sync(gq, gthr);
-      if (valid && k0 < k1) {
-        float *__restrict__ ox = phx + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
-        float *__restrict__ oy = phy + (size_t)tix * AP * ldn + jj - (size_t)po * ldn;
-        if (j == 0) {
-          const double mu = sh_tot[gq][tx] / (double)n2;
-          double pre = fcarry;
-          for (int k = k0; k < min(k1, nout); ++k) {
-            pre += (double)sbt[k * SJB];
-            const int y = tl.ty0 + k;
-            const double w = (y == n2 - 1) ? 0.0 : pre - mu * (double)(y + 1);
-            if (k >= po) {
-              ox[(size_t)k * ldn] = 0.f;
-              oy[(size_t)k * ldn] = (float)(s2 * w);
-            }
-          }
-        } else {
-          const double cx = -s2 * 2.0 * sinpi((double)j / (2.0 * n1));
-          double un = sh_c[gq][sg][tx];
-          const int klo = max(k0, po), khi = min(k1, nout);
-          int k = k1 - 1;
-          for (; k >= khi && k >= k0; --k) un = ri[k * SJB] * ((double)sbt[k * SJB] - un);
-          for (; k - SU + 1 >= klo; k -= SU) {
-            float zv[SU];
-            double rv[SU];
-#pragma unroll
-            for (int u = 0; u < SU; ++u) {
-              zv[u] = sbt[(k - u) * SJB];
-              rv[u] = ri[(k - u) * SJB];
-            }
-#pragma unroll
-            for (int u = 0; u < SU; ++u) {
-              const double uk = rv[u] * ((double)zv[u] - un);
-              ox[(size_t)(k - u) * ldn] = (float)(cx * uk);
-              oy[(size_t)(k - u) * ldn] = (k - u == nt - 1) ? 0.f : (float)(s2 * (un - uk));
-              un = uk;
-            }
-          }
-          for (; k >= klo; --k) {
-            const double uk = ri[k * SJB] * ((double)sbt[k * SJB] - un);
-            ox[(size_t)k * ldn] = (float)(cx * uk);
-            oy[(size_t)k * ldn] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
-            un = uk;
-          }
-        }
-      }
-    }
-    __syncthreads();   // both groups done with their Q-hat buffers before the next pair lands
-  }
-}
 
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
@@ -2291,6 +1798,36 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmDesc *__restrict__ descs
 
 // ----------------------------------------------------------------------------- launchers
 
+thread_local int g_extra_launches = 0;
+
+cudaError_t smem_optin(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> done;   // (device, kernel) -> bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &have = done[std::make_pair(dev, func)];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+int sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  cache[dev] = n;
+  return n;
+}
+
 static inline dim3 grid2(int nx, int ny, int bx, int by, int z = 1) {
   return dim3((nx + bx - 1) / bx, (ny + by - 1) / by, z);
 }
@@ -2313,6 +1850,7 @@ cudaError_t launch_irv2_f(const float *tau1, int ldt, const double *g_row0, cons
   }
   const int nch = (n2 + IRV2_ROWS - 1) / IRV2_ROWS;
   const dim3 grid((n1 + 127) / 128, nch);
+  g_extra_launches += 1;
   k_irv2_chunk_sums<<<grid, 128, 0, s>>>(tau1, ldt, n2, n1, csum);
   k_irv2_f_chunked<<<grid, 128, 0, s>>>(tau1, ldt, g_row0, d0, n2, n1, alpha, f, ldf, csum);
   return cudaGetLastError();
@@ -2347,28 +1885,13 @@ cudaError_t launch_sweep2x2(const SubDesc *subs, Geo g, const float *thy, const 
                             float t, cudaStream_t s) {
   const int strips = (g.B + SQ_OUT - 1) / SQ_OUT;
   dim3 grid((strips + SQ_WARPS - 1) / SQ_WARPS, (g.A + SQ_RB - 1) / SQ_RB, g.M);
-  static const int minb = getenv("TVS_X2_MINB") ? atoi(getenv("TVS_X2_MINB")) : 4;
-  if (minb >= 8)
-    k_sweep2q2<8><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
-  else if (minb >= 6)
-    k_sweep2q2<6><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
-  else
-    k_sweep2q2<4><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
+  k_sweep2q2<4><<<grid, dim3(32, SQ_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
   return cudaGetLastError();
 }
 cudaError_t launch_sweep2(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *om, float *vout, int n2, int n1, float t,
                           cudaStream_t s) {
-  static const bool tiled = getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "tiled") == 0;
-  if (tiled) {
-    k_sweep2<<<grid2(g.B, g.A, SW_TX, SW_TY, g.M), dim3(SW_TX, SW_TY), 0, s>>>(
-        subs, g, thy, thx, vin, om, vout, n2, n1, t);
-  } else if (getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "scalar") == 0) {
-    const int strips = (g.B + SS_OUT - 1) / SS_OUT;
-    dim3 grid((strips + SS_WARPS - 1) / SS_WARPS, (g.A + SS_RB - 1) / SS_RB, g.M);
-    k_sweep2s<<<grid, dim3(32, SS_WARPS), 0, s>>>(subs, g, thy, thx, vin, om, vout, n2, n1, t);
-  } else if ((getenv("TVS_SWEEP2") && strcmp(getenv("TVS_SWEEP2"), "pair") == 0) ||
-             (!getenv("TVS_SWEEP2") && g.B < 512)) {
+  if (g.B < 512) {
     // narrow subdomains (L2-resident regime): the 2-column form keeps more warps in flight
     const int strips = (g.B + SV_OUT - 1) / SV_OUT, rb = stencil_rb(g.A, g.M, strips);
     dim3 grid((strips + SV_WARPS - 1) / SV_WARPS, (g.A + rb - 1) / rb, g.M);
@@ -2418,12 +1941,14 @@ constexpr int RED_BLOCKS = 592;   // 4 x 148 SMs
 cudaError_t launch_dual_energy2(const float *p1, const float *p2, const float *f, int ld, int n2,
                                 int n1, int row0, int row1, double *part, double *out,
                                 cudaStream_t s) {
+  g_extra_launches += 1;
   k_dual2_partial<<<RED_BLOCKS, RED_T, 0, s>>>(p1, p2, f, ld, n2, n1, row0, row1, part);
   k_sum_partials<<<1, RED_T, 0, s>>>(part, RED_BLOCKS, out);
   return cudaGetLastError();
 }
 cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, int n1,
                                     float alpha, double *part, double *shift, cudaStream_t s) {
+  g_extra_launches += 2;
   k_sum_fd_partial<<<RED_BLOCKS / 2, RED_T, 0, s>>>(f, ldf, d0, n2, n1, part);
   k_fd_shift<<<1, 32, 0, s>>>(part, RED_BLOCKS / 2, (double)alpha, (double)n2 * n1, shift);
   k_add_shift<<<grid2(n1, n2, 32, 8), dim3(32, 8), 0, s>>>(f, ldf, n2, n1, shift);
@@ -2431,8 +1956,27 @@ cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, 
 }
 cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
                           double *part, double *out, cudaStream_t s) {
+  g_extra_launches += 1;
   k_sumsq2_partial<<<RED_BLOCKS, RED_T, 0, s>>>(r, plane, ld, n1, row0, row1, part);
   k_sum_partials<<<1, RED_T, 0, s>>>(part, RED_BLOCKS, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_primal1(const float *tau, size_t plane, int ld, const float *f, const float *p,
+                           int n2, int n1, int row0, int row1, float delta, double *part,
+                           double *out, cudaStream_t s) {
+  g_extra_launches += 1;
+  k_primal1_partial<<<RED_BLOCKS, RED_T, 0, s>>>(tau, plane, ld, f, p, n2, n1, row0, row1, delta,
+                                                 part);
+  k_sum_partials_multi<<<3, RED_T, 0, s>>>(part, RED_BLOCKS, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_primal2(const float *d, const float *d0, const float *f, const float *dxi,
+                           const float *p1, const float *p2, int ldf, int n2, int n1, int row0,
+                           int row1, float inv_alpha, double *part, double *out, cudaStream_t s) {
+  g_extra_launches += 1;
+  k_primal2_partial<<<RED_BLOCKS, RED_T, 0, s>>>(d, d0, f, dxi, p1, p2, ldf, n2, n1, row0, row1,
+                                                 inv_alpha, part);
+  k_sum_partials_multi<<<4, RED_T, 0, s>>>(part, RED_BLOCKS, out);
   return cudaGetLastError();
 }
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,
@@ -2464,14 +2008,9 @@ cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const f
 }
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
                            float *qlo, cudaStream_t s) {
-  static const bool naive = getenv("TVS_STENCIL1") && strcmp(getenv("TVS_STENCIL1"), "naive") == 0;
-  if (naive) {
-    k_prediv1<<<grid2(g.BT, g.AT, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, v, n2, n1, q, qlo);
-  } else {
-    const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M, strips);
-    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + rb - 1) / rb, g.M);
-    k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo, rb);
-  }
+  const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M, strips);
+  dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + rb - 1) / rb, g.M);
+  k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo, rb);
   return cudaGetLastError();
 }
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
@@ -2484,16 +2023,10 @@ cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, 
 cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *gphi, int ldg, const float *om,
                           float *vout, int n2, int n1, float t, cudaStream_t s) {
-  static const bool naive = getenv("TVS_STENCIL1") && strcmp(getenv("TVS_STENCIL1"), "naive") == 0;
-  if (naive) {
-    k_sweep1<<<grid2(g.B, g.A, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, thy, thx, vin, gphi,
-                                                                 ldg, om, vout, n2, n1, t);
-  } else {
-    const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M, strips);
-    dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + rb - 1) / rb, g.M);
-    k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
-                                                  n2, n1, t, rb);
-  }
+  const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M, strips);
+  dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + rb - 1) / rb, g.M);
+  k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout, n2, n1,
+                                                t, rb);
   return cudaGetLastError();
 }
 cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,
@@ -2509,23 +2042,6 @@ cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, 
 }
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s) {
   k_gemm<<<dim3((maxN + GBN - 1) / GBN, (maxM + GBM - 1) / GBM, batch), 256, 0, s>>>(descs);
-  return cudaGetLastError();
-}
-cudaError_t launch_proj_solve2(const ProjTile *tiles, int ntiles, int n2, int n1,
-                               const float *qhat, int AT, int ldn, const double *rinv, float *phx,
-                               float *phy, float *phx_lo, float *phy_lo, int AP, cudaStream_t s) {
-  const int nth = ntiles >= 16 ? 64 : 32;
-  const int nch = (AT + SC - 1) / SC;
-  const size_t smem = (size_t)(nch + 2 * SC) * nth * sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_proj_solve2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  k_proj_solve2<<<dim3((n1 + nth - 1) / nth, ntiles), nth, smem, s>>>(
-      tiles, n2, n1, qhat, AT, ldn, rinv, phx, phy, phx_lo, phy_lo, AP, nch);
   return cudaGetLastError();
 }
 int solve_nseg(int AT) {
@@ -2555,14 +2071,10 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   const int nseg = solve_nseg(AT), J = solve_j(AT);
   const int srows = maps ? smem_rows : AT;
   const size_t smem = (size_t)srows * J * (sizeof(float) + sizeof(double));
-  static size_t configured[2] = {0, 0};   // per instantiation
-  size_t &cfg = configured[J == 16 ? 0 : 1];
   // (the kernel also has up to ~8.5 KB of static shared memory: opt in whenever the sum passes 48 KB)
-  if (smem + 9 * 1024 > 48 * 1024 && smem > cfg) {
-    cudaError_t e = J == 16 ? cudaFuncSetAttribute(k_proj_solve4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                            : cudaFuncSetAttribute(k_proj_solve4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem + 9 * 1024 > 48 * 1024) {
+    cudaError_t e = smem_optin(J == 16 ? (const void *)k_proj_solve4<16> : (const void *)k_proj_solve4<32>, smem);
     if (e != cudaSuccess) return e;
-    cfg = smem;
   }
   (void)ntiles;
   if (J == 16)
@@ -2571,27 +2083,6 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   else
     k_proj_solve4<32><<<dim3((n1 + 31) / 32, per_chain, nchains), dim3(32, nseg), smem, s>>>(
         tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
-  return cudaGetLastError();
-}
-bool solve5_fits(int AT) {
-  return (size_t)(AT + 1) * SJB * (sizeof(double) + 2 * sizeof(float)) <= 180 * 1024 &&
-         2 * solve_nseg(AT) <= 2 * SSEG_MAX;
-}
-cudaError_t launch_proj_solve5(const ProjTile *tiles, int n2, int n1, int AT, int ldn,
-                               const double *segprod, float *phx, float *phy, int AP,
-                               const SolveMaps *maps, int smem_rows, const int *order, int nchains,
-                               int per_chain, cudaStream_t s) {
-  const int nseg = solve_nseg(AT);
-  const size_t smem = (size_t)smem_rows * SJB * (sizeof(double) + 2 * sizeof(float));
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_proj_solve5, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  k_proj_solve5<<<dim3((n1 + SJB - 1) / SJB, nchains), dim3(SJB, 2 * nseg), smem, s>>>(
-      tiles, n2, n1, AT, ldn, segprod, phx, phy, AP, maps, smem_rows, order, per_chain);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
@@ -2603,12 +2094,9 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
   const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);
   const size_t smem = (size_t)AT * SJB * sizeof(float);
   if (smem <= 160 * 1024) {
-    static size_t configured = 0;
-    if (smem + 9 * 1024 > 48 * 1024 && smem > configured) {
-      cudaError_t e = cudaFuncSetAttribute(k_proj_solve3<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem + 9 * 1024 > 48 * 1024) {
+      cudaError_t e = smem_optin((const void *)k_proj_solve3<true>, smem);
       if (e != cudaSuccess) return e;
-      configured = smem;
     }
     k_proj_solve3<true><<<grid, block, smem, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
                                                    phx_lo, phy_lo, AP);
@@ -2618,14 +2106,4 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
   }
   return cudaGetLastError();
 }
-cudaError_t launch_proj_solve(const ProjTile *tiles, int ntiles, int n2, int n1,
-                              const float *qhat, int AT, int ldn, const double *rinv, double *z,
-                              float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
-                              cudaStream_t s) {
-  const int nt = ntiles >= 16 ? 128 : 32;   // few tiles (global P): spread columns over more SMs
-  k_proj_solve<<<dim3((n1 + nt - 1) / nt, ntiles), nt, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv,
-                                                               z, phx, phy, phx_lo, phy_lo, AP);
-  return cudaGetLastError();
-}
-
 }  // namespace tvs

@@ -47,6 +47,24 @@ def _primal1(tau, d0, delta):
     return S.primal_energy_tfs(tau, ptau0, delta)
 
 
+def _gap2(d, p, d0, tau, lam, variant="irv2", eps=1e-3):
+    if variant == "irv1":
+        return S.duality_gap(d, p)
+    _, g, _ = S.irv2_data(d0, tau, lam)
+    return S.duality_gap(d - g, p)
+
+
+def check_energies(st, E_ref, gap_ref, what):
+    """The library's own primal energy and duality gap (tvs_stats, fp64 device reductions) vs the
+    oracle's on its own solution: energies at the north-star 1e-4 relative; the gap (a difference
+    of two energies) at 1e-4 of the energy."""
+    rel = abs(st.primal_energy - E_ref) / abs(E_ref)
+    assert rel <= TOL, f"{what}: library E {st.primal_energy} vs oracle {E_ref} (rel {rel})"
+    assert st.gap >= -TOL * abs(E_ref), (what, st.gap)
+    assert abs(st.gap - gap_ref) <= TOL * abs(E_ref), (what, st.gap, gap_ref)
+    return rel
+
+
 def _primal2(d, d0, tau, lam, variant="irv2", eps=1e-3):
     if variant == "irv1":
         alpha, dxi, _ = S.irv1_data(d0, tau, lam, eps)
@@ -66,8 +84,9 @@ def check_step1(ctx, img, delta, L, sweeps, inner, t=0.125):
     E_ref = _primal1(tau_ref, img.astype(np.float64), delta)
     E_gpu = _primal1(tau, img.astype(np.float64), delta)
     rel = abs(E_gpu - E_ref) / abs(E_ref) if E_ref else abs(E_gpu)
+    lib_rel = check_energies(st, E_ref, S.duality_gap(tau_ref, p_ref), "step 1")
     _log("step1", shape=list(img.shape), L=list(L), sweeps=sweeps, inner=inner, tau_err=e_tau,
-         p_err=e_p, E1_rel=rel)
+         p_err=e_p, E1_rel=rel, E1_lib_rel=lib_rel, gap=st.gap)
     assert e_tau <= TOL, f"max|tau - oracle| = {e_tau}"
     assert e_p <= P_TOL, f"max|p - oracle| = {e_p}"
     assert rel <= TOL, f"relative E1 error {rel}"
@@ -93,8 +112,11 @@ def check_step2(ctx, img, tau, lam, L, sweeps, inner, t=0.125, variant="irv2", e
     E_ref = _primal2(d_ref, img.astype(np.float64), tau, lam, variant, eps)
     E_gpu = _primal2(d, img.astype(np.float64), tau, lam, variant, eps)
     rel = abs(E_gpu - E_ref) / abs(E_ref)
+    lib_rel = check_energies(st, E_ref, _gap2(d_ref, p_ref, img.astype(np.float64), tau, lam,
+                                              variant, eps), "step 2 " + variant)
     _log("step2" if variant == "irv2" else "step2_irv1", shape=list(img.shape), L=list(L),
-         sweeps=sweeps, inner=inner, d_err=e_d, p_err=e_p, E2_rel=rel)
+         sweeps=sweeps, inner=inner, d_err=e_d, p_err=e_p, E2_rel=rel, E2_lib_rel=lib_rel,
+         gap=st.gap)
     assert e_d <= TOL, f"max|d - oracle| = {e_d}"
     assert e_p <= P_TOL, f"max|p - oracle| = {e_p}"
     assert rel <= TOL, f"relative E2 error {rel}"

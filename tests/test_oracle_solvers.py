@@ -270,3 +270,146 @@ def test_reported_dual_energy_is_the_objective():
     assert abs(i1["dual_energy"] - S.dual_energy_tfs(p1, i1["f"])) < 1e-10 * i1["dual_energy"]
     d, p2, i2 = S.dd_step2(d0, tau, 0.1, lay, 3, 3)
     assert abs(i2["dual_energy"] - S.dual_energy_irv2(p2, i2["f"])) < 1e-10 * i2["dual_energy"]
+
+
+# ----------------------------------------------------------------------------- primal energies / gaps (C-13, C-15)
+
+def _feasible(shape, seed):
+    """Random dual with every row strictly inside the unit ball (|p_k| <= 1, Eq. eq:DefDisB)."""
+    q = random_field(shape, seed, 1.0)
+    nrm = np.sqrt(q[..., 0, :, :] ** 2 + q[..., 1, :, :] ** 2) if q.ndim == 4 else np.sqrt(q[0] ** 2 + q[1] ** 2)
+    scale = 0.99 / np.maximum(nrm, 1.0)
+    return q * (scale[:, None] if q.ndim == 4 else scale)
+
+
+def _curl_minus(psi):
+    """curl^- psi = (D-_y psi, -D-_x psi): divergence-free on any grid (div curl^- = 0, SURVEY C-4)."""
+    return np.stack([ops.dminus_y(psi), -ops.dminus_x(psi)])
+
+
+def test_tfs_energy_gap_identity_for_any_feasible_dual():
+    """For EVERY feasible p, with tau(p) = P tau_0 - delta P multidiv p:
+    E_1(tau) - G_1(p) = sum_k (TV(tau_k) + <p_k, grad tau_k>) = duality_gap(tau, p) >= 0.
+    Three independently written formulas (primal_energy_tfs, dual_value_tfs, duality_gap) must agree
+    to rounding: a dropped 1/2, tau_0 in place of P tau_0, or a wrong sign breaks the identity."""
+    d0 = random_image(9, 12, 11).astype(np.float64)
+    delta = 0.05
+    ptau0 = spectral.project(S.tau0(d0))
+    for seed in (1, 2, 3):
+        p = _feasible((2, 2, 10, 13), 40 + seed)
+        tau = ptau0 - delta * spectral.project(ops.multidiv(p))
+        e = S.primal_energy_tfs(tau, ptau0, delta)
+        g = S.dual_value_tfs(p, ptau0, delta)
+        gap = S.duality_gap(tau, p)
+        assert gap >= 0.0
+        assert abs((e - g) - gap) < 1e-10 * max(1.0, abs(e))
+    # tau_0 instead of P tau_0 in the primal data term (the slip of Alg. 1, reading A1) breaks it
+    tau0 = S.tau0(d0)
+    assert abs(S.primal_energy_tfs(tau, tau0, delta) - S.dual_value_tfs(p, ptau0, delta) - gap) > 1e-3
+
+
+def test_irv2_energy_gap_identity_for_any_feasible_dual():
+    """Same identity for step 2 (Eq. modifiedStep2, dual P:504-510, d = d_0 - div p/alpha
+    P:509): E_2(d) - G_2(p) = TV(d - g) + <p, grad(d - g)> = duality_gap(d - g, p) >= 0."""
+    d0 = random_image(11, 8, 12).astype(np.float64)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 30)
+    alpha, g, f = S.irv2_data(d0, tau, 0.1)
+    for seed in (4, 5, 6):
+        p = _feasible((2, 11, 8), 50 + seed)
+        d = d0 - ops.div(p) / alpha
+        e = S.primal_energy_irv2(d, d0, g, alpha)
+        gv = S.dual_value_irv2(p, d0, g, alpha)
+        gap = S.duality_gap(d - g, p)
+        assert gap >= 0.0
+        assert abs((e - gv) - gap) < 1e-10 * max(1.0, abs(e))
+
+
+def test_channelwise_tv_dual_attains_zero_gap():
+    """The row-wise unit balls of the dual (Alg. 1 row-wise projection P:790) are the dual of
+    the CHANNEL-WISE vector TV (reading A15): p_k = -grad u_k/|grad u_k| attains the sup, so the gap
+    is 0 to rounding; an isotropic TV would leave sqrt(sum_k |.|^2) - sum_k |.| < 0 here."""
+    u = random_field((2, 7, 9), 61, 1.0)
+    gr = ops.multigrad(u)
+    nrm = np.sqrt(gr[:, 0] ** 2 + gr[:, 1] ** 2)
+    p = -gr / np.maximum(nrm, 1e-300)[:, None]
+    assert abs(S.duality_gap(u, p)) < 1e-12 * S.tv(u)
+    assert abs(S.tv(u) - sum(S.tv(u[k]) for k in range(2))) < 1e-13 * S.tv(u)
+
+
+def test_tfs_gap_closes_and_bounds_hold_over_chambolle_iterates():
+    """Weak duality across iterates: E_1(tau(p_a)) >= G_1(p_b) for all pairs; G_1 is monotone
+    (Alg. 1 decreases D); the gap closes over Chambolle's iterates."""
+    d0 = disk_on_ramp(16, 1001).astype(np.float64)
+    delta = 0.05
+    ptau0 = spectral.project(S.tau0(d0))
+    es, gs, gaps = [], [], []
+    for it in (5, 50, 500, 5000):
+        tau, p = S.chambolle_tfs(d0, delta, it)
+        es.append(S.primal_energy_tfs(tau, ptau0, delta))
+        gs.append(S.dual_value_tfs(p, ptau0, delta))
+        gaps.append(S.duality_gap(tau, p))
+    assert min(es) >= max(gs) - 1e-9
+    assert all(b >= a - 1e-12 for a, b in zip(gs, gs[1:]))
+    assert gaps[0] > gaps[1] > gaps[2] > gaps[3] and gaps[3] < 2e-2 * gaps[0]
+
+
+def test_irv2_gap_closes_over_chambolle_iterates():
+    d0 = disk_on_ramp(16, 1001).astype(np.float64)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 300)
+    alpha, g, _ = S.irv2_data(d0, tau, 0.1)
+    es, gs, gaps = [], [], []
+    for it in (5, 50, 500, 5000):
+        d, p = S.chambolle_irv2(d0, tau, 0.1, it)
+        es.append(S.primal_energy_irv2(d, d0, g, alpha))
+        gs.append(S.dual_value_irv2(p, d0, g, alpha))
+        gaps.append(S.duality_gap(d - g, p))
+    assert min(es) >= max(gs) - 1e-9
+    assert all(b >= a - 1e-12 for a, b in zip(gs, gs[1:]))
+    assert gaps[0] > gaps[1] > gaps[2] > gaps[3] and gaps[3] < 2e-2 * gaps[0]
+
+
+def test_tfs_primal_energy_is_minimised_at_the_dual_solution():
+    """Pins E_1's weights independently of the dual algebra: the long-run Chambolle tau* (computed
+    without primal_energy_tfs) minimises E_1 over K up to its gap: E_1(tau* + w) >= E_1(tau*) - gap
+    for divergence-free w = curl^- psi, and along the ray c tau* (in K; TV is differentiable along
+    it).  Doubling the fit weight moves the minimiser along that ray, so one of c = 1 +- 0.02
+    lowers the mis-written energy.  (Fitting tau_0 instead of P tau_0 only adds the constant
+    ||(I - P) tau_0||^2 / (2 delta) on K; the identity test above catches that slip.)"""
+    d0 = disk_on_ramp(16, 1001).astype(np.float64)
+    delta = 0.05
+    ptau0 = spectral.project(S.tau0(d0))
+    tau, p = S.chambolle_tfs(d0, delta, 20000)
+    gap = S.duality_gap(tau, p)
+    e0 = S.primal_energy_tfs(tau, ptau0, delta)
+    for seed in range(4):
+        w = _curl_minus(random_field((17, 17), 70 + seed, 1.0))
+        w *= 0.05 / np.abs(w).max()
+        assert np.abs(ops.div(w)).max() < 1e-13
+        for sgn in (1.0, -1.0):
+            assert S.primal_energy_tfs(tau + sgn * w, ptau0, delta) >= e0 - gap - 1e-9
+    for c in (0.98, 1.02):
+        assert S.primal_energy_tfs(c * tau, ptau0, delta) >= e0 - gap - 1e-9
+    wrong = lambda t: S.tv(t) + ops.inner(t - ptau0, t - ptau0) / delta   # noqa: E731 (1/delta)
+    assert min(wrong(c * tau) for c in (0.98, 1.02)) < wrong(tau) - 1e-9
+
+
+def test_irv2_primal_energy_is_minimised_at_the_dual_solution():
+    """E_2(d* + h) >= E_2(d*) - gap for perturbations h of the long-run Chambolle d*, including the
+    ray d = g + mean(u) + c (u - mean(u)), u = d* - g, along which TV(d - g) is differentiable; a
+    dropped 1/2 (alpha ||d - d_0||^2) moves the minimiser along that ray, so one of c = 1 +- 0.02
+    lowers the mis-written energy."""
+    d0 = disk_on_ramp(16, 1001).astype(np.float64)
+    tau, _ = S.chambolle_tfs(d0, 0.05, 300)
+    alpha, g, _ = S.irv2_data(d0, tau, 0.1)
+    d, p = S.chambolle_irv2(d0, tau, 0.1, 20000)
+    gap = S.duality_gap(d - g, p)
+    e0 = S.primal_energy_irv2(d, d0, g, alpha)
+    for seed in range(4):
+        h = random_field((16, 16), 80 + seed, 0.02)
+        for sgn in (1.0, -1.0):
+            assert S.primal_energy_irv2(d + sgn * h, d0, g, alpha) >= e0 - gap - 1e-9
+    u = d - g
+    ray = [g + u.mean() + c * (u - u.mean()) for c in (0.98, 1.02)]
+    assert all(S.primal_energy_irv2(x, d0, g, alpha) >= e0 - gap - 1e-9 for x in ray)
+    wrong = lambda x: S.tv(x - g) + alpha * ops.inner(x - d0, x - d0)   # noqa: E731
+    assert min(wrong(x) for x in ray) < wrong(d) - 1e-9
