@@ -98,6 +98,18 @@ typedef struct tvs_ctx tvs_ctx;   /* opaque: device, plans, scratch, profiling, 
  * (bad device), TVS_ENCCL (communicator init).  *ctx is NULL on failure. */
 tvs_status tvs_create(tvs_ctx **ctx, int rank, int world, const uint8_t *nccl_id, int device);
 tvs_status tvs_destroy(tvs_ctx *ctx);
+
+/* Virtual slab group on ONE GPU: creates `world` contexts ctxs[0..world-1] on `device`, ranks of a
+ * slab decomposition exactly as with one process per GPU, except that their
+ * exchanges -- the per-sweep band send/recv, the row all-gathers (partial x-DCT rows, outputs) and
+ * the energy all-reduces -- are device-to-device copies on that GPU instead of NCCL calls.  Each
+ * context must be driven from its own host thread (SPMD: every rank calls the same entry points
+ * with the same arguments) and should get its own CUDA stream; the threads rendezvous inside the
+ * calls.  Results are bitwise those of world = 1 (tests/test_gpu_virtual.py).  Purpose: run the
+ * multi-GPU data path under a single-GPU test (SURVEY 4 "virtual slab mode").  A rank that fails
+ * aborts the group (the others return TVS_ENCCL).  Free each context with tvs_destroy.
+ * Errors: TVS_EINVAL (world < 1 or > 64), TVS_ECUDA, TVS_ENOMEM. */
+tvs_status tvs_create_virtual_group(tvs_ctx **ctxs, int world, int device);
 const char *tvs_last_error(const tvs_ctx *ctx);
 tvs_status tvs_nccl_unique_id(uint8_t id_out[128]);
 

@@ -6,10 +6,30 @@ follows; readings A1..A21 are listed in DESIGN.md.  Rectangles are ((y0, y1), (x
 0-based global indices.  Fields: scalar (n2, n1); vector (2, n2, n1) with [0] = x-component;
 2x2 multi-field (2, 2, n2, n1) with [k] = row p_k.
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import ops, spectral
 from .layout import Layout
+
+
+def map_subdomains(fn, subs, workers=1):
+    """[fn(m) for m in subs], optionally on ``workers`` threads: one task per subdomain, the
+    paper's own parallelisation ("multi-threading, where each thread processes only a local
+    portion of the image").  The local solves of one outer sweep are independent
+    (Alg. 2 is additive) and their results are combined by the caller in subdomain
+    order, so the output is bitwise the same for every ``workers``.  NumPy releases the GIL in
+    its kernels; BLAS threads are split between the workers."""
+    subs = list(subs)
+    if workers <= 1 or len(subs) <= 1:
+        return [fn(m) for m in subs]
+    from threadpoolctl import threadpool_limits
+    workers = min(workers, len(subs))
+    with threadpool_limits(limits=max(1, (os.cpu_count() or 1) // workers), user_api="blas"):
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            return list(ex.map(fn, subs))
 
 # ----------------------------------------------------------------------------- rect helpers
 
@@ -250,12 +270,13 @@ def stop_rule(criterion, tol, d_prev, d_next, npts, cfac):
 
 
 def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False,
-             subdomains=None, variant="irv2", eps=1e-3, stop=(0, 0.0)):
+             subdomains=None, variant="irv2", eps=1e-3, stop=(0, 0.0), workers=1):
     """Alg. 2 for step 2 on Gamma = Omega with the localized Alg. 3; IRV2 (default,
     the variant the paper adopts) or IRV1 (``variant='irv1'``, xi smoothing ``eps``).
 
     Warm start v^0 = R_S qhat_m from the previous sweep, qhat = 0 initially (reading A9;
     ``warm='theta_p'`` uses R_S theta_m p^n instead).  Fixed schedule, no stopping test (A10).
+    ``workers`` > 1 runs the local solves of a sweep on threads (map_subdomains; same result).
     Returns (d, p, info) with d = d_0 - (div p + shift) / alpha (IRV1: Eq. tau_hat)."""
     n2, n1 = d0.shape
     alpha, f, shift = step2_data(d0, tau, lam, variant, eps)
@@ -268,14 +289,19 @@ def dd_step2(d0, tau, lam, lay: Layout, sweeps, inner, t=0.125, warm="qhat", tra
     sweeps_run = sweeps
     for n in range(sweeps):
         acc = np.zeros_like(p)
-        for m in lay.subdomains():
+
+        def local(m, p=p):
             s = lay.rect(m, extended=False)
             if warm == "qhat":
                 v0 = qhat[m]
             else:
                 v0 = restrict(lay.theta(m, False) * p, full_rect(n2, n1), s)
-            qhat[m] = _irv2_inner_local(m, lay, p, f, v0, inner, t)
-            acc += extend(qhat[m], s, full_rect(n2, n1))
+            return _irv2_inner_local(m, lay, p, f, v0, inner, t)
+
+        subs = lay.subdomains()
+        for m, q in zip(subs, map_subdomains(local, subs, workers)):
+            qhat[m] = q
+            acc += extend(q, lay.rect(m, extended=False), full_rect(n2, n1))
         p = (1.0 - lay.alpha_hat) * p + lay.alpha_hat * acc
         if trace or stop[0]:
             r = ops.div(p) - f
@@ -333,12 +359,13 @@ def tfs_inner_global(m, lay, p, f, v0_full, inner, t):
 
 
 def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=False,
-             stop=(0, 0.0)):
+             stop=(0, 0.0), workers=1):
     """Alg. 2 for TFS on Gamma = Omega~ with the localized Alg. 5.
 
     f = delta^{-1} P tau_0.  The global residual r^n = f - P multidiv p^n is
     evaluated once per outer sweep (reading A11 of P:1761-1766).  Output
-    tau = P tau_0 - delta P multidiv p^S = delta r^S (Cor. tfsdual / Eq. tfs_dualPK)."""
+    tau = P tau_0 - delta P multidiv p^S = delta r^S (Cor. tfsdual / Eq. tfs_dualPK).
+    ``workers`` > 1 runs the local solves of a sweep on threads (map_subdomains; same result)."""
     n2, n1 = d0.shape
     n2t, n1t = n2 + 1, n1 + 1
     whole = full_rect(n2t, n1t)
@@ -357,14 +384,19 @@ def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=
                 break
             e_prev = e
         acc = np.zeros_like(p)
-        for m in lay.subdomains():
+
+        def local(m, p=p, r=r):
             s = lay.rect(m, extended=True)
             if warm == "qhat":
                 v0 = qhat[m]
             else:
                 v0 = restrict(lay.theta(m, True) * p, whole, s)
-            qhat[m] = _tfs_inner_local(m, lay, p, r, v0, inner, t)
-            acc += extend(qhat[m], s, whole)
+            return _tfs_inner_local(m, lay, p, r, v0, inner, t)
+
+        subs = lay.subdomains()
+        for m, q in zip(subs, map_subdomains(local, subs, workers)):
+            qhat[m] = q
+            acc += extend(q, lay.rect(m, extended=True), whole)
         p = (1.0 - lay.alpha_hat) * p + lay.alpha_hat * acc
         if trace:
             rr = spectral.project(ops.multidiv(p)) - f
@@ -374,10 +406,10 @@ def dd_step1(d0, delta, lay: Layout, sweeps, inner, t=0.125, warm="qhat", trace=
                     "dual_energy": ops.inner(tau, tau) / delta ** 2}
 
 
-def dd_denoise(d0, delta, lam, lay: Layout, it1, it2, t=0.125):
+def dd_denoise(d0, delta, lam, lay: Layout, it1, it2, t=0.125, workers=1):
     """Step 1 then step 2 on the same splitting; it = (sweeps, inner)."""
-    tau, p1, _ = dd_step1(d0, delta, lay, it1[0], it1[1], t)
-    d, p2, info = dd_step2(d0, tau, lam, lay, it2[0], it2[1], t)
+    tau, p1, _ = dd_step1(d0, delta, lay, it1[0], it1[1], t, workers=workers)
+    d, p2, info = dd_step2(d0, tau, lam, lay, it2[0], it2[1], t, workers=workers)
     return d, tau, p1, p2
 
 

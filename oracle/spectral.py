@@ -28,6 +28,9 @@ def sigma(n):
     return 2.0 * np.sin(np.arange(n, dtype=np.float64) * np.pi / (2.0 * n))
 
 
+_LAM_CACHE = {}
+
+
 def spectral_inverse(n2, n1, printed_pairing=False):
     """The diagonal (Delta~)^dagger of Eq. form:DiscInvLaplTild.
 
@@ -36,6 +39,8 @@ def spectral_inverse(n2, n1, printed_pairing=False):
     i with N~1 and j with N~2; ``printed_pairing=True`` reproduces it literally (only used by the
     test that shows it fails the Penrose identities on non-square grids).
     """
+    if not printed_pairing and (n2, n1) in _LAM_CACHE:   # cached: pure function of (n2, n1)
+        return _LAM_CACHE[(n2, n1)]
     if printed_pairing:
         # literal: entry (i, j) -> -1/(sigma_{N1,i}^2 + sigma_{N2,j}^2); only defined if the
         # index ranges fit, i.e. used on grids where it can be evaluated
@@ -49,6 +54,9 @@ def spectral_inverse(n2, n1, printed_pairing=False):
     nz = den != 0.0
     nz[0, 0] = False
     lam[nz] = -1.0 / den[nz]
+    if not printed_pairing and n2 * n1 <= 8192 * 8192:
+        lam.setflags(write=False)
+        _LAM_CACHE[(n2, n1)] = lam
     return lam
 
 

@@ -23,7 +23,7 @@ ABI_SYMBOLS = [
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
     "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows", "tv_stokes_step2_irv1",
-    "tvs_set_stopping",
+    "tvs_set_stopping", "tvs_create_virtual_group",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH):
     LP, IP = ctypes.POINTER(Layout), ctypes.POINTER(Iters)
     lib.tvs_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
     lib.tvs_destroy.argtypes = [P]
+    lib.tvs_create_virtual_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int]
     lib.tvs_last_error.argtypes = [P]
     lib.tvs_last_error.restype = ctypes.c_char_p
     lib.tvs_nccl_unique_id.argtypes = [P]
@@ -200,6 +201,26 @@ class Context:
         if st:
             raise TvsError(st, "tvs_create")
         self.h = h
+
+    @classmethod
+    def virtual_group(cls, world: int, device: int = 0):
+        """`world` contexts on one GPU forming a virtual slab group (tvs_create_virtual_group):
+        drive each from its own thread and stream; exchanges are device-to-device copies."""
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("tvstokes needs a CUDA device (no CPU fallback)")
+        lib = load_library()
+        hs = (ctypes.c_void_p * world)()
+        st = lib.tvs_create_virtual_group(hs, world, device)
+        if st:
+            raise TvsError(st, "tvs_create_virtual_group")
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c.lib, c.device, c.h = lib, device, ctypes.c_void_p(hs[r])
+            c.vrank = r
+            out.append(c)
+        return out
 
     def close(self):
         if getattr(self, "h", None):

@@ -7,7 +7,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -240,6 +244,52 @@ struct PendingEv {
   double bytes, flops;
 };
 
+// Virtual slab group (tvs_create_virtual_group): `world` contexts on ONE device whose exchanges
+// are device-to-device copies instead of NCCL, so the multi-GPU data path (partial band sums,
+// band exchange, remote-band combine, row all-gathers, all-reduces) runs under a single-GPU test.
+// Every collective is a three-phase rendezvous of the ranks' host threads:
+//   A  record `ready` on the rank's stream after its producers, publish the exported pointers;
+//      barrier;
+//   B  pull: wait on the source rank's `ready`, cudaMemcpyAsync D2D from its exported buffer;
+//      record `done`; barrier;
+//   C  wait on every other rank's `done` (its pulls from this rank's buffers have completed
+//      before this rank writes them again), then the collective's local epilogue (all-reduce sum).
+// GPU work never waits on work that is enqueued later (events are recorded before the barrier
+// that precedes their waits), so no device-side cycle can form.
+struct VGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  bool broken = false;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<std::vector<void *>> exports;
+  int alive = 0;
+  // false when another rank aborted (error) or the rendezvous timed out
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return true;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::seconds(600),
+                                [&] { return generation != gen || broken; });
+    if (!ok) broken = true;
+    if (broken) cv.notify_all();
+    return !broken && generation != gen;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
 }  // namespace
 
 struct tvs_ctx {
@@ -267,6 +317,8 @@ struct tvs_ctx {
   // scratch for denoise / host variants
   std::unique_ptr<DevBuf> tau_scratch, h_d0, h_d, h_tau;
   ncclComm_t nccl = nullptr;   // world > 1 only
+  std::shared_ptr<VGroup> vgroup;   // virtual slab group (one device, D2D exchanges) or null
+  double *d_red = nullptr;          // virtual all-reduce scratch [world][16]
   // side stream: step 1 runs the global residual projection of a sweep on it, concurrently with
   // the omega0 local projection chain (independent until omega0 reads both; TVS_OVERLAP=0: off)
   bool overlap = true;
@@ -739,11 +791,57 @@ tvs_status nccl_ck(tvs_ctx *ctx, ncclResult_t r, const char *what) {
   return TVS_OK;
 }
 
+// One virtual-group collective (see VGroup): publish `exports`, pull `pulls`, then `post`.
+struct Pull {
+  int src, exp;
+  size_t src_off;
+  void *dst;
+  size_t bytes;
+};
+tvs_status vexchange(tvs_ctx *ctx, const std::vector<void *> &exports, const std::vector<Pull> &pulls,
+                     cudaStream_t s, const std::function<tvs_status()> &post = {}) {
+  VGroup &G = *ctx->vgroup;
+  const int r = ctx->rank;
+  CK(cudaEventRecord(G.ready[r], s));
+  {
+    std::lock_guard<std::mutex> lk(G.mu);
+    G.exports[r] = exports;
+  }
+  if (!G.barrier()) return fail(ctx, TVS_ENCCL, "virtual group: rendezvous aborted (another rank failed)");
+  std::vector<bool> waited(G.world, false);
+  for (const Pull &p : pulls) {
+    if (!waited[p.src]) {
+      CK(cudaStreamWaitEvent(s, G.ready[p.src], 0));
+      waited[p.src] = true;
+    }
+    const char *src = static_cast<const char *>(G.exports[p.src][p.exp]) + p.src_off;
+    if (p.bytes) CK(cudaMemcpyAsync(p.dst, src, p.bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaEventRecord(G.done[r], s));
+  if (!G.barrier()) return fail(ctx, TVS_ENCCL, "virtual group: rendezvous aborted (another rank failed)");
+  for (int q = 0; q < G.world; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(s, G.done[q], 0));
+  return post ? post() : TVS_OK;
+}
+
 // All-gather of row slabs: rank q contributes rows [Rlo[q], Rhi[q]) of every plane of `buf`
-// (row pitch ld, plane stride ps), in place -- one ncclBroadcast per (root, plane) in a group.
+// (row pitch ld, plane stride ps), in place -- one ncclBroadcast per (root, plane) in a group, or
+// D2D pulls from the other ranks' buffers in a virtual group (same layout on every rank).
 tvs_status allgather_rows(tvs_ctx *ctx, const Dist &D, float *buf, int planes, size_t ps, int ld,
                           cudaStream_t s) {
   if (D.world == 1) return TVS_OK;
+  if (ctx->vgroup) {
+    std::vector<Pull> pulls;
+    for (int q = 0; q < D.world; ++q) {
+      if (q == D.rank) continue;
+      for (int c = 0; c < planes; ++c) {
+        const size_t off = (size_t)c * ps + (size_t)D.Rlo[q] * ld;
+        pulls.push_back({q, 0, off * sizeof(float), buf + off,
+                         (size_t)(D.Rhi[q] - D.Rlo[q]) * ld * sizeof(float)});
+      }
+    }
+    return vexchange(ctx, {buf}, pulls, s);
+  }
   TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
   for (int q = 0; q < D.world; ++q)
     for (int c = 0; c < planes; ++c) {
@@ -752,6 +850,22 @@ tvs_status allgather_rows(tvs_ctx *ctx, const Dist &D, float *buf, int planes, s
       if (cnt) TRY(nccl_ck(ctx, ncclBroadcast(ptr, ptr, cnt, ncclFloat, q, ctx->nccl, s), "ncclBroadcast"));
     }
   return nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// In-place sum over ranks of n doubles (ncclAllReduce; a virtual group pulls every rank's values
+// and sums them in rank order on the device).
+tvs_status allreduce_sum(tvs_ctx *ctx, double *buf, int n, cudaStream_t s) {
+  if (ctx->world == 1) return TVS_OK;
+  if (ctx->vgroup) {
+    if (n > 16) return fail(ctx, TVS_EINVAL, "virtual all-reduce of more than 16 values");
+    std::vector<Pull> pulls;
+    for (int q = 0; q < ctx->world; ++q)
+      pulls.push_back({q, 0, 0, ctx->d_red + (size_t)q * 16, n * sizeof(double)});
+    return vexchange(ctx, {buf}, pulls, s, [&]() -> tvs_status {
+      return run(ctx, s, F_OTHER, 0, 0, [&] { return launch_sum_ranks(ctx->d_red, ctx->world, 16, n, buf, s); });
+    });
+  }
+  return nccl_ck(ctx, ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, ctx->nccl, s), "ncclAllReduce");
 }
 
 // Alg. 2 combine on this rank's valid rows, after exchanging the partial sums of the
@@ -769,21 +883,30 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
       return launch_partial(P.d_subs, g, C, P.d_covy, P.d_covx, P.d_loy, P.d_lox, P.m2loc, D.k0,
                             D.k1, q, D.ds0, D.ds1, P.G1, P.ld, P.send_dn, s);
     }));
-    TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
     auto cnt = [&](int a, int b) { return (size_t)C * (b - a) * P.ld; };
-    if (D.rank > 0) {
-      if (D.us1 > D.us0)
-        TRY(nccl_ck(ctx, ncclSend(P.send_up, cnt(D.us0, D.us1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclSend"));
-      if (D.ur1 > D.ur0)
-        TRY(nccl_ck(ctx, ncclRecv(P.recv_up, cnt(D.ur0, D.ur1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclRecv"));
+    if (ctx->vgroup) {   // export {send_up, send_dn}; pull the neighbours' bands facing this rank
+      std::vector<Pull> pulls;
+      if (D.rank > 0 && D.ur1 > D.ur0)
+        pulls.push_back({D.rank - 1, 1, 0, P.recv_up, cnt(D.ur0, D.ur1) * sizeof(float)});
+      if (D.rank < D.world - 1 && D.dr1 > D.dr0)
+        pulls.push_back({D.rank + 1, 0, 0, P.recv_dn, cnt(D.dr0, D.dr1) * sizeof(float)});
+      TRY(vexchange(ctx, {P.send_up, P.send_dn}, pulls, s));
+    } else {
+      TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
+      if (D.rank > 0) {
+        if (D.us1 > D.us0)
+          TRY(nccl_ck(ctx, ncclSend(P.send_up, cnt(D.us0, D.us1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclSend"));
+        if (D.ur1 > D.ur0)
+          TRY(nccl_ck(ctx, ncclRecv(P.recv_up, cnt(D.ur0, D.ur1), ncclFloat, D.rank - 1, ctx->nccl, s), "ncclRecv"));
+      }
+      if (D.rank < D.world - 1) {
+        if (D.ds1 > D.ds0)
+          TRY(nccl_ck(ctx, ncclSend(P.send_dn, cnt(D.ds0, D.ds1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclSend"));
+        if (D.dr1 > D.dr0)
+          TRY(nccl_ck(ctx, ncclRecv(P.recv_dn, cnt(D.dr0, D.dr1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclRecv"));
+      }
+      TRY(nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd"));
     }
-    if (D.rank < D.world - 1) {
-      if (D.ds1 > D.ds0)
-        TRY(nccl_ck(ctx, ncclSend(P.send_dn, cnt(D.ds0, D.ds1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclSend"));
-      if (D.dr1 > D.dr0)
-        TRY(nccl_ck(ctx, ncclRecv(P.recv_dn, cnt(D.dr0, D.dr1), ncclFloat, D.rank + 1, ctx->nccl, s), "ncclRecv"));
-    }
-    TRY(nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd"));
   }
   return run(ctx, s, F_OTHER, 0, 0, [&] {
     return launch_combine(P.d_subs, g, C, P.d_covy, P.d_covx, P.d_loy, P.d_lox, P.m2loc, D.k0,
@@ -797,9 +920,7 @@ tvs_status combine_step(tvs_ctx *ctx, Plan &P, const float *q, cudaStream_t s) {
 // after the call's final stream synchronisation).
 tvs_status fetch_energy(tvs_ctx *ctx, Plan &P, cudaStream_t s, double *out, bool sync = true,
                         int off = 0, int n = 1) {
-  if (P.dist.world > 1)
-    TRY(nccl_ck(ctx, ncclAllReduce(P.d_energy + off, P.d_energy + off, n, ncclDouble, ncclSum,
-                                   ctx->nccl, s), "ncclAllReduce"));
+  if (P.dist.world > 1) TRY(allreduce_sum(ctx, P.d_energy + off, n, s));
   if (!ctx->h_energy) CK(cudaMallocHost(&ctx->h_energy, 16 * sizeof(double)));
   CK(cudaMemcpyAsync(ctx->h_energy + off, P.d_energy + off, n * sizeof(double),
                      cudaMemcpyDeviceToHost, s));
@@ -1156,6 +1277,13 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
 
 }  // namespace
 
+// A failing rank of a virtual group aborts the group's rendezvous so the other ranks' host
+// threads return TVS_ENCCL instead of waiting for it forever.
+static tvs_status guard(tvs_ctx *ctx, tvs_status st) {
+  if (st != TVS_OK && ctx && ctx->vgroup) ctx->vgroup->abort();
+  return st;
+}
+
 // ============================================================================= C ABI
 
 extern "C" {
@@ -1205,7 +1333,41 @@ tvs_status tvs_destroy(tvs_ctx *ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+  if (ctx->d_red) cudaFree(ctx->d_red);
+  if (ctx->vgroup) {
+    std::lock_guard<std::mutex> lk(ctx->vgroup->mu);
+    if (--ctx->vgroup->alive == 0) {
+      for (auto e : ctx->vgroup->ready) cudaEventDestroy(e);
+      for (auto e : ctx->vgroup->done) cudaEventDestroy(e);
+    }
+  }
   delete ctx;
+  return TVS_OK;
+}
+
+tvs_status tvs_create_virtual_group(tvs_ctx **ctxs, int world, int device) {
+  if (!ctxs || world < 1 || world > 64) return TVS_EINVAL;
+  for (int r = 0; r < world; ++r) ctxs[r] = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return TVS_ECUDA;
+  auto G = std::make_shared<VGroup>();
+  G->world = world;
+  G->ready.resize(world);
+  G->done.resize(world);
+  G->exports.resize(world);
+  for (int r = 0; r < world; ++r)
+    if (cudaEventCreateWithFlags(&G->ready[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&G->done[r], cudaEventDisableTiming) != cudaSuccess)
+      return TVS_ECUDA;
+  for (int r = 0; r < world; ++r) {
+    tvs_status st = tvs_create(&ctxs[r], 0, 1, nullptr, device);
+    if (st) return st;
+    ctxs[r]->rank = r;
+    ctxs[r]->world = world;
+    ctxs[r]->vgroup = G;
+    G->alive++;
+    if (cudaMalloc(&ctxs[r]->d_red, (size_t)world * 16 * sizeof(double)) != cudaSuccess)
+      return TVS_ENOMEM;
+  }
   return TVS_OK;
 }
 
@@ -1276,7 +1438,7 @@ tvs_status tv_stokes_step1(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1
   if (!ctx) return TVS_EINVAL;
   if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
   cudaSetDevice(ctx->device);
-  return step1_impl(ctx, d0, n2, n1, delta, *L, *it, tau, p, st, (cudaStream_t)cuda_stream);
+  return guard(ctx, step1_impl(ctx, d0, n2, n1, delta, *L, *it, tau, p, st, (cudaStream_t)cuda_stream));
 }
 
 tvs_status tv_stokes_step2(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2,
@@ -1285,7 +1447,7 @@ tvs_status tv_stokes_step2(tvs_ctx *ctx, const float *tau, const float *d0, int3
   if (!ctx) return TVS_EINVAL;
   if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
   cudaSetDevice(ctx->device);
-  return step2_impl(ctx, tau, d0, n2, n1, lambda, *L, *it, d, p, st, (cudaStream_t)cuda_stream);
+  return guard(ctx, step2_impl(ctx, tau, d0, n2, n1, lambda, *L, *it, d, p, st, (cudaStream_t)cuda_stream));
 }
 
 tvs_status tv_stokes_step2_irv1(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n2,
@@ -1295,8 +1457,8 @@ tvs_status tv_stokes_step2_irv1(tvs_ctx *ctx, const float *tau, const float *d0,
   if (!ctx) return TVS_EINVAL;
   if (!L || !it) return fail(ctx, TVS_EINVAL, "null layout or schedule");
   cudaSetDevice(ctx->device);
-  return step2_impl(ctx, tau, d0, n2, n1, mu, *L, *it, d, p, st, (cudaStream_t)cuda_stream, 1,
-                    epsilon);
+  return guard(ctx, step2_impl(ctx, tau, d0, n2, n1, mu, *L, *it, d, p, st,
+                               (cudaStream_t)cuda_stream, 1, epsilon));
 }
 
 tvs_status tv_stokes_denoise(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,
@@ -1321,8 +1483,8 @@ tvs_status tv_stokes_denoise(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t 
   }
   cudaStream_t s = (cudaStream_t)cuda_stream;
   tvs_status st = step1_impl(ctx, d0, n2, n1, delta, L, it1, tau_buf, nullptr, st1, s);
-  if (st) return st;
-  return step2_impl(ctx, tau_buf, d0, n2, n1, lambda, L, it2, d, nullptr, st2, s);
+  if (st) return guard(ctx, st);
+  return guard(ctx, step2_impl(ctx, tau_buf, d0, n2, n1, lambda, L, it2, d, nullptr, st2, s));
 }
 
 static tvs_status ensure(tvs_ctx *ctx, std::unique_ptr<DevBuf> &b, size_t bytes) {

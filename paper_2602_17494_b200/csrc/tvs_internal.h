@@ -168,6 +168,8 @@ cudaError_t launch_primal1(const float *tau, size_t plane, int ld, const float *
 cudaError_t launch_primal2(const float *d, const float *d0, const float *f, const float *dxi,
                            const float *p1, const float *p2, int ldf, int n2, int n1, int row0,
                            int row1, float inv_alpha, double *part, double *out, cudaStream_t s);
+cudaError_t launch_sum_ranks(const double *vals, int world, int stride, int n, double *out,
+                             cudaStream_t s);
 cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0, int row1,
                           double *part, double *out, cudaStream_t s);
 

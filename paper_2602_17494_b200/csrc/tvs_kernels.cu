@@ -832,6 +832,17 @@ __global__ void __launch_bounds__(RED_T) k_sum_partials_multi(const double *__re
   block_sum_store(acc, out + blockIdx.x);
 }
 
+// out[i] = sum over ranks q = 0..world-1, in that order, of vals[q * stride + i] (the virtual
+// group's all-reduce; every rank forms the same fixed-order sum).
+__global__ void k_sum_ranks(const double *__restrict__ vals, int world, int stride, int n,
+                            double *__restrict__ out) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int q = 0; q < world; ++q) acc += vals[(size_t)q * stride + i];
+  out[i] = acc;
+}
+
 // ----------------------------------------------------------------------------- step 1 (TFS)
 
 // w = multidiv p: w_k = div(p_k1, p_k2); p has 4 planes [p11 p12 p21 p22].
@@ -1977,6 +1988,11 @@ cudaError_t launch_primal2(const float *d, const float *d0, const float *f, cons
   k_primal2_partial<<<RED_BLOCKS, RED_T, 0, s>>>(d, d0, f, dxi, p1, p2, ldf, n2, n1, row0, row1,
                                                  inv_alpha, part);
   k_sum_partials_multi<<<4, RED_T, 0, s>>>(part, RED_BLOCKS, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_ranks(const double *vals, int world, int stride, int n, double *out,
+                             cudaStream_t s) {
+  k_sum_ranks<<<1, 32, 0, s>>>(vals, world, stride, n, out);
   return cudaGetLastError();
 }
 cudaError_t launch_multidiv(const float *p, int ld, int n2, int n1, float *w, int row0, int row1,

@@ -413,3 +413,16 @@ def test_irv2_primal_energy_is_minimised_at_the_dual_solution():
     assert all(S.primal_energy_irv2(x, d0, g, alpha) >= e0 - gap - 1e-9 for x in ray)
     wrong = lambda x: S.tv(x - g) + alpha * ops.inner(x - d0, x - d0)   # noqa: E731
     assert min(wrong(x) for x in ray) < wrong(d) - 1e-9
+
+
+def test_threaded_subdomains_are_bitwise_identical():
+    """One task per subdomain on threads (the paper's threading) combines the local solves
+    in subdomain order: the DD iterates are bitwise those of the sequential loop."""
+    d0 = random_image(21, 19, 13).astype(np.float64)
+    lay = layout.Layout(21, 19, 2, 3, 3, 4)
+    t1, p1, _ = S.dd_step1(d0, 0.05, lay, 3, 2)
+    t4, p4, _ = S.dd_step1(d0, 0.05, lay, 3, 2, workers=4)
+    assert np.array_equal(t1, t4) and np.array_equal(p1, p4)
+    a1, q1, _ = S.dd_step2(d0, t1, 0.1, lay, 3, 4)
+    a4, q4, _ = S.dd_step2(d0, t1, 0.1, lay, 3, 4, workers=4)
+    assert np.array_equal(a1, a4) and np.array_equal(q1, q4)
