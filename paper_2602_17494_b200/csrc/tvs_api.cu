@@ -197,6 +197,11 @@ struct ProjBatch {
   // algorithmic work per launch: contraction flops (dense 2MNK), FFT flops of the chirp-z form
   // (2 x 5 M log2 M per FFT pair and row chunk), and the y-solve's HBM bytes
   double fwd_flops = 0, inv_flops = 0, fwd_fft_flops = 0, inv_fft_flops = 0, solve_bytes = 0;
+  // tile groups sharing the scratch (see build_proj): group k = tiles [g0[k], g0[k+1]), with its
+  // FFT flops and solve bytes per launch
+  int gtiles = 0;
+  std::vector<int> g0;
+  std::vector<double> gfwd, ginv, gsolve;
 };
 
 struct Plan {
@@ -220,9 +225,13 @@ struct Plan {
   int *d_bad = nullptr;
   double *d_part = nullptr, *d_energy = nullptr;   // dual-energy reduction scratch
   // step 1 only
-  float *vtmp = nullptr, *q = nullptr, *gphi = nullptr;
+  float *q = nullptr, *gphi = nullptr;   // theta_m p^n for omega0 lives in v[cur ^ 1]
   float *t0 = nullptr, *w = nullptr, *r = nullptr, *qg = nullptr, *Gg = nullptr;
   ProjBatch local, global;
+  // step 1: subdomain groups [sg0[k], sg0[k+1]) solved one after the other (see get_plan), with
+  // their sums of |S| and |T| (algorithmic bytes per launch)
+  std::vector<int> sg0;
+  std::vector<std::pair<int64_t, int64_t>> sgs;
   int64_t sum_S = 0, sum_T = 0;
   Dist dist;
   int m2loc = 0;                       // local layout rows (k1 - k0)
@@ -301,6 +310,7 @@ struct tvs_ctx {
   // partial x-DCTs: 0 = choose per batch by estimated time, 1 = dense GEMM, 2 = chirp-z (TVS_DCT)
   int dct_mode = 0;
   int czt_max_m = 16384;
+  int proj_group = 0;            // max tiles per projection group (TVS_PROJ_GROUP; 0 = by memory)
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
   int x2_minw = 512;             // ... on subdomains at least this wide (TVS_X2_MINW)
@@ -441,12 +451,61 @@ tvs_status get_tables(tvs_ctx *ctx, int n, Tables **out) {
   return TVS_OK;
 }
 
+// Partial x-DCT form of a projection batch: chirp-z FFT pairs or the dense tcgen05 GEMM, by
+// estimated time (measured rates: 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~12 TF/s of
+// 5 M log2 M flops per FFT); long axes (N > 4096) always take the chirp-z for accuracy: the
+// tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193 (config-4 global
+// projection) while the chirp-z stays at ~1e-7.  TVS_DCT=gemm|czt forces one.
+bool choose_czt(const tvs_ctx *ctx, const std::vector<ProjTile> &tiles, int n1t, bool have_tables,
+                int fr0, int fr1) {
+  int bt_max = 0, bo_max = 0;
+  for (const ProjTile &t : tiles) {
+    bt_max = std::max(bt_max, t.tx1 - t.tx0 + 1);
+    bo_max = std::max(bo_max, t.px1 - t.tx0 + 1);
+  }
+  CztGeom gf{}, gi{};
+  const bool ok = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &gf) &&
+                  czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &gi);
+  if (!ok) return false;
+  if (!have_tables || ctx->dct_mode == 2) return true;
+  if (ctx->dct_mode == 1) return false;
+  if (n1t > 4096) return true;
+  const double f1 = 2.0 * 5.0 * gf.M * std::log2((double)std::max(2, gf.M));
+  const double f2 = 2.0 * 5.0 * gi.M * std::log2((double)std::max(2, gi.M));
+  double t_gemm = 0, t_czt = 0;
+  for (const ProjTile &t : tiles) {
+    const int nt = fr0 >= 0 ? fr1 - fr0 : t.ty1 - t.ty0 + 1;
+    const int no = t.py1 - t.ty0 + 1 - t.po;
+    t_gemm += 3.0 * (2.0 * nt * (t.tx1 - t.tx0 + 1) * n1t + 4.0 * no * (t.px1 - t.tx0 + 1) * n1t) / 400e12;
+    t_czt += ((double)nt * gf.nvp * gf.nuc * f1 + 2.0 * no * gi.nvp * gi.nuc * f2) / 12e12;
+  }
+  return t_czt < t_gemm;
+}
+
+// Scratch bytes per tile of a projection batch (Q-hat, the long-tile solve's fp32 z, the two
+// spectral gradient planes) and of its pivot table (all chains).
+double proj_tile_bytes(int AT, int AP, int n1t) {
+  const bool need_z = (size_t)AT * 32 * sizeof(float) > 160 * 1024;
+  return ((double)AT * (need_z ? 2 : 1) + 2.0 * AP) * round_up(n1t, 4) * sizeof(float);
+}
+
 // Build the projection batch for tiles (chains = distinct row ranges).
 // fr0/fr1 (global batch only): rows whose partial x-DCT this rank computes (its core rows; the
 // rest of qhat arrives by all-gather); gplane: plane stride of G (0 = ntiles * AP * ldG).
+//
+// Tile groups.  The scratch of a projection (Q-hat, the fp32 z of the long-tile solve, the two
+// spectral gradient planes) is ~(AT + 2 AP) x N~1 x 4 B per tile: at config 5 (256 tiles of
+// 2083 rows x 32772 frequencies) that is ~280 GB for the whole batch.  The tiles are therefore
+// processed in groups of consecutive tiles that share one scratch sized to the free device memory
+// (the paper's locality argument: "never needing more access memory than a constant times the
+// biggest block").  Groups apply to the chirp-z form (long axes); the dense GEMM form
+// (short axes, configs 1-3) always fits in one group.
+// gtiles: tiles per group (chirp-z form; the GEMM form is always one group); local_io: q and G
+// hold only one group's tiles (indexed by the slot within the group) instead of the whole batch.
 tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
                       int n2t, int n1t, float *q, int ldq, float *G, int ldG, const Tables *T,
-                      int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0) {
+                      int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0, int gtiles = 0,
+                      bool local_io = false) {
   B.tiles = tiles_in;
   B.ntiles = (int)tiles_in.size();
   std::map<std::pair<int, int>, int> chain_of;
@@ -470,123 +529,161 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   B.ldG = ldG;
   TRY(upload(ctx, P.bufs, &B.d_tiles, B.tiles));
   TRY(upload(ctx, P.bufs, &B.d_first, first));
-  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)B.ntiles * B.AT * B.ldn));
-  // fp32 z scratch for the segmented solve only when its column block does not fit in shared memory
-  const size_t nz = (size_t)B.ntiles * B.AT * B.ldn;
-  if ((size_t)B.AT * 32 * sizeof(float) > 160 * 1024) TRY(dalloc(ctx, P.bufs, &B.z, nz));
-  TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
-  TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)B.ntiles * B.AP * B.ldn));
-  TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)B.ntiles * B.AP * B.ldn));
-  // ∇φ output is plane-major: G[c][tile][AP][ldG]
-  const size_t gplane = gplane_arg ? gplane_arg : (size_t)B.ntiles * B.AP * ldG;
-  std::vector<GemmDesc2> fwd2, inv2;
-  for (int i = 0; T && i < B.ntiles;) {
-    // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
-    int j = i + 1;
-    while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
-           B.tiles[j].px1 == B.tiles[i].px1)
-      ++j;
-    const ProjTile &t = B.tiles[i];
-    const int cnt = j - i;
-    const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
-    int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
-    const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1 - B.tiles[j - 1].po);
-    int f0 = 0;   // forward rows [f0, f0 + Mf) of the stacked operand; inverse output rows from po
-    if (fr0 >= 0) {
-      f0 = fr0;
-      Mf = fr1 - fr0;
-    }
-    const size_t goff = (size_t)t.po * ldG;
-    // 3xTF32: A (q, Phi) is one fp32 plane split in the kernel, B = the pre-split DCT tables; q
-    // carries a leading zero offset of (tx0 & 3) columns so the table rows start 16-byte aligned:
-    // K = bt + off, tables from column tx0 - off
-    const int off = t.tx0 & 3;
-    fwd2.push_back({q + ((size_t)i * B.AT + f0) * ldq, nullptr, T->part(2) + (t.tx0 - off),
-                    T->part(3) + (t.tx0 - off), B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t,
-                    bt + off, ldq, T->ld, B.ldn});
-    inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, nullptr, T->part(4) + (size_t)t.tx0 * T->ld,
-                    T->part(5) + (size_t)t.tx0 * T->ld, G + (size_t)i * B.AP * ldG + goff, Mi, bo,
-                    n1t, B.ldn, T->ld, ldG});
-    inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, nullptr, T->part(0) + (size_t)t.tx0 * T->ld,
-                    T->part(1) + (size_t)t.tx0 * T->ld, G + gplane + (size_t)i * B.AP * ldG + goff,
-                    Mi, bo, n1t, B.ldn, T->ld, ldG});
-    B.tcM_fwd = std::max(B.tcM_fwd, Mf);
-    B.tcM_inv = std::max(B.tcM_inv, Mi);
-    B.fwdN = std::max(B.fwdN, n1t);
-    B.invN = std::max(B.invN, bo);
-    i = j;
-  }
-  // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
-  std::vector<CztJob> fj, ij;
+  // ---- geometry of the two contractions per tile; x-DCT form by estimated time
+  struct Geom { int nt, f0, bt, bo, no; };
+  std::vector<Geom> gm(B.ntiles);
   int bt_max = 0, bo_max = 0;
   for (int i = 0; i < B.ntiles; ++i) {
     const ProjTile &t = B.tiles[i];
-    int nt = t.ty1 - t.ty0 + 1, f0 = 0;
+    Geom &g = gm[i];
+    g.nt = t.ty1 - t.ty0 + 1;
+    g.f0 = 0;
     if (fr0 >= 0) {
-      f0 = fr0;
-      nt = fr1 - fr0;
+      g.f0 = fr0;
+      g.nt = fr1 - fr0;
     }
-    const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
-    const int no = t.py1 - t.ty0 + 1 - t.po;
-    const size_t goff = (size_t)t.po * ldG;
+    g.bt = t.tx1 - t.tx0 + 1;
+    g.bo = t.px1 - t.tx0 + 1;
+    g.no = t.py1 - t.ty0 + 1 - t.po;
+    bt_max = std::max(bt_max, g.bt);
+    bo_max = std::max(bo_max, g.bo);
+    B.fj_rows = std::max(B.fj_rows, g.nt);
+    B.ij_rows = std::max(B.ij_rows, g.no);
+  }
+  czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
+  czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
+  const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)std::max(2, B.gf.M));
+  const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)std::max(2, B.gi.M));
+  std::vector<double> tf(B.ntiles), ti(B.ntiles), tb(B.ntiles);
+  for (int i = 0; i < B.ntiles; ++i) {
+    const Geom &g = gm[i];
+    tf[i] = (double)g.nt * B.gf.nvp * B.gf.nuc * f1;
+    ti[i] = 2.0 * g.no * B.gi.nvp * B.gi.nuc * f2;
     // algorithmic work: the contraction flops (2MNK of each partial x-DCT) and, for the y-solve,
     // Q-hat read (4 B) per (T row, frequency) plus the two fp32 gradient planes written (8 B)
     // per (output row, frequency); the fp64 pivots are added once per chain below
-    B.fwd_flops += 2.0 * nt * bt * n1t;
-    B.inv_flops += 2.0 * 2.0 * no * bo * n1t;
-    B.solve_bytes += (double)nt * n1t * 4.0 + (double)no * n1t * 8.0;
-    fj.push_back({q + ((size_t)i * B.AT + f0) * ldq + (t.tx0 & 3),
-                  B.qhat + ((size_t)i * B.AT + f0) * B.ldn, nt, ldq, B.ldn, t.tx0, bt, n1t, 0});
-    ij.push_back({B.phx + (size_t)i * B.AP * B.ldn, G + (size_t)i * B.AP * ldG + goff, no, B.ldn,
-                  ldG, t.tx0, n1t, bo, 2});
-    ij.push_back({B.phy + (size_t)i * B.AP * B.ldn, G + gplane + (size_t)i * B.AP * ldG + goff, no,
-                  B.ldn, ldG, t.tx0, n1t, bo, 1});
-    bt_max = std::max(bt_max, bt);
-    bo_max = std::max(bo_max, bo);
-    B.fj_rows = std::max(B.fj_rows, nt);
-    B.ij_rows = std::max(B.ij_rows, no);
+    B.fwd_flops += 2.0 * g.nt * g.bt * n1t;
+    B.inv_flops += 2.0 * 2.0 * g.no * g.bo * n1t;
+    tb[i] = (double)g.nt * n1t * 4.0 + (double)g.no * n1t * 8.0;
   }
-  for (int c = 0; c < B.nchains; ++c) {
-    const ProjTile &t = B.tiles[first[c]];
-    B.solve_bytes += (double)(t.ty1 - t.ty0 + 1) * n1t * 8.0;
-  }
-  B.nfj = (int)fj.size();
-  B.nij = (int)ij.size();
-  const bool okf = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
-  const bool oki = czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
-  // estimated times (measured rates): 3xTF32 GEMM at ~400 TF/s tf32, fp32 FFT pairs at ~12 TF/s
-  // (5 M log2 M flops per FFT; config-4 forward launch: 14 TF/s)
-  double t_gemm = 0, t_czt = 0;
-  const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)std::max(2, B.gf.M));
-  const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)std::max(2, B.gi.M));
-  for (int i = 0; i < B.ntiles; ++i) {
-    t_gemm += 3.0 * (2.0 * fj[i].rows * fj[i].ulen * fj[i].vlen +
-                     2.0 * 2.0 * ij[2 * i].rows * ij[2 * i].ulen * ij[2 * i].vlen) / 400e12;
-    B.fwd_fft_flops += (double)fj[i].rows * B.gf.nvp * B.gf.nuc * f1;
-    B.inv_fft_flops += 2.0 * ij[2 * i].rows * B.gi.nvp * B.gi.nuc * f2;
-  }
-  t_czt = (B.fwd_fft_flops + B.inv_fft_flops) / 12e12;
-  // accuracy: the tensor-core fp32 accumulation over K = N terms loses ~4e-5 of tau at N = 8193
-  // (config-4 global projection) while the chirp-z stays at ~1e-7, so long axes always take it
-  const bool long_axis = n1t > 4096;
-  B.czt = okf && oki && (!T || ctx->dct_mode == 2 || (ctx->dct_mode == 0 && (long_axis || t_czt < t_gemm)));
+  B.czt = choose_czt(ctx, B.tiles, n1t, T != nullptr, fr0, fr1);
   if (!T && !B.czt) return fail(ctx, TVS_EINVAL, "projection batch without DCT tables needs chirp-z");
-  if (B.czt) {
-    std::vector<float2> gt, tw;
-    czt_tables(B.gf, gt, tw);
-    TRY(upload(ctx, P.bufs, &B.gtab_f, gt));
+  // ---- tile groups sharing one scratch (chirp-z form only)
+  const bool need_z = (size_t)B.AT * 32 * sizeof(float) > 160 * 1024;   // solve3 z in global memory
+  int gt = B.ntiles;
+  if (B.czt && gtiles > 0) gt = std::min(gt, gtiles);
+  if (local_io && gt != gtiles) return fail(ctx, TVS_EINVAL, "group-local projection needs the chirp-z form");
+  B.gtiles = gt;
+  B.g0.clear();
+  for (int i = 0; i < B.ntiles; i += gt) B.g0.push_back(i);
+  B.g0.push_back(B.ntiles);
+  const int ng = (int)B.g0.size() - 1;
+  B.gfwd.assign(ng, 0.0);
+  B.ginv.assign(ng, 0.0);
+  B.gsolve.assign(ng, 0.0);
+  for (int k = 0; k < ng; ++k)
+    for (int i = B.g0[k]; i < B.g0[k + 1]; ++i) {
+      B.gfwd[k] += tf[i];
+      B.ginv[k] += ti[i];
+      B.gsolve[k] += tb[i];
+    }
+  for (int c = 0; c < B.nchains; ++c) {   // pivots read once per chain (per group that holds it)
+    const ProjTile &t = B.tiles[first[c]];
+    for (int k = 0; k < ng; ++k) {
+      bool has = false;
+      for (int i = B.g0[k]; i < B.g0[k + 1] && !has; ++i) has = B.tiles[i].chain == c;
+      if (has) B.gsolve[k] += (double)(t.ty1 - t.ty0 + 1) * n1t * 8.0;
+    }
+  }
+  for (int k = 0; k < ng; ++k) {
+    B.fwd_fft_flops += B.gfwd[k];
+    B.inv_fft_flops += B.ginv[k];
+    B.solve_bytes += B.gsolve[k];
+  }
+  TRY(dalloc(ctx, P.bufs, &B.qhat, (size_t)gt * B.AT * B.ldn));
+  if (need_z) TRY(dalloc(ctx, P.bufs, &B.z, (size_t)gt * B.AT * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.rinv, (size_t)B.nchains * B.AT * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phx, (size_t)gt * B.AP * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.phy, (size_t)gt * B.AP * B.ldn));
+  // ∇φ output is plane-major: G[c][tile][AP][ldG]
+  const size_t gplane = gplane_arg ? gplane_arg : (size_t)B.ntiles * B.AP * ldG;
+  if (!B.czt) {   // dense 3xTF32 tcgen05 contractions, one group
+    std::vector<GemmDesc2> fwd2, inv2;
+    for (int i = 0; i < B.ntiles;) {
+      // run of consecutive tiles sharing (tx0, tx1, px1): one stacked GEMM (rows = count * AT/AP)
+      int j = i + 1;
+      while (j < B.ntiles && B.tiles[j].tx0 == B.tiles[i].tx0 && B.tiles[j].tx1 == B.tiles[i].tx1 &&
+             B.tiles[j].px1 == B.tiles[i].px1)
+        ++j;
+      const ProjTile &t = B.tiles[i];
+      const int cnt = j - i;
+      const int bt = t.tx1 - t.tx0 + 1, bo = t.px1 - t.tx0 + 1;
+      int Mf = (cnt - 1) * B.AT + (B.tiles[j - 1].ty1 - B.tiles[j - 1].ty0 + 1);
+      const int Mi = (cnt - 1) * B.AP + (B.tiles[j - 1].py1 - B.tiles[j - 1].ty0 + 1 - B.tiles[j - 1].po);
+      int f0 = 0;   // forward rows [f0, f0 + Mf) of the stacked operand; inverse output rows from po
+      if (fr0 >= 0) {
+        f0 = fr0;
+        Mf = fr1 - fr0;
+      }
+      const size_t goff = (size_t)t.po * ldG;
+      // 3xTF32: A (q, Phi) is one fp32 plane split in the kernel, B = the pre-split DCT tables; q
+      // carries a leading zero offset of (tx0 & 3) columns so the table rows start 16-byte
+      // aligned: K = bt + off, tables from column tx0 - off
+      const int off = t.tx0 & 3;
+      fwd2.push_back({q + ((size_t)i * B.AT + f0) * ldq, nullptr, T->part(2) + (t.tx0 - off),
+                      T->part(3) + (t.tx0 - off), B.qhat + ((size_t)i * B.AT + f0) * B.ldn, Mf, n1t,
+                      bt + off, ldq, T->ld, B.ldn});
+      inv2.push_back({B.phx + (size_t)i * B.AP * B.ldn, nullptr, T->part(4) + (size_t)t.tx0 * T->ld,
+                      T->part(5) + (size_t)t.tx0 * T->ld, G + (size_t)i * B.AP * ldG + goff, Mi, bo,
+                      n1t, B.ldn, T->ld, ldG});
+      inv2.push_back({B.phy + (size_t)i * B.AP * B.ldn, nullptr, T->part(0) + (size_t)t.tx0 * T->ld,
+                      T->part(1) + (size_t)t.tx0 * T->ld, G + gplane + (size_t)i * B.AP * ldG + goff,
+                      Mi, bo, n1t, B.ldn, T->ld, ldG});
+      B.tcM_fwd = std::max(B.tcM_fwd, Mf);
+      B.tcM_inv = std::max(B.tcM_inv, Mi);
+      B.fwdN = std::max(B.fwdN, n1t);
+      B.invN = std::max(B.invN, bo);
+      i = j;
+    }
+    B.nstack = (int)fwd2.size();
+    std::vector<TmaGemmDesc> fwd3(fwd2.size()), inv3(inv2.size());
+    for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
+    for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
+    TRY(upload(ctx, P.bufs, &B.d_fwd, fwd3));
+    TRY(upload(ctx, P.bufs, &B.d_inv, inv3));
+  } else {   // chirp-z jobs: one forward job per tile, two inverse jobs (x: sin, y: cos) per tile
+    std::vector<CztJob> fj, ij;
+    for (int k = 0; k < ng; ++k)
+      for (int i = B.g0[k]; i < B.g0[k + 1]; ++i) {
+        const ProjTile &t = B.tiles[i];
+        const Geom &g = gm[i];
+        const size_t sl = (size_t)(i - B.g0[k]);   // scratch slot within the group
+        const size_t goff = (size_t)t.po * ldG;
+        const size_t io = local_io ? sl : (size_t)i;   // slot of q / G
+        fj.push_back({q + (io * B.AT + g.f0) * ldq + (t.tx0 & 3),
+                      B.qhat + (sl * B.AT + g.f0) * B.ldn, g.nt, ldq, B.ldn, t.tx0, g.bt, n1t, 0});
+        ij.push_back({B.phx + sl * B.AP * B.ldn, G + io * B.AP * ldG + goff, g.no, B.ldn,
+                      ldG, t.tx0, n1t, g.bo, 2});
+        ij.push_back({B.phy + sl * B.AP * B.ldn, G + gplane + io * B.AP * ldG + goff, g.no,
+                      B.ldn, ldG, t.tx0, n1t, g.bo, 1});
+      }
+    B.nfj = (int)fj.size();
+    B.nij = (int)ij.size();
+    std::vector<float2> gt2, tw;
+    czt_tables(B.gf, gt2, tw);
+    TRY(upload(ctx, P.bufs, &B.gtab_f, gt2));
     TRY(upload(ctx, P.bufs, &B.tw_f, tw));
-    czt_tables(B.gi, gt, tw);
-    TRY(upload(ctx, P.bufs, &B.gtab_i, gt));
+    czt_tables(B.gi, gt2, tw);
+    TRY(upload(ctx, P.bufs, &B.gtab_i, gt2));
     TRY(upload(ctx, P.bufs, &B.tw_i, tw));
     {   // chirp tables: one device buffer for both job lists
       std::vector<size_t> pf, qf, pi, qi;
-      std::vector<float2> tf = czt_chirp_tables(B.gf.N, fj, pf, qf);
-      std::vector<float2> ti = czt_chirp_tables(B.gi.N, ij, pi, qi);
-      const size_t nf = tf.size();
-      tf.insert(tf.end(), ti.begin(), ti.end());
+      std::vector<float2> tfw = czt_chirp_tables(B.gf.N, fj, pf, qf);
+      std::vector<float2> tiv = czt_chirp_tables(B.gi.N, ij, pi, qi);
+      const size_t nf = tfw.size();
+      tfw.insert(tfw.end(), tiv.begin(), tiv.end());
       float2 *dch = nullptr;
-      TRY(upload(ctx, P.bufs, &dch, tf));
+      TRY(upload(ctx, P.bufs, &dch, tfw));
       for (size_t k = 0; k < fj.size(); ++k) {
         fj[k].pre = dch + pf[k];
         fj[k].post = dch + qf[k];
@@ -598,25 +695,24 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     }
     TRY(upload(ctx, P.bufs, &B.d_fj, fj));
     TRY(upload(ctx, P.bufs, &B.d_ij, ij));
-  } else {
-    B.nstack = (int)fwd2.size();
-    std::vector<TmaGemmDesc> fwd3(fwd2.size()), inv3(inv2.size());
-    for (size_t i = 0; i < fwd2.size(); ++i) CK(make_tma_desc(&fwd3[i], fwd2[i], 144));
-    for (size_t i = 0; i < inv2.size(); ++i) CK(make_tma_desc(&inv3[i], inv2[i], 144));
-    TRY(upload(ctx, P.bufs, &B.d_fwd, fwd3));
-    TRY(upload(ctx, P.bufs, &B.d_inv, inv3));
   }
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
     CK(launch_segprod(B.d_tiles, B.d_first, B.nchains, B.rinv, B.ldn, B.AT, n1t, B.segprod, 0));
-    {   // tiles grouped by chain (layout row) for the solve's launch order
-      std::vector<std::vector<int>> byc(B.nchains);
-      for (int i = 0; i < B.ntiles; ++i) byc[B.tiles[i].chain].push_back(i);
-      for (auto &v : byc) B.per_chain = std::max(B.per_chain, (int)v.size());
-      std::vector<int> order((size_t)B.nchains * B.per_chain, -1);
-      for (int c = 0; c < B.nchains; ++c)
-        for (size_t k = 0; k < byc[c].size(); ++k) order[(size_t)c * B.per_chain + k] = byc[c][k];
+    {   // per group: its tiles grouped by chain (layout row) for the solve's launch order
+      for (int k = 0; k < ng; ++k) {
+        std::vector<int> cntc(B.nchains, 0);
+        for (int i = B.g0[k]; i < B.g0[k + 1]; ++i) B.per_chain = std::max(B.per_chain, ++cntc[B.tiles[i].chain]);
+      }
+      std::vector<int> order((size_t)ng * B.nchains * B.per_chain, -1);
+      for (int k = 0; k < ng; ++k) {
+        std::vector<int> cntc(B.nchains, 0);
+        for (int i = B.g0[k]; i < B.g0[k + 1]; ++i) {
+          const int c = B.tiles[i].chain;
+          order[((size_t)k * B.nchains + c) * B.per_chain + cntc[c]++] = i - B.g0[k];
+        }
+      }
       TRY(upload(ctx, P.bufs, &B.d_order, order));
     }
     if (ctx->solve_tma) {   // TMA boxes of {J columns, <= 256 rows} for the staged blocks
@@ -624,7 +720,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       m.nbox = (B.AT + 255) / 256;
       // even row counts: every box of the fp32 block then starts 128-byte aligned (J = 16 columns)
       m.box_rows = round_up((B.AT + m.nbox - 1) / m.nbox, 2);
-      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, B.ntiles * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
+      CK(encode_plain_2d(&m.q, B.qhat, false, n1t, gt * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       CK(encode_plain_2d(&m.r, B.rinv, true, n1t, B.nchains * B.AT, B.ldn, solve4_width(B.AT), m.box_rows));
       B.smem_rows = m.nbox * m.box_rows;
       TRY(upload(ctx, P.bufs, &B.d_smaps, std::vector<SolveMaps>{m}));
@@ -737,9 +833,9 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
   TRY(upload(ctx, P->bufs, &P->d_loy, ly));
   TRY(upload(ctx, P->bufs, &P->d_lox, lx));
   const int C = P->planes;
-  size_t vsz = (size_t)g.M * C * g.A * g.ldS;
-  TRY(dalloc(ctx, P->bufs, &P->v[0], vsz));
-  TRY(dalloc(ctx, P->bufs, &P->v[1], vsz));
+  const size_t vsub = (size_t)C * g.A * g.ldS;   // one subdomain's dual planes
+  g.MG = g.M;
+  TRY(dalloc(ctx, P->bufs, &P->v[0], g.M * vsub));   // qhat_m of every local subdomain
   TRY(dalloc(ctx, P->bufs, &P->p, (size_t)C * G2 * P->ld));
   TRY(dalloc(ctx, P->bufs, &P->d_bad, 1));
   TRY(dalloc(ctx, P->bufs, &P->d_part, 4 * 1024));
@@ -751,6 +847,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->recv_dn, (size_t)C * std::max(1, D.dr1 - D.dr0) * P->ld));
   }
   if (step == 2) {
+    TRY(dalloc(ctx, P->bufs, &P->v[1], g.M * vsub));
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->f, (size_t)G2 * P->ld));
     TRY(dalloc(ctx, P->bufs, &P->g0, (size_t)G1));
@@ -761,25 +858,62 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     const bool czt_only = G1 > 4096 && ctx->dct_mode != 1;
     Tables *T = nullptr;
     if (!czt_only) TRY(get_tables(ctx, G1, &T));
-    TRY(dalloc(ctx, P->bufs, &P->om, (size_t)g.M * 2 * g.AP * g.ldP));
-    TRY(dalloc(ctx, P->bufs, &P->vtmp, vsz));
-    TRY(dalloc(ctx, P->bufs, &P->q, (size_t)g.M * g.AT * g.ldT));
-    TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)g.M * 2 * g.AP * g.ldP));
     size_t pl = (size_t)G2 * P->ld;
     TRY(dalloc(ctx, P->bufs, &P->f, 2 * pl));
-    TRY(dalloc(ctx, P->bufs, &P->t0, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->w, 2 * pl));
+    P->t0 = P->w;   // tau_0 is needed only for f, before the first residual writes w
     TRY(dalloc(ctx, P->bufs, &P->r, 2 * pl));
     TRY(dalloc(ctx, P->bufs, &P->qg, pl));
     TRY(dalloc(ctx, P->bufs, &P->Gg, 2 * pl));
-    std::vector<ProjTile> lt;
-    for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
-    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T));
     // global projection: the y-solves span every row; this rank transforms its core rows
-    // (qhat of the others arrives by all-gather) and needs grad phi only on its valid rows V
+    // (qhat of the others arrives by all-gather) and needs grad phi only on its valid rows V.
+    // Built first: the local subdomain groups are then sized to the memory that is left.
     std::vector<ProjTile> gt = {{0, G2 - 1, 0, G1 - 1, D.V1 - 1, G1 - 1, 0, D.V0}};
     TRY(build_proj(ctx, *P, P->global, gt, G2, G1, P->qg, P->ld, P->Gg, P->ld, T, D.R0,
                    D.R1, pl));
+    // Subdomain groups.  Every buffer of a local solve -- theta p / the ping-pong dual, q, grad
+    // phi, omega0 and the projection scratch -- is held for one group of consecutive subdomains
+    // only; the groups of a sweep run one after the other (the local solves are independent,
+    // Alg. 2 is additive) and only qhat_m of every subdomain persists.  One group whenever the
+    // whole batch fits (configs 1-4); config 5 on one GPU (256 subdomains of 2080^2 with 32769
+    // frequencies, ~1.1 GB of scratch each) needs ~20.  The paper: each block is solved "with
+    // never needing more access memory than a constant times the biggest block".
+    std::vector<ProjTile> lt;
+    for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
+    const bool czt_local = choose_czt(ctx, lt, G1, T != nullptr, -1, -1);
+    int sg = g.M;
+    if (czt_local) {
+      const double per_sub = (double)vsub * 4 + (double)g.AT * g.ldT * 4 +
+                             2.0 * 2.0 * g.AP * g.ldP * 4 + proj_tile_bytes(g.AT, g.AP, G1);
+      const double rinv = (double)P->m2loc * g.AT * round_up(G1, 4) * 8;
+      size_t freeb = 0, totb = 0;
+      if (cudaMemGetInfo(&freeb, &totb) == cudaSuccess) {
+        // keep 4 GB and a third of the rest free (outputs, the other step's plan, allocator slack)
+        const double budget = ((double)freeb - 4e9) * 2.0 / 3.0 - rinv;
+        if (per_sub * g.M > budget) sg = std::max(1, (int)(budget / per_sub));
+      }
+      if (ctx->proj_group > 0) sg = std::min(sg, ctx->proj_group);
+    }
+    P->sg0.clear();
+    for (int i = 0; i < g.M; i += sg) P->sg0.push_back(i);
+    P->sg0.push_back(g.M);
+    P->sgs.clear();
+    for (size_t k = 0; k + 1 < P->sg0.size(); ++k) {
+      int64_t sS = 0, sT = 0;
+      for (int i = P->sg0[k]; i < P->sg0[k + 1]; ++i) {
+        const SubDesc &s = P->subs[i];
+        sS += (int64_t)(s.y1 - s.y0 + 1) * (s.x1 - s.x0 + 1);
+        sT += (int64_t)(s.ty1 - s.y0 + 1) * (s.tx1 - s.x0 + 1);
+      }
+      P->sgs.push_back({sS, sT});
+    }
+    g.MG = sg;
+    TRY(dalloc(ctx, P->bufs, &P->v[1], (size_t)sg * vsub));
+    TRY(dalloc(ctx, P->bufs, &P->om, (size_t)sg * 2 * g.AP * g.ldP));
+    TRY(dalloc(ctx, P->bufs, &P->q, (size_t)sg * g.AT * g.ldT));
+    TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)sg * 2 * g.AP * g.ldP));
+    TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T, -1, -1,
+                   (size_t)sg * g.AP * g.ldP, sg, sg < g.M));
   }
   *out = P.get();
   ctx->plans[key] = std::move(P);
@@ -943,11 +1077,16 @@ bool stop_now(const tvs_ctx *ctx, double d_prev, double d_next, double npts, dou
 
 // grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).  For the
 // global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
-tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
+// grad phi of phi = R_T Delta^dagger E_T q for the tiles of group k of the batch (kernel b).  For
+// the global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
+tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_t s,
+                         bool gather = false) {
   const int G2 = P.G2, G1 = P.G1;
+  if (gather && B.g0.size() != 2) return fail(ctx, TVS_EINVAL, "gathered projection batch must be one group");
+  const int t0 = B.g0[k], nt = B.g0[k + 1] - t0;
   if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
-    TRY(run(ctx, s, F_CZT_FWD, 0, B.fwd_fft_flops, [&] {
-      return launch_czt(B.d_fj, B.nfj, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
+    TRY(run(ctx, s, F_CZT_FWD, 0, B.gfwd[k], [&] {
+      return launch_czt(B.d_fj + t0, nt, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
     }));
   } else {       // dense 3xTF32 tcgen05 contraction (persistent, A in tensor memory)
     TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
@@ -955,23 +1094,30 @@ tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bo
     }));
   }
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
-  TRY(run(ctx, s, F_SOLVE, B.solve_bytes, 0, [&] {
+  TRY(run(ctx, s, F_SOLVE, B.gsolve[k], 0, [&] {
     // segmented fp64 y-solve: staged in shared memory (solve4) when the tile height allows,
     // else solve3 (shared-memory z up to 160 KB per column block, fp32 global scratch beyond)
     if (B.segprod)
-      return launch_proj_solve4(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
+      return launch_proj_solve4(B.d_tiles + t0, nt, G2, G1, B.qhat, B.AT, B.ldn, B.rinv,
                                 B.segprod, B.phx, B.phy, B.AP, B.d_smaps, B.smem_rows,
-                                B.d_order, B.nchains, B.per_chain, s);
-    return launch_proj_solve3(B.d_tiles, B.ntiles, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
+                                B.d_order + (size_t)k * B.nchains * B.per_chain, B.nchains,
+                                B.per_chain, s);
+    return launch_proj_solve3(B.d_tiles + t0, nt, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
                               B.phx, B.phy, nullptr, nullptr, B.AP, s);
   }));
   if (B.czt)
-    return run(ctx, s, F_CZT_INV, 0, B.inv_fft_flops, [&] {
-      return launch_czt(B.d_ij, B.nij, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
+    return run(ctx, s, F_CZT_INV, 0, B.ginv[k], [&] {
+      return launch_czt(B.d_ij + 2 * t0, 2 * nt, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
     });
   return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
     return launch_gemm_tma_ts(B.d_inv, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
   });
+}
+
+// All groups of a batch (the global batch is one group).
+tvs_status project_batch(tvs_ctx *ctx, Plan &P, ProjBatch &B, cudaStream_t s, bool gather = false) {
+  for (int k = 0; k + 1 < (int)B.g0.size(); ++k) TRY(project_group(ctx, P, B, k, s, gather));
+  return TVS_OK;
 }
 
 tvs_status check_common(tvs_ctx *ctx, int32_t n2, int32_t n1, tvs_layout L, tvs_iters it) {
@@ -1174,7 +1320,8 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       return launch_axpby2(P->f, P->w, P->Gg, ld, G2, G1, scale, -scale, scale, out, D.E0, D.V1, rs);
     });
   };
-  int cur = 0;
+  const int ngs = (int)P->sg0.size() - 1;
+  const size_t vsub = (size_t)4 * g.A * g.ldS;
   const double prediv_bytes = 16.0 * P->sum_S + 4.0 * P->sum_T;
   const double sweep_bytes = 48.0 * (double)P->sum_S;
   // D_TFS(p^n) = ||r^n||^2 (Eq. tfsdualdis) on this rank's core rows
@@ -1214,27 +1361,41 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       }
       e_prev = e;
     }
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_load_tp(P->d_subs, g, P->d_thy, P->d_thx, P->p, ld, G2, G1, P->vtmp, s);
-    }));
-    TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-            [&] { return launch_prediv1(P->d_subs, g, P->vtmp, G2, G1, P->q, nullptr, s); }));
-    TRY(project_batch(ctx, *P, P->local, s));
-    if (overlap) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-      return launch_omega0_1(P->d_subs, g, P->r, ld, P->vtmp, P->gphi, g.ldP, G2, G1, P->om, s);
-    }));
-    for (int k = 0; k < it.inner; ++k) {
-      TRY(run(ctx, s, F_PREDIV, prediv_bytes, 0,
-              [&] { return launch_prediv1(P->d_subs, g, P->v[cur], G2, G1, P->q, nullptr, s); }));
-      TRY(project_batch(ctx, *P, P->local, s));
-      TRY(run(ctx, s, F_SWEEP1, sweep_bytes, 0, [&] {
-        return launch_sweep1(P->d_subs, g, P->d_thy, P->d_thx, P->v[cur], P->gphi, g.ldP, P->om,
-                             P->v[cur ^ 1], G2, G1, it.t, s);
+    // the local solves, one subdomain group after the other (one group unless memory-bound)
+    for (int k = 0; k < ngs; ++k) {
+      Geo gk = g;
+      gk.M = P->sg0[k + 1] - P->sg0[k];
+      const SubDesc *sk = P->d_subs + P->sg0[k];
+      float *vper = P->v[0] + (size_t)P->sg0[k] * vsub;   // qhat_m of the group (persistent)
+      float *vscr = P->v[1];                               // group scratch
+      const double pdb = 16.0 * P->sgs[k].first + 4.0 * P->sgs[k].second;   // pre-div bytes
+      const double swb = 48.0 * P->sgs[k].first;                             // kernel (a') bytes
+      // omega0_m = R r^n + P_loc multidiv (theta_m p^n)  (theta p in the scratch dual)
+      TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+        return launch_load_tp(sk, gk, P->d_thy, P->d_thx, P->p, ld, G2, G1, vscr, s);
       }));
-      cur ^= 1;
+      TRY(run(ctx, s, F_PREDIV, pdb, 0,
+              [&] { return launch_prediv1(sk, gk, vscr, G2, G1, P->q, nullptr, s); }));
+      TRY(project_group(ctx, *P, P->local, k, s));
+      if (overlap && k == 0) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+      TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+        return launch_omega0_1(sk, gk, P->r, ld, vscr, P->gphi, g.ldP, G2, G1, P->om, s);
+      }));
+      float *vin = vper, *vout = vscr;
+      for (int kk = 0; kk < it.inner; ++kk) {
+        TRY(run(ctx, s, F_PREDIV, pdb, 0,
+                [&] { return launch_prediv1(sk, gk, vin, G2, G1, P->q, nullptr, s); }));
+        TRY(project_group(ctx, *P, P->local, k, s));
+        TRY(run(ctx, s, F_SWEEP1, swb, 0, [&] {
+          return launch_sweep1(sk, gk, P->d_thy, P->d_thx, vin, P->gphi, g.ldP, P->om, vout, G2,
+                               G1, it.t, s);
+        }));
+        std::swap(vin, vout);
+      }
+      if (vin != vper)   // odd inner count: the last update landed in the scratch
+        CK(cudaMemcpyAsync(vper, vin, (size_t)gk.M * vsub * sizeof(float), cudaMemcpyDeviceToDevice, s));
     }
-    TRY(combine_step(ctx, *P, P->v[cur], s));
+    TRY(combine_step(ctx, *P, P->v[0], s));
   }
   // tau = P tau_0 - delta P multidiv p = delta r^S; every rank ends with the full field
   TRY(residual(P->r, delta, s));
@@ -1300,6 +1461,7 @@ tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id
   if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
+  if (const char *pg = getenv("TVS_PROJ_GROUP")) c->proj_group = std::max(0, atoi(pg));
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {

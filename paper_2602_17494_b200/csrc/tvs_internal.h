@@ -111,7 +111,9 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
 
 // Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
 struct Geo {
-  int M;          // number of subdomains in the batch
+  int M;          // number of subdomains in the batch (grid z of the launches)
+  int MG;         // plane stride of the grad-phi planes, in subdomains (>= M; the capacity of a
+                  // subdomain group, see Plan::sg in tvs_api.cu)
   int A, B;       // rows/cols of S (max)
   int AP, BP;     // rows/cols of S+ (max)
   int AT, BT;     // rows/cols of T (max)

@@ -929,7 +929,7 @@ __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float 
   size_t pl = (size_t)n2 * ld;
   for (int k = 0; k < 2; ++k) {
     float w = w_S(vb, k, li, lj, gi, gj, a, b, g, n2, n1);
-    float gp = gphi[(((size_t)k * g.M + blockIdx.z) * g.AP + li) * ldg + lj];
+    float gp = gphi[(((size_t)k * g.MG + blockIdx.z) * g.AP + li) * ldg + lj];
     om[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * g.ldP + lj] =
         r[k * pl + (size_t)gi * ld + gj] + (w - gp);
   }
@@ -1068,8 +1068,8 @@ k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   const float *vb = vin + (size_t)blockIdx.z * 4 * g.A * g.ldS;
   float *ob = vout + (size_t)blockIdx.z * 4 * g.A * g.ldS;
   const size_t pl = (size_t)g.A * g.ldS;
-  const float *g1 = gphi + ((size_t)0 * g.M + blockIdx.z) * g.AP * ldg;
-  const float *g2 = gphi + ((size_t)1 * g.M + blockIdx.z) * g.AP * ldg;
+  const float *g1 = gphi + ((size_t)0 * g.MG + blockIdx.z) * g.AP * ldg;
+  const float *g2 = gphi + ((size_t)1 * g.MG + blockIdx.z) * g.AP * ldg;
   const float *o1 = om + ((size_t)blockIdx.z * 2 + 0) * g.AP * g.ldP;
   const float *o2 = om + ((size_t)blockIdx.z * 2 + 1) * g.AP * g.ldP;
   const float thA = pc.SA ? thx[sd.ix * g.B + pc.jA] : 0.f;

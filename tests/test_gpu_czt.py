@@ -81,3 +81,33 @@ def test_config3_czt_full_size(ctx):
     img = c.image()
     L = (c.m2, c.m1, c.overlap, c.overlap)
     check_step1(ctx, img, c.delta, L, 1, 2)
+
+
+@pytest.fixture(scope="module")
+def ctx_grouped():
+    """Tile groups of at most 3 tiles sharing one projection scratch (TVS_PROJ_GROUP=3): the path
+    config 5 takes at full size, where the whole local batch's scratch would exceed HBM."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = _context(TVS_DCT="czt", TVS_PROJ_GROUP="3")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("shape,L", [((37, 53), (3, 2, 3, 5)), ((64, 64), (4, 4, 4, 4)),
+                                     ((40, 18), (4, 1, 4, 0)), ((300, 90), (2, 2, 8, 4)),
+                                     ((1400, 40), (1, 4, 0, 4))])
+def test_step1_czt_tile_groups(ctx, ctx_grouped, shape, L):
+    """Groups of 3 consecutive tiles (ragged last group; groups spanning several layout rows, so
+    solve4's per-group launch order and solve3's tile offsets are both exercised -- the 300-row
+    case has tiles taller than solve4's shared-memory limit): parity with the oracle, and bitwise
+    equality with the ungrouped batch (same kernels, same per-tile arithmetic).  The 1400-row
+    tiles are taller than solve4's shared-memory limit and than solve3's shared z (global z
+    scratch, shared by the group), as config 5's 2083-row tiles."""
+    img = random_image(*shape, seed=shape[0] * 11 + shape[1])
+    check_step1(ctx_grouped, img, 0.05, L, 3, 4)
+    d0 = torch.from_numpy(img).cuda()
+    t1, p1, _ = ctx.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125), want_p=True)
+    t2, p2, _ = ctx_grouped.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125), want_p=True)
+    torch.cuda.synchronize()
+    assert torch.equal(t1, t2) and torch.equal(p1, p2)
