@@ -324,8 +324,7 @@ def _tfs_inner_local(m, lay, p, r_global, qhat_m, inner, t):
     """Alg. 5, localized TFS inner loop on Omega~_m / Omega~_{m,+}:
     omega0_loc = R_{S+}(f - P multidiv sum_{l != m} theta_l p)
                = R_{S+} r + R_{S+} P E_{S+} multidiv_{S+} E_S (theta_m p)   (r = f - P multidiv p);
-    psi = R_S E multigrad_{S+}(R_{S+} P E_{S+} multidiv_{S+} E_S v - omega0_loc);
-    v_k <- (theta v_k + t theta psi_k)/(theta + t |psi_k|)."""
+    then tfs_local_iterations."""
     n2t, n1t = lay.n2 + 1, lay.n1 + 1
     cy = spectral.cut_points(n2t, lay.m2)
     cx = spectral.cut_points(n1t, lay.m1)
@@ -336,7 +335,20 @@ def _tfs_inner_local(m, lay, p, r_global, qhat_m, inner, t):
     tp = th * restrict(p, whole, s)
     w_m = ops.multidiv(extend(tp, s, sp))
     omega0 = restrict(r_global, whole, sp) + local_projection(w_m, sp, n2t, n1t, cy, cx)
-    v = np.array(qhat_m, np.float64)
+    return tfs_local_iterations(lay, m, omega0, qhat_m, inner, t)
+
+
+def tfs_local_iterations(lay, m, omega0, v0, inner, t):
+    """The inner loop of Alg. 5 given omega0 on S+: ``inner`` times
+    psi = R_S E multigrad_{S+}(R_{S+} P E_{S+} multidiv_{S+} E_S v - omega0);
+    v_k <- (theta v_k + t theta psi_k)/(theta + t |psi_k|).  Only arrays on S / S+ / T."""
+    n2t, n1t = lay.n2 + 1, lay.n1 + 1
+    cy = spectral.cut_points(n2t, lay.m2)
+    cx = spectral.cut_points(n1t, lay.m1)
+    s = lay.rect(m, extended=True)
+    sp = rect_plus(s, n2t, n1t)
+    th = lay.theta_rect(m, extended=True)
+    v = np.array(v0, np.float64)
     for _ in range(inner):
         w = ops.multidiv(extend(v, s, sp))
         pw = local_projection(w, sp, n2t, n1t, cy, cx)

@@ -80,6 +80,52 @@ def project_multi(w):
     return project(w)
 
 
+def lap_pinv_rows(q, rows):
+    """Rows ``rows`` of (Delta)^dagger q (the restriction R_B of Eq. form:DiscInvLapl, P:611-625,
+    to the rows B of the output): C_{N2}[:, B]^T ((Delta~)^dagger * (C_{N2} q C_{N1}^T)) C_{N1}.
+    Same formula as lap_pinv with only the needed output rows formed -- for grids too large to
+    hold the full result next to the DCT matrices (config 5: N~ = 32769)."""
+    n2, n1 = q.shape
+    rows = np.asarray(rows, dtype=np.int64)
+    c2 = dct_matrix(n2)
+    c1 = c2 if n1 == n2 else dct_matrix(n1)
+    x = c2 @ (np.asarray(q, np.float64) @ c1.T)
+    for a in range(0, n2, 1024):   # x *= (Delta~)^dagger, a row block of the diagonal at a time
+        b = min(n2, a + 1024)
+        si = sigma(n2)[a:b, None] ** 2
+        den = si + sigma(n1)[None, :] ** 2
+        lam = np.zeros_like(den)
+        nz = den != 0.0
+        lam[nz] = -1.0 / den[nz]
+        x[a:b] *= lam
+    return (c2[:, rows].T @ x) @ c1
+
+
+def project_rows(w, rows):
+    """Rows ``rows`` of P_{K^h} w = w - grad (Delta)^dagger div w (Eq. formula:PKh, P:606-610);
+    grad = (D+_x, D+_y) needs phi on rows r and r + 1 (zero D+_y on the last row).
+    Returns (sorted rows, (2, len(rows), n1))."""
+    w = np.asarray(w, np.float64)
+    rows = np.asarray(sorted(set(int(r) for r in rows)), dtype=np.int64)
+    return project_rows_div(ops.div(w), w[:, rows], rows)
+
+
+def project_rows_div(q, w_rows, rows):
+    """project_rows given q = div w and the rows of w (sorted ``rows``): lets a caller free w
+    before the DCT products (config 5: 32769^2 planes)."""
+    n2, n1 = q.shape
+    rows = np.asarray(rows, dtype=np.int64)
+    need = np.asarray(sorted(set(rows.tolist()) | set(min(int(r) + 1, n2 - 1) for r in rows)), dtype=np.int64)
+    phi = lap_pinv_rows(q, need)
+    at = {int(r): k for k, r in enumerate(need)}
+    out = np.empty((2, len(rows), n1))
+    for k, r in enumerate(rows):
+        pr = phi[at[int(r)]]
+        out[0, k] = w_rows[0, k] - np.concatenate([pr[1:] - pr[:-1], [0.0]])
+        out[1, k] = w_rows[1, k] - ((phi[at[int(r) + 1]] - pr) if r < n2 - 1 else 0.0)
+    return rows, out
+
+
 def cut_points(n, m):
     """Near-uniform core cuts c_k = floor(k n / M), k = 0..M (reading A8)."""
     return [k * n // m for k in range(m + 1)]

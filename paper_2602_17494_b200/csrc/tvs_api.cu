@@ -311,6 +311,8 @@ struct tvs_ctx {
   int dct_mode = 0;
   int czt_max_m = 16384;
   int proj_group = 0;            // max tiles per projection group (TVS_PROJ_GROUP; 0 = by memory)
+  bool makhoul = true;           // Makhoul form of the chirp-z where M = 2N - 2 is a power of 4
+                                 // (TVS_CZT_MAKHOUL=0: the general chirp-z form everywhere)
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
   int x2_minw = 512;             // ... on subdomains at least this wide (TVS_X2_MINW)
@@ -464,8 +466,10 @@ bool choose_czt(const tvs_ctx *ctx, const std::vector<ProjTile> &tiles, int n1t,
     bo_max = std::max(bo_max, t.px1 - t.tx0 + 1);
   }
   CztGeom gf{}, gi{};
-  const bool ok = czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &gf) &&
-                  czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &gi);
+  const bool mk = ctx->makhoul && czt_makhoul_geometry(n1t, ctx->czt_max_m, &gf);
+  if (mk) gi = gf;
+  const bool ok = mk || (czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &gf) &&
+                         czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &gi));
   if (!ok) return false;
   if (!have_tables || ctx->dct_mode == 2) return true;
   if (ctx->dct_mode == 1) return false;
@@ -477,7 +481,8 @@ bool choose_czt(const tvs_ctx *ctx, const std::vector<ProjTile> &tiles, int n1t,
     const int nt = fr0 >= 0 ? fr1 - fr0 : t.ty1 - t.ty0 + 1;
     const int no = t.py1 - t.ty0 + 1 - t.po;
     t_gemm += 3.0 * (2.0 * nt * (t.tx1 - t.tx0 + 1) * n1t + 4.0 * no * (t.px1 - t.tx0 + 1) * n1t) / 400e12;
-    t_czt += ((double)nt * gf.nvp * gf.nuc * f1 + 2.0 * no * gi.nvp * gi.nuc * f2) / 12e12;
+    t_czt += mk ? ((double)((nt + 1) / 2) * f1 + (double)((no + 1) / 2 + no) * f2) / 12e12
+                : ((double)nt * gf.nvp * gf.nuc * f1 + 2.0 * no * gi.nvp * gi.nuc * f2) / 12e12;
   }
   return t_czt < t_gemm;
 }
@@ -550,15 +555,22 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.fj_rows = std::max(B.fj_rows, g.nt);
     B.ij_rows = std::max(B.ij_rows, g.no);
   }
-  czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
-  czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
+  const bool mk = ctx->makhoul && czt_makhoul_geometry(n1t, ctx->czt_max_m, &B.gf);
+  if (mk) {
+    B.gi = B.gf;
+  } else {
+    czt_geometry(n1t, bt_max, n1t, ctx->czt_max_m, &B.gf);
+    czt_geometry(n1t, n1t, bo_max, ctx->czt_max_m, &B.gi);
+  }
   const double f1 = 2.0 * 5.0 * B.gf.M * std::log2((double)std::max(2, B.gf.M));
   const double f2 = 2.0 * 5.0 * B.gi.M * std::log2((double)std::max(2, B.gi.M));
   std::vector<double> tf(B.ntiles), ti(B.ntiles), tb(B.ntiles);
   for (int i = 0; i < B.ntiles; ++i) {
     const Geom &g = gm[i];
-    tf[i] = (double)g.nt * B.gf.nvp * B.gf.nuc * f1;
-    ti[i] = 2.0 * g.no * B.gi.nvp * B.gi.nuc * f2;
+    // FFT flops per launch: one FFT pair per CTA (Makhoul form: forward per row pair, inverse
+    // per row pair (y) plus per row (x); general form: per row, chunk and pass, two jobs inverse)
+    tf[i] = mk ? (double)((g.nt + 1) / 2) * f1 : (double)g.nt * B.gf.nvp * B.gf.nuc * f1;
+    ti[i] = mk ? (double)((g.no + 1) / 2 + g.no) * f2 : 2.0 * g.no * B.gi.nvp * B.gi.nuc * f2;
     // algorithmic work: the contraction flops (2MNK of each partial x-DCT) and, for the y-solve,
     // Q-hat read (4 B) per (T row, frequency) plus the two fp32 gradient planes written (8 B)
     // per (output row, frequency); the fp64 pivots are added once per chain below
@@ -661,11 +673,12 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
         const size_t goff = (size_t)t.po * ldG;
         const size_t io = local_io ? sl : (size_t)i;   // slot of q / G
         fj.push_back({q + (io * B.AT + g.f0) * ldq + (t.tx0 & 3),
-                      B.qhat + (sl * B.AT + g.f0) * B.ldn, g.nt, ldq, B.ldn, t.tx0, g.bt, n1t, 0});
+                      B.qhat + (sl * B.AT + g.f0) * B.ldn, g.nt, ldq, B.ldn, t.tx0, g.bt, n1t,
+                      mk ? 3 : 0});
         ij.push_back({B.phx + sl * B.AP * B.ldn, G + io * B.AP * ldG + goff, g.no, B.ldn,
-                      ldG, t.tx0, n1t, g.bo, 2});
+                      ldG, t.tx0, n1t, g.bo, mk ? 5 : 2});
         ij.push_back({B.phy + sl * B.AP * B.ldn, G + gplane + io * B.AP * ldG + goff, g.no,
-                      B.ldn, ldG, t.tx0, n1t, g.bo, 1});
+                      B.ldn, ldG, t.tx0, n1t, g.bo, mk ? 4 : 1});
       }
     B.nfj = (int)fj.size();
     B.nij = (int)ij.size();
@@ -676,7 +689,15 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     czt_tables(B.gi, gt2, tw);
     TRY(upload(ctx, P.bufs, &B.gtab_i, gt2));
     TRY(upload(ctx, P.bufs, &B.tw_i, tw));
-    {   // chirp tables: one device buffer for both job lists
+    if (mk) {   // Makhoul form: the axis tables c_n, e_k shared by every job
+      std::vector<float2> ct, et;
+      czt_makhoul_tables(n1t, ct, et);
+      float2 *dc = nullptr, *de = nullptr;
+      TRY(upload(ctx, P.bufs, &dc, ct));
+      TRY(upload(ctx, P.bufs, &de, et));
+      for (auto &j : fj) j.pre = dc, j.post = de;
+      for (auto &j : ij) j.pre = dc, j.post = de;
+    } else {   // chirp tables: one device buffer for both job lists
       std::vector<size_t> pf, qf, pi, qi;
       std::vector<float2> tfw = czt_chirp_tables(B.gf.N, fj, pf, qf);
       std::vector<float2> tiv = czt_chirp_tables(B.gi.N, ij, pi, qi);
@@ -1086,7 +1107,8 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
   const int t0 = B.g0[k], nt = B.g0[k + 1] - t0;
   if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
     TRY(run(ctx, s, F_CZT_FWD, 0, B.gfwd[k], [&] {
-      return launch_czt(B.d_fj + t0, nt, B.fj_rows, B.gf, B.gtab_f, B.tw_f, s);
+      return launch_czt(B.d_fj + t0, nt, B.gf.mk ? (B.fj_rows + 1) / 2 : B.fj_rows, B.gf,
+                        B.gtab_f, B.tw_f, s);
     }));
   } else {       // dense 3xTF32 tcgen05 contraction (persistent, A in tensor memory)
     TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
@@ -1462,6 +1484,7 @@ tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   if (const char *pg = getenv("TVS_PROJ_GROUP")) c->proj_group = std::max(0, atoi(pg));
+  if (const char *mk = getenv("TVS_CZT_MAKHOUL")) c->makhoul = atoi(mk) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {

@@ -16,6 +16,22 @@
 // (config 3), the chirp-z for full-width strips and large N (configs 4, 5).  fp32 FFT arithmetic;
 // pre/post chirps from per-job tables built on the host (phases reduced exactly mod 4N in
 // integers, angles in fp64, one rounding), kernel FFTs in fp64 on the host.
+//
+// Makhoul form (CztGeom::mk; whenever M = 2N - 2 is a power of 4, e.g. N = 2049, 8193): every
+// transform is a DFT_N of a COMPLEX sequence that packs two real ones, evaluated by Bluestein
+// (X_k = conj(c_k) sum_n z_n conj(c_n) c_{k-n}, c_m = e^{i pi m^2 / N}, even, so the one aliased
+// lag of the cyclic length 2N - 2 holds the same value):
+//   kind 3, forward, rows r and r+1 at once: Makhoul's DCT-II, v_n = q_{2n} (n < (N+1)/2),
+//     v_{N-1-n} = q_{2n+1}; Z = DFT_N(v_a + i v_b); A_k = (Z_k + conj Z_{N-k}) / 2,
+//     B_k = (Z_k - conj Z_{N-k}) / (2i); Qhat_a[k] = Re(e^{-i pi k/(2N)} A_k), same for b;
+//   kind 4, inverse y, rows r and r+1: the DCT-III T(a)[x] = sum_j a_j cos(theta j (2x+1)) by the
+//     inverse Makhoul map V_k = e^{i pi k/(2N)} (a''_k - i a''_{N-k}) (a''_0 = 2 a_0, a''_N = 0),
+//     v = (N/2) IDFT_N(V_a + i V_b) (both real parts), T(a)[2n] = v_n, T(a)[2n+1] = v_{N-1-n};
+//   kind 5, inverse x, one row: sum_j b_j sin(theta j (2x+2)) = (-1)^x T(c)[x] + T(d)[x] with
+//     c_k = b_{N-k} cos(delta_{N-k}) (c_0 = 0), d_k = b_k sin(delta_k), delta_k = pi k/(2N)
+//     (sin(theta j (2x+2)) = sin(A_j + delta_j) and sin A_j = (-1)^x cos A_{N-j}), both DCT-IIIs
+//     packed in one DFT.
+// Per pair of rows: 1 transform forward (general form: 2) and 3 inverse (general form: 4).
 #include "tvs_internal.h"
 
 #include <cmath>
@@ -326,6 +342,101 @@ __device__ __forceinline__ void czt_fft_pair(float2 *z, int logM4, const Tw &tw,
   }
 }
 
+// Makhoul form (see the file header): one CTA per (row pair or row, job).  pre = c table,
+// post = e table (n, k < N).
+__device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
+                                            const float2 *__restrict__ gtab,
+                                            const float2 *__restrict__ tw, float2 *zsm, int MP) {
+  const int N = G.N, M = G.M, tid = threadIdx.x, nth = blockDim.x;
+  const int kind = jb.kind;
+  const int r0 = kind == 5 ? blockIdx.x : 2 * blockIdx.x;
+  if (r0 >= jb.rows) return;
+  const bool two = kind != 5 && r0 + 1 < jb.rows;
+  float2 *tfine = zsm + MP, *tcoarse = tfine + 256;
+  for (int i = tid; i < 256; i += nth) tfine[i] = i < M ? __ldg(tw + i) : make_float2(1.f, 0.f);
+  for (int i = tid; i <= (M >> 8); i += nth) tcoarse[i] = (i << 8) < M ? __ldg(tw + (i << 8)) : make_float2(1.f, 0.f);
+  const Tw twd{tfine, tcoarse};
+  const float2 *__restrict__ cc = jb.pre;    // c_n = e^{i pi n^2 / N}
+  const float2 *__restrict__ ee = jb.post;   // e_k = e^{i pi k / (2N)}
+  const float *__restrict__ ia = jb.in + (size_t)r0 * jb.ldin;
+  const float *__restrict__ ib = two ? ia + jb.ldin : nullptr;
+  const int h = (N + 1) >> 1;
+  if (kind == 3) {   // forward: z_n = (v_a[n] + i v_b[n]) conj(c_n), v = Makhoul permutation of q
+    for (int n = tid; n < M; n += nth) {
+      float2 u = make_float2(0.f, 0.f);
+      if (n < N) {
+        const int x = (n < h ? 2 * n : 2 * (N - 1 - n) + 1) - jb.tx0;   // tile-relative column
+        if (x >= 0 && x < jb.ulen) {
+          const float a = __ldg(ia + x), b = ib ? __ldg(ib + x) : 0.f;
+          const float2 c = __ldg(cc + n);
+          u = make_float2(a * c.x + b * c.y, b * c.x - a * c.y);   // (a + i b) conj(c)
+        }
+      }
+      zsm[pz(n)] = u;
+    }
+  } else {           // inverse: u_k = conj(V_a + i V_b)_k conj(c_k)
+    for (int k = tid; k < M; k += nth) {
+      float2 u = make_float2(0.f, 0.f);
+      if (k < N) {
+        const int km = N - k;   // N - k in [1, N]; index N reads as 0
+        float p, q, r, s;       // V_a = e (p - i q), V_b = e (r - i s)
+        if (kind == 4) {
+          p = __ldg(ia + k) * (k == 0 ? 2.f : 1.f);
+          q = k ? __ldg(ia + km) : 0.f;
+          r = ib ? __ldg(ib + k) * (k == 0 ? 2.f : 1.f) : 0.f;
+          s = (ib && k) ? __ldg(ib + km) : 0.f;
+        } else {                // c''_k, c''_{N-k}, d''_k, d''_{N-k} of one Phi_x row
+          const float bk = __ldg(ia + k), bm = k ? __ldg(ia + km) : 0.f;
+          const float2 ek = __ldg(ee + k), em = k ? __ldg(ee + km) : make_float2(1.f, 0.f);
+          p = k ? bm * em.x : 0.f;   // c_k = b_{N-k} cos(delta_{N-k})
+          q = bk * ek.x;             // c_{N-k} = b_k cos(delta_k) (0 for k = 0: c''_N = 0)
+          if (!k) q = 0.f;
+          r = bk * ek.y;             // d_k = b_k sin(delta_k) (0 at k = 0)
+          s = k ? bm * em.y : 0.f;   // d_{N-k}
+        }
+        const float2 e = __ldg(ee + k);
+        // V_a = e (p - i q), V_b = e (r - i s); W = V_a + i V_b
+        const float2 va = make_float2(e.x * p + e.y * q, e.y * p - e.x * q);
+        const float2 vb = make_float2(e.x * r + e.y * s, e.y * r - e.x * s);
+        const float2 w = make_float2(va.x - vb.y, va.y + vb.x);
+        const float2 c = __ldg(cc + k);
+        // conj(w) conj(c) = conj(w c)
+        u = make_float2(w.x * c.x - w.y * c.y, -(w.x * c.y + w.y * c.x));
+      }
+      zsm[pz(k)] = u;
+    }
+  }
+  __syncthreads();
+  const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, 0, 0, false, false};
+  czt_fft_pair(zsm, G.logM4, twd, gtab, io);
+  float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
+  float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
+  if (kind == 3) {   // Qhat_a[k] = Re(conj(e_k) A_k), Qhat_b[k] = Re(conj(e_k) B_k)
+    for (int k = tid; k < jb.vlen; k += nth) {
+      const int m = k ? N - k : 0;
+      const float2 zk = cmulc(zsm[pz(k)], __ldg(cc + k)), zm = cmulc(zsm[pz(m)], __ldg(cc + m));
+      const float2 e = __ldg(ee + k);
+      // A = (zk + conj zm)/2, B = (zk - conj zm)/(2i); Re(conj(e) A) = (e.x A.x + e.y A.y)
+      const float ax = 0.5f * (zk.x + zm.x), ay = 0.5f * (zk.y - zm.y);
+      const float bx = 0.5f * (zk.y + zm.y), by = -0.5f * (zk.x - zm.x);
+      oa[k] = e.x * ax + e.y * ay;
+      if (ob) ob[k] = e.x * bx + e.y * by;
+    }
+  } else {           // v = conj(conj(c_n) z_n) / 2 at the Makhoul position of column x
+    for (int i = tid; i < jb.vlen; i += nth) {
+      const int x = jb.tx0 + i;
+      const int n = (x & 1) ? N - 1 - (x >> 1) : (x >> 1);
+      const float2 y = cmulc(zsm[pz(n)], __ldg(cc + n));   // Y_n; v = conj(Y) / 2
+      if (kind == 4) {
+        oa[i] = 0.5f * y.x;
+        if (ob) ob[i] = -0.5f * y.y;
+      } else {
+        oa[i] = 0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y;
+      }
+    }
+  }
+}
+
 // One CTA per (row, job, output pass).  kind 0: forward cos (pre u^2, post v^2 + v(2tx0+1), Re);
 // kind 1: inverse cos (pre u^2 + u(2tx0+1), post v^2, Re); kind 2: inverse sin (pre u^2 +
 // u(2tx0+2), post v^2, Im).
@@ -337,6 +448,10 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   float2 *tfine = zsm + MP, *tcoarse = tfine + 256;      // twiddle tables
   float *acc = reinterpret_cast<float *>(tcoarse + (G.M >> 8) + 1);
   const CztJob jb = jobs[blockIdx.y];
+  if (G.mk) {
+    czt_makhoul(jb, G, gtab, tw, zsm, MP);
+    return;
+  }
   const int row = blockIdx.x;
   if (row >= jb.rows) return;
   const int v0 = blockIdx.z * G.Vp;
@@ -470,6 +585,35 @@ bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g) {
   return (1 << (2 * g->logM4)) == g->M && g->logM4 >= 1 && g->logM4 <= 7;   // k_czt instantiates M = 4 .. 16384
 }
 
+bool czt_makhoul_geometry(int N, int max_m, CztGeom *g) {
+  const long long M = 2LL * N - 2;
+  long long p4 = 4;
+  while (p4 < M) p4 <<= 2;
+  if (N < 3 || p4 != M || M > max_m) return false;
+  g->N = N;
+  g->M = (int)M;
+  g->Uc = g->Vp = N;
+  g->nuc = g->nvp = 1;
+  g->logM4 = 0;
+  while ((1 << (2 * g->logM4)) < g->M) ++g->logM4;
+  g->mk = 1;
+  g->prune = 0;
+  return g->logM4 >= 2 && g->logM4 <= 7;
+}
+
+void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab) {
+  ctab.resize(N);
+  etab.resize(N);
+  const long long n2 = 2LL * N;
+  for (long long n = 0; n < N; ++n) {
+    const long long r = (n * n) % n2;   // e^{i pi n^2 / N}: n^2 mod 2N exactly
+    const double a = M_PI * (double)r / (double)N;
+    ctab[n] = make_float2((float)std::cos(a), (float)std::sin(a));
+    const double d = M_PI * (double)n / (2.0 * N);
+    etab[n] = make_float2((float)std::cos(d), (float)std::sin(d));
+  }
+}
+
 // Kernel tables: for output pass p and input chunk c the digit-reversed FFT of the circular window
 // g[n] = h[(p Vp - c Uc) + n], n in [-(M - Vp), Vp - 1], scaled by 1/M (fp64 on the host).
 // Chirp tables of the jobs: pre-chirp offset c = 0 (forward) or 2 tx0 + kind (inverse cos / sin),
@@ -517,6 +661,13 @@ void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2>
       for (int i = 0; i < M; ++i) {
         const long long n = i < g.Vp ? i : (long long)i - M;
         const long long m = d + n;
+        if (g.mk) {   // Makhoul form: h_m = c_m = e^{i pi m^2 / N}, m^2 mod 2N exactly
+          const long long n2 = 2LL * g.N;
+          const long long r = ((m % n2) * (m % n2)) % n2;
+          const double ph = M_PI * (double)r / (double)g.N;
+          a[i] = std::complex<double>(std::cos(ph), std::sin(ph));
+          continue;
+        }
         long long r = ((m % n4) * (m % n4)) % n4;   // m^2 mod 4N exactly
         if (r < 0) r += n4;
         const double ph = -M_PI * (double)r / (2.0 * g.N);

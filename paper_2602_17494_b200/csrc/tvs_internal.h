@@ -103,8 +103,14 @@ struct CztGeom {
   int Uc, Vp;     // input chunk and output pass lengths (Uc + Vp - 1 <= M, or the M = 2N-2 case)
   int nuc, nvp;   // numbers of chunks / passes for the largest job
   int prune = 1;  // pruned first / last FFT passes for narrow jobs (TVS_CZT_PRUNE=0: off)
+  int mk = 0;     // 1: Makhoul form -- the partial x-DCTs as DFT_N's of packed real sequences by
+                  // Bluestein with M = 2N - 2 (job kinds 3, 4, 5; see tvs_czt.cu)
 };
 bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g);
+// Makhoul form on an axis of N (any tile): M = 2N - 2 must be a power of 4 <= max_m.
+bool czt_makhoul_geometry(int N, int max_m, CztGeom *g);
+// its per-axis tables: c[n] = e^{i pi n^2 / N} and e[k] = e^{i pi k / (2N)}, n, k < N
+void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab);
 void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw);
 cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
                        const float2 *gtab, const float2 *tw, cudaStream_t s);

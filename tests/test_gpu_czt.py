@@ -111,3 +111,31 @@ def test_step1_czt_tile_groups(ctx, ctx_grouped, shape, L):
     t2, p2, _ = ctx_grouped.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125), want_p=True)
     torch.cuda.synchronize()
     assert torch.equal(t1, t2) and torch.equal(p1, p2)
+
+
+@pytest.fixture(scope="module")
+def ctx_general():
+    """The general chirp-z form everywhere (TVS_CZT_MAKHOUL=0), for A/B against the Makhoul form."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = _context(TVS_DCT="czt", TVS_CZT_MAKHOUL="0")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("shape,L", [((40, 32), (2, 2, 4, 4)), ((20, 128), (1, 3, 0, 6)),
+                                     ((33, 128), (3, 1, 4, 0)), ((8, 8), (1, 1, 0, 0)),
+                                     ((129, 512), (2, 4, 6, 8))])
+def test_step1_makhoul_form(ctx, ctx_general, shape, L):
+    """Axes with N~1 = n1 + 1 in {9, 33, 129, 513}, where M = 2N - 2 is a power of 4: the partial
+    x-DCTs run in the Makhoul form (forward: two rows per DFT_N; inverse: the DCT-III pair and the
+    shifted sine transform as two packed DCT-IIIs).  Parity with the oracle on full-width, narrow
+    and ragged tiles (odd and even row counts: the row pairs of the forward and y-inverse jobs),
+    and agreement with the general chirp-z form to fp32 rounding."""
+    img = random_image(*shape, seed=shape[0] * 3 + shape[1] + 5)
+    check_step1(ctx, img, 0.05, L, 3, 4)
+    d0 = torch.from_numpy(img).cuda()
+    t1, _, _ = ctx.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125))
+    t2, _, _ = ctx_general.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125))
+    torch.cuda.synchronize()
+    assert float((t1 - t2).abs().max()) < 2e-5

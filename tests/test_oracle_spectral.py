@@ -108,3 +108,17 @@ def test_block_dct_equals_restricted_global(m2, m1):
     full[3:10, 5:15] = qa
     ref = spectral.lap_pinv(full)[0:7, 11:20]
     assert np.abs(blk - ref).max() < 1e-13
+
+
+def test_row_restricted_pinv_and_projection():
+    """lap_pinv_rows / project_rows (output rows of the same formulas, for config-5 sizes) equal the
+    corresponding rows of lap_pinv / project on square and non-square grids."""
+    from tvs_synth import random_field
+    for shape in ((9, 9), (8, 13), (17, 6)):
+        q = random_field(shape, 3 + shape[0], 1.0)
+        rows = [0, 2, shape[0] - 1]
+        assert np.abs(spectral.lap_pinv_rows(q, rows) - spectral.lap_pinv(q)[rows]).max() < 1e-12
+        w = random_field((2,) + shape, 9 + shape[1], 1.0)
+        r, pw = spectral.project_rows(w, [shape[0] - 1, 1, 3])
+        assert list(r) == [1, 3, shape[0] - 1]
+        assert np.abs(pw - spectral.project(w)[:, r]).max() < 1e-12
