@@ -361,49 +361,74 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   const float *__restrict__ ia = jb.in + (size_t)r0 * jb.ldin;
   const float *__restrict__ ib = two ? ia + jb.ldin : nullptr;
   const int h = (N + 1) >> 1;
+  // loads are issued in batches of B per thread (all loads of a batch before any use: the
+  // kernel is latency-bound on them otherwise)
+  constexpr int B = 8;
   if (kind == 3) {   // forward: z_n = (v_a[n] + i v_b[n]) conj(c_n), v = Makhoul permutation of q
-    for (int n = tid; n < M; n += nth) {
-      float2 u = make_float2(0.f, 0.f);
-      if (n < N) {
-        const int x = (n < h ? 2 * n : 2 * (N - 1 - n) + 1) - jb.tx0;   // tile-relative column
-        if (x >= 0 && x < jb.ulen) {
-          const float a = __ldg(ia + x), b = ib ? __ldg(ib + x) : 0.f;
-          const float2 c = __ldg(cc + n);
-          u = make_float2(a * c.x + b * c.y, b * c.x - a * c.y);   // (a + i b) conj(c)
-        }
+    for (int n0 = tid; n0 < M; n0 += B * nth) {
+      float a[B], b[B];
+      float2 c[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int n = n0 + r * nth;
+        const int x = n < N ? (n < h ? 2 * n : 2 * (N - 1 - n) + 1) - jb.tx0 : -1;
+        const bool ok = x >= 0 && x < jb.ulen;
+        a[r] = ok ? __ldg(ia + x) : 0.f;
+        b[r] = ok && ib ? __ldg(ib + x) : 0.f;
+        c[r] = n < N ? __ldg(cc + n) : make_float2(0.f, 0.f);
       }
-      zsm[pz(n)] = u;
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int n = n0 + r * nth;
+        if (n < M) zsm[pz(n)] = make_float2(a[r] * c[r].x + b[r] * c[r].y, b[r] * c[r].x - a[r] * c[r].y);
+      }
     }
   } else {           // inverse: u_k = conj(V_a + i V_b)_k conj(c_k)
-    for (int k = tid; k < M; k += nth) {
-      float2 u = make_float2(0.f, 0.f);
-      if (k < N) {
-        const int km = N - k;   // N - k in [1, N]; index N reads as 0
-        float p, q, r, s;       // V_a = e (p - i q), V_b = e (r - i s)
-        if (kind == 4) {
-          p = __ldg(ia + k) * (k == 0 ? 2.f : 1.f);
-          q = k ? __ldg(ia + km) : 0.f;
-          r = ib ? __ldg(ib + k) * (k == 0 ? 2.f : 1.f) : 0.f;
-          s = (ib && k) ? __ldg(ib + km) : 0.f;
-        } else {                // c''_k, c''_{N-k}, d''_k, d''_{N-k} of one Phi_x row
-          const float bk = __ldg(ia + k), bm = k ? __ldg(ia + km) : 0.f;
-          const float2 ek = __ldg(ee + k), em = k ? __ldg(ee + km) : make_float2(1.f, 0.f);
-          p = k ? bm * em.x : 0.f;   // c_k = b_{N-k} cos(delta_{N-k})
-          q = bk * ek.x;             // c_{N-k} = b_k cos(delta_k) (0 for k = 0: c''_N = 0)
-          if (!k) q = 0.f;
-          r = bk * ek.y;             // d_k = b_k sin(delta_k) (0 at k = 0)
-          s = k ? bm * em.y : 0.f;   // d_{N-k}
+    for (int k0 = tid; k0 < M; k0 += B * nth) {
+      float p[B], q[B], r_[B], s[B];
+      float2 e[B], c[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int k = k0 + r * nth;
+        const bool in = k < N, nz = in && k > 0;
+        const int km = nz ? N - k : 0;   // N - k in [1, N - 1] (index N reads as 0)
+        e[r] = in ? __ldg(ee + k) : make_float2(0.f, 0.f);
+        c[r] = in ? __ldg(cc + k) : make_float2(0.f, 0.f);
+        if (kind == 4) {   // V_a = e (a''_k - i a''_{N-k}), V_b likewise
+          p[r] = in ? __ldg(ia + k) : 0.f;
+          q[r] = nz ? __ldg(ia + km) : 0.f;
+          r_[r] = in && ib ? __ldg(ib + k) : 0.f;
+          s[r] = nz && ib ? __ldg(ib + km) : 0.f;
+        } else {           // b_k, b_{N-k} and e_{N-k} of one Phi_x row (cos / sin of delta)
+          p[r] = in ? __ldg(ia + k) : 0.f;
+          q[r] = nz ? __ldg(ia + km) : 0.f;
+          const float2 em = nz ? __ldg(ee + km) : make_float2(0.f, 0.f);
+          r_[r] = em.x;
+          s[r] = em.y;
         }
-        const float2 e = __ldg(ee + k);
-        // V_a = e (p - i q), V_b = e (r - i s); W = V_a + i V_b
-        const float2 va = make_float2(e.x * p + e.y * q, e.y * p - e.x * q);
-        const float2 vb = make_float2(e.x * r + e.y * s, e.y * r - e.x * s);
-        const float2 w = make_float2(va.x - vb.y, va.y + vb.x);
-        const float2 c = __ldg(cc + k);
-        // conj(w) conj(c) = conj(w c)
-        u = make_float2(w.x * c.x - w.y * c.y, -(w.x * c.y + w.y * c.x));
       }
-      zsm[pz(k)] = u;
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int k = k0 + r * nth;
+        if (k >= M) break;
+        float pp, qq, rr, ss;
+        if (kind == 4) {
+          pp = k == 0 ? 2.f * p[r] : p[r];   // a''_0 = 2 a_0
+          qq = q[r];
+          rr = k == 0 ? 2.f * r_[r] : r_[r];
+          ss = s[r];
+        } else {   // c_k = b_{N-k} cos(delta_{N-k}), c_{N-k} = b_k cos(delta_k), d_k, d_{N-k}
+          pp = q[r] * r_[r];
+          qq = k ? p[r] * e[r].x : 0.f;
+          rr = p[r] * e[r].y;
+          ss = q[r] * s[r];
+        }
+        const float2 ek = e[r];
+        const float2 va = make_float2(ek.x * pp + ek.y * qq, ek.y * pp - ek.x * qq);
+        const float2 vb = make_float2(ek.x * rr + ek.y * ss, ek.y * rr - ek.x * ss);
+        const float2 w = make_float2(va.x - vb.y, va.y + vb.x);   // W = V_a + i V_b
+        zsm[pz(k)] = make_float2(w.x * c[r].x - w.y * c[r].y, -(w.x * c[r].y + w.y * c[r].x));
+      }
     }
   }
   __syncthreads();
@@ -412,26 +437,49 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
   float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
   if (kind == 3) {   // Qhat_a[k] = Re(conj(e_k) A_k), Qhat_b[k] = Re(conj(e_k) B_k)
-    for (int k = tid; k < jb.vlen; k += nth) {
-      const int m = k ? N - k : 0;
-      const float2 zk = cmulc(zsm[pz(k)], __ldg(cc + k)), zm = cmulc(zsm[pz(m)], __ldg(cc + m));
-      const float2 e = __ldg(ee + k);
-      // A = (zk + conj zm)/2, B = (zk - conj zm)/(2i); Re(conj(e) A) = (e.x A.x + e.y A.y)
-      const float ax = 0.5f * (zk.x + zm.x), ay = 0.5f * (zk.y - zm.y);
-      const float bx = 0.5f * (zk.y + zm.y), by = -0.5f * (zk.x - zm.x);
-      oa[k] = e.x * ax + e.y * ay;
-      if (ob) ob[k] = e.x * bx + e.y * by;
+    for (int k0 = tid; k0 < jb.vlen; k0 += B * nth) {
+      float2 ck[B], cm[B], e[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int k = min(k0 + r * nth, jb.vlen - 1), m = k ? N - k : 0;
+        ck[r] = __ldg(cc + k);
+        cm[r] = __ldg(cc + m);
+        e[r] = __ldg(ee + k);
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int k = k0 + r * nth;
+        if (k >= jb.vlen) break;
+        const int m = k ? N - k : 0;
+        const float2 zk = cmulc(zsm[pz(k)], ck[r]), zm = cmulc(zsm[pz(m)], cm[r]);
+        // A = (zk + conj zm)/2, B = (zk - conj zm)/(2i); Re(conj(e) A) = e.x A.x + e.y A.y
+        const float ax = 0.5f * (zk.x + zm.x), ay = 0.5f * (zk.y - zm.y);
+        const float bx = 0.5f * (zk.y + zm.y), by = -0.5f * (zk.x - zm.x);
+        oa[k] = e[r].x * ax + e[r].y * ay;
+        if (ob) ob[k] = e[r].x * bx + e[r].y * by;
+      }
     }
   } else {           // v = conj(conj(c_n) z_n) / 2 at the Makhoul position of column x
-    for (int i = tid; i < jb.vlen; i += nth) {
-      const int x = jb.tx0 + i;
-      const int n = (x & 1) ? N - 1 - (x >> 1) : (x >> 1);
-      const float2 y = cmulc(zsm[pz(n)], __ldg(cc + n));   // Y_n; v = conj(Y) / 2
-      if (kind == 4) {
-        oa[i] = 0.5f * y.x;
-        if (ob) ob[i] = -0.5f * y.y;
-      } else {
-        oa[i] = 0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y;
+    for (int i0 = tid; i0 < jb.vlen; i0 += B * nth) {
+      float2 cn[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int x = jb.tx0 + min(i0 + r * nth, jb.vlen - 1);
+        cn[r] = __ldg(cc + ((x & 1) ? N - 1 - (x >> 1) : (x >> 1)));
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int i = i0 + r * nth;
+        if (i >= jb.vlen) break;
+        const int x = jb.tx0 + i;
+        const int n = (x & 1) ? N - 1 - (x >> 1) : (x >> 1);
+        const float2 y = cmulc(zsm[pz(n)], cn[r]);   // Y_n; v = conj(Y) / 2
+        if (kind == 4) {
+          oa[i] = 0.5f * y.x;
+          if (ob) ob[i] = -0.5f * y.y;
+        } else {
+          oa[i] = 0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y;
+        }
       }
     }
   }
@@ -588,17 +636,20 @@ bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g) {
 bool czt_makhoul_geometry(int N, int max_m, CztGeom *g) {
   const long long M = 2LL * N - 2;
   long long p4 = 4;
-  while (p4 < M) p4 <<= 2;
-  if (N < 3 || p4 != M || M > max_m) return false;
+  int lg = 1;
+  while (p4 < M) {
+    p4 <<= 2;
+    ++lg;
+  }
+  if (N < 3 || p4 != M || M > max_m || lg < 2 || lg > 7) return false;   // g untouched
   g->N = N;
   g->M = (int)M;
   g->Uc = g->Vp = N;
   g->nuc = g->nvp = 1;
-  g->logM4 = 0;
-  while ((1 << (2 * g->logM4)) < g->M) ++g->logM4;
+  g->logM4 = lg;
   g->mk = 1;
   g->prune = 0;
-  return g->logM4 >= 2 && g->logM4 <= 7;
+  return true;
 }
 
 void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab) {
