@@ -143,6 +143,18 @@ tvs_status tvs_layout_theta(int32_t n, int32_t m, int32_t s, int32_t k, int32_t 
  * stream synchronisation per sweep.  TVS_EINVAL for an unknown criterion or tol < 0. */
 tvs_status tvs_set_stopping(tvs_ctx *ctx, int32_t criterion, double tol);
 
+/* Per-sweep energy trace (the energy-convergence protocol of section 6.3 / Fig. 7, P:1769-1782;
+ * SURVEY 8(f) NEXT 3).  With cap > 0 every following tv_stokes_step1 / step2 / step2_irv1 call of
+ * this context writes, for the Schwarz iterates n = 0 .. sweeps_run (at most cap), the primal energy
+ * E(u(p^n)), the dual energy D(p^n) (Eq. opt_dual_discrete) and the duality gap
+ * (SURVEY C-15) to out[3 n + {0, 1, 2}] (host memory owned by the caller, valid until the call
+ * returns) and the number of entries to *count (nullable).  Step 1: tau^n = delta r^n, r^n the
+ * sweep's global residual; step 2: d^n = d0 - div p^n / alpha.  fp64
+ * device reductions summed over ranks; one extra reduction pass per sweep (and the step-1 side
+ * stream overlap is off while tracing).  cap = 0 turns it off.  TVS_EINVAL for cap < 0 or a null
+ * buffer with cap > 0. */
+tvs_status tvs_set_trace(tvs_ctx *ctx, double *out, int32_t cap, int32_t *count);
+
 /* Step 1 (TFS).  d0: device [n2*n1]; tau: device out [2][(n2+1)*(n1+1)];
  * p: device out (nullable) [4][(n2+1)*(n1+1)]. */
 tvs_status tv_stokes_step1(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, float delta,

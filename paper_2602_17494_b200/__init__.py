@@ -23,7 +23,7 @@ ABI_SYMBOLS = [
     "tvs_layout_range", "tvs_layout_theta", "tv_stokes_step1", "tv_stokes_step2",
     "tv_stokes_denoise", "tv_stokes_denoise_host", "tvs_set_profiling", "tvs_kernel_times",
     "tvs_reset_kernel_times", "tvs_selftest_gemm", "tvs_dist_rows", "tv_stokes_step2_irv1",
-    "tvs_set_stopping", "tvs_create_virtual_group",
+    "tvs_set_stopping", "tvs_create_virtual_group", "tvs_set_trace",
 ]
 
 STATUS = {0: "TVS_OK", 1: "TVS_EINVAL", 2: "TVS_ELAYOUT", 4: "TVS_ENUMERIC", 5: "TVS_ECUDA",
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH):
     lib.tv_stokes_denoise_host.argtypes = lib.tv_stokes_denoise.argtypes
     lib.tvs_set_profiling.argtypes = [P, ctypes.c_int]
     lib.tvs_set_stopping.argtypes = [P, i32, ctypes.c_double]
+    lib.tvs_set_trace.argtypes = [P, ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(i32)]
     arr7i = ctypes.c_int64 * len(KERNEL_FAMILIES)
     arr7d = ctypes.c_double * len(KERNEL_FAMILIES)
     lib.tvs_kernel_times.argtypes = [P, arr7i, arr7d, arr7d, arr7d]
@@ -331,6 +332,20 @@ class Context:
         """Outer-loop stopping rule (tvs_set_stopping): 0 fixed schedule, 1 the sqrt(D) criterion
         of section 5.2, 2 the D^2 criterion of section 6.3."""
         self._check(self.lib.tvs_set_stopping(self.h, int(criterion), float(tol)), "tvs_set_stopping")
+
+    def set_trace(self, cap: int):
+        """Per-sweep (E, D, gap) of the Schwarz iterates of the following calls (tvs_set_trace);
+        read them with ``trace()`` after a call; cap = 0 turns it off."""
+        import numpy as np
+        self._trace_buf = np.zeros((max(cap, 1), 3))
+        self._trace_n = ctypes.c_int32(0)
+        self._check(self.lib.tvs_set_trace(
+            self.h, self._trace_buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if cap else None,
+            int(cap), ctypes.byref(self._trace_n)), "tvs_set_trace")
+
+    def trace(self):
+        """(n_entries, 3) array of the last traced call: columns E, D, gap."""
+        return self._trace_buf[: self._trace_n.value].copy()
 
     def set_profiling(self, on: bool):
         self._check(self.lib.tvs_set_profiling(self.h, 1 if on else 0), "tvs_set_profiling")

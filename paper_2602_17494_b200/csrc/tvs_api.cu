@@ -181,6 +181,8 @@ struct ProjBatch {
   float *qhat = nullptr;
   float *z = nullptr;       // fp32 z scratch of solve3 when its column block exceeds shared memory
   double *rinv = nullptr, *segprod = nullptr;
+  int *pcut = nullptr;                        // pivot table constant-tail compression (k_pivots)
+  double *pinf = nullptr, *plast = nullptr;
   SolveMaps *d_smaps = nullptr;   // TMA maps of the solve's staged blocks (solve4)
   int smem_rows = 0;
   int *d_order = nullptr;         // solve4 launch order: tiles grouped by chain [nchains][per_chain]
@@ -221,6 +223,7 @@ struct Plan {
   float *v[2] = {nullptr, nullptr};
   float *om = nullptr, *p = nullptr, *f = nullptr;
   float *dxi = nullptr;   // IRV1: div xi (allocated on first use)
+  float *dtr = nullptr;   // step 2: d of the traced iterates (allocated on first use)
   double *g0 = nullptr, *gsum = nullptr;
   int *d_bad = nullptr;
   double *d_part = nullptr, *d_energy = nullptr;   // dual-energy reduction scratch
@@ -311,6 +314,11 @@ struct tvs_ctx {
   int dct_mode = 0;
   int czt_max_m = 16384;
   int proj_group = 0;            // max tiles per projection group (TVS_PROJ_GROUP; 0 = by memory)
+  // per-sweep energy trace (tvs_set_trace): host destination [cap][3], entry count, device buffer
+  double *trace_out = nullptr;
+  int32_t trace_cap = 0, *trace_count = nullptr;
+  double *d_trace = nullptr;
+  int d_trace_cap = 0;
   bool makhoul = true;           // Makhoul form of the chirp-z where M = 2N - 2 is a power of 4
                                  // (TVS_CZT_MAKHOUL=0: the general chirp-z form everywhere)
   double *h_energy = nullptr;   // pinned slot for dual energies
@@ -717,7 +725,11 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     TRY(upload(ctx, P.bufs, &B.d_fj, fj));
     TRY(upload(ctx, P.bufs, &B.d_ij, ij));
   }
-  CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, 0));
+  TRY(dalloc(ctx, P.bufs, &B.pcut, (size_t)B.nchains * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.pinf, (size_t)B.nchains * B.ldn));
+  TRY(dalloc(ctx, P.bufs, &B.plast, (size_t)B.nchains * B.ldn));
+  CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, B.pcut, B.pinf,
+                   B.plast, 0));
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
     CK(launch_segprod(B.d_tiles, B.d_first, B.nchains, B.rinv, B.ldn, B.AT, n1t, B.segprod, 0));
@@ -1125,7 +1137,7 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
                                 B.d_order + (size_t)k * B.nchains * B.per_chain, B.nchains,
                                 B.per_chain, s);
     return launch_proj_solve3(B.d_tiles + t0, nt, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
-                              B.phx, B.phy, nullptr, nullptr, B.AP, s);
+                              B.phx, B.phy, nullptr, nullptr, B.AP, B.pcut, B.pinf, B.plast, s);
   }));
   if (B.czt)
     return run(ctx, s, F_CZT_INV, 0, B.ginv[k], [&] {
@@ -1174,6 +1186,43 @@ tvs_status finish_call(tvs_ctx *ctx, Plan &P, cudaStream_t s, CallTimer &tm, tvs
     st->launches = ctx->launches - launches0;
   }
   if (bad) return fail(ctx, TVS_ENUMERIC, "non-finite value in the dual after a sweep");
+  return TVS_OK;
+}
+
+// Per-sweep energy trace: device slots [cap][8] of raw sums, summed over ranks per entry, turned
+// into (E, D, gap) on the host at the end of the call.
+tvs_status trace_begin(tvs_ctx *ctx, int sweeps) {
+  if (ctx->trace_cap <= 0) return TVS_OK;
+  const int need = std::min(ctx->trace_cap, sweeps + 1);
+  if (ctx->d_trace_cap < need) {
+    if (ctx->d_trace) cudaFree(ctx->d_trace);
+    ctx->d_trace = nullptr;
+    ctx->d_trace_cap = 0;
+    if (cudaMalloc(&ctx->d_trace, (size_t)need * 8 * sizeof(double)) != cudaSuccess)
+      return fail(ctx, TVS_ENOMEM, "trace buffer");
+    ctx->d_trace_cap = need;
+  }
+  return TVS_OK;
+}
+// slot of entry n (null when the trace is off or full)
+double *trace_slot(tvs_ctx *ctx, int n) {
+  if (ctx->trace_cap <= 0 || n >= std::min(ctx->trace_cap, ctx->d_trace_cap)) return nullptr;
+  return ctx->d_trace + (size_t)n * 8;
+}
+// copy `count` entries back and form (E, D, gap) with the step's weights: E = s[1] + wfit s[2]
+// (+ s[4] for IRV1), D = s[0] dscale, gap = s[3]
+tvs_status trace_end(tvs_ctx *ctx, int count, double wfit, double dscale, bool cross) {
+  if (ctx->trace_cap <= 0) return TVS_OK;
+  count = std::min(count, std::min(ctx->trace_cap, ctx->d_trace_cap));
+  std::vector<double> h((size_t)count * 8);
+  if (count) CK(cudaMemcpy(h.data(), ctx->d_trace, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int n = 0; n < count; ++n) {
+    const double *s = &h[(size_t)n * 8];
+    ctx->trace_out[3 * n + 0] = s[1] + wfit * s[2] + (cross ? s[4] : 0.0);
+    ctx->trace_out[3 * n + 1] = s[0] * dscale;
+    ctx->trace_out[3 * n + 2] = s[3];
+  }
+  if (ctx->trace_count) *ctx->trace_count = count;
   return TVS_OK;
 }
 
@@ -1229,6 +1278,29 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
   const bool stopping = ctx->stop_crit != 0;
   double e_prev = 0.0;
   int sweeps_run = it.sweeps;
+  TRY(trace_begin(ctx, it.sweeps));
+  if (ctx->trace_cap > 0 && !P->dtr) TRY(dalloc(ctx, P->bufs, &P->dtr, pl));
+  // trace entry n: D(p^n), E_2(d(p^n)) and the gap, d(p^n) = d0 - (div p^n + shift)/alpha on the
+  // core rows and the row below (grad d at the last core row)
+  auto trace2 = [&](int n) -> tvs_status {
+    double *slot = trace_slot(ctx, n);
+    if (!slot) return TVS_OK;
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_recover2(d0, P->p, P->p + pl, ld, n2, n1, 1.f / alpha,
+                             variant == 1 ? P->dxi : nullptr, P->dtr, D2.R0,
+                             std::min(n2, D2.R1 + 1), s);
+    }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_dual_energy2(P->p, P->p + pl, P->f, ld, n2, n1, D2.R0, D2.R1, P->d_part, slot, s);
+    }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_primal2(P->dtr, d0, P->f, variant == 1 ? P->dxi : nullptr, P->p, P->p + pl, ld,
+                            n2, n1, D2.R0, D2.R1, 1.f / alpha, P->d_part, slot + 1, s);
+    }));
+    if (D2.world > 1) TRY(allreduce_sum(ctx, slot, 5, s));
+    return TVS_OK;
+  };
+  TRY(trace2(0));
   if (stopping) TRY(energy2(&e_prev, true));
   for (int n = 0; n < it.sweeps; ++n) {
     TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
@@ -1250,6 +1322,7 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
       k += two ? 2 : 1;
     }
     TRY(combine_step(ctx, *P, P->v[cur], s));
+    TRY(trace2(n + 1));
     if (stopping) {
       double e = 0.0;
       TRY(energy2(&e, true));
@@ -1289,6 +1362,7 @@ tvs_status step2_impl(tvs_ctx *ctx, const float *tau, const float *d0, int32_t n
     st->sweeps_run = sweeps_run;
   }
   TRY(finish_call(ctx, *P, s, tm, st, l0));
+  TRY(trace_end(ctx, sweeps_run + 1, 0.5 * (double)alpha, 1.0, variant == 1));
   if (st) {
     const double *h = ctx->h_energy;   // D, TV(u), ||d - d0||^2, gap, <d, div xi>
     st->dual_energy = h[4];
@@ -1359,7 +1433,24 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
   // overlap the global residual with the omega0 chain: one GPU, no stopping test (which needs r^n
   // first); the chains write disjoint buffers and join before omega0 reads r^n and grad phi
   // (not while profiling: concurrent kernels would stretch each other's per-launch event times)
-  const bool overlap = ctx->overlap && D.world == 1 && !stopping && !ctx->profiling;
+  const bool overlap = ctx->overlap && D.world == 1 && !stopping && !ctx->profiling &&
+                       ctx->trace_cap <= 0;
+  TRY(trace_begin(ctx, it.sweeps));
+  // trace entry n (at the start of sweep n, from r^n): D(p^n) = ||r^n||^2, E_1(tau^n) with
+  // tau^n = delta r^n and the gap of (tau^n, p^n)
+  auto trace1 = [&](int n) -> tvs_status {
+    double *slot = trace_slot(ctx, n);
+    if (!slot) return TVS_OK;
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_sumsq2(P->r, pl, ld, G1, D.R0, D.R1, P->d_part, slot, s);
+    }));
+    TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
+      return launch_primal1(P->r, pl, ld, P->f, P->p, G2, G1, D.R0, D.R1, delta, delta, P->d_part,
+                            slot + 1, s);
+    }));
+    if (D.world > 1) TRY(allreduce_sum(ctx, slot, 4, s));
+    return TVS_OK;
+  };
   if (overlap && !ctx->side) {
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -1374,6 +1465,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     } else {
       TRY(residual(P->r, 1.f, s));
     }
+    TRY(trace1(n));
     if (stopping) {   // r^n is D(p^n)'s residual: test the previous sweep before starting this one
       double e = 0.0;
       TRY(energy1(&e, true));
@@ -1428,7 +1520,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     return launch_sumsq2(P->r, pl, ld, G1, D.R0, D.R1, P->d_part, P->d_energy + 4, s);
   }));
   TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-    return launch_primal1(P->r, pl, ld, P->f, P->p, G2, G1, D.R0, D.R1, delta, P->d_part,
+    return launch_primal1(P->r, pl, ld, P->f, P->p, G2, G1, D.R0, D.R1, delta, 1.f, P->d_part,
                           P->d_energy + 5, s);
   }));
   TRY(fetch_energy(ctx, *P, s, nullptr, false, 4, 4));
@@ -1449,6 +1541,15 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
     st->sweeps_run = sweeps_run;
   }
   TRY(finish_call(ctx, *P, s, tm, st, l0));
+  // entries 0 .. sweeps_run - 1 from the sweeps' residuals, entry sweeps_run = the returned solution
+  TRY(trace_end(ctx, sweeps_run, 1.0 / (2.0 * (double)delta), 1.0, false));
+  if (ctx->trace_cap > sweeps_run && ctx->d_trace_cap > sweeps_run) {
+    const double *h = ctx->h_energy;
+    ctx->trace_out[3 * sweeps_run + 0] = h[5] + h[6] / (2.0 * (double)delta);
+    ctx->trace_out[3 * sweeps_run + 1] = h[4] / ((double)delta * (double)delta);
+    ctx->trace_out[3 * sweeps_run + 2] = h[7];
+    if (ctx->trace_count) *ctx->trace_count = sweeps_run + 1;
+  }
   if (st) {
     const double *h = ctx->h_energy;   // ||tau||^2, TV(tau), ||tau - P tau_0||^2, gap
     st->dual_energy = h[4] / ((double)delta * (double)delta);
@@ -1519,6 +1620,7 @@ tvs_status tvs_destroy(tvs_ctx *ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->nccl) ncclCommDestroy(ctx->nccl);
   if (ctx->d_red) cudaFree(ctx->d_red);
+  if (ctx->d_trace) cudaFree(ctx->d_trace);
   if (ctx->vgroup) {
     std::lock_guard<std::mutex> lk(ctx->vgroup->mu);
     if (--ctx->vgroup->alive == 0) {
@@ -1849,6 +1951,15 @@ tvs_status tvs_set_stopping(tvs_ctx *ctx, int32_t criterion, double tol) {
     return fail(ctx, TVS_EINVAL, "stopping: criterion must be 0, 1 or 2 and tol >= 0");
   ctx->stop_crit = criterion;
   ctx->stop_tol = tol;
+  return TVS_OK;
+}
+
+tvs_status tvs_set_trace(tvs_ctx *ctx, double *out, int32_t cap, int32_t *count) {
+  if (!ctx) return TVS_EINVAL;
+  if (cap < 0 || (cap > 0 && !out)) return fail(ctx, TVS_EINVAL, "trace: cap >= 0 and a buffer");
+  ctx->trace_out = out;
+  ctx->trace_cap = cap;
+  ctx->trace_count = count;
   return TVS_OK;
 }
 

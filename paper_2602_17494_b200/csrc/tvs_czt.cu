@@ -63,6 +63,10 @@ struct CztIo {
 // Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
 // makes every access pattern below at most 2-way bank-conflicted.
 __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
+// pz(base + m S) - pz(base) for the 16-element groups of the fused passes: exact whenever S is a
+// multiple of 16, or S = 4 with base % 16 < 4 (every call below); with S and m compile-time
+// constants the group's 16 accesses become immediate offsets from one address.
+__device__ __forceinline__ int pzo(int m, int S) { return m * S + ((m * S) >> 4); }
 
 // Twiddle w^n = e^{-2 pi i n / M} from a two-level table in shared memory:
 // fine[n & 255] * coarse[n >> 8] (fine: 256 entries, coarse: M/256).
@@ -141,12 +145,17 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
 #pragma unroll
   for (int lg = PIN ? logM4 - 3 : logM4 - 1; lg >= 2; lg -= 2) {
     const int L = 1 << (2 * lg), Q = L >> 2, s1 = M >> (2 * lg + 2);
-    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+#pragma unroll
+    for (int it = 0; it < ((M >> 4) + nth - 1) / nth; ++it) {   // compile-time trip count
+      const int gidx = tid + it * nth;
+      if (((M >> 4) % nth) && gidx >= (M >> 4)) break;
       const int blk = gidx >> (2 * lg - 2), kp = gidx & (Q - 1);
       const int base = blk * 4 * L + kp;
       float2 x[16];
 #pragma unroll
-      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m * Q)];
+      float2 *zb = z + pz(base);   // base % 16 = kp < Q when Q = 4
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, Q)];
       // twiddles of the pair from two lookups: stage 1 (span L, k = kp + r Q) uses
       // w^{c k s1} = W^c * e^{-2 pi i c r / 16} with W = w^{kp s1}; stage 2 (span Q, k = kp,
       // stride 4 s1) uses V^c with V = w^{4 kp s1} (looked up, not W^4: keeps the error flat).
@@ -167,7 +176,7 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
         x[4 * t + 3] = cmul(x[4 * t + 3], V3);
       }
 #pragma unroll
-      for (int m = 0; m < 16; ++m) z[pz(base + m * Q)] = x[m];
+      for (int m = 0; m < 16; ++m) zb[pzo(m, Q)] = x[m];
     }
     __syncthreads();
   }
@@ -197,14 +206,19 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
       z[pz(4 * b + 3)] = x3;
     }
   } else {
-    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+#pragma unroll
+    for (int it = 0; it < ((M >> 4) + nth - 1) / nth; ++it) {   // compile-time trip count
+      const int gidx = tid + it * nth;
+      if (((M >> 4) % nth) && gidx >= (M >> 4)) break;
       const int base = gidx * 16;
       float4 g[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) g[m] = __ldg(reinterpret_cast<const float4 *>(gk + base) + m);
       float2 x[16];
 #pragma unroll
-      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m)];
+      float2 *zb = z + 17 * gidx;   // pz(16 gidx + m) = 17 gidx + m
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = zb[m];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {   // DIF span 4, k = r
         bfly4_dif(x[r], x[r + 4], x[r + 8], x[r + 12]);
@@ -233,7 +247,7 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
         bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
       }
 #pragma unroll
-      for (int m = 0; m < 16; ++m) z[pz(base + m)] = x[m];
+      for (int m = 0; m < 16; ++m) zb[m] = x[m];
     }
   }
   __syncthreads();
@@ -253,12 +267,17 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
 #pragma unroll
   for (int lg = (logM4 & 1) ? 1 : 2; lg < (POUT ? logM4 - 2 : logM4); lg += 2) {   // first pass: czt_middle
     const int L = 1 << (2 * lg), s2 = M >> (2 * lg + 4);
-    for (int gidx = tid; gidx < (M >> 4); gidx += nth) {
+#pragma unroll
+    for (int it = 0; it < ((M >> 4) + nth - 1) / nth; ++it) {   // compile-time trip count
+      const int gidx = tid + it * nth;
+      if (((M >> 4) % nth) && gidx >= (M >> 4)) break;
       const int blk = gidx >> (2 * lg), kp = gidx & (L - 1);
       const int base = blk * 16 * L + kp;
       float2 x[16];
 #pragma unroll
-      for (int m = 0; m < 16; ++m) x[m] = z[pz(base + m * L)];
+      float2 *zb = z + pz(base);   // base % 16 = kp < L when L = 4
+#pragma unroll
+      for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, L)];
       // stage 2 (span 4L, k = kp + r L, stride s2) uses U^c e^{-2 pi i c r/16}, U = w^{kp s2};
       // stage 1 (span L, k = kp, stride 4 s2) uses U^{4c}
       const float2 U1 = tw(kp * s2), U2 = cmul(U1, U1), U3 = cmul(U1, U2);
@@ -278,7 +297,7 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
         bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
       }
 #pragma unroll
-      for (int m = 0; m < 16; ++m) z[pz(base + m * L)] = x[m];
+      for (int m = 0; m < 16; ++m) zb[pzo(m, L)] = x[m];
     }
     __syncthreads();
   }

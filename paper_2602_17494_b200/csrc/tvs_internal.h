@@ -171,8 +171,8 @@ cudaError_t launch_irv2_zero_mean_g(float *f, int ldf, const float *d0, int n2, 
 // Primal-energy / duality-gap raw sums (see k_primal1_partial / k_primal2_partial): part needs
 // 3 (step 1) or 4 (step 2) x 592 doubles; out receives 3 or 4 doubles.
 cudaError_t launch_primal1(const float *tau, size_t plane, int ld, const float *f, const float *p,
-                           int n2, int n1, int row0, int row1, float delta, double *part,
-                           double *out, cudaStream_t s);
+                           int n2, int n1, int row0, int row1, float delta, float scale,
+                           double *part, double *out, cudaStream_t s);
 cudaError_t launch_primal2(const float *d, const float *d0, const float *f, const float *dxi,
                            const float *p1, const float *p2, int ldf, int n2, int n1, int row0,
                            int row1, float inv_alpha, double *part, double *out, cudaStream_t s);
@@ -203,8 +203,10 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
 // projection (kernel b)
 cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,
                               int ld, cudaStream_t s);
+// pivots r_k of every chain, plus the constant-tail compression (pcut, pinf, plast: [chain][ldn])
 cudaError_t launch_pivots(const ProjTile *chains_tiles, const int *chain_first_tile, int nchains,
-                          int n2, int n1, double *rinv, int ldn, int AT, cudaStream_t s);
+                          int n2, int n1, double *rinv, int ldn, int AT, int *pcut, double *pinf,
+                          double *plast, cudaStream_t s);
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s);
 // tcgen05 3xTF32 GEMM: C = A * Bt^T, Bt given as [N][K] row-major (tvs_gemm_tc.cu)
 cudaError_t launch_gemm_tc(const GemmDesc *descs, int batch, int maxM, int maxN, int bn,
@@ -239,6 +241,7 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
+                               const int *pcut, const double *pinf, const double *plast,
                                cudaStream_t s);
 
 }  // namespace tvs

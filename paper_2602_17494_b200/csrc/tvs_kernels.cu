@@ -771,7 +771,7 @@ __device__ __forceinline__ void block_sum_store3(double a, double b, double c, d
 __global__ void __launch_bounds__(RED_T)
 k_primal1_partial(const float *__restrict__ tau, size_t plane, int ld, const float *__restrict__ f,
                   const float *__restrict__ p, int n2, int n1, int row0, int row1, float delta,
-                  double *__restrict__ part) {
+                  float scale, double *__restrict__ part) {
   double tv = 0.0, fit = 0.0, gap = 0.0;
   const long long total = (long long)(row1 - row0) * n1;
   for (long long e = (long long)blockIdx.x * RED_T + threadIdx.x; e < total;
@@ -780,9 +780,9 @@ k_primal1_partial(const float *__restrict__ tau, size_t plane, int ld, const flo
     const size_t o = (size_t)i * ld + j;
     for (int k = 0; k < 2; ++k) {
       const float *t = tau + k * plane;
-      const double u = t[o];
-      const double ur = j < n1 - 1 ? (double)t[o + 1] : u;
-      const double ud = i < n2 - 1 ? (double)t[o + ld] : u;
+      const double u = (double)scale * t[o];   // tau = scale * the plane (1 or delta)
+      const double ur = j < n1 - 1 ? (double)scale * t[o + 1] : u;
+      const double ud = i < n2 - 1 ? (double)scale * t[o + ld] : u;
       tv_gap_terms(u, ur, ud, p[2 * k * plane + o], p[(2 * k + 1) * plane + o], tv, gap);
       const double r = u - (double)delta * (double)f[k * plane + o];
       fit += r * r;
@@ -1171,16 +1171,28 @@ __global__ void k_dct_tables(int n, float *__restrict__ cf, float *__restrict__ 
 // length n2 (Neumann Laplacian L_y), one thread per (chain, j >= 1):
 //   exterior chain of length L (far end Neumann): e_1 = -1 - s, e_k = -2 - s - 1/e_{k-1};
 //   the Schur complement adds -1/e_L to T's end diagonal; rinv_k = 1 / (Thomas pivot k).
+// Pivots r_k = 1/e_k of the Schur-corrected tridiagonal y-systems (one chain per distinct row
+// range).  Tail compression: the interior recurrence e_k = -2 - s - 1/e_{k-1} reaches an exact
+// fp64 fixed point after ~18 / sqrt(s) rows (every frequency but the lowest ~N/250), from which
+// all interior pivots are bitwise equal; pcut[c][j] = first row of that constant run (nt - 1 if
+// none), pinf = its value, plast = the last row's pivot (bottom Schur correction).  The solve reads
+// the table only above pcut (the table below it is still written, and identical).
 __global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restrict__ first,
-                         int nchains, int n2, int n1, double *__restrict__ rinv, int ldn, int AT) {
+                         int nchains, int n2, int n1, double *__restrict__ rinv, int ldn, int AT,
+                         int *__restrict__ pcut, double *__restrict__ pinf,
+                         double *__restrict__ plast) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   int c = blockIdx.y;
   if (j >= n1 || c >= nchains) return;
   const ProjTile tl = tiles[first[c]];
   double *out = rinv + (size_t)c * AT * ldn;
   int nt = tl.ty1 - tl.ty0 + 1;
+  const size_t pj = (size_t)c * ldn + j;
   if (j == 0) {
     for (int k = 0; k < nt; ++k) out[(size_t)k * ldn] = 0.0;
+    pcut[pj] = 0;
+    pinf[pj] = 0.0;
+    plast[pj] = 0.0;
     return;
   }
   double sg = 2.0 * sinpi((double)j / (2.0 * n1));
@@ -1194,13 +1206,18 @@ __global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restri
   double dbot = tl.ty1 < n2 - 1 ? (-2.0 - s + chain_corr(n2 - 1 - tl.ty1)) : (-1.0 - s);
   double e = dtop;
   out[j] = 1.0 / e;
+  int cut = nt - 1;
   for (int k = 1; k < nt; ++k) {
     double dk = (k == nt - 1) ? dbot : (-2.0 - s);
+    const double prev = e;
     e = dk - 1.0 / e;
     out[(size_t)k * ldn + j] = 1.0 / e;
+    if (cut == nt - 1 && k < nt - 1 && e == prev) cut = k - 1;   // r_{k-1} = r_k = ... = r_{nt-2}
   }
+  pcut[pj] = cut;
+  pinf[pj] = out[(size_t)min(cut, nt - 1) * ldn + j];
+  plast[pj] = out[(size_t)(nt - 1) * ldn + j];
 }
-
 
 
 // Segmented form of the per-frequency y-solve (default).  Both Thomas sweeps are first-order
@@ -1224,7 +1241,8 @@ __global__ void __launch_bounds__(SJB *SSEG_MAX)
 k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
               int AT, int ldn, const double *__restrict__ rinv, float *__restrict__ zs,
               float *__restrict__ phx, float *__restrict__ phy, float *__restrict__ phx_lo,
-              float *__restrict__ phy_lo, int AP) {
+              float *__restrict__ phy_lo, int AP, const int *__restrict__ pcut,
+              const double *__restrict__ pinf, const double *__restrict__ plast) {
   __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
   __shared__ double sh_tot[SJB];
   extern __shared__ __align__(16) float sbuf[];   // SMEM: [AT][SJB]
@@ -1240,6 +1258,12 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const size_t st = (size_t)ldn;   // row stride of every global plane
   const float *__restrict__ b = qhat + (size_t)tix * AT * st + jj;
   const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * st + jj;
+  // pivot r_k: the table above the constant tail (see k_pivots), the tail value below it
+  const int pc = pcut[(size_t)tl.chain * st + jj];
+  const double rinf = pinf[(size_t)tl.chain * st + jj], rlast = plast[(size_t)tl.chain * st + jj];
+  auto piv = [&](int kk) -> double {
+    return kk < pc ? __ldg(ri + (size_t)kk * st) : (kk == nt - 1 ? rlast : rinf);
+  };
   // z (and, in SMEM mode, the staged b) live at zb with row stride zst
   float *zb = SMEM ? sbuf + tx : zs + (size_t)tix * AT * st + jj;
   const size_t zst = SMEM ? (size_t)SJB : st;
@@ -1282,14 +1306,13 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         k = 1;
       }
       const float *bp = b1 + (size_t)k * b1st;
-      const double *rp = ri + (size_t)(k - 1) * st;
-      for (; k + SU <= k1; k += SU, bp += SU * b1st, rp += SU * st) {
+      for (; k + SU <= k1; k += SU, bp += SU * b1st) {
         float bv[SU];
         double rv[SU];
 #pragma unroll
         for (int u = 0; u < SU; ++u) {   // the whole batch of loads first (latency-bound)
           bv[u] = bp[u * b1st];
-          rv[u] = rp[u * st];
+          rv[u] = piv(k - 1 + u);
         }
 #pragma unroll
         for (int u = 0; u < SU; ++u) {
@@ -1297,8 +1320,8 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
           g *= -rv[u];
         }
       }
-      for (; k < k1; ++k, bp += b1st, rp += st) {
-        const double r = *rp;
+      for (; k < k1; ++k, bp += b1st) {
+        const double r = piv(k - 1);
         a = fma(-r, a, (double)*bp);
         g *= -r;
       }
@@ -1329,15 +1352,14 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
       k = 1;
     }
     const float *bp = bb + (size_t)k * zst;
-    const double *rp = ri + (size_t)(k - 1) * st;
     float *zp = zb + (size_t)k * zst;
-    for (; k + SU <= k1; k += SU, bp += SU * zst, rp += SU * st, zp += SU * zst) {
+    for (; k + SU <= k1; k += SU, bp += SU * zst, zp += SU * zst) {
       float bv[SU];
       double rv[SU];
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         bv[u] = bp[u * zst];
-        rv[u] = rp[u * st];
+        rv[u] = piv(k - 1 + u);
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
@@ -1345,8 +1367,8 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         zp[u * zst] = (float)zc;
       }
     }
-    for (; k < k1; ++k, bp += zst, rp += st, zp += zst) {
-      zc = fma(-*rp, zc, (double)*bp);
+    for (; k < k1; ++k, bp += zst, zp += zst) {
+      zc = fma(-piv(k - 1), zc, (double)*bp);
       *zp = (float)zc;
     }
   }
@@ -1356,14 +1378,13 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   if (valid && j > 0 && k0 < k1) {
     int k = k1 - 1;
     const float *zp = zb + (size_t)k * zst;
-    const double *rp = ri + (size_t)k * st;
-    for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst, rp -= SU * st) {
+    for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst) {
       float zv[SU];
       double rv[SU];
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         zv[u] = zp[-(ptrdiff_t)(u * zst)];
-        rv[u] = rp[-(ptrdiff_t)(u * st)];
+        rv[u] = piv(k - u);
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
@@ -1371,8 +1392,8 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         g *= -rv[u];
       }
     }
-    for (; k >= k0; --k, zp -= zst, rp -= st) {
-      const double r = *rp;
+    for (; k >= k0; --k, zp -= zst) {
+      const double r = piv(k);
       a = r * ((double)*zp - a);
       g *= -r;
     }
@@ -1416,7 +1437,6 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   double un = sh_c[sg][tx];
   int k = k1 - 1;
   const float *zp = zb + (size_t)k * zst;
-  const double *rp = ri + (size_t)k * st;
   auto emit = [&](int kk, double uk) {
     if (kk >= po && kk < nout) {
       store_split(ox, oxl, (size_t)kk * st, cx * uk);
@@ -1425,18 +1445,18 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     }
     un = uk;
   };
-  for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst, rp -= SU * st) {
+  for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst) {
     float zv[SU];
     double rv[SU];
 #pragma unroll
     for (int u = 0; u < SU; ++u) {
       zv[u] = zp[-(ptrdiff_t)(u * zst)];
-      rv[u] = rp[-(ptrdiff_t)(u * st)];
+      rv[u] = piv(k - u);
     }
 #pragma unroll
     for (int u = 0; u < SU; ++u) emit(k - u, rv[u] * ((double)zv[u] - un));
   }
-  for (; k >= k0; --k, zp -= zst, rp -= st) emit(k, *rp * ((double)*zp - un));
+  for (; k >= k0; --k, zp -= zst) emit(k, piv(k) * ((double)*zp - un));
 }
 
 // Products of the recurrence coefficients over each solve segment (data-independent, computed
@@ -1973,11 +1993,11 @@ cudaError_t launch_sumsq2(const float *r, size_t plane, int ld, int n1, int row0
   return cudaGetLastError();
 }
 cudaError_t launch_primal1(const float *tau, size_t plane, int ld, const float *f, const float *p,
-                           int n2, int n1, int row0, int row1, float delta, double *part,
-                           double *out, cudaStream_t s) {
+                           int n2, int n1, int row0, int row1, float delta, float scale,
+                           double *part, double *out, cudaStream_t s) {
   g_extra_launches += 1;
   k_primal1_partial<<<RED_BLOCKS, RED_T, 0, s>>>(tau, plane, ld, f, p, n2, n1, row0, row1, delta,
-                                                 part);
+                                                 scale, part);
   k_sum_partials_multi<<<3, RED_T, 0, s>>>(part, RED_BLOCKS, out);
   return cudaGetLastError();
 }
@@ -2051,9 +2071,10 @@ cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT
   return cudaGetLastError();
 }
 cudaError_t launch_pivots(const ProjTile *tiles, const int *first, int nchains, int n2, int n1,
-                          double *rinv, int ldn, int AT, cudaStream_t s) {
+                          double *rinv, int ldn, int AT, int *pcut, double *pinf, double *plast,
+                          cudaStream_t s) {
   k_pivots<<<dim3((n1 + 127) / 128, nchains), 128, 0, s>>>(tiles, first, nchains, n2, n1, rinv,
-                                                           ldn, AT);
+                                                           ldn, AT, pcut, pinf, plast);
   return cudaGetLastError();
 }
 cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cudaStream_t s) {
@@ -2104,6 +2125,7 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
+                               const int *pcut, const double *pinf, const double *plast,
                                cudaStream_t s) {
   // one warp per segment of ~32 rows, at most SSEG_MAX segments (the max tile height AT decides)
   const int nseg = std::min(SSEG_MAX, std::max(1, (AT + 31) / 32));
@@ -2115,10 +2137,10 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
       if (e != cudaSuccess) return e;
     }
     k_proj_solve3<true><<<grid, block, smem, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
-                                                   phx_lo, phy_lo, AP);
+                                                   phx_lo, phy_lo, AP, pcut, pinf, plast);
   } else {
     k_proj_solve3<false><<<grid, block, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
-                                                 phx_lo, phy_lo, AP);
+                                                 phx_lo, phy_lo, AP, pcut, pinf, plast);
   }
   return cudaGetLastError();
 }

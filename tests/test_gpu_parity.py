@@ -376,3 +376,38 @@ def test_step1_side_stream_overlap_bitwise(ctx):
             assert torch.equal(t0, t1) and torch.equal(p0, p1), shape
     finally:
         serial.close()
+
+
+def test_energy_trace_matches_oracle(ctx):
+    """tvs_set_trace: the per-sweep (E, D, gap) of the Schwarz iterates (the Fig. 7 protocol,
+    P:1769-1782) match the oracle's energies of the same iterates at every sweep, both steps."""
+    img = random_image(29, 34, seed=91)
+    d0 = img.astype(np.float64)
+    L = (2, 2, 3, 4)
+    lay = olayout.Layout(29, 34, *L)
+    sweeps, inner = 6, 3
+    ctx.set_trace(sweeps + 1)
+    try:
+        tau, _, st1 = ctx.tv_stokes_step1(_dev(img), 0.05, L, (sweeps, inner, 0.125))
+        tr1 = ctx.trace()
+        tau_np = tau.cpu().numpy().astype(np.float64)
+        d, _, st2 = ctx.tv_stokes_step2(tau, _dev(img), 0.1, L, (sweeps, inner, 0.125))
+        tr2 = ctx.trace()
+    finally:
+        ctx.set_trace(0)
+    assert tr1.shape == (sweeps + 1, 3) and tr2.shape == (sweeps + 1, 3)
+    ptau0 = spectral.project(S.tau0(d0))
+    alpha, g, _ = S.irv2_data(d0, tau_np, 0.1)
+    for n in range(sweeps + 1):
+        t_ref, p_ref, i_ref = S.dd_step1(d0, 0.05, lay, n, inner)
+        e_ref = S.primal_energy_tfs(t_ref, ptau0, 0.05)
+        assert abs(tr1[n, 0] - e_ref) <= TOL * abs(e_ref), (n, tr1[n], e_ref)
+        assert abs(tr1[n, 1] - i_ref["dual_energy"]) <= TOL * i_ref["dual_energy"], n
+        assert abs(tr1[n, 2] - S.duality_gap(t_ref, p_ref)) <= TOL * abs(e_ref), n
+        d_ref, q_ref, j_ref = S.dd_step2(d0, tau_np, 0.1, lay, n, inner)
+        e2 = S.primal_energy_irv2(d_ref, d0, g, alpha)
+        assert abs(tr2[n, 0] - e2) <= TOL * abs(e2), (n, tr2[n], e2)
+        assert abs(tr2[n, 1] - j_ref["dual_energy"]) <= TOL * j_ref["dual_energy"], n
+        assert abs(tr2[n, 2] - S.duality_gap(d_ref - g, q_ref)) <= TOL * abs(e2), n
+    # the last entry is the returned solution
+    assert tr1[-1, 0] == st1.primal_energy and abs(tr2[-1, 0] - st2.primal_energy) <= 1e-12 * abs(st2.primal_energy)
