@@ -15,7 +15,8 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtvstokes.so")
+# TVS_LIB_PATH: an alternative build of the same library (A/B experiments of build-time variants)
+LIB_PATH = os.environ.get("TVS_LIB_PATH") or os.path.join(HERE, "libtvstokes.so")
 
 # exported symbols declared in include/tvstokes.h
 ABI_SYMBOLS = [

@@ -43,15 +43,17 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in SOURCES + HEADERS)
 
 
-def build(force=False, verbose=False):
-    """Compile every CUDA source into libtvstokes.so (sm_100a).  Returns the library path."""
-    if not force and up_to_date():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile every CUDA source into libtvstokes.so (sm_100a).  Returns the library path.
+    defines / out: a build-time variant into another file (A/B experiments via TVS_LIB_PATH)."""
+    out = out or LIB
+    if not force and not defines and out == LIB and up_to_date():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + SOURCES
+    cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", out] + SOURCES
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -47,7 +47,10 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
   return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
-constexpr int CZT_THREADS = 512;   // threads per chirp-z CTA (the FFT passes assume it)
+#ifndef TVS_CZT_THREADS
+#define TVS_CZT_THREADS 512
+#endif
+constexpr int CZT_THREADS = TVS_CZT_THREADS;   // threads per chirp-z CTA (build-time A/B: 512 / 1024)
 
 // Row pointers of one chunk for the pruned first / last FFT passes.
 struct CztIo {

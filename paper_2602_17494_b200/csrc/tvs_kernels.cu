@@ -1232,18 +1232,23 @@ __global__ void k_pivots(const ProjTile *__restrict__ tiles, const int *__restri
 // (flat in N).  j = 0 (singular Neumann L_y^dagger) uses the same skeleton for
 // its prefix sums: D+_y u = prefix(b) - mu (y + 1), mu = sum(b) / n2.
 constexpr int SJB = 32, SSEG_MAX = 16, SU = 8;
+// solve3 (tall tiles: config-4 strips, the global projections, config 5) takes up to 32 segments
+// per column (1024 threads): its fp64 recurrences are latency-bound chains, and with one CTA per SM
+// (the staged column block fills shared memory) shorter chains and twice the warps hide them
+// (TVS_SOLVE3_SEG caps it, A/B)
+constexpr int S3SEG_MAX = 32;
 // SMEM = true: the CTA's column block of qhat is staged in shared memory by the first pass and
 // overwritten in place by z (fp32), so qhat is read from HBM once and z never leaves the SM
 // (AT x 128 B of dynamic shared memory; used when that fits).  SMEM = false: z in a global
 // scratch.
 template <bool SMEM>
-__global__ void __launch_bounds__(SJB *SSEG_MAX)
+__global__ void __launch_bounds__(SJB *S3SEG_MAX)
 k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
               int AT, int ldn, const double *__restrict__ rinv, float *__restrict__ zs,
               float *__restrict__ phx, float *__restrict__ phy, float *__restrict__ phx_lo,
               float *__restrict__ phy_lo, int AP, const int *__restrict__ pcut,
               const double *__restrict__ pinf, const double *__restrict__ plast) {
-  __shared__ double sh_a[SSEG_MAX][SJB], sh_c[SSEG_MAX][SJB];
+  __shared__ double sh_a[S3SEG_MAX][SJB], sh_c[S3SEG_MAX][SJB];
   __shared__ double sh_tot[SJB];
   extern __shared__ __align__(16) float sbuf[];   // SMEM: [AT][SJB]
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
@@ -2127,8 +2132,9 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
                                const int *pcut, const double *pinf, const double *plast,
                                cudaStream_t s) {
-  // one warp per segment of ~32 rows, at most SSEG_MAX segments (the max tile height AT decides)
-  const int nseg = std::min(SSEG_MAX, std::max(1, (AT + 31) / 32));
+  // one warp per segment of >= 32 rows, at most S3SEG_MAX segments (the max tile height decides)
+  static const int cap = getenv("TVS_SOLVE3_SEG") ? std::max(1, std::min(S3SEG_MAX, atoi(getenv("TVS_SOLVE3_SEG")))) : S3SEG_MAX;
+  const int nseg = std::min(cap, std::max(1, AT / 32));
   const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);
   const size_t smem = (size_t)AT * SJB * sizeof(float);
   if (smem <= 160 * 1024) {

@@ -109,6 +109,31 @@ def ellipses_on_sinusoid(n: int = 512, seed: int = 1002, sigma: float = 0.08,
     return np.clip(img, 0.0, 1.0).astype(np.float32)
 
 
+def ellipses_rect(n2: int = 270, n1: int = 480, seed: int = 1010, sigma: float = 0.1,
+                  count: int = 12) -> np.ndarray:
+    """Stand-in for the paper's DD validation image (Image 10, 270 x 480, sigma^2 = 0.01, P:1771;
+    not distributed): the config-2 recipe on a rectangle -- seeded ellipses (U[0,1] intensity,
+    semi-axes U[min/32, min/8]) on 0.5 + 0.2 sin(2pi j/128) cos(2pi i/128), Gaussian noise
+    sigma = 0.1, clipped to [0, 1]."""
+    i = np.arange(n2, dtype=np.float64)[:, None]
+    j = np.arange(n1, dtype=np.float64)[None, :]
+    img = 0.5 + 0.2 * np.sin(2 * np.pi * j / 128.0) * np.cos(2 * np.pi * i / 128.0)
+    g = _Seq(seed)
+    m = min(n2, n1)
+    for _ in range(count):
+        cy, cx = g.u(1, 0.0, n2)[0], g.u(1, 0.0, n1)[0]
+        ay, ax = g.u(2, m / 32.0, m / 8.0)
+        ang = g.u(1, 0.0, np.pi)[0]
+        val = g.u(1)[0]
+        ca, sa = np.cos(ang), np.sin(ang)
+        dx, dy = j - cx, i - cy
+        xr = ca * dx + sa * dy
+        yr = -sa * dx + ca * dy
+        img = np.where((xr / ax) ** 2 + (yr / ay) ** 2 <= 1.0, val, img)
+    img = img + gaussian_field(seed, n2, n1, sigma)
+    return np.clip(img, 0.0, 1.0).astype(np.float32)
+
+
 def _voronoi_geometry(n, cells, seed):
     g = int(round(np.sqrt(cells)))
     assert g * g == cells
