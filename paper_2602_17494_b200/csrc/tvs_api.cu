@@ -194,6 +194,7 @@ struct ProjBatch {
   bool czt = false;
   CztGeom gf{}, gi{};
   CztJob *d_fj = nullptr, *d_ij = nullptr;
+  CztJob *d_ij_add = nullptr;   // inverse jobs writing grad phi + omega0 (the inner loop's)
   int nfj = 0, nij = 0, fj_rows = 0, ij_rows = 0;
   float2 *gtab_f = nullptr, *gtab_i = nullptr, *tw_f = nullptr, *tw_i = nullptr;
   // algorithmic work per launch: contraction flops (dense 2MNK), FFT flops of the chirp-z form
@@ -518,7 +519,8 @@ double proj_tile_bytes(int AT, int AP, int n1t) {
 tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<ProjTile> &tiles_in,
                       int n2t, int n1t, float *q, int ldq, float *G, int ldG, const Tables *T,
                       int fr0 = -1, int fr1 = -1, size_t gplane_arg = 0, int gtiles = 0,
-                      bool local_io = false) {
+                      bool local_io = false, const float *om = nullptr, int AP_om = 0,
+                      int ld_om = 0) {
   B.tiles = tiles_in;
   B.ntiles = (int)tiles_in.size();
   std::map<std::pair<int, int>, int> chain_of;
@@ -724,6 +726,18 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     }
     TRY(upload(ctx, P.bufs, &B.d_fj, fj));
     TRY(upload(ctx, P.bufs, &B.d_ij, ij));
+    if (om) {   // omega0 [slot][2][AP_om][ld_om] of the group, added by the inner loop's jobs
+      std::vector<CztJob> ija = ij;
+      for (int k = 0; k < ng; ++k)
+        for (int i = B.g0[k]; i < B.g0[k + 1]; ++i) {
+          const size_t sl = local_io ? (size_t)(i - B.g0[k]) : (size_t)i;
+          for (int c = 0; c < 2; ++c) {   // job 2i: x (plane 0), 2i + 1: y (plane 1)
+            ija[2 * i + c].add = om + ((sl * 2 + c) * AP_om + B.tiles[i].po) * ld_om;
+            ija[2 * i + c].ldadd = ld_om;
+          }
+        }
+      TRY(upload(ctx, P.bufs, &B.d_ij_add, ija));
+    }
   }
   TRY(dalloc(ctx, P.bufs, &B.pcut, (size_t)B.nchains * B.ldn));
   TRY(dalloc(ctx, P.bufs, &B.pinf, (size_t)B.nchains * B.ldn));
@@ -946,7 +960,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->q, (size_t)sg * g.AT * g.ldT));
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)sg * 2 * g.AP * g.ldP));
     TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T, -1, -1,
-                   (size_t)sg * g.AP * g.ldP, sg, sg < g.M));
+                   (size_t)sg * g.AP * g.ldP, sg, sg < g.M, P->om, g.AP, g.ldP));
   }
   *out = P.get();
   ctx->plans[key] = std::move(P);
@@ -1113,7 +1127,7 @@ bool stop_now(const tvs_ctx *ctx, double d_prev, double d_next, double npts, dou
 // grad phi of phi = R_T Delta^dagger E_T q for the tiles of group k of the batch (kernel b).  For
 // the global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
 tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_t s,
-                         bool gather = false) {
+                         bool gather = false, bool add_om = false) {
   const int G2 = P.G2, G1 = P.G1;
   if (gather && B.g0.size() != 2) return fail(ctx, TVS_EINVAL, "gathered projection batch must be one group");
   const int t0 = B.g0[k], nt = B.g0[k + 1] - t0;
@@ -1141,7 +1155,8 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
   }));
   if (B.czt)
     return run(ctx, s, F_CZT_INV, 0, B.ginv[k], [&] {
-      return launch_czt(B.d_ij + 2 * t0, 2 * nt, B.ij_rows, B.gi, B.gtab_i, B.tw_i, s);
+      return launch_czt((add_om ? B.d_ij_add : B.d_ij) + 2 * t0, 2 * nt, B.ij_rows, B.gi, B.gtab_i,
+                        B.tw_i, s);
     });
   return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
     return launch_gemm_tma_ts(B.d_inv, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
@@ -1499,10 +1514,13 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       for (int kk = 0; kk < it.inner; ++kk) {
         TRY(run(ctx, s, F_PREDIV, pdb, 0,
                 [&] { return launch_prediv1(sk, gk, vin, G2, G1, P->q, nullptr, s); }));
-        TRY(project_group(ctx, *P, P->local, k, s));
-        TRY(run(ctx, s, F_SWEEP1, swb, 0, [&] {
-          return launch_sweep1(sk, gk, P->d_thy, P->d_thx, vin, P->gphi, g.ldP, P->om, vout, G2,
-                               G1, it.t, s);
+        // chirp-z form: the inverse transforms write grad phi + omega0 (kernel a' then reads one
+        // field: 40 instead of 48 B per update); GEMM form: kernel (a') adds omega0 itself
+        const bool fused = P->local.czt && P->local.d_ij_add;
+        TRY(project_group(ctx, *P, P->local, k, s, false, fused));
+        TRY(run(ctx, s, F_SWEEP1, fused ? swb * 40.0 / 48.0 : swb, 0, [&] {
+          return launch_sweep1(sk, gk, P->d_thy, P->d_thx, vin, P->gphi, g.ldP,
+                               fused ? nullptr : P->om, vout, G2, G1, it.t, s);
         }));
         std::swap(vin, vout);
       }

@@ -58,6 +58,7 @@ struct CztIo {
   const float2 *pre;
   int ucnt;
   float *out;
+  const float *add;   // nullable: out = transform + add (same row layout as out)
   const float2 *post;
   int vcnt, kind;
   bool pin, pout;
@@ -71,13 +72,21 @@ __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
 // constants the group's 16 accesses become immediate offsets from one address.
 __device__ __forceinline__ int pzo(int m, int S) { return m * S + ((m * S) >> 4); }
 
-// Twiddle w^n = e^{-2 pi i n / M} from a two-level table in shared memory:
-// fine[n & 255] * coarse[n >> 8] (fine: 256 entries, coarse: M/256).
+// Twiddle w^n = e^{-2 pi i n / M}.  TVS_CZT_TWG (default): one read of the full M-entry table in
+// global memory (L1 / L2-resident, off the shared-memory pipe the FFT passes saturate);
+// otherwise a two-level table in shared memory, fine[n & 255] * coarse[n >> 8].
+#ifndef TVS_CZT_TWG
+#define TVS_CZT_TWG 1
+#endif
 struct Tw {
-  const float2 *fine, *coarse;
+  const float2 *fine, *coarse, *full;
   __device__ __forceinline__ float2 operator()(int n) const {
+#if TVS_CZT_TWG
+    return __ldg(full + n);
+#else
     const float2 f = fine[n & 255];
     return (n >> 8) ? cmul(f, coarse[n >> 8]) : f;
+#endif
   }
 };
 
@@ -264,7 +273,8 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
 // goes through the post-chirp straight to global memory (kind 2: imaginary part).
 template <int logM4, bool POUT>
 __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__restrict__ out,
-                                            const float2 *__restrict__ post, int vcnt, int kind) {
+                                            const float2 *__restrict__ post, int vcnt, int kind,
+                                            const float *__restrict__ add) {
   constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
   const int tid = threadIdx.x;
 #pragma unroll
@@ -326,7 +336,7 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
       const float2 a0 = make_float2(y[0].x + c2.x, y[0].y + c2.y);
       const float2 a2 = make_float2(c1.x + c3.x, c1.y + c3.y);
       const float2 o = cmul(__ldg(post + kp), make_float2(a0.x + a2.x, a0.y + a2.y));
-      out[kp] = kind == 2 ? o.y : o.x;
+      out[kp] = (kind == 2 ? o.y : o.x) + (add ? add[kp] : 0.f);
     }
   }
 }
@@ -339,7 +349,7 @@ __device__ __forceinline__ void czt_fft_pair_t(float2 *z, const Tw &tw, const fl
                                                const CztIo &io) {
   fft_dif<logM4, PIN>(z, tw, io.in, io.pre, io.ucnt);
   czt_middle<logM4>(z, gk);
-  fft_dit_inv<logM4, POUT>(z, tw, io.out, io.post, io.vcnt, io.kind);
+  fft_dit_inv<logM4, POUT>(z, tw, io.out, io.post, io.vcnt, io.kind, io.add);
 }
 template <int logM4>
 __device__ __forceinline__ void czt_fft_pair_p(float2 *z, const Tw &tw, const float2 *__restrict__ gk,
@@ -377,7 +387,7 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   float2 *tfine = zsm + MP, *tcoarse = tfine + 256;
   for (int i = tid; i < 256; i += nth) tfine[i] = i < M ? __ldg(tw + i) : make_float2(1.f, 0.f);
   for (int i = tid; i <= (M >> 8); i += nth) tcoarse[i] = (i << 8) < M ? __ldg(tw + (i << 8)) : make_float2(1.f, 0.f);
-  const Tw twd{tfine, tcoarse};
+  const Tw twd{tfine, tcoarse, tw};
   const float2 *__restrict__ cc = jb.pre;    // c_n = e^{i pi n^2 / N}
   const float2 *__restrict__ ee = jb.post;   // e_k = e^{i pi k / (2N)}
   const float *__restrict__ ia = jb.in + (size_t)r0 * jb.ldin;
@@ -454,10 +464,13 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
     }
   }
   __syncthreads();
-  const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, 0, 0, false, false};
+  const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, false, false};
   czt_fft_pair(zsm, G.logM4, twd, gtab, io);
   float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
   float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
+  // inverse jobs of the inner loop: out = grad phi + omega0 (added here, see CztJob::add)
+  const float *__restrict__ aa = jb.add ? jb.add + (size_t)r0 * jb.ldadd : nullptr;
+  const float *__restrict__ ab = (jb.add && two) ? aa + jb.ldadd : nullptr;
   if (kind == 3) {   // Qhat_a[k] = Re(conj(e_k) A_k), Qhat_b[k] = Re(conj(e_k) B_k)
     for (int k0 = tid; k0 < jb.vlen; k0 += B * nth) {
       float2 ck[B], cm[B], e[B];
@@ -497,10 +510,10 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
         const int n = (x & 1) ? N - 1 - (x >> 1) : (x >> 1);
         const float2 y = cmulc(zsm[pz(n)], cn[r]);   // Y_n; v = conj(Y) / 2
         if (kind == 4) {
-          oa[i] = 0.5f * y.x;
-          if (ob) ob[i] = -0.5f * y.y;
+          oa[i] = 0.5f * y.x + (aa ? aa[i] : 0.f);
+          if (ob) ob[i] = -0.5f * y.y + (ab ? ab[i] : 0.f);
         } else {
-          oa[i] = 0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y;
+          oa[i] = (0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y) + (aa ? aa[i] : 0.f);
         }
       }
     }
@@ -531,10 +544,11 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   for (int i = tid; i < vcnt; i += nth) acc[i] = 0.f;
   for (int i = tid; i < 256; i += nth) tfine[i] = i < G.M ? __ldg(tw + i) : make_float2(1.f, 0.f);
   for (int i = tid; i <= (G.M >> 8); i += nth) tcoarse[i] = (i << 8) < G.M ? __ldg(tw + (i << 8)) : make_float2(1.f, 0.f);
-  const Tw twd{tfine, tcoarse};
+  const Tw twd{tfine, tcoarse, tw};
   const float *__restrict__ in = jb.in + (size_t)row * jb.ldin;
   const int nuc = (jb.ulen + G.Uc - 1) / G.Uc;
   float *__restrict__ out = jb.out + (size_t)row * jb.ldout + v0;
+  const float *__restrict__ addr = jb.add ? jb.add + (size_t)row * jb.ldadd + v0 : nullptr;
   // pruned first / last passes for narrow inputs / outputs (tiles of a wide layout)
   const bool pin = G.prune && G.logM4 >= 3 && jb.ulen <= (G.M >> 4);
   const bool pout = G.prune && G.logM4 >= 3 && nuc == 1 && vcnt <= (G.M >> 4);
@@ -559,7 +573,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
       }
     }
     __syncthreads();
-    const CztIo io{in + u0, jb.pre + u0, ucnt, out, jb.post + v0, vcnt, jb.kind, pin, pout};
+    const CztIo io{in + u0, jb.pre + u0, ucnt, out, addr, jb.post + v0, vcnt, jb.kind, pin, pout};
     czt_fft_pair(zsm, G.logM4, twd, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M, io);
     for (int i0 = tid; i0 < (pout ? 0 : vcnt); i0 += 4 * nth) {
       float2 pv[4];
@@ -574,14 +588,14 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
         if (i >= vcnt) break;
         const float2 c = cmul(pv[r], zsm[pz(i)]);
         const float val = jb.kind == 2 ? c.y : c.x;
-        if (nuc == 1) out[i] = val;   // one input chunk: straight to global memory
+        if (nuc == 1) out[i] = val + (addr ? addr[i] : 0.f);   // one input chunk: straight out
         else acc[i] += val;
       }
     }
     __syncthreads();
   }
   if (nuc > 1)
-    for (int i = tid; i < vcnt; i += nth) out[i] = acc[i];
+    for (int i = tid; i < vcnt; i += nth) out[i] = acc[i] + (addr ? addr[i] : 0.f);
 }
 
 // ------------------------------------------------------------------------------------ host side

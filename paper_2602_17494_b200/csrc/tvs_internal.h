@@ -93,6 +93,10 @@ struct CztJob {
   // chirp tables (fp64-accurate, rounded once): pre[u] = e^{i theta (u^2 + cpre u)} for
   // u in [0, ulen), post[v] = e^{i theta (v^2 + cpost v)} for v in [0, vlen)
   const float2 *pre = nullptr, *post = nullptr;
+  // nullable: out = transform + add (rows of ldadd floats) -- the inner loop's inverse jobs write
+  // grad phi + omega0 so kernel (a') reads one field instead of two (bitwise the same sum)
+  const float *add = nullptr;
+  int ldadd = 0;
 };
 // host: fill the chirp tables of every job (deduplicated by (c, length)); returns the table
 std::vector<float2> czt_chirp_tables(int N, std::vector<CztJob> &jobs, std::vector<size_t> &pre_off,

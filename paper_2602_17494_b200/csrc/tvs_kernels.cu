@@ -1040,6 +1040,7 @@ k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
 
 // Kernel (a') streaming form: rho_k = w_k - grad phi_k - omega0_k on S+, psi_k = grad rho_k,
 // row-wise ball update of (v_k1, v_k2) (Alg. 5)
+template <bool OM>
 __global__ void __launch_bounds__(32 * S1_WARPS)
 k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
           const float *__restrict__ thx, const float *__restrict__ vin,
@@ -1070,8 +1071,8 @@ k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
   const size_t pl = (size_t)g.A * g.ldS;
   const float *g1 = gphi + ((size_t)0 * g.MG + blockIdx.z) * g.AP * ldg;
   const float *g2 = gphi + ((size_t)1 * g.MG + blockIdx.z) * g.AP * ldg;
-  const float *o1 = om + ((size_t)blockIdx.z * 2 + 0) * g.AP * g.ldP;
-  const float *o2 = om + ((size_t)blockIdx.z * 2 + 1) * g.AP * g.ldP;
+  const float *o1 = OM ? om + ((size_t)blockIdx.z * 2 + 0) * g.AP * g.ldP : nullptr;
+  const float *o2 = OM ? om + ((size_t)blockIdx.z * 2 + 1) * g.AP * g.ldP : nullptr;
   const float thA = pc.SA ? thx[sd.ix * g.B + pc.jA] : 0.f;
   const float thB = pc.SB ? thx[sd.ix * g.B + pc.jB] : 0.f;
   struct Row { float2 a11, a12, a21, a22, h1, h2; };   // h_k = grad phi_k + omega0_k
@@ -1083,10 +1084,15 @@ k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy
     r.a22 = ld_pair(vb + 3 * pl, g.ldS, li, a, pc, pc.SA, pc.SB);
     const float2 ga = ld_pair(g1, ldg, li, ap, pc, pc.PA, pc.PB);
     const float2 gb = ld_pair(g2, ldg, li, ap, pc, pc.PA, pc.PB);
-    const float2 oa = ld_pair(o1, g.ldP, li, ap, pc, pc.PA, pc.PB);
-    const float2 obb = ld_pair(o2, g.ldP, li, ap, pc, pc.PA, pc.PB);
-    r.h1 = make_float2(ga.x + oa.x, ga.y + oa.y);
-    r.h2 = make_float2(gb.x + obb.x, gb.y + obb.y);
+    if constexpr (OM) {   // h = grad phi + omega0; OM = false: gphi already holds the sum
+      const float2 oa = ld_pair(o1, g.ldP, li, ap, pc, pc.PA, pc.PB);
+      const float2 obb = ld_pair(o2, g.ldP, li, ap, pc, pc.PA, pc.PB);
+      r.h1 = make_float2(ga.x + oa.x, ga.y + oa.y);
+      r.h2 = make_float2(gb.x + obb.x, gb.y + obb.y);
+    } else {
+      r.h1 = ga;
+      r.h2 = gb;
+    }
     return r;
   };
   auto rho = [&](int li, const Row &r, float2 v12m, float2 v22m, float2 &r1o, float2 &r2o) {
@@ -2066,8 +2072,12 @@ cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const fl
                           float *vout, int n2, int n1, float t, cudaStream_t s) {
   const int strips = (g.B + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.A, g.M, strips);
   dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.A + rb - 1) / rb, g.M);
-  k_sweep1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout, n2, n1,
-                                                t, rb);
+  if (om)
+    k_sweep1s<true><<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
+                                                        n2, n1, t, rb);
+  else
+    k_sweep1s<false><<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, thy, thx, vin, gphi, ldg, om, vout,
+                                                         n2, n1, t, rb);
   return cudaGetLastError();
 }
 cudaError_t launch_dct_tables(int n, float *cf, float *cn, float *sn, float *snT, float *split6,

@@ -411,3 +411,25 @@ def test_energy_trace_matches_oracle(ctx):
         assert abs(tr2[n, 2] - S.duality_gap(d_ref - g, q_ref)) <= TOL * abs(e2), n
     # the last entry is the returned solution
     assert tr1[-1, 0] == st1.primal_energy and abs(tr2[-1, 0] - st2.primal_energy) <= 1e-12 * abs(st2.primal_energy)
+
+
+@pytest.mark.parametrize("shape,L,it", [((64, 64), (2, 2, 4, 4), (20, 20)),
+                                        ((37, 53), (3, 2, 3, 5), (4, 3)),
+                                        ((40, 18), (4, 1, 4, 0), (5, 2))])
+def test_against_c_oracle(ctx, shape, L, it):
+    """The CUDA path vs the plain C11 oracle (oracle/c/tvo.c, the NumPy-free tvo_* calls of
+    SURVEY 8(b), threaded per subdomain): tau, d and the primal energies of both steps."""
+    from oracle import c_oracle as C
+    from tvs_synth import disk_on_ramp
+    img = disk_on_ramp(64, 1001) if shape == (64, 64) else random_image(*shape, seed=sum(shape))
+    d0 = img.astype(np.float64)
+    t_ref, _, s1 = C.step1(d0, 0.05, L, it[0], it[1], threads=4)
+    d_ref, _, s2 = C.step2(d0, t_ref, 0.1, L, it[0], it[1], threads=4)
+    tau, _, g1 = ctx.tv_stokes_step1(_dev(img), 0.05, L, (it[0], it[1], 0.125))
+    d, _, g2 = ctx.tv_stokes_step2(_dev(t_ref), _dev(img), 0.1, L, (it[0], it[1], 0.125))
+    e_tau = np.abs(tau.cpu().numpy() - t_ref).max()
+    e_d = np.abs(d.cpu().numpy() - d_ref).max()
+    _log("c_oracle", shape=list(shape), tau_err=e_tau, d_err=e_d)
+    assert e_tau <= TOL and e_d <= TOL, (e_tau, e_d)
+    assert abs(g1.primal_energy - s1["E"]) <= TOL * abs(s1["E"])
+    assert abs(g2.primal_energy - s2["E"]) <= TOL * abs(s2["E"])
