@@ -236,6 +236,11 @@ struct Plan {
   // their sums of |S| and |T| (algorithmic bytes per launch)
   std::vector<int> sg0;
   std::vector<std::pair<int64_t, int64_t>> sgs;
+  // two scratch sets (chirp-z local batches): groups alternate between them and between two
+  // streams, so one group's FFT-bound projection overlaps the other's memory-bound stencils
+  int npipe = 1;
+  float *v1b = nullptr, *omb = nullptr, *qb = nullptr, *gphib = nullptr;
+  ProjBatch local_b;
   int64_t sum_S = 0, sum_T = 0;
   Dist dist;
   int m2loc = 0;                       // local layout rows (k1 - k0)
@@ -320,6 +325,9 @@ struct tvs_ctx {
   int32_t trace_cap = 0, *trace_count = nullptr;
   double *d_trace = nullptr;
   int d_trace_cap = 0;
+  bool pipe = true;              // step 1: two subdomain groups in flight on two streams (TVS_PIPE)
+  cudaStream_t pipe_s = nullptr;
+  cudaEvent_t ev_pf = nullptr, ev_pj = nullptr;
   bool makhoul = true;           // Makhoul form of the chirp-z where M = 2N - 2 is a power of 4
                                  // (TVS_CZT_MAKHOUL=0: the general chirp-z form everywhere)
   double *h_energy = nullptr;   // pinned slot for dual energies
@@ -929,6 +937,9 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     for (auto &s : P->subs) lt.push_back({s.y0, s.ty1, s.x0, s.tx1, s.py1, s.px1, 0, 0});
     const bool czt_local = choose_czt(ctx, lt, G1, T != nullptr, -1, -1);
     int sg = g.M;
+    // chirp-z local batches of >= 2 subdomains run as two pipelined groups (two scratch sets)
+    P->npipe = (czt_local && ctx->pipe && g.M >= 2) ? 2 : 1;
+    if (P->npipe == 2) sg = (g.M + 1) / 2;
     if (czt_local) {
       const double per_sub = (double)vsub * 4 + (double)g.AT * g.ldT * 4 +
                              2.0 * 2.0 * g.AP * g.ldP * 4 + proj_tile_bytes(g.AT, g.AP, G1);
@@ -936,8 +947,8 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
       size_t freeb = 0, totb = 0;
       if (cudaMemGetInfo(&freeb, &totb) == cudaSuccess) {
         // keep 4 GB and a third of the rest free (outputs, the other step's plan, allocator slack)
-        const double budget = ((double)freeb - 4e9) * 2.0 / 3.0 - rinv;
-        if (per_sub * g.M > budget) sg = std::max(1, (int)(budget / per_sub));
+        const double budget = ((double)freeb - 4e9) * 2.0 / 3.0 - rinv * P->npipe;
+        if (per_sub * sg * P->npipe > budget) sg = std::max(1, (int)(budget / (per_sub * P->npipe)));
       }
       if (ctx->proj_group > 0) sg = std::min(sg, ctx->proj_group);
     }
@@ -961,6 +972,16 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)sg * 2 * g.AP * g.ldP));
     TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T, -1, -1,
                    (size_t)sg * g.AP * g.ldP, sg, sg < g.M, P->om, g.AP, g.ldP));
+    if (P->npipe == 2 && (int)P->sg0.size() - 1 >= 2) {   // the second scratch set and batch
+      TRY(dalloc(ctx, P->bufs, &P->v1b, (size_t)sg * vsub));
+      TRY(dalloc(ctx, P->bufs, &P->omb, (size_t)sg * 2 * g.AP * g.ldP));
+      TRY(dalloc(ctx, P->bufs, &P->qb, (size_t)sg * g.AT * g.ldT));
+      TRY(dalloc(ctx, P->bufs, &P->gphib, (size_t)sg * 2 * g.AP * g.ldP));
+      TRY(build_proj(ctx, *P, P->local_b, lt, G2, G1, P->qb, g.ldT, P->gphib, g.ldP, T, -1, -1,
+                     (size_t)sg * g.AP * g.ldP, sg, true, P->omb, g.AP, g.ldP));
+    } else {
+      P->npipe = 1;
+    }
   }
   *out = P.get();
   ctx->plans[key] = std::move(P);
@@ -1490,42 +1511,62 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       }
       e_prev = e;
     }
-    // the local solves, one subdomain group after the other (one group unless memory-bound)
+    // the local solves, one subdomain group after the other; with two scratch sets (npipe = 2)
+    // consecutive groups alternate between them and between streams s and pipe_s
+    const int npipe = (P->npipe == 2 && !ctx->profiling) ? 2 : 1;
+    if (npipe == 2) {
+      if (!ctx->pipe_s) {
+        CK(cudaStreamCreateWithFlags(&ctx->pipe_s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_pf, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_pj, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(ctx->ev_pf, s));
+      CK(cudaStreamWaitEvent(ctx->pipe_s, ctx->ev_pf, 0));
+    }
     for (int k = 0; k < ngs; ++k) {
+      const int set = npipe == 2 ? (k & 1) : 0;
+      cudaStream_t gs = set ? ctx->pipe_s : s;
+      ProjBatch &LB = set ? P->local_b : P->local;
+      float *qk = set ? P->qb : P->q, *gphik = set ? P->gphib : P->gphi;
+      float *omk = set ? P->omb : P->om;
       Geo gk = g;
       gk.M = P->sg0[k + 1] - P->sg0[k];
       const SubDesc *sk = P->d_subs + P->sg0[k];
       float *vper = P->v[0] + (size_t)P->sg0[k] * vsub;   // qhat_m of the group (persistent)
-      float *vscr = P->v[1];                               // group scratch
+      float *vscr = set ? P->v1b : P->v[1];                // group scratch
       const double pdb = 16.0 * P->sgs[k].first + 4.0 * P->sgs[k].second;   // pre-div bytes
       const double swb = 48.0 * P->sgs[k].first;                             // kernel (a') bytes
       // omega0_m = R r^n + P_loc multidiv (theta_m p^n)  (theta p in the scratch dual)
-      TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-        return launch_load_tp(sk, gk, P->d_thy, P->d_thx, P->p, ld, G2, G1, vscr, s);
+      TRY(run(ctx, gs, F_OTHER, 0, 0, [&] {
+        return launch_load_tp(sk, gk, P->d_thy, P->d_thx, P->p, ld, G2, G1, vscr, gs);
       }));
-      TRY(run(ctx, s, F_PREDIV, pdb, 0,
-              [&] { return launch_prediv1(sk, gk, vscr, G2, G1, P->q, nullptr, s); }));
-      TRY(project_group(ctx, *P, P->local, k, s));
-      if (overlap && k == 0) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-      TRY(run(ctx, s, F_OTHER, 0, 0, [&] {
-        return launch_omega0_1(sk, gk, P->r, ld, vscr, P->gphi, g.ldP, G2, G1, P->om, s);
+      TRY(run(ctx, gs, F_PREDIV, pdb, 0,
+              [&] { return launch_prediv1(sk, gk, vscr, G2, G1, qk, nullptr, gs); }));
+      TRY(project_group(ctx, *P, LB, k, gs));
+      if (overlap && k < npipe) CK(cudaStreamWaitEvent(gs, ctx->ev_join, 0));
+      TRY(run(ctx, gs, F_OTHER, 0, 0, [&] {
+        return launch_omega0_1(sk, gk, P->r, ld, vscr, gphik, g.ldP, G2, G1, omk, gs);
       }));
       float *vin = vper, *vout = vscr;
       for (int kk = 0; kk < it.inner; ++kk) {
-        TRY(run(ctx, s, F_PREDIV, pdb, 0,
-                [&] { return launch_prediv1(sk, gk, vin, G2, G1, P->q, nullptr, s); }));
+        TRY(run(ctx, gs, F_PREDIV, pdb, 0,
+                [&] { return launch_prediv1(sk, gk, vin, G2, G1, qk, nullptr, gs); }));
         // chirp-z form: the inverse transforms write grad phi + omega0 (kernel a' then reads one
         // field: 40 instead of 48 B per update); GEMM form: kernel (a') adds omega0 itself
-        const bool fused = P->local.czt && P->local.d_ij_add;
-        TRY(project_group(ctx, *P, P->local, k, s, false, fused));
-        TRY(run(ctx, s, F_SWEEP1, fused ? swb * 40.0 / 48.0 : swb, 0, [&] {
-          return launch_sweep1(sk, gk, P->d_thy, P->d_thx, vin, P->gphi, g.ldP,
-                               fused ? nullptr : P->om, vout, G2, G1, it.t, s);
+        const bool fused = LB.czt && LB.d_ij_add;
+        TRY(project_group(ctx, *P, LB, k, gs, false, fused));
+        TRY(run(ctx, gs, F_SWEEP1, fused ? swb * 40.0 / 48.0 : swb, 0, [&] {
+          return launch_sweep1(sk, gk, P->d_thy, P->d_thx, vin, gphik, g.ldP,
+                               fused ? nullptr : omk, vout, G2, G1, it.t, gs);
         }));
         std::swap(vin, vout);
       }
       if (vin != vper)   // odd inner count: the last update landed in the scratch
-        CK(cudaMemcpyAsync(vper, vin, (size_t)gk.M * vsub * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(vper, vin, (size_t)gk.M * vsub * sizeof(float), cudaMemcpyDeviceToDevice, gs));
+    }
+    if (npipe == 2) {   // join before the combine reads every qhat
+      CK(cudaEventRecord(ctx->ev_pj, ctx->pipe_s));
+      CK(cudaStreamWaitEvent(s, ctx->ev_pj, 0));
     }
     TRY(combine_step(ctx, *P, P->v[0], s));
   }
@@ -1604,6 +1645,7 @@ tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id
   if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   if (const char *pg = getenv("TVS_PROJ_GROUP")) c->proj_group = std::max(0, atoi(pg));
   if (const char *mk = getenv("TVS_CZT_MAKHOUL")) c->makhoul = atoi(mk) != 0;
+  if (const char *pp = getenv("TVS_PIPE")) c->pipe = atoi(pp) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;
   if (const char *mm = getenv("TVS_CZT_MAXM")) {
@@ -1636,6 +1678,9 @@ tvs_status tvs_destroy(tvs_ctx *ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->pipe_s) cudaStreamDestroy(ctx->pipe_s);
+  if (ctx->ev_pf) cudaEventDestroy(ctx->ev_pf);
+  if (ctx->ev_pj) cudaEventDestroy(ctx->ev_pj);
   if (ctx->nccl) ncclCommDestroy(ctx->nccl);
   if (ctx->d_red) cudaFree(ctx->d_red);
   if (ctx->d_trace) cudaFree(ctx->d_trace);

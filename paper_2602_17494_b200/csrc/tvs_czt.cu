@@ -336,7 +336,8 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
       const float2 a0 = make_float2(y[0].x + c2.x, y[0].y + c2.y);
       const float2 a2 = make_float2(c1.x + c3.x, c1.y + c3.y);
       const float2 o = cmul(__ldg(post + kp), make_float2(a0.x + a2.x, a0.y + a2.y));
-      out[kp] = (kind == 2 ? o.y : o.x) + (add ? add[kp] : 0.f);
+      const float v = kind == 2 ? o.y : o.x;
+      out[kp] = add ? v + add[kp] : v;
     }
   }
 }
@@ -497,10 +498,13 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   } else {           // v = conj(conj(c_n) z_n) / 2 at the Makhoul position of column x
     for (int i0 = tid; i0 < jb.vlen; i0 += B * nth) {
       float2 cn[B];
+      float av[B], bv[B];   // omega0 of the inner loop's jobs, loaded with the chirp values
 #pragma unroll
       for (int r = 0; r < B; ++r) {
-        const int x = jb.tx0 + min(i0 + r * nth, jb.vlen - 1);
+        const int ic = min(i0 + r * nth, jb.vlen - 1), x = jb.tx0 + ic;
         cn[r] = __ldg(cc + ((x & 1) ? N - 1 - (x >> 1) : (x >> 1)));
+        av[r] = aa ? __ldg(aa + ic) : 0.f;
+        bv[r] = ab ? __ldg(ab + ic) : 0.f;
       }
 #pragma unroll
       for (int r = 0; r < B; ++r) {
@@ -509,11 +513,13 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
         const int x = jb.tx0 + i;
         const int n = (x & 1) ? N - 1 - (x >> 1) : (x >> 1);
         const float2 y = cmulc(zsm[pz(n)], cn[r]);   // Y_n; v = conj(Y) / 2
+        // (no "+ 0" when there is nothing to add: the plain outputs keep their signed zeros)
         if (kind == 4) {
-          oa[i] = 0.5f * y.x + (aa ? aa[i] : 0.f);
-          if (ob) ob[i] = -0.5f * y.y + (ab ? ab[i] : 0.f);
+          oa[i] = aa ? 0.5f * y.x + av[r] : 0.5f * y.x;
+          if (ob) ob[i] = ab ? -0.5f * y.y + bv[r] : -0.5f * y.y;
         } else {
-          oa[i] = (0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y) + (aa ? aa[i] : 0.f);
+          const float v = 0.5f * ((x & 1) ? -y.x : y.x) - 0.5f * y.y;
+          oa[i] = aa ? v + av[r] : v;
         }
       }
     }
@@ -577,10 +583,12 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
     czt_fft_pair(zsm, G.logM4, twd, gtab + (size_t)(blockIdx.z * G.nuc + uc) * G.M, io);
     for (int i0 = tid; i0 < (pout ? 0 : vcnt); i0 += 4 * nth) {
       float2 pv[4];
+      float av[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int i = i0 + r * nth;
         pv[r] = i < vcnt ? __ldg(jb.post + v0 + i) : make_float2(0.f, 0.f);
+        av[r] = (addr && nuc == 1 && i < vcnt) ? __ldg(addr + i) : 0.f;
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -588,14 +596,14 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
         if (i >= vcnt) break;
         const float2 c = cmul(pv[r], zsm[pz(i)]);
         const float val = jb.kind == 2 ? c.y : c.x;
-        if (nuc == 1) out[i] = val + (addr ? addr[i] : 0.f);   // one input chunk: straight out
+        if (nuc == 1) out[i] = addr ? val + av[r] : val;   // one input chunk: straight out
         else acc[i] += val;
       }
     }
     __syncthreads();
   }
   if (nuc > 1)
-    for (int i = tid; i < vcnt; i += nth) out[i] = acc[i] + (addr ? addr[i] : 0.f);
+    for (int i = tid; i < vcnt; i += nth) out[i] = addr ? acc[i] + addr[i] : acc[i];
 }
 
 // ------------------------------------------------------------------------------------ host side

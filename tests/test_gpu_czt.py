@@ -139,3 +139,26 @@ def test_step1_makhoul_form(ctx, ctx_general, shape, L):
     t2, _, _ = ctx_general.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125))
     torch.cuda.synchronize()
     assert float((t1 - t2).abs().max()) < 2e-5
+
+
+def test_pipelined_groups_bitwise(ctx):
+    """Two subdomain groups in flight on two streams with separate scratch (the default for
+    chirp-z local batches) give bitwise the serial schedule's tau and p (TVS_PIPE=0), also with
+    more than two groups (TVS_PROJ_GROUP) and odd inner counts."""
+    serial = _context(TVS_DCT="czt", TVS_PIPE="0")
+    grouped = _context(TVS_DCT="czt", TVS_PROJ_GROUP="2")
+    try:
+        for shape, L, it in (((40, 32), (4, 2, 4, 4), (3, 4)), ((64, 64), (4, 4, 4, 4), (2, 3)),
+                             ((37, 53), (3, 2, 3, 5), (3, 3))):
+            img = random_image(*shape, seed=shape[0] + 2 * shape[1])
+            d0 = torch.from_numpy(img).cuda()
+            sch = (it[0], it[1], 0.125)
+            t0, p0, _ = serial.tv_stokes_step1(d0, 0.05, L, sch, want_p=True)
+            t1, p1, _ = ctx.tv_stokes_step1(d0, 0.05, L, sch, want_p=True)
+            t2, p2, _ = grouped.tv_stokes_step1(d0, 0.05, L, sch, want_p=True)
+            torch.cuda.synchronize()
+            assert torch.equal(t0, t1) and torch.equal(p0, p1), shape
+            assert torch.equal(t0, t2) and torch.equal(p0, p2), shape
+    finally:
+        serial.close()
+        grouped.close()
