@@ -2,9 +2,9 @@
 """Writes tests/golden/c5_step1_sampled.npz: fp64 oracle values for BASELINE config 5 at full size
 (32768 x 32768 Voronoi-16384, 16 x 16 subdomains, overlap 32, delta 0.05, t 1/8), step 1:
 
-* P tau_0 (the global projection of Eq. formula:PKh) on sampled rows: every core cut
-  row of the layout, its neighbours, the first / last rows, and 24 seeded rows -- each in full
-  (32769 columns);
+* P tau_0 (the global projection of Eq. formula:PKh) on sampled rows -- every core cut
+  row of the layout, its neighbours, the first / last rows, and 24 seeded rows -- at the first,
+  middle and last 512 columns and every 32nd;
 * the first outer sweep's local solves qhat_m (Alg. 5) of three subdomains -- corner
   (0, 0), interior (7, 9) and the far corner (15, 15), which touches the extra row and column of
   Omega~ -- after 2 inner updates.  With p^0 = 0 and qhat = 0 (reading A9), omega0_m = R_{S+} f,
@@ -48,6 +48,13 @@ def windows(shape, seed, w=32, nrand=4000):
     return (k // b).astype(np.int32), (k % b).astype(np.int32)
 
 
+def ptau0_columns(n):
+    """Columns stored for P tau_0: the first, middle and last 512 and every 32nd."""
+    cols = set(range(512)) | set(range(n // 2 - 256, n // 2 + 256)) | set(range(n - 512, n)) \
+        | set(range(0, n, 32))
+    return np.array(sorted(cols), dtype=np.int32)
+
+
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "c5_step1_sampled.npz")
     c = CONFIGS["c5"]
@@ -80,8 +87,9 @@ def main():
     print(f"P tau_0 on {len(rows)} rows: {time.time() - t0:.0f} s", flush=True)
     at = {int(r): k for k, r in enumerate(rows)}
     f_rows = ptau0 / c.delta
-    res = {"ptau0_rows": np.array(sample_rows, np.int32),
-           "ptau0": ptau0[:, [at[r] for r in sample_rows]].astype(np.float32)}
+    pcols = ptau0_columns(n2t)
+    res = {"ptau0_rows": np.array(sample_rows, np.int32), "ptau0_cols": pcols,
+           "ptau0": ptau0[:, [at[r] for r in sample_rows]][:, :, pcols].astype(np.float32)}
     for (iy, ix) in SUBS:
         m = (iy, ix)
         s, sp = rects[m]

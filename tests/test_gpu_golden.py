@@ -123,9 +123,10 @@ def test_config5_step1_full_size_sampled(ctx):
     L = (c.m2, c.m1, c.overlap, c.overlap)
     lay = olayout.Layout(n, n, *L)
     d0 = torch.from_numpy(c.image()).cuda()
-    tau, _, _ = ctx.tv_stokes_step1(d0, c.delta, L, (1, 0, c.t))
+    tau, _, _ = ctx.tv_stokes_step1(d0, c.delta, L, (0, 1, c.t))   # no sweep: tau = P tau_0
     rows = torch.from_numpy(g["ptau0_rows"]).long().cuda()
-    e_P = float(np.abs(tau[:, rows, :].cpu().numpy().astype(np.float64) - g["ptau0"]).max())
+    cols = torch.from_numpy(g["ptau0_cols"]).long().cuda()
+    e_P = float(np.abs(tau[:, rows][:, :, cols].cpu().numpy().astype(np.float64) - g["ptau0"]).max())
     del tau
     _log("c5_global_P", err=e_P)
     assert e_P <= TOL, e_P
