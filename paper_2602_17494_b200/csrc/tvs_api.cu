@@ -325,7 +325,9 @@ struct tvs_ctx {
   int32_t trace_cap = 0, *trace_count = nullptr;
   double *d_trace = nullptr;
   int d_trace_cap = 0;
-  bool pipe = true;              // step 1: two subdomain groups in flight on two streams (TVS_PIPE)
+  // step 1: two subdomain groups in flight on two streams (TVS_PIPE=1; measured -1 % at config 4:
+  // the half-size launches lose about what the overlap wins, so off by default)
+  bool pipe = false;
   cudaStream_t pipe_s = nullptr;
   cudaEvent_t ev_pf = nullptr, ev_pj = nullptr;
   bool makhoul = true;           // Makhoul form of the chirp-z where M = 2N - 2 is a power of 4

@@ -142,11 +142,11 @@ def test_step1_makhoul_form(ctx, ctx_general, shape, L):
 
 
 def test_pipelined_groups_bitwise(ctx):
-    """Two subdomain groups in flight on two streams with separate scratch (the default for
-    chirp-z local batches) give bitwise the serial schedule's tau and p (TVS_PIPE=0), also with
-    more than two groups (TVS_PROJ_GROUP) and odd inner counts."""
-    serial = _context(TVS_DCT="czt", TVS_PIPE="0")
-    grouped = _context(TVS_DCT="czt", TVS_PROJ_GROUP="2")
+    """Two subdomain groups in flight on two streams with separate scratch (TVS_PIPE=1) give
+    bitwise the serial schedule's tau and p, also with more than two groups (TVS_PROJ_GROUP) and
+    odd inner counts."""
+    serial = _context(TVS_DCT="czt", TVS_PIPE="1")
+    grouped = _context(TVS_DCT="czt", TVS_PIPE="1", TVS_PROJ_GROUP="2")
     try:
         for shape, L, it in (((40, 32), (4, 2, 4, 4), (3, 4)), ((64, 64), (4, 4, 4, 4), (2, 3)),
                              ((37, 53), (3, 2, 3, 5), (3, 3))):

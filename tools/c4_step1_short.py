@@ -21,6 +21,7 @@ d0 = torch.from_numpy(img).cuda()
 L = (c.m2, c.m1, c.overlap, c.overlap)
 ctx.tv_stokes_step1(d0, c.delta, L, (1, 1, c.t))
 torch.cuda.synchronize()
+_, _, st0 = ctx.tv_stokes_step1(d0, c.delta, L, (1, inner, c.t))   # unprofiled (device time)
 ctx.set_profiling(True)
 ctx.reset_kernel_times()
 tau, _, st = ctx.tv_stokes_step1(d0, c.delta, L, (1, inner, c.t))
@@ -29,5 +30,5 @@ kt = ctx.kernel_times()
 fam = {nm: {"n": kt.counts[i], "avg_us": round(kt.ms[i] / kt.counts[i] * 1e3, 1),
             **({"tflops": round(kt.flops[i] / (kt.ms[i] / 1e3) / 1e12, 2)} if kt.flops[i] else {})}
        for i, nm in enumerate(pkg.KERNEL_FAMILIES) if kt.counts[i]}
-print(json.dumps({"inner": inner, "seconds": st.seconds, "E1": st.primal_energy,
+print(json.dumps({"inner": inner, "seconds": st0.seconds, "seconds_profiled": st.seconds, "E1": st.primal_energy,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("TVS_")}, "families": fam}))
