@@ -334,8 +334,8 @@ struct tvs_ctx {
                                  // (TVS_CZT_MAKHOUL=0: the general chirp-z form everywhere)
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
-  int x2_minw = 512;             // ... on subdomains at least this wide (TVS_X2_MINW)
-  bool solve_tma = true;         // y-solve blocks staged by TMA (TVS_SOLVE_TMA=0: cp.async)
+  int x2_minw = 512;             // ... on subdomains at least this wide (config 3's 272-wide
+                                 // tiles: 57 vs 34 us per update with the two-update form)
   int stop_crit = 0;       // tvs_set_stopping
   double stop_tol = 0.0;   // largest chirp-z FFT (power of 4; TVS_CZT_MAXM, tests force chunking)
   std::vector<cudaEvent_t> ev_pool;
@@ -772,7 +772,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
       }
       TRY(upload(ctx, P.bufs, &B.d_order, order));
     }
-    if (ctx->solve_tma) {   // TMA boxes of {J columns, <= 256 rows} for the staged blocks
+    {   // TMA boxes of {J columns, <= 256 rows} for the staged blocks
       SolveMaps m{};
       m.nbox = (B.AT + 255) / 256;
       // even row counts: every box of the fp32 block then starts 128-byte aligned (J = 16 columns)
@@ -1642,9 +1642,7 @@ tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id
   c->rank = rank;
   c->world = world;
   if (const char *x2 = getenv("TVS_SWEEP2X2")) c->sweep2x2 = atoi(x2) != 0;
-  if (const char *x2 = getenv("TVS_X2_MINW")) c->x2_minw = atoi(x2);
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
-  if (const char *st = getenv("TVS_SOLVE_TMA")) c->solve_tma = atoi(st) != 0;
   if (const char *pg = getenv("TVS_PROJ_GROUP")) c->proj_group = std::max(0, atoi(pg));
   if (const char *mk = getenv("TVS_CZT_MAKHOUL")) c->makhoul = atoi(mk) != 0;
   if (const char *pp = getenv("TVS_PIPE")) c->pipe = atoi(pp) != 0;

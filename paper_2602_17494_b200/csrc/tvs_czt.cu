@@ -791,9 +791,8 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
     if (e != cudaSuccess) return e;
   }
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
-  static const int prune = getenv("TVS_CZT_PRUNE") ? atoi(getenv("TVS_CZT_PRUNE")) : 1;
   CztGeom gg = g;
-  gg.prune = prune;
+  gg.prune = g.mk ? 0 : 1;
   k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
   return cudaGetLastError();
 }

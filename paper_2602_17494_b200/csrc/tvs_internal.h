@@ -106,7 +106,7 @@ struct CztGeom {
   int M, logM4;   // FFT size (power of 4) and log4 M
   int Uc, Vp;     // input chunk and output pass lengths (Uc + Vp - 1 <= M, or the M = 2N-2 case)
   int nuc, nvp;   // numbers of chunks / passes for the largest job
-  int prune = 1;  // pruned first / last FFT passes for narrow jobs (TVS_CZT_PRUNE=0: off)
+  int prune = 1;  // pruned first / last FFT passes for narrow jobs (general form)
   int mk = 0;     // 1: Makhoul form -- the partial x-DCTs as DFT_N's of packed real sequences by
                   // Bluestein with M = 2N - 2 (job kinds 3, 4, 5; see tvs_czt.cu)
 };

@@ -1241,7 +1241,6 @@ constexpr int SJB = 32, SSEG_MAX = 16, SU = 8;
 // solve3 (tall tiles: config-4 strips, the global projections, config 5) takes up to 32 segments
 // per column (1024 threads): its fp64 recurrences are latency-bound chains, and with one CTA per SM
 // (the staged column block fills shared memory) shorter chains and twice the warps hide them
-// (TVS_SOLVE3_SEG caps it, A/B)
 constexpr int S3SEG_MAX = 32;
 // SMEM = true: the CTA's column block of qhat is staged in shared memory by the first pass and
 // overwritten in place by z (fp32), so qhat is read from HBM once and z never leaves the SM
@@ -1530,7 +1529,7 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const double *__restrict__ gp = segprod + (size_t)tl.chain * 2 * nseg * ldn + jj;
   const double gpf = (valid && j > 0) ? __ldg(gp + (size_t)sg * ldn) : 1.0;
   const double gpb = (valid && j > 0) ? __ldg(gp + (size_t)(nseg + sg) * ldn) : 1.0;
-  if (maps) {   // stage both column blocks with TMA (nbox boxes of {32 columns, box_rows rows})
+  {   // stage both column blocks with TMA (nbox boxes of {J columns, box_rows rows})
     const int lt = sg * J + tx;
     if (lt == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sbar)));
@@ -1563,34 +1562,6 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
         "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
         "@!P1 bra W_%=;\n\t}" ::"r"(bar) : "memory");
-  } else {   // stage the column blocks (16-byte asynchronous copies, all rows in flight)
-    const float *blk = qhat + (size_t)tix * AT * ldn + (size_t)jb * J;
-    const double *rblk = rinv + (size_t)tl.chain * AT * ldn + (size_t)jb * J;
-    const int nthr = J * nseg, lt = sg * J + tx;
-    for (int e = lt; e < nt * (J / 4); e += nthr) {
-      const int k = e / (J / 4), c = e % (J / 4);
-      float *dst = sb4 + k * J + 4 * c;
-      if (jb * J + 4 * c < ldn) {
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
-                     "l"(blk + (size_t)k * ldn + 4 * c) : "memory");
-      } else {
-        dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
-      }
-    }
-    for (int e = lt; e < nt * (J / 2); e += nthr) {
-      const int k = e / (J / 2), c = e % (J / 2);
-      double *dst = sr4 + k * J + 2 * c;
-      if (jb * J + 2 * c < ldn) {
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
-                     "l"(rblk + (size_t)k * ldn + 2 * c) : "memory");
-      } else {
-        dst[0] = dst[1] = 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
   }
   const double *ri = sr4 + tx;   // pivot of row k at ri[k * J]
   float *sbt = sb4 + tx;                                                     // row k at sbt[k*J]
@@ -1914,10 +1885,8 @@ cudaError_t launch_omega0_2(const SubDesc *subs, Geo g, const float *thy, const 
 // Rows per warp of the streaming stencil kernels: the longest of 32 / 16 / 8 that still gives
 // >= 8192 warps (~55 per SM) -- short row blocks cost 2-3 halo rows each, but small subdomains
 // (config 3: 64 x 274 x 274) need the extra warps to keep loads in flight (measured: kernel (a)
-// 46 -> 34 us, (a') 95 -> 76 us from 32 to 8 rows).  TVS_RB overrides.
+// 46 -> 34 us, (a') 95 -> 76 us from 32 to 8 rows).
 static int stencil_rb(int rows, int nsub, int strips) {
-  static const int env = getenv("TVS_RB") ? atoi(getenv("TVS_RB")) : 0;
-  if (env >= 4) return env;
   for (int rb : {32, 16})
     if ((long long)strips * nsub * ((rows + rb - 1) / rb) >= 8192) return rb;
   return 8;
@@ -2097,14 +2066,12 @@ cudaError_t launch_gemm(const GemmDesc *descs, int batch, int maxM, int maxN, cu
   return cudaGetLastError();
 }
 int solve_nseg(int AT) {
-  static const int ls = getenv("TVS_SOLVE_LS") ? std::max(4, atoi(getenv("TVS_SOLVE_LS"))) : 32;
+  constexpr int ls = 32;   // target rows per segment
   return std::min(SSEG_MAX, std::max(1, (AT + ls - 1) / ls));
 }
 // column block width of solve4: 16 for tiles up to 512 rows (four CTAs per SM instead of two:
 // config 3 -3 %), else 32; TVS_SOLVE_J=16|32 forces one
 static int solve_j(int AT) {
-  static const int forced = getenv("TVS_SOLVE_J") ? atoi(getenv("TVS_SOLVE_J")) : 0;
-  if (forced == 16 || forced == 32) return forced;
   return AT <= 512 ? 16 : 32;
 }
 int solve4_width(int AT) { return solve_j(AT); }
@@ -2143,8 +2110,7 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
                                const int *pcut, const double *pinf, const double *plast,
                                cudaStream_t s) {
   // one warp per segment of >= 32 rows, at most S3SEG_MAX segments (the max tile height decides)
-  static const int cap = getenv("TVS_SOLVE3_SEG") ? std::max(1, std::min(S3SEG_MAX, atoi(getenv("TVS_SOLVE3_SEG")))) : S3SEG_MAX;
-  const int nseg = std::min(cap, std::max(1, AT / 32));
+  const int nseg = std::min(S3SEG_MAX, std::max(1, AT / 32));
   const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);
   const size_t smem = (size_t)AT * SJB * sizeof(float);
   if (smem <= 160 * 1024) {
