@@ -89,6 +89,7 @@ struct Dist {
   int us0 = 0, us1 = 0, ur0 = 0, ur1 = 0;  // rows sent to / received from rank - 1
   int ds0 = 0, ds1 = 0, dr0 = 0, dr1 = 0;  // rows sent to / received from rank + 1
   std::vector<int> Rlo, Rhi;               // core rows of every rank (all-gathers)
+  std::vector<int> Vlo, Vhi, Klo, Khi;     // valid rows and layout rows of every rank
 };
 
 // cuts: core cuts of the layout axis (on the N~ grid); ly/hy: subdomain ranges; G2: step rows.
@@ -120,6 +121,10 @@ bool compute_dist(int G2, int M2, const std::vector<int> &ly, const std::vector<
     rows(r, k0, k1, R0, R1, E0, E1, V0, V1);
     d.Rlo.push_back(R0);
     d.Rhi.push_back(R1);
+    d.Vlo.push_back(V0);
+    d.Vhi.push_back(V1);
+    d.Klo.push_back(k0);
+    d.Khi.push_back(k1);
   }
   rows(rank, d.k0, d.k1, d.R0, d.R1, d.E0, d.E1, d.V0, d.V1);
   auto isect = [](int a0, int a1, int b0, int b1, int &o0, int &o1) {
@@ -200,6 +205,14 @@ struct ProjBatch {
   // algorithmic work per launch: contraction flops (dense 2MNK), FFT flops of the chirp-z form
   // (2 x 5 M log2 M per FFT pair and row chunk), and the y-solve's HBM bytes
   double fwd_flops = 0, inv_flops = 0, fwd_fft_flops = 0, inv_fft_flops = 0, solve_bytes = 0;
+  // global batch: the y-solve in fixed segments (k_gsolve_*): segment row bounds, this rank's
+  // segments [s0, s1), every rank's segment range, the forward / backward aggregates
+  bool spike = false;
+  int nseg = 0, s0 = 0, s1 = 0;
+  int *d_seglo = nullptr;
+  std::vector<int> sr_lo, sr_hi;
+  double *agg = nullptr, *aggb = nullptr;
+  float *zg = nullptr;
   // tile groups sharing the scratch (see build_proj): group k = tiles [g0[k], g0[k+1]), with its
   // FFT flops and solve bytes per launch
   int gtiles = 0;
@@ -754,6 +767,37 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   TRY(dalloc(ctx, P.bufs, &B.plast, (size_t)B.nchains * B.ldn));
   CK(launch_pivots(B.d_tiles, B.d_first, B.nchains, n2t, n1t, B.rinv, B.ldn, B.AT, B.pcut, B.pinf,
                    B.plast, 0));
+  if (fr0 >= 0) {   // the global tile: segments at the layout's core cuts (one virtual slab per
+                    // layout row), each cut into equal sub-segments of ~256 rows
+    const Dist &D = P.dist;
+    const int M2 = P.L.m2, naxis = P.n2 + 1;
+    std::vector<int> lo;
+    std::vector<int> slab_first(M2 + 1, 0);
+    for (int k = 0; k < M2; ++k) {
+      const int c0 = (int)((long long)k * naxis / M2);
+      const int c1 = k + 1 < M2 ? (int)((long long)(k + 1) * naxis / M2) : n2t;
+      const int len = c1 - c0, ns = std::max(1, (len + 128) / 256);
+      slab_first[k] = (int)lo.size();
+      for (int i = 0; i < ns; ++i) lo.push_back(c0 + (int)((long long)i * len / ns));
+    }
+    slab_first[M2] = (int)lo.size();
+    lo.push_back(n2t);
+    B.spike = true;
+    B.nseg = (int)lo.size() - 1;
+    B.s0 = slab_first[D.k0];
+    B.s1 = slab_first[D.k1];
+    for (int r = 0; r < D.world; ++r) {
+      B.sr_lo.push_back(slab_first[D.Klo[r]]);
+      B.sr_hi.push_back(slab_first[D.Khi[r]]);
+    }
+    if (lo[B.s0] != D.R0 || lo[B.s1] != D.R1)
+      return fail(ctx, TVS_EINVAL, "global solve segments do not match the rank's core rows");
+    TRY(upload(ctx, P.bufs, &B.d_seglo, lo));
+    TRY(dalloc(ctx, P.bufs, &B.agg, (size_t)B.nseg * 2 * B.ldn));
+    TRY(dalloc(ctx, P.bufs, &B.aggb, (size_t)B.nseg * 2 * B.ldn));
+    if (B.z) B.zg = B.z;
+    else TRY(dalloc(ctx, P.bufs, &B.zg, (size_t)B.AT * B.ldn));
+  }
   if (solve4_fits(B.AT)) {
     TRY(dalloc(ctx, P.bufs, &B.segprod, (size_t)B.nchains * 2 * solve_nseg(B.AT) * B.ldn));
     CK(launch_segprod(B.d_tiles, B.d_first, B.nchains, B.rinv, B.ldn, B.AT, n1t, B.segprod, 0));
@@ -1147,6 +1191,75 @@ bool stop_now(const tvs_ctx *ctx, double d_prev, double d_next, double npts, dou
 
 // grad phi of phi = R_T Delta^dagger E_T q for every tile of the batch (kernel b).  For the
 // global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
+// All-gather of the per-segment aggregates [segment][2][ldn] (doubles): rank q contributes its
+// segments [sr_lo[q], sr_hi[q]) -- one ncclBroadcast per rank in a group, or virtual-group pulls.
+tvs_status allgather_segments(tvs_ctx *ctx, const Dist &D, const ProjBatch &B, double *buf,
+                              cudaStream_t s) {
+  if (D.world == 1) return TVS_OK;
+  const size_t row = (size_t)2 * B.ldn;   // doubles per segment
+  if (ctx->vgroup) {
+    std::vector<Pull> pulls;
+    for (int q = 0; q < D.world; ++q)
+      if (q != D.rank && B.sr_hi[q] > B.sr_lo[q])
+        pulls.push_back({q, 0, (size_t)B.sr_lo[q] * row * sizeof(double), buf + (size_t)B.sr_lo[q] * row,
+                         (size_t)(B.sr_hi[q] - B.sr_lo[q]) * row * sizeof(double)});
+    return vexchange(ctx, {buf}, pulls, s);
+  }
+  TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
+  for (int q = 0; q < D.world; ++q) {
+    double *ptr = buf + (size_t)B.sr_lo[q] * row;
+    const size_t cnt = (size_t)(B.sr_hi[q] - B.sr_lo[q]) * row;
+    if (cnt) TRY(nccl_ck(ctx, ncclBroadcast(ptr, ptr, cnt, ncclDouble, q, ctx->nccl, s), "ncclBroadcast"));
+  }
+  return nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// The global solve's outputs on the valid rows beyond this rank's own: rows [V0, R0) from rank - 1
+// and [R1, V1) from rank + 1 (their owned rows), both spectral gradient planes (row pitch ldn,
+// row y of rank q at (y - V0_q) * ldn).
+tvs_status halo_rows(tvs_ctx *ctx, const Dist &D, const ProjBatch &B, cudaStream_t s) {
+  if (D.world == 1) return TVS_OK;
+  const size_t ld = B.ldn;
+  auto rows_of = [&](float *base, int y0, int v0) { return base + (size_t)(y0 - v0) * ld; };
+  const int r = D.rank;
+  if (ctx->vgroup) {
+    std::vector<Pull> pulls;
+    for (int c = 0; c < 2; ++c) {
+      float *mine = c ? B.phy : B.phx;
+      if (r > 0 && D.R0 > D.V0)
+        pulls.push_back({r - 1, c, (size_t)(D.V0 - D.Vlo[r - 1]) * ld * sizeof(float),
+                         rows_of(mine, D.V0, D.V0), (size_t)(D.R0 - D.V0) * ld * sizeof(float)});
+      if (r < D.world - 1 && D.V1 > D.R1)
+        pulls.push_back({r + 1, c, (size_t)(D.R1 - D.Vlo[r + 1]) * ld * sizeof(float),
+                         rows_of(mine, D.R1, D.V0), (size_t)(D.V1 - D.R1) * ld * sizeof(float)});
+    }
+    return vexchange(ctx, {B.phx, B.phy}, pulls, s);
+  }
+  TRY(nccl_ck(ctx, ncclGroupStart(), "ncclGroupStart"));
+  for (int c = 0; c < 2; ++c) {
+    float *mine = c ? B.phy : B.phx;
+    if (r > 0) {   // send my rows [R0, V1_{r-1}) up, receive [V0, R0)
+      const int up_hi = D.Vhi[r - 1];
+      if (up_hi > D.R0)
+        TRY(nccl_ck(ctx, ncclSend(rows_of(mine, D.R0, D.V0), (size_t)(up_hi - D.R0) * ld, ncclFloat, r - 1,
+                                  ctx->nccl, s), "ncclSend"));
+      if (D.R0 > D.V0)
+        TRY(nccl_ck(ctx, ncclRecv(rows_of(mine, D.V0, D.V0), (size_t)(D.R0 - D.V0) * ld, ncclFloat, r - 1,
+                                  ctx->nccl, s), "ncclRecv"));
+    }
+    if (r < D.world - 1) {   // send my rows [V0_{r+1}, R1) down, receive [R1, V1)
+      const int dn_lo = D.Vlo[r + 1];
+      if (D.R1 > dn_lo)
+        TRY(nccl_ck(ctx, ncclSend(rows_of(mine, dn_lo, D.V0), (size_t)(D.R1 - dn_lo) * ld, ncclFloat, r + 1,
+                                  ctx->nccl, s), "ncclSend"));
+      if (D.V1 > D.R1)
+        TRY(nccl_ck(ctx, ncclRecv(rows_of(mine, D.R1, D.V0), (size_t)(D.V1 - D.R1) * ld, ncclFloat, r + 1,
+                                  ctx->nccl, s), "ncclRecv"));
+    }
+  }
+  return nccl_ck(ctx, ncclGroupEnd(), "ncclGroupEnd");
+}
+
 // grad phi of phi = R_T Delta^dagger E_T q for the tiles of group k of the batch (kernel b).  For
 // the global batch on several ranks the partial x-DCT rows are all-gathered before the y-solves.
 tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_t s,
@@ -1164,6 +1277,20 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
       return launch_gemm_tma_ts(B.d_fwd, B.nstack, B.tcM_fwd, B.fwdN, 144, s);
     }));
   }
+  if (B.spike) {   // the global tile: fixed segments, aggregates exchanged (see k_gsolve_*)
+    const Dist &D = P.dist;
+    const int nt = B.tiles[0].ty1 - B.tiles[0].ty0 + 1, po = B.tiles[0].po;
+    const double share = (double)(B.s1 - B.s0) / std::max(1, B.nseg);
+    for (int ph = 0; ph < 3; ++ph) {
+      TRY(run(ctx, s, F_SOLVE, ph == 2 ? B.gsolve[k] * share : 0, 0, [&] {
+        return launch_gsolve(ph, B.d_seglo, B.nseg, B.s0, B.s1, G1, G2, B.qhat, B.ldn, B.rinv,
+                             B.pcut, B.pinf, B.plast, nt, B.agg, ph == 0 ? B.agg : B.aggb, B.zg,
+                             B.phx, B.phy, po, s);
+      }));
+      if (ph < 2) TRY(allgather_segments(ctx, D, B, ph == 0 ? B.agg : B.aggb, s));
+    }
+    TRY(halo_rows(ctx, D, B, s));
+  } else {
   if (gather) TRY(allgather_rows(ctx, P.dist, B.qhat, 1, 0, B.ldn, s));
   TRY(run(ctx, s, F_SOLVE, B.gsolve[k], 0, [&] {
     // segmented fp64 y-solve: staged in shared memory (solve4) when the tile height allows,
@@ -1176,6 +1303,7 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
     return launch_proj_solve3(B.d_tiles + t0, nt, G2, G1, B.qhat, B.AT, B.ldn, B.rinv, B.z,
                               B.phx, B.phy, nullptr, nullptr, B.AP, B.pcut, B.pinf, B.plast, s);
   }));
+  }
   if (B.czt)
     return run(ctx, s, F_CZT_INV, 0, B.ginv[k], [&] {
       return launch_czt((add_om ? B.d_ij_add : B.d_ij) + 2 * t0, 2 * nt, B.ij_rows, B.gi, B.gtab_i,

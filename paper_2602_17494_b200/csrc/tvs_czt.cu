@@ -164,7 +164,6 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
       const int blk = gidx >> (2 * lg - 2), kp = gidx & (Q - 1);
       const int base = blk * 4 * L + kp;
       float2 x[16];
-#pragma unroll
       float2 *zb = z + pz(base);   // base % 16 = kp < Q when Q = 4
 #pragma unroll
       for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, Q)];
@@ -227,7 +226,6 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
 #pragma unroll
       for (int m = 0; m < 8; ++m) g[m] = __ldg(reinterpret_cast<const float4 *>(gk + base) + m);
       float2 x[16];
-#pragma unroll
       float2 *zb = z + 17 * gidx;   // pz(16 gidx + m) = 17 gidx + m
 #pragma unroll
       for (int m = 0; m < 16; ++m) x[m] = zb[m];
@@ -287,7 +285,6 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
       const int blk = gidx >> (2 * lg), kp = gidx & (L - 1);
       const int base = blk * 16 * L + kp;
       float2 x[16];
-#pragma unroll
       float2 *zb = z + pz(base);   // base % 16 = kp < L when L = 4
 #pragma unroll
       for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, L)];

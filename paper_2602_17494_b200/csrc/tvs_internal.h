@@ -241,6 +241,15 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
                                const SolveMaps *maps, int smem_rows, const int *order,
                                int nchains, int per_chain, cudaStream_t s);
 // chain-shared y-solve (one pivot block per CTA for the tiles of a layout row); needs the TMA maps
+// global y-solve in fixed segments (see k_gsolve_* in tvs_kernels.cu): phase 0 writes the forward
+// aggregates of segments [s0, s1) into aggb_or_out; phase 1 reads the all-gathered forward
+// aggregates `agg`, writes z and the backward aggregates into aggb_or_out; phase 2 reads both
+// (agg forward, aggb_or_out backward) and writes the spectral gradient planes of the owned rows
+cudaError_t launch_gsolve(int phase, const int *seglo, int nseg, int s0, int s1, int n1, int n2,
+                          const float *qhat, int ldn, const double *rinv, const int *pcut,
+                          const double *pinf, const double *plast, int nt, const double *agg,
+                          double *aggb_or_out, float *zs, float *phx, float *phy, int po,
+                          cudaStream_t s);
 // segmented y-solve: fp32 z scratch [tile][AT][ldn]
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
                                const float *qhat, int AT, int ldn, const double *rinv, float *z,

@@ -1469,6 +1469,142 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   for (; k >= k0; --k, zp -= zst) emit(k, piv(k) * ((double)*zp - un));
 }
 
+// ---------------------------------------------------------------------------------------------
+// Global y-solve in fixed segments (the global projection r^n = f - P multidiv p^n):
+// the rows of the whole-grid tile are cut into segments at the layout's core cuts (one "virtual
+// slab" per layout row, each split into equal sub-segments of ~256 rows) -- the same segments at
+// every GPU count.  A rank solves only the segments of its own slabs:
+//   A  forward pass of each owned segment from a zero carry -> (a_s, g_s) per frequency;
+//      all-gather of the (a, g) of every segment (2 doubles per segment and frequency);
+//   B  every rank scans ALL segments in the same order (identical carries on every rank), runs
+//      the owned segments' forward pass with the exact carry (z, fp32 scratch) and their backward
+//      pass from a zero carry -> (a'_s, g'_s); all-gather;
+//   C  reverse scan, backward pass with the exact carry, outputs grad phi's spectral planes on the
+//      owned rows (the rows of the valid band beyond them arrive from the slab neighbours).
+// Only the (a, g) pairs travel (not the partial x-DCT of every row), no rank solves the whole
+// grid, and tau is bitwise the same for every GPU count.  Same recurrences and fma orders as
+// k_proj_solve3; j = 0 (the singular Neumann column) is the prefix sum D+_y u = prefix(b) - mu (y+1).
+// agg layout: [segment][2][ldn] doubles.  One thread per (frequency, owned segment).
+__device__ __forceinline__ double gs_piv(const double *ri, int k, size_t st, int pc, int nt,
+                                         double rinf, double rlast) {
+  return k < pc ? __ldg(ri + (size_t)k * st) : (k == nt - 1 ? rlast : rinf);
+}
+__global__ void __launch_bounds__(128)
+k_gsolve_a(const int *__restrict__ seglo, int s0, int s1, int n1, const float *__restrict__ qhat,
+           int ldn, const double *__restrict__ rinv, const int *__restrict__ pcut,
+           const double *__restrict__ pinf, const double *__restrict__ plast, int nt,
+           double *__restrict__ agg) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
+  if (j >= n1 || s >= s1) return;
+  const size_t st = ldn;
+  const int k0 = seglo[s], k1 = seglo[s + 1];
+  const float *b = qhat + j;
+  double a = 0.0, g = 1.0;
+  if (j == 0) {
+    for (int k = k0; k < k1; ++k) a += (double)b[(size_t)k * st];
+  } else {
+    const double *ri = rinv + j;
+    const int pc = pcut[j];
+    const double rinf = pinf[j], rlast = plast[j];
+    int k = k0;
+    if (k == 0) {   // z_0 = b_0 (no coupling above row 0)
+      a = (double)b[0];
+      g = 0.0;
+      k = 1;
+    }
+    for (; k < k1; ++k) {
+      const double r = gs_piv(ri, k - 1, st, pc, nt, rinf, rlast);
+      a = fma(-r, a, (double)b[(size_t)k * st]);
+      g *= -r;
+    }
+  }
+  agg[((size_t)s * 2 + 0) * st + j] = a;
+  agg[((size_t)s * 2 + 1) * st + j] = g;
+}
+__global__ void __launch_bounds__(128)
+k_gsolve_b(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1,
+           const float *__restrict__ qhat, int ldn, const double *__restrict__ rinv,
+           const int *__restrict__ pcut, const double *__restrict__ pinf,
+           const double *__restrict__ plast, int nt, const double *__restrict__ agg,
+           float *__restrict__ zs, double *__restrict__ aggb) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
+  if (j >= n1 || s >= s1 || j == 0) return;   // j = 0 needs no z / backward pass
+  const size_t st = ldn;
+  const int k0 = seglo[s], k1 = seglo[s + 1];
+  double Z = 0.0;   // forward carry into segment s: Z_t = a_t + g_t Z_{t-1}, all ranks alike
+  for (int t = 0; t < s; ++t)
+    Z = fma(agg[((size_t)t * 2 + 1) * st + j], Z, agg[((size_t)t * 2 + 0) * st + j]);
+  const double *ri = rinv + j;
+  const int pc = pcut[j];
+  const double rinf = pinf[j], rlast = plast[j];
+  const float *b = qhat + j;
+  float *z = zs + j;
+  double zc = Z;
+  int k = k0;
+  if (k == 0) {
+    zc = (double)b[0];
+    z[0] = (float)zc;
+    k = 1;
+  }
+  for (; k < k1; ++k) {
+    zc = fma(-gs_piv(ri, k - 1, st, pc, nt, rinf, rlast), zc, (double)b[(size_t)k * st]);
+    z[(size_t)k * st] = (float)zc;
+  }
+  double a = 0.0, g = 1.0;   // backward, zero carry: u_k = r_k (z_k - u_{k+1})
+  for (k = k1 - 1; k >= k0; --k) {
+    const double r = gs_piv(ri, k, st, pc, nt, rinf, rlast);
+    a = r * ((double)z[(size_t)k * st] - a);
+    g *= -r;
+  }
+  aggb[((size_t)s * 2 + 0) * st + j] = a;
+  aggb[((size_t)s * 2 + 1) * st + j] = g;
+}
+__global__ void __launch_bounds__(128)
+k_gsolve_c(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1, int n2,
+           const float *__restrict__ qhat, int ldn, const double *__restrict__ rinv,
+           const int *__restrict__ pcut, const double *__restrict__ pinf,
+           const double *__restrict__ plast, int nt, const double *__restrict__ agg,
+           const double *__restrict__ aggb, const float *__restrict__ zs, float *__restrict__ phx,
+           float *__restrict__ phy, int po) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
+  if (j >= n1 || s >= s1) return;
+  const size_t st = ldn;
+  const int k0 = seglo[s], k1 = seglo[s + 1];
+  float *ox = phx + j - (size_t)po * st, *oy = phy + j - (size_t)po * st;
+  const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;   // s_j^2 (Eq. form:DCTmat normalisation)
+  if (j == 0) {   // L_y^dagger: D+_y u = prefix(b) - mu (y + 1), mu = sum(b) / n2
+    double pre = 0.0, tot = 0.0;
+    for (int t = 0; t < nseg; ++t) {
+      const double at = agg[((size_t)t * 2 + 0) * st];
+      if (t < s) pre += at;
+      tot += at;
+    }
+    const double mu = tot / (double)n2;
+    for (int k = k0; k < k1; ++k) {
+      pre += (double)qhat[(size_t)k * st];
+      const double w = (k == n2 - 1) ? 0.0 : pre - mu * (double)(k + 1);
+      ox[(size_t)k * st] = 0.f;
+      oy[(size_t)k * st] = (float)(s2 * w);
+    }
+    return;
+  }
+  double U = 0.0;   // backward carry into segment s from below: U_t = a'_t + g'_t U_{t+1}
+  for (int t = nseg - 1; t > s; --t)
+    U = fma(aggb[((size_t)t * 2 + 1) * st + j], U, aggb[((size_t)t * 2 + 0) * st + j]);
+  const double *ri = rinv + j;
+  const int pc = pcut[j];
+  const double rinf = pinf[j], rlast = plast[j];
+  const double cx = -s2 * (2.0 * sinpi((double)j / (2.0 * n1)));
+  double un = U;
+  for (int k = k1 - 1; k >= k0; --k) {
+    const double uk = gs_piv(ri, k, st, pc, nt, rinf, rlast) * ((double)zs[(size_t)k * st + j] - un);
+    ox[(size_t)k * st] = (float)(cx * uk);
+    // D+_y u = u_{k+1} - u_k; 0 on the global last row
+    oy[(size_t)k * st] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+    un = uk;
+  }
+}
+
 // Products of the recurrence coefficients over each solve segment (data-independent, computed
 // once per plan): forward GF_s = prod_{k in seg} (-r_{k-1}) (r_{-1} = 0), backward GB_s =
 // prod_{k in seg} (-r_k); segments of LS = ceil(nt / nseg) rows as in k_proj_solve4.
@@ -2102,6 +2238,24 @@ cudaError_t launch_proj_solve4(const ProjTile *tiles, int ntiles, int n2, int n1
   else
     k_proj_solve4<32><<<dim3((n1 + 31) / 32, per_chain, nchains), dim3(32, nseg), smem, s>>>(
         tiles, n2, n1, qhat, AT, ldn, rinv, segprod, phx, phy, AP, maps, srows, order, per_chain);
+  return cudaGetLastError();
+}
+cudaError_t launch_gsolve(int phase, const int *seglo, int nseg, int s0, int s1, int n1, int n2,
+                          const float *qhat, int ldn, const double *rinv, const int *pcut,
+                          const double *pinf, const double *plast, int nt, const double *agg,
+                          double *aggb_or_out, float *zs, float *phx, float *phy, int po,
+                          cudaStream_t s) {
+  if (s1 <= s0) return cudaSuccess;
+  const dim3 grid((n1 + 127) / 128, s1 - s0);
+  if (phase == 0)
+    k_gsolve_a<<<grid, 128, 0, s>>>(seglo, s0, s1, n1, qhat, ldn, rinv, pcut, pinf, plast, nt,
+                                    aggb_or_out);
+  else if (phase == 1)
+    k_gsolve_b<<<grid, 128, 0, s>>>(seglo, nseg, s0, s1, n1, qhat, ldn, rinv, pcut, pinf, plast,
+                                    nt, agg, zs, aggb_or_out);
+  else
+    k_gsolve_c<<<grid, 128, 0, s>>>(seglo, nseg, s0, s1, n1, n2, qhat, ldn, rinv, pcut, pinf,
+                                    plast, nt, agg, aggb_or_out, zs, phx, phy, po);
   return cudaGetLastError();
 }
 cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1,
