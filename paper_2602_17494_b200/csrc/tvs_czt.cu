@@ -62,6 +62,7 @@ struct CztIo {
   const float2 *post;
   int vcnt, kind;
   bool pin, pout;
+  bool half = false;   // Makhoul form: nonzero inputs / needed outputs only at indices 0 .. M/2
 };
 
 // Shared-memory FFT layout: element i lives at i + i/16 (one float2 of padding per 16), which
@@ -127,7 +128,9 @@ __device__ __forceinline__ float2 w16(int e) {
 // group, element kp = in[kp] pre[kp] (kp < M/16), so its 16 outputs are that value times W^t V^c;
 // it reads the input row straight from global memory (no staging pass) and performs exactly the
 // products of the full pass (the butterflies only add zeros), so the result is bitwise the same.
-template <int logM4, bool PIN>
+// HALF (Makhoul form, inputs zero at and beyond index M/2 + 1): the first pair (spans M/4, M/16,
+// base = kp) reads only its elements m < 8 and, for kp = 0, m = 8 (index M/2); the rest are zero.
+template <int logM4, bool PIN, bool HALF = false>
 __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__restrict__ in,
                                         const float2 *__restrict__ pre, int ucnt) {
   constexpr int M = 1 << (2 * logM4), nth = CZT_THREADS;
@@ -165,8 +168,16 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
       const int base = blk * 4 * L + kp;
       float2 x[16];
       float2 *zb = z + pz(base);   // base % 16 = kp < Q when Q = 4
+      if (HALF && lg == logM4 - 1) {
 #pragma unroll
-      for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, Q)];
+        for (int m = 0; m < 8; ++m) x[m] = zb[pzo(m, Q)];
+        x[8] = kp == 0 ? zb[pzo(8, Q)] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 9; m < 16; ++m) x[m] = make_float2(0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, Q)];
+      }
       // twiddles of the pair from two lookups: stage 1 (span L, k = kp + r Q) uses
       // w^{c k s1} = W^c * e^{-2 pi i c r / 16} with W = w^{kp s1}; stage 2 (span Q, k = kp,
       // stride 4 s1) uses V^c with V = w^{4 kp s1} (looked up, not W^4: keeps the error flat).
@@ -269,7 +280,9 @@ __device__ __forceinline__ void czt_middle(float2 *z, const float2 *__restrict__
 // POUT (narrow output, vcnt <= M/16): the last pair (spans M/16, M/4) is evaluated only for its
 // output element 0 of each group, kp < vcnt, in the full pass's operation order, and the result
 // goes through the post-chirp straight to global memory (kind 2: imaginary part).
-template <int logM4, bool POUT>
+// HALF (Makhoul form, only outputs 0 .. M/2 are read): the last pair (spans M/16, M/4, base = kp)
+// stores only its elements m < 8 and, for kp = 0, m = 8.
+template <int logM4, bool POUT, bool HALF = false>
 __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__restrict__ out,
                                             const float2 *__restrict__ post, int vcnt, int kind,
                                             const float *__restrict__ add) {
@@ -306,8 +319,14 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
         x[r + 12] = cmulc(x[r + 12], r ? cmul(U3, w16(3 * r)) : U3);
         bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
       }
+      if (HALF && lg == logM4 - 2) {
 #pragma unroll
-      for (int m = 0; m < 16; ++m) zb[pzo(m, L)] = x[m];
+        for (int m = 0; m < 8; ++m) zb[pzo(m, L)] = x[m];
+        if (kp == 0) zb[pzo(8, L)] = x[8];
+      } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) zb[pzo(m, L)] = x[m];
+      }
     }
     __syncthreads();
   }
@@ -342,17 +361,18 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
 
 // FFT -> kernel multiply -> inverse FFT of one chunk, with the size a compile-time constant so
 // every shared-memory offset inside a pass folds to an immediate.
-template <int logM4, bool PIN, bool POUT>
+template <int logM4, bool PIN, bool POUT, bool HALF = false>
 __device__ __forceinline__ void czt_fft_pair_t(float2 *z, const Tw &tw, const float2 *__restrict__ gk,
                                                const CztIo &io) {
-  fft_dif<logM4, PIN>(z, tw, io.in, io.pre, io.ucnt);
+  fft_dif<logM4, PIN, HALF>(z, tw, io.in, io.pre, io.ucnt);
   czt_middle<logM4>(z, gk);
-  fft_dit_inv<logM4, POUT>(z, tw, io.out, io.post, io.vcnt, io.kind, io.add);
+  fft_dit_inv<logM4, POUT, HALF>(z, tw, io.out, io.post, io.vcnt, io.kind, io.add);
 }
 template <int logM4>
 __device__ __forceinline__ void czt_fft_pair_p(float2 *z, const Tw &tw, const float2 *__restrict__ gk,
                                                const CztIo &io) {
   if constexpr (logM4 >= 3) {
+    if (io.half) return czt_fft_pair_t<logM4, false, false, true>(z, tw, gk, io);
     if (io.pin && io.pout) return czt_fft_pair_t<logM4, true, true>(z, tw, gk, io);
     if (io.pin) return czt_fft_pair_t<logM4, true, false>(z, tw, gk, io);
     if (io.pout) return czt_fft_pair_t<logM4, false, true>(z, tw, gk, io);
@@ -394,8 +414,9 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   // loads are issued in batches of B per thread (all loads of a batch before any use: the
   // kernel is latency-bound on them otherwise)
   constexpr int B = 8;
+  // (only indices 0 .. N - 1 = M/2 are written: the HALF first FFT pair reads no others)
   if (kind == 3) {   // forward: z_n = (v_a[n] + i v_b[n]) conj(c_n), v = Makhoul permutation of q
-    for (int n0 = tid; n0 < M; n0 += B * nth) {
+    for (int n0 = tid; n0 < N; n0 += B * nth) {
       float a[B], b[B];
       float2 c[B];
 #pragma unroll
@@ -410,11 +431,11 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
 #pragma unroll
       for (int r = 0; r < B; ++r) {
         const int n = n0 + r * nth;
-        if (n < M) zsm[pz(n)] = make_float2(a[r] * c[r].x + b[r] * c[r].y, b[r] * c[r].x - a[r] * c[r].y);
+        if (n < N) zsm[pz(n)] = make_float2(a[r] * c[r].x + b[r] * c[r].y, b[r] * c[r].x - a[r] * c[r].y);
       }
     }
   } else {           // inverse: u_k = conj(V_a + i V_b)_k conj(c_k)
-    for (int k0 = tid; k0 < M; k0 += B * nth) {
+    for (int k0 = tid; k0 < N; k0 += B * nth) {
       float p[B], q[B], r_[B], s[B];
       float2 e[B], c[B];
 #pragma unroll
@@ -440,7 +461,7 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
 #pragma unroll
       for (int r = 0; r < B; ++r) {
         const int k = k0 + r * nth;
-        if (k >= M) break;
+        if (k >= N) break;
         float pp, qq, rr, ss;
         if (kind == 4) {
           pp = k == 0 ? 2.f * p[r] : p[r];   // a''_0 = 2 a_0
@@ -462,7 +483,7 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
     }
   }
   __syncthreads();
-  const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, false, false};
+  const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, false, false, true};
   czt_fft_pair(zsm, G.logM4, twd, gtab, io);
   float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
   float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
