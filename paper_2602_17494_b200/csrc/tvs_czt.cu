@@ -414,9 +414,11 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   // loads are issued in batches of B per thread (all loads of a batch before any use: the
   // kernel is latency-bound on them otherwise)
   constexpr int B = 8;
-  // (only indices 0 .. N - 1 = M/2 are written: the HALF first FFT pair reads no others)
+  // only indices 0 .. N - 1 = M/2 are written when the HALF first FFT pair runs (M >= 64); the
+  // smaller transforms read every index, so the tail is zero-filled for them
+  const int nw = G.logM4 >= 3 ? N : M;
   if (kind == 3) {   // forward: z_n = (v_a[n] + i v_b[n]) conj(c_n), v = Makhoul permutation of q
-    for (int n0 = tid; n0 < N; n0 += B * nth) {
+    for (int n0 = tid; n0 < nw; n0 += B * nth) {
       float a[B], b[B];
       float2 c[B];
 #pragma unroll
@@ -431,11 +433,11 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
 #pragma unroll
       for (int r = 0; r < B; ++r) {
         const int n = n0 + r * nth;
-        if (n < N) zsm[pz(n)] = make_float2(a[r] * c[r].x + b[r] * c[r].y, b[r] * c[r].x - a[r] * c[r].y);
+        if (n < nw) zsm[pz(n)] = make_float2(a[r] * c[r].x + b[r] * c[r].y, b[r] * c[r].x - a[r] * c[r].y);
       }
     }
   } else {           // inverse: u_k = conj(V_a + i V_b)_k conj(c_k)
-    for (int k0 = tid; k0 < N; k0 += B * nth) {
+    for (int k0 = tid; k0 < nw; k0 += B * nth) {
       float p[B], q[B], r_[B], s[B];
       float2 e[B], c[B];
 #pragma unroll
@@ -461,7 +463,7 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
 #pragma unroll
       for (int r = 0; r < B; ++r) {
         const int k = k0 + r * nth;
-        if (k >= N) break;
+        if (k >= nw) break;
         float pp, qq, rr, ss;
         if (kind == 4) {
           pp = k == 0 ? 2.f * p[r] : p[r];   // a''_0 = 2 a_0
