@@ -79,11 +79,8 @@ __device__ __forceinline__ int pzo(int m, int S) { return m * S + ((m * S) >> 4)
 #ifndef TVS_CZT_TWG
 #define TVS_CZT_TWG 1
 #endif
-// TVS_CZT_TWDIRECT (build-time A/B): every twiddle of a fused pair read from the table (15 reads,
-// each correctly rounded) instead of 2 reads and 13 complex products
-#ifndef TVS_CZT_TWDIRECT
-#define TVS_CZT_TWDIRECT 0
-#endif
+// (Measured and rejected: all 15 twiddles of a fused pair read from the table instead of 2 reads
+// and 13 complex products -- forward +43 %, inverse +41 % at config 4: L2 latency.)
 struct Tw {
   const float2 *fine, *coarse, *full;
   __device__ __forceinline__ float2 operator()(int n) const {
@@ -186,18 +183,6 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
       // twiddles of the pair from two lookups: stage 1 (span L, k = kp + r Q) uses
       // w^{c k s1} = W^c * e^{-2 pi i c r / 16} with W = w^{kp s1}; stage 2 (span Q, k = kp,
       // stride 4 s1) uses V^c with V = w^{4 kp s1} (looked up, not W^4: keeps the error flat).
-#if TVS_CZT_TWDIRECT
-      const int e0 = kp * s1;   // w^{c (e0 + r M/16)}: indices below 3M/4
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        bfly4_dif(x[r], x[r + 4], x[r + 8], x[r + 12]);
-        const int e = e0 + r * (M >> 4);
-        x[r + 4] = cmul(x[r + 4], tw(e));
-        x[r + 8] = cmul(x[r + 8], tw(2 * e));
-        x[r + 12] = cmul(x[r + 12], tw(3 * e));
-      }
-      const float2 V1 = tw(4 * e0), V2 = tw(8 * e0), V3 = tw(12 * e0);
-#else
       const float2 W1 = tw(kp * s1), W2 = cmul(W1, W1), W3 = cmul(W1, W2);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -207,7 +192,6 @@ __device__ __forceinline__ void fft_dif(float2 *z, const Tw &tw, const float *__
         x[r + 12] = cmul(x[r + 12], r ? cmul(W3, w16(3 * r)) : W3);
       }
       const float2 V1 = tw(4 * kp * s1), V2 = cmul(V1, V1), V3 = cmul(V1, V2);   // direct lookup
-#endif
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         bfly4_dif(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
@@ -321,13 +305,8 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
       for (int m = 0; m < 16; ++m) x[m] = zb[pzo(m, L)];
       // stage 2 (span 4L, k = kp + r L, stride s2) uses U^c e^{-2 pi i c r/16}, U = w^{kp s2};
       // stage 1 (span L, k = kp, stride 4 s2) uses U^{4c}
-#if TVS_CZT_TWDIRECT
-      const int e0 = kp * s2;
-      const float2 V1 = tw(4 * e0), V2 = tw(8 * e0), V3 = tw(12 * e0);
-#else
       const float2 U1 = tw(kp * s2), U2 = cmul(U1, U1), U3 = cmul(U1, U2);
       const float2 V1 = tw(4 * kp * s2), V2 = cmul(V1, V1), V3 = cmul(V1, V2);   // direct lookup
-#endif
 #pragma unroll
       for (int t = 0; t < 4; ++t) {   // span L, k = kp
         x[4 * t + 1] = cmulc(x[4 * t + 1], V1);
@@ -337,16 +316,9 @@ __device__ __forceinline__ void fft_dit_inv(float2 *z, const Tw &tw, float *__re
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {   // span 4L, k = kp + r L
-#if TVS_CZT_TWDIRECT
-        const int e = e0 + r * (M >> 4);
-        x[r + 4] = cmulc(x[r + 4], tw(e));
-        x[r + 8] = cmulc(x[r + 8], tw(2 * e));
-        x[r + 12] = cmulc(x[r + 12], tw(3 * e));
-#else
         x[r + 4] = cmulc(x[r + 4], r ? cmul(U1, w16(r)) : U1);
         x[r + 8] = cmulc(x[r + 8], r ? cmul(U2, w16(2 * r)) : U2);
         x[r + 12] = cmulc(x[r + 12], r ? cmul(U3, w16(3 * r)) : U3);
-#endif
         bfly4_dit(x[r], x[r + 4], x[r + 8], x[r + 12]);
       }
       if (HALF && lg == logM4 - 2) {
