@@ -1242,6 +1242,49 @@ constexpr int SJB = 32, SSEG_MAX = 16, SU = 8;
 // per column (1024 threads): its fp64 recurrences are latency-bound chains, and with one CTA per SM
 // (the staged column block fills shared memory) shorter chains and twice the warps hide them
 constexpr int S3SEG_MAX = 32;
+// Pivots r_kk of one batch of SU rows, kk = kb + D u (D = +1 ascending, -1 descending), handed to
+// f as a functor R(u).  pcb is the CTA's largest pcut (warp-uniform: a CTA's warps share its 32
+// columns): the table is exact at every row (k_pivots writes all of them) and bitwise the tail
+// value from pcut on, so reading it above pcb and the tail values from pcb on gives every column
+// its own pivots -- with one uniform branch per batch instead of a per-row select, no loads at all
+// in the (common) all-tail batch, and a pointer walk instead of per-row 64-bit indexing.
+template <int D, class F>
+__device__ __forceinline__ void with_piv(int kb, int pcb, int nt, const double *__restrict__ ri,
+                                         size_t st, double rinf, double rlast, F &&f) {
+  const int lo = D > 0 ? kb : kb - (SU - 1), hi = D > 0 ? kb + SU - 1 : kb;
+  if (lo >= pcb && hi < nt - 1) {
+    f([&](int) { return rinf; });
+    return;
+  }
+  double rv[SU];
+  if (hi < pcb) {
+    const double *p = ri + (size_t)kb * st;
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      rv[u] = __ldg(p);
+      if (D > 0) p += st; else p -= st;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int kk = kb + D * u;
+      rv[u] = kk < pcb ? __ldg(ri + (size_t)kk * st) : (kk == nt - 1 ? rlast : rinf);
+    }
+  }
+  f([&](int u) { return rv[u]; });
+}
+
+// store v (fp32), or its tf32 head and fp32 tail at p + dl when the split planes are requested
+__device__ __forceinline__ void put_split(float *p, ptrdiff_t dl, bool split, double v) {
+  if (split) {
+    const float h = tf32_rna((float)v);
+    p[0] = h;
+    p[dl] = (float)(v - (double)h);
+  } else {
+    p[0] = (float)v;
+  }
+}
+
 // SMEM = true: the CTA's column block of qhat is staged in shared memory by the first pass and
 // overwritten in place by z (fp32), so qhat is read from HBM once and z never leaves the SM
 // (AT x 128 B of dynamic shared memory; used when that fits).  SMEM = false: z in a global
@@ -1270,9 +1313,10 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   const double *__restrict__ ri = rinv + (size_t)tl.chain * AT * st + jj;
   // pivot r_k: the table above the constant tail (see k_pivots), the tail value below it
   const int pc = pcut[(size_t)tl.chain * st + jj];
+  const int pcb = __reduce_max_sync(0xffffffffu, pc);
   const double rinf = pinf[(size_t)tl.chain * st + jj], rlast = plast[(size_t)tl.chain * st + jj];
   auto piv = [&](int kk) -> double {
-    return kk < pc ? __ldg(ri + (size_t)kk * st) : (kk == nt - 1 ? rlast : rinf);
+    return kk < pcb ? __ldg(ri + (size_t)kk * st) : (kk == nt - 1 ? rlast : rinf);
   };
   // z (and, in SMEM mode, the staged b) live at zb with row stride zst
   float *zb = SMEM ? sbuf + tx : zs + (size_t)tix * AT * st + jj;
@@ -1318,17 +1362,15 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
       const float *bp = b1 + (size_t)k * b1st;
       for (; k + SU <= k1; k += SU, bp += SU * b1st) {
         float bv[SU];
-        double rv[SU];
 #pragma unroll
-        for (int u = 0; u < SU; ++u) {   // the whole batch of loads first (latency-bound)
-          bv[u] = bp[u * b1st];
-          rv[u] = piv(k - 1 + u);
-        }
+        for (int u = 0; u < SU; ++u) bv[u] = bp[u * b1st];   // the whole batch of loads first
+        with_piv<1>(k - 1, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
 #pragma unroll
-        for (int u = 0; u < SU; ++u) {
-          a = fma(-rv[u], a, (double)bv[u]);
-          g *= -rv[u];
-        }
+          for (int u = 0; u < SU; ++u) {
+            a = fma(-R(u), a, (double)bv[u]);
+            g *= -R(u);
+          }
+        });
       }
       for (; k < k1; ++k, bp += b1st) {
         const double r = piv(k - 1);
@@ -1365,17 +1407,15 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     float *zp = zb + (size_t)k * zst;
     for (; k + SU <= k1; k += SU, bp += SU * zst, zp += SU * zst) {
       float bv[SU];
-      double rv[SU];
 #pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        bv[u] = bp[u * zst];
-        rv[u] = piv(k - 1 + u);
-      }
+      for (int u = 0; u < SU; ++u) bv[u] = bp[u * zst];
+      with_piv<1>(k - 1, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
 #pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        zc = fma(-rv[u], zc, (double)bv[u]);
-        zp[u * zst] = (float)zc;
-      }
+        for (int u = 0; u < SU; ++u) {
+          zc = fma(-R(u), zc, (double)bv[u]);
+          zp[u * zst] = (float)zc;
+        }
+      });
     }
     for (; k < k1; ++k, bp += zst, zp += zst) {
       zc = fma(-piv(k - 1), zc, (double)*bp);
@@ -1390,17 +1430,15 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
     const float *zp = zb + (size_t)k * zst;
     for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst) {
       float zv[SU];
-      double rv[SU];
 #pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        zv[u] = zp[-(ptrdiff_t)(u * zst)];
-        rv[u] = piv(k - u);
-      }
+      for (int u = 0; u < SU; ++u) zv[u] = zp[-(ptrdiff_t)(u * zst)];
+      with_piv<-1>(k, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
 #pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        a = rv[u] * ((double)zv[u] - a);
-        g *= -rv[u];
-      }
+        for (int u = 0; u < SU; ++u) {
+          a = R(u) * ((double)zv[u] - a);
+          g *= -R(u);
+        }
+      });
     }
     for (; k >= k0; --k, zp -= zst) {
       const double r = piv(k);
@@ -1443,6 +1481,8 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   }
   const double sg_j = 2.0 * sinpi((double)j / (2.0 * n1));
   const double cx = -s2 * sg_j;
+  const bool split = oxl != nullptr;
+  const ptrdiff_t dlx = split ? oxl - ox : 0, dly = split ? oyl - oy : 0;
   // ---- backward, final pass with the exact carry; outputs on rows [po, nout)
   double un = sh_c[sg][tx];
   int k = k1 - 1;
@@ -1457,14 +1497,24 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   };
   for (; k - SU + 1 >= k0; k -= SU, zp -= SU * zst) {
     float zv[SU];
-    double rv[SU];
 #pragma unroll
-    for (int u = 0; u < SU; ++u) {
-      zv[u] = zp[-(ptrdiff_t)(u * zst)];
-      rv[u] = piv(k - u);
-    }
+    for (int u = 0; u < SU; ++u) zv[u] = zp[-(ptrdiff_t)(u * zst)];
+    const bool inner = k - SU + 1 >= po && k < nout && k < nt - 1;   // all rows are output rows
+    with_piv<-1>(k, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
+      if (inner) {
+        float *px = ox + (size_t)k * st, *py = oy + (size_t)k * st;
 #pragma unroll
-    for (int u = 0; u < SU; ++u) emit(k - u, rv[u] * ((double)zv[u] - un));
+        for (int u = 0; u < SU; ++u, px -= st, py -= st) {
+          const double uk = R(u) * ((double)zv[u] - un);
+          put_split(px, dlx, split, cx * uk);
+          put_split(py, dly, split, s2 * (un - uk));
+          un = uk;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) emit(k - u, R(u) * ((double)zv[u] - un));
+      }
+    });
   }
   for (; k >= k0; --k, zp -= zst) emit(k, piv(k) * ((double)*zp - un));
 }

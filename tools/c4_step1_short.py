@@ -30,5 +30,7 @@ kt = ctx.kernel_times()
 fam = {nm: {"n": kt.counts[i], "avg_us": round(kt.ms[i] / kt.counts[i] * 1e3, 1),
             **({"tflops": round(kt.flops[i] / (kt.ms[i] / 1e3) / 1e12, 2)} if kt.flops[i] else {})}
        for i, nm in enumerate(pkg.KERNEL_FAMILIES) if kt.counts[i]}
+tau_hash = int(tau.contiguous().view(torch.int32).to(torch.int64).sum())   # bitwise A/B check
 print(json.dumps({"inner": inner, "seconds": st0.seconds, "seconds_profiled": st.seconds, "E1": st.primal_energy,
+                  "tau_hash": tau_hash,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("TVS_")}, "families": fam}))
