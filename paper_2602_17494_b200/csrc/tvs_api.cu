@@ -253,6 +253,7 @@ struct Plan {
   // streams, so one group's FFT-bound projection overlaps the other's memory-bound stencils
   int npipe = 1;
   float *v1b = nullptr, *omb = nullptr, *qb = nullptr, *gphib = nullptr;
+  float *qth = nullptr, *qthb = nullptr;   // pre-div of theta_m p^n per scratch set (omega0)
   ProjBatch local_b;
   int64_t sum_S = 0, sum_T = 0;
   Dist dist;
@@ -987,7 +988,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     P->npipe = (czt_local && ctx->pipe && g.M >= 2) ? 2 : 1;
     if (P->npipe == 2) sg = (g.M + 1) / 2;
     if (czt_local) {
-      const double per_sub = (double)vsub * 4 + (double)g.AT * g.ldT * 4 +
+      const double per_sub = (double)vsub * 4 + 2.0 * g.AT * g.ldT * 4 +
                              2.0 * 2.0 * g.AP * g.ldP * 4 + proj_tile_bytes(g.AT, g.AP, G1);
       const double rinv = (double)P->m2loc * g.AT * round_up(G1, 4) * 8;
       size_t freeb = 0, totb = 0;
@@ -1015,6 +1016,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
     TRY(dalloc(ctx, P->bufs, &P->v[1], (size_t)sg * vsub));
     TRY(dalloc(ctx, P->bufs, &P->om, (size_t)sg * 2 * g.AP * g.ldP));
     TRY(dalloc(ctx, P->bufs, &P->q, (size_t)sg * g.AT * g.ldT));
+    TRY(dalloc(ctx, P->bufs, &P->qth, (size_t)sg * g.AT * g.ldT));
     TRY(dalloc(ctx, P->bufs, &P->gphi, (size_t)sg * 2 * g.AP * g.ldP));
     TRY(build_proj(ctx, *P, P->local, lt, G2, G1, P->q, g.ldT, P->gphi, g.ldP, T, -1, -1,
                    (size_t)sg * g.AP * g.ldP, sg, sg < g.M, P->om, g.AP, g.ldP));
@@ -1022,6 +1024,7 @@ tvs_status get_plan(tvs_ctx *ctx, int n2, int n1, tvs_layout L, int step, Plan *
       TRY(dalloc(ctx, P->bufs, &P->v1b, (size_t)sg * vsub));
       TRY(dalloc(ctx, P->bufs, &P->omb, (size_t)sg * 2 * g.AP * g.ldP));
       TRY(dalloc(ctx, P->bufs, &P->qb, (size_t)sg * g.AT * g.ldT));
+      TRY(dalloc(ctx, P->bufs, &P->qthb, (size_t)sg * g.AT * g.ldT));
       TRY(dalloc(ctx, P->bufs, &P->gphib, (size_t)sg * 2 * g.AP * g.ldP));
       TRY(build_proj(ctx, *P, P->local_b, lt, G2, G1, P->qb, g.ldT, P->gphib, g.ldP, T, -1, -1,
                      (size_t)sg * g.AP * g.ldP, sg, true, P->omb, g.AP, g.ldP));
@@ -1658,6 +1661,7 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       cudaStream_t gs = set ? ctx->pipe_s : s;
       ProjBatch &LB = set ? P->local_b : P->local;
       float *qk = set ? P->qb : P->q, *gphik = set ? P->gphib : P->gphi;
+      float *qthk = set ? P->qthb : P->qth;
       float *omk = set ? P->omb : P->om;
       Geo gk = g;
       gk.M = P->sg0[k + 1] - P->sg0[k];
@@ -1666,21 +1670,23 @@ tvs_status step1_impl(tvs_ctx *ctx, const float *d0, int32_t n2, int32_t n1, flo
       float *vscr = set ? P->v1b : P->v[1];                // group scratch
       const double pdb = 16.0 * P->sgs[k].first + 4.0 * P->sgs[k].second;   // pre-div bytes
       const double swb = 48.0 * P->sgs[k].first;                             // kernel (a') bytes
-      // omega0_m = R r^n + P_loc multidiv (theta_m p^n)  (theta p in the scratch dual)
+      // omega0_m = R r^n + P_loc multidiv (theta_m p^n) = c - grad phi(q(theta p)) with
+      // c = R r^n + multidiv(theta p): the inner loop needs only grad phi(v) + omega0 =
+      // c + grad phi(q(v) - q(theta p)) (the local projection is linear), so q(theta p) is kept
+      // and subtracted by every pre-div, and theta p is never projected on its own
       TRY(run(ctx, gs, F_OTHER, 0, 0, [&] {
         return launch_load_tp(sk, gk, P->d_thy, P->d_thx, P->p, ld, G2, G1, vscr, gs);
       }));
       TRY(run(ctx, gs, F_PREDIV, pdb, 0,
-              [&] { return launch_prediv1(sk, gk, vscr, G2, G1, qk, nullptr, gs); }));
-      TRY(project_group(ctx, *P, LB, k, gs));
+              [&] { return launch_prediv1(sk, gk, vscr, G2, G1, qthk, nullptr, gs); }));
       if (overlap && k < npipe) CK(cudaStreamWaitEvent(gs, ctx->ev_join, 0));
       TRY(run(ctx, gs, F_OTHER, 0, 0, [&] {
-        return launch_omega0_1(sk, gk, P->r, ld, vscr, gphik, g.ldP, G2, G1, omk, gs);
+        return launch_omega0_1(sk, gk, P->r, ld, vscr, G2, G1, omk, gs);
       }));
       float *vin = vper, *vout = vscr;
       for (int kk = 0; kk < it.inner; ++kk) {
-        TRY(run(ctx, gs, F_PREDIV, pdb, 0,
-                [&] { return launch_prediv1(sk, gk, vin, G2, G1, qk, nullptr, gs); }));
+        TRY(run(ctx, gs, F_PREDIV, pdb + 4.0 * P->sgs[k].second, 0,
+                [&] { return launch_prediv1(sk, gk, vin, G2, G1, qk, qthk, gs); }));
         // chirp-z form: the inverse transforms write grad phi + omega0 (kernel a' then reads one
         // field: 40 instead of 48 B per update); GEMM form: kernel (a') adds omega0 itself
         const bool fused = LB.czt && LB.d_ij_add;

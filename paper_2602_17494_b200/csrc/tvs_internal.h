@@ -196,10 +196,9 @@ cudaError_t launch_axpby2(const float *a, const float *b, const float *c, int ld
 cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                            const float *p, int ld, int n2, int n1, float *v, cudaStream_t s);
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
-                           float *qlo, cudaStream_t s);
+                           const float *qsub, cudaStream_t s);
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
-                            const float *gphi, int ldg, int n2, int n1, float *om,
-                            cudaStream_t s);
+                            int n2, int n1, float *om, cudaStream_t s);
 cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
                           const float *vin, const float *gphi, int ldg, const float *om,
                           float *vout, int n2, int n1, float t, cudaStream_t s);

@@ -915,10 +915,14 @@ __device__ __forceinline__ float w_S(const float *vb, int k, int li, int lj, int
 
 
 // omega0_loc = R_{S+} r^n + (R_{S+} P E_{S+}) multidiv_{S+} E_S (theta_m p^n)  (Alg. 5, P:1740;
-// r^n = f - P multidiv p^n is the global part, reading A11), with P w = w - grad phi.
+// r^n = f - P multidiv p^n is the global part, reading A11), with P w = w - grad phi.  The inner
+// loop only ever needs grad phi(v) + omega0, and the local projection is linear, so this kernel
+// stores the projection-free part c = R r^n + multidiv(theta p) and every inner update projects
+// q(v) - q(theta p) (k_prediv1s with qsub) and adds c: the same sum, one projection per sweep and
+// subdomain group fewer than projecting theta p on its own.
 __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ r,
-                           int ld, const float *__restrict__ v, const float *__restrict__ gphi,
-                           int ldg, int n2, int n1, float *__restrict__ om) {
+                           int ld, const float *__restrict__ v, int n2, int n1,
+                           float *__restrict__ om) {
   const SubDesc sd = subs[blockIdx.z];
   int lj = blockIdx.x * blockDim.x + threadIdx.x;
   int li = blockIdx.y * blockDim.y + threadIdx.y;
@@ -928,10 +932,8 @@ __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float 
   const float *vb = v + (size_t)blockIdx.z * 4 * g.A * g.ldS;
   size_t pl = (size_t)n2 * ld;
   for (int k = 0; k < 2; ++k) {
-    float w = w_S(vb, k, li, lj, gi, gj, a, b, g, n2, n1);
-    float gp = gphi[(((size_t)k * g.MG + blockIdx.z) * g.AP + li) * ldg + lj];
-    om[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * g.ldP + lj] =
-        r[k * pl + (size_t)gi * ld + gj] + (w - gp);
+    const float w = w_S(vb, k, li, lj, gi, gj, a, b, g, n2, n1);
+    om[(((size_t)blockIdx.z * 2 + k) * g.AP + li) * g.ldP + lj] = r[k * pl + (size_t)gi * ld + gj] + w;
   }
 }
 
@@ -979,10 +981,12 @@ __device__ __forceinline__ float2 div_pair(const PairCtx &pc, int gi, int n2, fl
                      pc.xkB * vx.y - vx.x + gy * vy.y - vym.y);
 }
 
-// q = div_T E_{S+} multidiv E_S v on T (Alg. 5 pre-div)
+// q = div_T E_{S+} multidiv E_S v on T (Alg. 5 pre-div), minus qsub when given (the
+// inner loop passes the pre-div of theta_m p^n: the projection is linear, so one projection of
+// q(v) - q(theta p) gives grad phi(v) - grad phi(theta p), see step1_impl)
 __global__ void __launch_bounds__(32 * S1_WARPS)
 k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v, int n2, int n1,
-           float *__restrict__ q, float *__restrict__ qlo, int rb) {
+           float *__restrict__ q, const float *__restrict__ qsub, int rb) {
   const SubDesc sd = subs[blockIdx.z];
   const int a = sd.y1 - sd.y0 + 1, b = sd.x1 - sd.x0 + 1;
   const int at = sd.ty1 - sd.y0 + 1, bt = sd.tx1 - sd.x0 + 1;
@@ -1018,7 +1022,7 @@ k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
   Row n = ldrow(r0);
   const int qo = sd.x0 & 3;
   float *qb = q + (size_t)blockIdx.z * g.AT * g.ldT + qo;
-  float *qlb = qlo ? qlo + (size_t)blockIdx.z * g.AT * g.ldT + qo : nullptr;
+  const float *qsb = qsub ? qsub + (size_t)blockIdx.z * g.AT * g.ldT + qo : nullptr;
   for (int li = r0; li < r1; ++li) {
     const Row m = ldrow(li + 1);
     const int gi = sd.y0 + li;
@@ -1030,8 +1034,8 @@ k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
     const float qA = pc.xkA * w1.x - gxA * w1left + gyk * w2.x - gyp * w2p.x;
     const float qB = pc.xkB * w1.y - w1.x + gyk * w2.y - gyp * w2p.y;
     const size_t o = (size_t)li * g.ldT + pc.jA;
-    if (outA) store_split(qb, qlb, o, qA);
-    if (outB) store_split(qb, qlb, o + 1, qB);
+    if (outA) qb[o] = qsb ? qA - __ldg(qsb + o) : qA;
+    if (outB) qb[o + 1] = qsb ? qB - __ldg(qsb + o + 1) : qB;
     w2p = w2;
     c = n;
     n = m;
@@ -2209,17 +2213,15 @@ cudaError_t launch_load_tp(const SubDesc *subs, Geo g, const float *thy, const f
   return cudaGetLastError();
 }
 cudaError_t launch_prediv1(const SubDesc *subs, Geo g, const float *v, int n2, int n1, float *q,
-                           float *qlo, cudaStream_t s) {
+                           const float *qsub, cudaStream_t s) {
   const int strips = (g.BT + S1_OUT - 1) / S1_OUT, rb = stencil_rb(g.AT, g.M, strips);
   dim3 grid((strips + S1_WARPS - 1) / S1_WARPS, (g.AT + rb - 1) / rb, g.M);
-  k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qlo, rb);
+  k_prediv1s<<<grid, dim3(32, S1_WARPS), 0, s>>>(subs, g, v, n2, n1, q, qsub, rb);
   return cudaGetLastError();
 }
 cudaError_t launch_omega0_1(const SubDesc *subs, Geo g, const float *r, int ld, const float *v,
-                            const float *gphi, int ldg, int n2, int n1, float *om,
-                            cudaStream_t s) {
-  k_omega0_1<<<grid2(g.BP, g.AP, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, r, ld, v, gphi, ldg,
-                                                                   n2, n1, om);
+                            int n2, int n1, float *om, cudaStream_t s) {
+  k_omega0_1<<<grid2(g.BP, g.AP, 32, 8, g.M), dim3(32, 8), 0, s>>>(subs, g, r, ld, v, n2, n1, om);
   return cudaGetLastError();
 }
 cudaError_t launch_sweep1(const SubDesc *subs, Geo g, const float *thy, const float *thx,
