@@ -1903,28 +1903,6 @@ k_proj_solve4(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   }
 }
 
-// y-solve, chain-shared form: one CTA per (layout row = pivot chain, frequency block) runs the
-// chain's tiles two at a time (two groups of nseg warps, group-local named barriers) against ONE
-// staged pivot block, so the pivots cross L2 -> SM once per chain instead of once per tile.  Same
-// passes and arithmetic as k_proj_solve4.
-__device__ __forceinline__ void group_sync(int g, int nthr) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthr) : "memory");
-}
-__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
-                                      uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t ph) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra W_%=;\n\t}" ::"r"(bar), "r"(ph) : "memory");
-}
-
-
 // Batched fp32 SIMT GEMM, C = A * B (row-major), 128 x 128 x 8 CTA tile, 256 threads, 8 x 8
 // register micro-tile, double-buffered shared memory.  blockIdx.z selects the batch entry.
 constexpr int GBM = 128, GBN = 128, GBK = 8;
