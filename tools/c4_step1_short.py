@@ -1,6 +1,6 @@
 """Config 4 step 1 (8192^2, 8 strips, overlap 32), one outer sweep x `inner` Alg. 5 updates after
 a warm-up call: per-family device times.  Used for A/B runs and ncu captures of the chirp-z
-kernels.  Usage: python tools/c4_step1_short.py [inner]"""
+kernels.  Usage: python tools/c4_step1_short.py [inner] [config, default c4]"""
 import json
 import os
 import sys
@@ -14,7 +14,7 @@ import paper_2602_17494_b200 as pkg  # noqa: E402
 from tvs_synth import CONFIGS  # noqa: E402
 
 inner = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-c = CONFIGS["c4"]
+c = CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c4"]
 img = c.image()
 ctx = pkg.Context(0)
 d0 = torch.from_numpy(img).cuda()
