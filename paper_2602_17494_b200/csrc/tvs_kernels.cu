@@ -1289,22 +1289,22 @@ __device__ __forceinline__ void put_split(float *p, ptrdiff_t dl, bool split, do
   }
 }
 
-// SMEM = true: the CTA's column block of qhat is staged in shared memory by the first pass and
-// overwritten in place by z (fp32), so qhat is read from HBM once and z never leaves the SM
-// (AT x 128 B of dynamic shared memory; used when that fits).  SMEM = false: z in a global
-// scratch.
-template <bool SMEM>
-__global__ void __launch_bounds__(SJB *S3SEG_MAX)
+// SMEM = true: the CTA's column block of qhat (JB columns) is staged in shared memory by the
+// first pass and overwritten in place by z (fp32), so qhat is read from HBM once and z never
+// leaves the SM (AT x 4 JB B of dynamic shared memory; JB = 16: two CTAs per SM).  SMEM = false:
+// z in a global scratch (JB = 32).
+template <bool SMEM, int JB>
+__global__ void __launch_bounds__(JB *S3SEG_MAX, 1024 / (JB * S3SEG_MAX))
 k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *__restrict__ qhat,
               int AT, int ldn, const double *__restrict__ rinv, float *__restrict__ zs,
               float *__restrict__ phx, float *__restrict__ phy, float *__restrict__ phx_lo,
               float *__restrict__ phy_lo, int AP, const int *__restrict__ pcut,
               const double *__restrict__ pinf, const double *__restrict__ plast) {
-  __shared__ double sh_a[S3SEG_MAX][SJB], sh_c[S3SEG_MAX][SJB];
-  __shared__ double sh_tot[SJB];
-  extern __shared__ __align__(16) float sbuf[];   // SMEM: [AT][SJB]
+  __shared__ double sh_a[S3SEG_MAX][JB], sh_c[S3SEG_MAX][JB];
+  __shared__ double sh_tot[JB];
+  extern __shared__ __align__(16) float sbuf[];   // SMEM: [AT][JB]
   const int tx = threadIdx.x, sg = threadIdx.y, nseg = blockDim.y;
-  const int j = blockIdx.x * SJB + tx;
+  const int j = blockIdx.x * JB + tx;
   const int tix = blockIdx.y;
   const bool valid = j < n1;
   const ProjTile tl = tiles[tix];
@@ -1324,19 +1324,19 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
   };
   // z (and, in SMEM mode, the staged b) live at zb with row stride zst
   float *zb = SMEM ? sbuf + tx : zs + (size_t)tix * AT * st + jj;
-  const size_t zst = SMEM ? (size_t)SJB : st;
+  const size_t zst = SMEM ? (size_t)JB : st;
   const float *bb = SMEM ? zb : b;   // second read of b
   const double s2 = (j == 0 ? 1.0 : 2.0) / (double)n1;   // s_j^2 (Eq. form:DCTmat normalisation)
 
   if constexpr (SMEM) {
     // stage the CTA's [nt x 32] column block of qhat in shared memory with asynchronous 16-byte
     // copies issued by every thread (all rows in flight at once), then every pass reads it there
-    const float *blk = qhat + (size_t)tix * AT * st + (size_t)blockIdx.x * SJB;
-    const int nthr = SJB * nseg, lt = sg * SJB + tx;
-    for (int e = lt; e < nt * (SJB / 4); e += nthr) {
-      const int k = e / (SJB / 4), c = e % (SJB / 4);
-      float *dst = sbuf + k * SJB + 4 * c;
-      if (blockIdx.x * SJB + 4 * c < ldn) {
+    const float *blk = qhat + (size_t)tix * AT * st + (size_t)blockIdx.x * JB;
+    const int nthr = JB * nseg, lt = sg * JB + tx;
+    for (int e = lt; e < nt * (JB / 4); e += nthr) {
+      const int k = e / (JB / 4), c = e % (JB / 4);
+      float *dst = sbuf + k * JB + 4 * c;
+      if (blockIdx.x * JB + 4 * c < ldn) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
                      "l"(blk + (size_t)k * st + 4 * c) : "memory");
@@ -2293,21 +2293,26 @@ cudaError_t launch_proj_solve3(const ProjTile *tiles, int ntiles, int n2, int n1
                                float *phx, float *phy, float *phx_lo, float *phy_lo, int AP,
                                const int *pcut, const double *pinf, const double *plast,
                                cudaStream_t s) {
-  // one warp per segment of >= 32 rows, at most S3SEG_MAX segments (the max tile height decides)
+  // one warp per segment of >= 32 rows, at most S3SEG_MAX segments (the max tile height decides);
+  // the staged form whenever a 32-column block would fit 160 KB (the plan sizes the global z
+  // scratch with the same rule, proj_tile_bytes)
   const int nseg = std::min(S3SEG_MAX, std::max(1, AT / 32));
-  const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);
-  const size_t smem = (size_t)AT * SJB * sizeof(float);
-  if (smem <= 160 * 1024) {
-    if (smem + 9 * 1024 > 48 * 1024) {
-      cudaError_t e = smem_optin((const void *)k_proj_solve3<true>, smem);
-      if (e != cudaSuccess) return e;
-    }
-    k_proj_solve3<true><<<grid, block, smem, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
-                                                   phx_lo, phy_lo, AP, pcut, pinf, plast);
-  } else {
-    k_proj_solve3<false><<<grid, block, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
-                                                 phx_lo, phy_lo, AP, pcut, pinf, plast);
+  if ((size_t)AT * SJB * sizeof(float) <= 160 * 1024) {
+    // staged form in 16-column blocks (512 threads, <= 64 registers): two CTAs per SM, so one
+    // CTA's staging overlaps the other's passes (config-4 local solve 286 -> 273 us against
+    // 32-column blocks, bitwise the same)
+    const dim3 grid16((n1 + 15) / 16, ntiles), block16(16, nseg);
+    const size_t smem16 = (size_t)AT * 16 * sizeof(float);
+    cudaError_t e = smem_optin((const void *)k_proj_solve3<true, 16>, smem16);
+    if (e != cudaSuccess) return e;
+    k_proj_solve3<true, 16><<<grid16, block16, smem16, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z,
+                                                             phx, phy, phx_lo, phy_lo, AP, pcut,
+                                                             pinf, plast);
+    return cudaGetLastError();
   }
+  const dim3 grid((n1 + SJB - 1) / SJB, ntiles), block(SJB, nseg);   // z in the global scratch
+  k_proj_solve3<false, SJB><<<grid, block, 0, s>>>(tiles, n2, n1, qhat, AT, ldn, rinv, z, phx, phy,
+                                               phx_lo, phy_lo, AP, pcut, pinf, plast);
   return cudaGetLastError();
 }
 }  // namespace tvs
