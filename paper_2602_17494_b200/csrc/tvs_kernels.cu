@@ -552,6 +552,9 @@ __device__ __forceinline__ float ky_part(const float *__restrict__ q, const Geo 
 // is grouped as sum_ky (sum_kx qhat) in ascending ky, where the parts of layout rows owned by the
 // slab neighbours (ky < k0: `up`, ky >= k1: `dn`, rows [*_r0, *_r1)) arrive as partial sums over
 // NCCL -- so overlaps are bitwise identical for every GPU count.  Flags non-finite values.
+// Four consecutive columns per thread: float4 loads and stores whenever the quad has one x-cover
+// and its subdomain rows are 16-byte aligned (every interior quad of a strip layout), else the
+// columns one by one.  Per element the same operations in the same order either way.
 template <int C>
 __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
                           const int2 *__restrict__ covy, const int2 *__restrict__ covx,
@@ -560,62 +563,134 @@ __global__ void k_combine(const SubDesc *__restrict__ subs, Geo g,
                           int ld, int n2, int row0, int row1, int n1, float ahat, int *bad,
                           const float *__restrict__ up, int up_r0, int up_r1,
                           const float *__restrict__ dn, int dn_r0, int dn_r1) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jq = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int i = row0 + blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= row1 || j >= n1) return;
-  const int2 cy = covy[i], cx = covx[j];
+  if (i >= row1 || jq >= n1) return;
+  const int2 cy = covy[i];
   const size_t qpl = (size_t)g.A * g.ldS;   // plane stride inside one subdomain's block
-  // every load is issued before the sums: p first, then the (at most 2 x 2, layout check) covering
-  // subdomains' values, so a thread has all its reads in flight at once
-  float pv[C];
+  const int2 cx = covx[jq];
+  bool quad = jq + 3 < n1;
+  if (quad) {
+    const int2 cx3 = covx[jq + 3];
+    quad = cx3.x == cx.x && cx3.y == cx.y && ((jq - lox[cx.x]) & 3) == 0 &&
+           (cx.y < 2 || ((jq - lox[cx.x + 1]) & 3) == 0);
+  }
+  bool finite = true;
+  if (quad) {
+    // every load is issued before the sums: p first, then the (at most 2 x 2, layout check)
+    // covering subdomains' values
+    float4 pv[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) pv[c] = p[(size_t)c * n2 * ld + (size_t)i * ld + j];
-  float acc[C];
+    for (int c = 0; c < C; ++c)
+      pv[c] = *reinterpret_cast<const float4 *>(p + (size_t)c * n2 * ld + (size_t)i * ld + jq);
+    float4 acc[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.f;
+    for (int c = 0; c < C; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    if (t >= cy.y) break;
-    const int ky = cy.x + t;
-    float part[C];
+    for (int t = 0; t < 2; ++t) {
+      if (t >= cy.y) break;
+      const int ky = cy.x + t;
+      float4 part[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) part[c] = 0.f;
-    if (ky < k0) {
-      if (i >= up_r0 && i < up_r1)
+      for (int c = 0; c < C; ++c) part[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ky < k0) {
+        if (i >= up_r0 && i < up_r1)
 #pragma unroll
-        for (int c = 0; c < C; ++c) part[c] = up[((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + j];
-    } else if (ky >= k1) {
-      if (i >= dn_r0 && i < dn_r1)
+          for (int c = 0; c < C; ++c)
+            part[c] = *reinterpret_cast<const float4 *>(up + ((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + jq);
+      } else if (ky >= k1) {
+        if (i >= dn_r0 && i < dn_r1)
 #pragma unroll
-        for (int c = 0; c < C; ++c) part[c] = dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j];
-    } else {   // sum over kx of this layout row (same grouping as k_partial)
-      const int li = i - loy[ky];
-      const float *qa = q + ((size_t)(cx.x * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[cx.x]);
-      float a[C], b[C];
+          for (int c = 0; c < C; ++c)
+            part[c] = *reinterpret_cast<const float4 *>(dn + ((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + jq);
+      } else {   // sum over kx of this layout row (same grouping as k_partial)
+        const int li = i - loy[ky];
+        const float *qa = q + ((size_t)(cx.x * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (jq - lox[cx.x]);
+        float4 av[C], bv[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) a[c] = __ldg(qa + c * qpl);
-      if (cx.y > 1) {
-        const int kx = cx.x + 1;
-        const float *qb = q + ((size_t)(kx * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[kx]);
+        for (int c = 0; c < C; ++c) av[c] = __ldg(reinterpret_cast<const float4 *>(qa + c * qpl));
+        if (cx.y > 1) {
+          const int kx = cx.x + 1;
+          const float *qb = q + ((size_t)(kx * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (jq - lox[kx]);
 #pragma unroll
-        for (int c = 0; c < C; ++c) b[c] = __ldg(qb + c * qpl);
+          for (int c = 0; c < C; ++c) bv[c] = __ldg(reinterpret_cast<const float4 *>(qb + c * qpl));
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          part[c].x += av[c].x; part[c].y += av[c].y; part[c].z += av[c].z; part[c].w += av[c].w;
+          if (cx.y > 1) {
+            part[c].x += bv[c].x; part[c].y += bv[c].y; part[c].z += bv[c].z; part[c].w += bv[c].w;
+          }
+        }
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        part[c] += a[c];
-        if (cx.y > 1) part[c] += b[c];
+        acc[c].x += part[c].x; acc[c].y += part[c].y; acc[c].z += part[c].z; acc[c].w += part[c].w;
       }
     }
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[c] += part[c];
-  }
-  bool finite = true;
+    for (int c = 0; c < C; ++c) {
+      float4 v;
+      v.x = (1.f - ahat) * pv[c].x + ahat * acc[c].x;
+      v.y = (1.f - ahat) * pv[c].y + ahat * acc[c].y;
+      v.z = (1.f - ahat) * pv[c].z + ahat * acc[c].z;
+      v.w = (1.f - ahat) * pv[c].w + ahat * acc[c].w;
+      finite = finite && isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+      *reinterpret_cast<float4 *>(p + (size_t)c * n2 * ld + (size_t)i * ld + jq) = v;
+    }
+  } else {
+    for (int j = jq; j < min(jq + 4, n1); ++j) {
+      const int2 cxj = covx[j];
+      float pv[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    const size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
-    const float v = (1.f - ahat) * pv[c] + ahat * acc[c];
-    finite = finite && isfinite(v);
-    p[idx] = v;
+      for (int c = 0; c < C; ++c) pv[c] = p[(size_t)c * n2 * ld + (size_t)i * ld + j];
+      float acc[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.f;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t >= cy.y) break;
+        const int ky = cy.x + t;
+        float part[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) part[c] = 0.f;
+        if (ky < k0) {
+          if (i >= up_r0 && i < up_r1)
+#pragma unroll
+            for (int c = 0; c < C; ++c) part[c] = up[((size_t)c * (up_r1 - up_r0) + (i - up_r0)) * ld + j];
+        } else if (ky >= k1) {
+          if (i >= dn_r0 && i < dn_r1)
+#pragma unroll
+            for (int c = 0; c < C; ++c) part[c] = dn[((size_t)c * (dn_r1 - dn_r0) + (i - dn_r0)) * ld + j];
+        } else {
+          const int li = i - loy[ky];
+          const float *qa = q + ((size_t)(cxj.x * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[cxj.x]);
+          float av[C], bv[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) av[c] = __ldg(qa + c * qpl);
+          if (cxj.y > 1) {
+            const int kx = cxj.x + 1;
+            const float *qb = q + ((size_t)(kx * m2loc + (ky - k0)) * C * g.A + li) * g.ldS + (j - lox[kx]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) bv[c] = __ldg(qb + c * qpl);
+          }
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            part[c] += av[c];
+            if (cxj.y > 1) part[c] += bv[c];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += part[c];
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const size_t idx = (size_t)c * n2 * ld + (size_t)i * ld + j;
+        const float v = (1.f - ahat) * pv[c] + ahat * acc[c];
+        finite = finite && isfinite(v);
+        p[idx] = v;
+      }
+    }
   }
   if (!finite) atomicOr(bad, 1);
 }
@@ -2089,11 +2164,11 @@ cudaError_t launch_combine(const SubDesc *subs, Geo g, int planes, const int2 *c
                            const float *dn, int dn_r0, int dn_r1, cudaStream_t s) {
   if (row1 <= row0) return cudaSuccess;
   if (planes == 4)
-    k_combine<4><<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
+    k_combine<4><<<grid2((n1 + 3) / 4, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
         subs, g, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat, bad, up,
         up_r0, up_r1, dn, dn_r0, dn_r1);
   else
-    k_combine<2><<<grid2(n1, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
+    k_combine<2><<<grid2((n1 + 3) / 4, row1 - row0, 32, 8), dim3(32, 8), 0, s>>>(
         subs, g, covy, covx, loy, lox, m2loc, k0, k1, q, p, ld, n2, row0, row1, n1, ahat, bad, up,
         up_r0, up_r1, dn, dn_r0, dn_r1);
   return cudaGetLastError();
