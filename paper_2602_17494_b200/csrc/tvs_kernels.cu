@@ -1614,6 +1614,9 @@ k_proj_solve3(const ProjTile *__restrict__ tiles, int n2, int n1, const float *_
 // grid, and tau is bitwise the same for every GPU count.  Same recurrences and fma orders as
 // k_proj_solve3; j = 0 (the singular Neumann column) is the prefix sum D+_y u = prefix(b) - mu (y+1).
 // agg layout: [segment][2][ldn] doubles.  One thread per (frequency, owned segment).
+// The pivots come through with_piv with the warp's largest pcut (the frequencies of a warp are 32
+// consecutive j), the rows in batches of SU loads -- the per-row latency chain otherwise bounds
+// these one-thread-per-(frequency, segment) loops.
 __device__ __forceinline__ double gs_piv(const double *ri, int k, size_t st, int pc, int nt,
                                          double rinf, double rlast) {
   return k < pc ? __ldg(ri + (size_t)k * st) : (k == nt - 1 ? rlast : rinf);
@@ -1624,7 +1627,9 @@ k_gsolve_a(const int *__restrict__ seglo, int s0, int s1, int n1, const float *_
            const double *__restrict__ pinf, const double *__restrict__ plast, int nt,
            double *__restrict__ agg) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
-  if (j >= n1 || s >= s1) return;
+  const bool ok = j < n1 && s < s1;
+  const int pcb = __reduce_max_sync(0xffffffffu, ok ? pcut[j] : 0);
+  if (!ok) return;
   const size_t st = ldn;
   const int k0 = seglo[s], k1 = seglo[s + 1];
   const float *b = qhat + j;
@@ -1633,7 +1638,6 @@ k_gsolve_a(const int *__restrict__ seglo, int s0, int s1, int n1, const float *_
     for (int k = k0; k < k1; ++k) a += (double)b[(size_t)k * st];
   } else {
     const double *ri = rinv + j;
-    const int pc = pcut[j];
     const double rinf = pinf[j], rlast = plast[j];
     int k = k0;
     if (k == 0) {   // z_0 = b_0 (no coupling above row 0)
@@ -1641,9 +1645,22 @@ k_gsolve_a(const int *__restrict__ seglo, int s0, int s1, int n1, const float *_
       g = 0.0;
       k = 1;
     }
-    for (; k < k1; ++k) {
-      const double r = gs_piv(ri, k - 1, st, pc, nt, rinf, rlast);
-      a = fma(-r, a, (double)b[(size_t)k * st]);
+    const float *bp = b + (size_t)k * st;
+    for (; k + SU <= k1; k += SU, bp += SU * st) {
+      float bv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) bv[u] = __ldg(bp + u * st);
+      with_piv<1>(k - 1, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          a = fma(-R(u), a, (double)bv[u]);
+          g *= -R(u);
+        }
+      });
+    }
+    for (; k < k1; ++k, bp += st) {
+      const double r = gs_piv(ri, k - 1, st, pcb, nt, rinf, rlast);
+      a = fma(-r, a, (double)*bp);
       g *= -r;
     }
   }
@@ -1657,14 +1674,15 @@ k_gsolve_b(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1,
            const double *__restrict__ plast, int nt, const double *__restrict__ agg,
            float *__restrict__ zs, double *__restrict__ aggb) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
-  if (j >= n1 || s >= s1 || j == 0) return;   // j = 0 needs no z / backward pass
+  const bool ok = j < n1 && s < s1;
+  const int pcb = __reduce_max_sync(0xffffffffu, ok ? pcut[j] : 0);
+  if (!ok || j == 0) return;   // j = 0 needs no z / backward pass
   const size_t st = ldn;
   const int k0 = seglo[s], k1 = seglo[s + 1];
   double Z = 0.0;   // forward carry into segment s: Z_t = a_t + g_t Z_{t-1}, all ranks alike
   for (int t = 0; t < s; ++t)
     Z = fma(agg[((size_t)t * 2 + 1) * st + j], Z, agg[((size_t)t * 2 + 0) * st + j]);
   const double *ri = rinv + j;
-  const int pc = pcut[j];
   const double rinf = pinf[j], rlast = plast[j];
   const float *b = qhat + j;
   float *z = zs + j;
@@ -1675,15 +1693,47 @@ k_gsolve_b(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1,
     z[0] = (float)zc;
     k = 1;
   }
-  for (; k < k1; ++k) {
-    zc = fma(-gs_piv(ri, k - 1, st, pc, nt, rinf, rlast), zc, (double)b[(size_t)k * st]);
-    z[(size_t)k * st] = (float)zc;
+  {
+    const float *bp = b + (size_t)k * st;
+    float *zp = z + (size_t)k * st;
+    for (; k + SU <= k1; k += SU, bp += SU * st, zp += SU * st) {
+      float bv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) bv[u] = __ldg(bp + u * st);
+      with_piv<1>(k - 1, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          zc = fma(-R(u), zc, (double)bv[u]);
+          zp[u * st] = (float)zc;
+        }
+      });
+    }
+    for (; k < k1; ++k, bp += st, zp += st) {
+      zc = fma(-gs_piv(ri, k - 1, st, pcb, nt, rinf, rlast), zc, (double)*bp);
+      *zp = (float)zc;
+    }
   }
   double a = 0.0, g = 1.0;   // backward, zero carry: u_k = r_k (z_k - u_{k+1})
-  for (k = k1 - 1; k >= k0; --k) {
-    const double r = gs_piv(ri, k, st, pc, nt, rinf, rlast);
-    a = r * ((double)z[(size_t)k * st] - a);
-    g *= -r;
+  k = k1 - 1;
+  {
+    const float *zp = z + (size_t)k * st;
+    for (; k - SU + 1 >= k0; k -= SU, zp -= SU * st) {
+      float zv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) zv[u] = zp[-(ptrdiff_t)(u * st)];
+      with_piv<-1>(k, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          a = R(u) * ((double)zv[u] - a);
+          g *= -R(u);
+        }
+      });
+    }
+    for (; k >= k0; --k, zp -= st) {
+      const double r = gs_piv(ri, k, st, pcb, nt, rinf, rlast);
+      a = r * ((double)*zp - a);
+      g *= -r;
+    }
   }
   aggb[((size_t)s * 2 + 0) * st + j] = a;
   aggb[((size_t)s * 2 + 1) * st + j] = g;
@@ -1696,7 +1746,9 @@ k_gsolve_c(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1, int 
            const double *__restrict__ aggb, const float *__restrict__ zs, float *__restrict__ phx,
            float *__restrict__ phy, int po) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x, s = s0 + blockIdx.y;
-  if (j >= n1 || s >= s1) return;
+  const bool ok = j < n1 && s < s1;
+  const int pcb = __reduce_max_sync(0xffffffffu, ok ? pcut[j] : 0);
+  if (!ok) return;
   const size_t st = ldn;
   const int k0 = seglo[s], k1 = seglo[s + 1];
   float *ox = phx + j - (size_t)po * st, *oy = phy + j - (size_t)po * st;
@@ -1721,17 +1773,27 @@ k_gsolve_c(const int *__restrict__ seglo, int nseg, int s0, int s1, int n1, int 
   for (int t = nseg - 1; t > s; --t)
     U = fma(aggb[((size_t)t * 2 + 1) * st + j], U, aggb[((size_t)t * 2 + 0) * st + j]);
   const double *ri = rinv + j;
-  const int pc = pcut[j];
   const double rinf = pinf[j], rlast = plast[j];
   const double cx = -s2 * (2.0 * sinpi((double)j / (2.0 * n1)));
   double un = U;
-  for (int k = k1 - 1; k >= k0; --k) {
-    const double uk = gs_piv(ri, k, st, pc, nt, rinf, rlast) * ((double)zs[(size_t)k * st + j] - un);
-    ox[(size_t)k * st] = (float)(cx * uk);
+  int k = k1 - 1;
+  const float *zp = zs + (size_t)k * st + j;
+  auto emit = [&](int kk, double uk) {
+    ox[(size_t)kk * st] = (float)(cx * uk);
     // D+_y u = u_{k+1} - u_k; 0 on the global last row
-    oy[(size_t)k * st] = (k == nt - 1) ? 0.f : (float)(s2 * (un - uk));
+    oy[(size_t)kk * st] = (kk == nt - 1) ? 0.f : (float)(s2 * (un - uk));
     un = uk;
+  };
+  for (; k - SU + 1 >= k0; k -= SU, zp -= SU * st) {
+    float zv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) zv[u] = zp[-(ptrdiff_t)(u * st)];
+    with_piv<-1>(k, pcb, nt, ri, st, rinf, rlast, [&](auto R) {
+#pragma unroll
+      for (int u = 0; u < SU; ++u) emit(k - u, R(u) * ((double)zv[u] - un));
+    });
   }
+  for (; k >= k0; --k, zp -= st) emit(k, gs_piv(ri, k, st, pcb, nt, rinf, rlast) * ((double)*zp - un));
 }
 
 // Products of the recurrence coefficients over each solve segment (data-independent, computed
