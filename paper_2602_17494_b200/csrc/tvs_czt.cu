@@ -548,373 +548,6 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// M = 16384 Makhoul form as a four-step FFT 32 x 32 x 16 (the config-4 axis N = 8193 and the
-// config-3 global axis are the hot path; TVS_CZT_R32 = 0 builds the radix-4 pair form instead).
-// With n = kp + 512 m (kp < 512, m < 32) and k = k1 + 32 c1 + 1024 c2 (k1, c1 < 32, c2 < 16),
-//   X[k] = sum_a w16^{a c2} w512^{a c1} sum_b w32^{b c1} [ w^{kp k1} sum_m x[n] w32^{m k1} ],
-// kp = a + 16 b, w = e^{-2 pi i / M}:
-//   pass A  (thread kp):        32-point DFT over m, twiddle w^{kp k1}; fused with the row loads
-//   pass B  (thread (j, a)):    32-point DFT over b, twiddle w512^{a c1}
-//   pass C  (two (j, j') each): 16-point DFT over a, times the window FFT, inverse 16-point DFT
-//   pass B', pass A':           the adjoints of B and A (conjugate twiddles, DIT), A' fused with
-//                               the Makhoul output map and the global stores
-// Register DFTs are radix-2 DIF (natural in, bit-reversed out) and their exact adjoints (DIT);
-// the window FFT is stored in the resulting position order (czt_tables).  Shared memory is read
-// and written four times per element instead of eight, and every access of a half-warp is
-// conflict-free with the i + i/16 padding.
-#ifndef TVS_CZT_R32
-#define TVS_CZT_R32 1
-#endif
-
-__device__ __forceinline__ int brev5(int j) {
-  return ((j & 1) << 4) | ((j & 2) << 2) | (j & 4) | ((j & 8) >> 2) | ((j & 16) >> 4);
-}
-__device__ __forceinline__ int brev4(int j) {
-  return ((j & 1) << 3) | ((j & 2) << 1) | ((j & 4) >> 1) | ((j & 8) >> 3);
-}
-// x e^{-2 pi i e / 32} for e a compile-time constant after unrolling (trivial factors folded)
-__device__ __forceinline__ float2 mulw32(float2 x, int e) {
-  constexpr float C[32] = {
-      1.f, 0.98078528040323044f, 0.92387953251128674f, 0.83146961230254524f, 0.70710678118654752f,
-      0.55557023301960218f, 0.38268343236508977f, 0.19509032201612826f, 0.f, -0.19509032201612826f,
-      -0.38268343236508977f, -0.55557023301960218f, -0.70710678118654752f, -0.83146961230254524f,
-      -0.92387953251128674f, -0.98078528040323044f, -1.f, -0.98078528040323044f, -0.92387953251128674f,
-      -0.83146961230254524f, -0.70710678118654752f, -0.55557023301960218f, -0.38268343236508977f,
-      -0.19509032201612826f, 0.f, 0.19509032201612826f, 0.38268343236508977f, 0.55557023301960218f,
-      0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f, 0.98078528040323044f};
-  constexpr float s = 0.70710678118654752f;
-  e &= 31;
-  if (e == 0) return x;
-  if (e == 8) return make_float2(x.y, -x.x);                                  // -i
-  if (e == 16) return make_float2(-x.x, -x.y);
-  if (e == 24) return make_float2(-x.y, x.x);                                 // +i
-  if (e == 4) return make_float2((x.x + x.y) * s, (x.y - x.x) * s);
-  if (e == 12) return make_float2((x.y - x.x) * s, -(x.x + x.y) * s);
-  if (e == 20) return make_float2(-(x.x + x.y) * s, (x.x - x.y) * s);
-  if (e == 28) return make_float2((x.x - x.y) * s, (x.x + x.y) * s);
-  const float c = C[e], sn = C[(e + 24) & 31];                                // cos, sin(2 pi e/32)
-  return make_float2(x.x * c + x.y * sn, x.y * c - x.x * sn);
-}
-// radix-2 DIF stages of spans S0, S0/2, .., 1 on R registers (x[j] = X[bitrev(j)] after all)
-template <int R, int S0>
-__device__ __forceinline__ void dif_stages(float2 (&x)[R]) {
-#pragma unroll
-  for (int span = S0; span >= 1; span >>= 1)
-#pragma unroll
-    for (int s0 = 0; s0 < R; s0 += 2 * span)
-#pragma unroll
-      for (int i = 0; i < span; ++i) {
-        const float2 a = x[s0 + i], b = x[s0 + i + span];
-        x[s0 + i] = make_float2(a.x + b.x, a.y + b.y);
-        x[s0 + i + span] = mulw32(make_float2(a.x - b.x, a.y - b.y), i * (16 / span));
-      }
-}
-// the adjoint: bit-reversed in, natural out, conjugate twiddles (R times the inverse DFT)
-template <int R>
-__device__ __forceinline__ void dit_stages(float2 (&x)[R]) {
-#pragma unroll
-  for (int span = 1; span < R; span <<= 1)
-#pragma unroll
-    for (int s0 = 0; s0 < R; s0 += 2 * span)
-#pragma unroll
-      for (int i = 0; i < span; ++i) {
-        const float2 t = mulw32(x[s0 + i + span], 32 - i * (16 / span)), a = x[s0 + i];
-        x[s0 + i] = make_float2(a.x + t.x, a.y + t.y);
-        x[s0 + i + span] = make_float2(a.x - t.x, a.y - t.y);
-      }
-}
-// x[j] *= T(brev5(j)) (CONJ: conj T), T(e) = B^e from the five looked-up powers b[t] = B^{2^t}:
-// T(e) = L(e & 3) H(e >> 2) with L = {1, b0, b1, b0 b1} and H(h) the products of b2, b3, b4 --
-// at most four roundings deep, ten partial products live.
-template <bool CONJ>
-__device__ __forceinline__ void twiddle32(float2 (&x)[32], const float2 (&b)[5]) {
-  const float2 one = make_float2(1.f, 0.f);
-  const float2 L[4] = {one, b[0], b[1], cmul(b[0], b[1])};
-  const float2 b23 = cmul(b[2], b[3]);
-  const float2 H[8] = {one, b[2], b[3], b23, b[4], cmul(b[4], b[2]), cmul(b[4], b[3]), cmul(b[4], b23)};
-#pragma unroll
-  for (int e = 1; e < 32; ++e) {
-    const int lo = e & 3, hi = e >> 2;
-    const float2 t = lo == 0 ? H[hi] : hi == 0 ? L[lo] : cmul(L[lo], H[hi]);
-    const int j = brev5(e);
-    x[j] = CONJ ? cmulc(x[j], t) : cmul(x[j], t);
-  }
-}
-
-// twiddle-table load that the compiler may not merge with an earlier load of the same entry
-// (passes A and A', B and B' read the same bases; merged, their products stay live -- and
-// spilled -- across the passes in between)
-__device__ __forceinline__ float2 ldtw(const float2 *p) {
-  float2 v;
-  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  return v;
-}
-
-template <int kind>
-__device__ __forceinline__ void czt_makhoul_r32(const CztJob &jb, const CztGeom &G,
-                                                const float2 *__restrict__ gtab,
-                                                const float2 *__restrict__ tw, float2 *zsm) {
-  constexpr int nth = 512;
-  const int N = G.N, tid = threadIdx.x;
-#if TVS_CZT_PHASES   // build-time instrumentation: clock64 at every barrier of two sample CTAs
-  long long ph_t[6];
-  const bool ph_on = tid == 0 && blockIdx.x == 300 && (blockIdx.y < 2);
-#define TVS_PH(k) (ph_t[k] = clock64())
-  TVS_PH(0);
-#else
-#define TVS_PH(k) ((void)0)
-#endif
-  const int r0 = kind == 5 ? blockIdx.x : 2 * blockIdx.x;
-  if (r0 >= jb.rows) return;
-  const bool two = kind != 5 && r0 + 1 < jb.rows;
-  const float2 *__restrict__ cc = jb.pre;    // c_n = e^{i pi n^2 / N}
-  const float2 *__restrict__ ee = jb.post;   // e_k = e^{i pi k / (2N)}
-  const float *__restrict__ ia = jb.in + (size_t)r0 * jb.ldin;
-  const float *__restrict__ ib = two ? ia + jb.ldin : nullptr;
-  const int h = (N + 1) >> 1;
-  float2 x[32];
-  // ---- pass A: the Makhoul input map and pre-chirp of n = kp + 512 m (m <= 16: n <= N - 1 =
-  // M/2; the upper half is zero), 32-point DFT over m, twiddle w^{kp k1}
-  {
-    const int kp = tid;
-    float2 bt[5];   // twiddle bases w^{kp 2^t}, in flight with the row loads
-#pragma unroll
-    for (int t = 0; t < 5; ++t) bt[t] = ldtw(tw + (kp << t));
-#pragma unroll
-    for (int m0 = 0; m0 < 17; m0 += (kind == 3 ? 17 : 9)) {   // loads in one (forward) or two
-      constexpr int B = kind == 3 ? 17 : 9;                     // batches, all before any use
-      float a[B], bb[B], p4[B], q4[B];
-      float2 c[B], e[B];
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const int m = m0 + r;
-        if (m >= 17) break;
-        const int n = kp + 512 * m;
-        const bool in = n < N;
-        c[r] = in ? __ldg(cc + n) : make_float2(0.f, 0.f);
-        if (kind == 3) {
-          const int xx = in ? (n < h ? 2 * n : 2 * (N - 1 - n) + 1) - jb.tx0 : -1;
-          const bool ok = xx >= 0 && xx < jb.ulen;
-          a[r] = ok ? __ldg(ia + xx) : 0.f;
-          bb[r] = ok && ib ? __ldg(ib + xx) : 0.f;
-        } else {
-          const bool nz = in && n > 0;
-          const int km = nz ? N - n : 0;
-          e[r] = in ? __ldg(ee + n) : make_float2(0.f, 0.f);
-          a[r] = in ? __ldg(ia + n) : 0.f;
-          bb[r] = nz ? __ldg(ia + km) : 0.f;
-          if (kind == 4) {
-            p4[r] = in && ib ? __ldg(ib + n) : 0.f;
-            q4[r] = nz && ib ? __ldg(ib + km) : 0.f;
-          } else {
-            const float2 em = nz ? __ldg(ee + km) : make_float2(0.f, 0.f);
-            p4[r] = em.x;
-            q4[r] = em.y;
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const int m = m0 + r;
-        if (m >= 17) break;
-        if (kind == 3) {   // z = (v_a + i v_b) conj(c)
-          x[m] = make_float2(a[r] * c[r].x + bb[r] * c[r].y, bb[r] * c[r].x - a[r] * c[r].y);
-        } else {           // z = conj(V_a + i V_b) conj(c)
-          float pp, qq, rr, ss;
-          const bool k0 = kp == 0 && m == 0;
-          if (kind == 4) {
-            pp = k0 ? 2.f * a[r] : a[r];   // a''_0 = 2 a_0
-            qq = bb[r];
-            rr = k0 ? 2.f * p4[r] : p4[r];
-            ss = q4[r];
-          } else {   // c_k = b_{N-k} cos(delta_{N-k}), c_{N-k}, d_k, d_{N-k}
-            pp = bb[r] * p4[r];
-            qq = k0 ? 0.f : a[r] * e[r].x;
-            rr = a[r] * e[r].y;
-            ss = bb[r] * q4[r];
-          }
-          const float2 ek = e[r];
-          const float2 va = make_float2(ek.x * pp + ek.y * qq, ek.y * pp - ek.x * qq);
-          const float2 vb = make_float2(ek.x * rr + ek.y * ss, ek.y * rr - ek.x * ss);
-          const float2 w = make_float2(va.x - vb.y, va.y + vb.x);
-          x[m] = make_float2(w.x * c[r].x - w.y * c[r].y, -(w.x * c[r].y + w.y * c[r].x));
-        }
-      }
-    }
-    // first DIF stage (span 16) with x[17..31] = 0: x[i + 16] = x[i] w32^i for i >= 1
-    {
-      const float2 a = x[0], b = x[16];
-      x[0] = make_float2(a.x + b.x, a.y + b.y);
-      x[16] = make_float2(a.x - b.x, a.y - b.y);
-    }
-#pragma unroll
-    for (int i = 1; i < 16; ++i) x[i + 16] = mulw32(x[i], i);
-    dif_stages<32, 8>(x);
-    twiddle32<false>(x, bt);
-    float2 *zb = zsm + pz(kp);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) zb[544 * j] = x[j];
-  }
-  const int ja = tid >> 4, aa = tid & 15;
-  float2 ub[5];   // w512^{a 2^t}, loaded before the barriers that precede passes B and B'
-#pragma unroll
-  for (int t = 0; t < 5; ++t) ub[t] = ldtw(tw + (32 << t) * aa);
-  __syncthreads();
-  TVS_PH(1);
-  // ---- pass B: thread (j, a), 32-point DFT over b (positions a + 16 b + 512 j), twiddle w512^{a c1}
-  float4 gk[8];   // window FFT of pass C's first group: in flight across the barrier
-  {
-    float2 *zb = zsm + aa + 544 * ja;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) x[b] = zb[17 * b];
-    dif_stages<32, 16>(x);
-    twiddle32<false>(x, ub);
-#pragma unroll
-    for (int b = 0; b < 32; ++b) zb[17 * b] = x[b];
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) gk[i] = __ldg(reinterpret_cast<const float4 *>(gtab + 16 * tid) + i);
-  __syncthreads();
-  TVS_PH(2);
-  // ---- pass C: two groups g = (j, j') per thread: DFT16 over a, window, inverse DFT16; the
-  // second group's window loads are issued before the first group's arithmetic
-#pragma unroll
-  for (int gi = 0; gi < 2; ++gi) {
-    const int g = tid + gi * nth;
-    float4 gn[8];
-    if (gi == 0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) gn[i] = __ldg(reinterpret_cast<const float4 *>(gtab + 16 * (g + nth)) + i);
-    }
-    float2 y[16];
-    float2 *zb = zsm + 17 * g;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) y[i] = zb[i];
-    dif_stages<16, 8>(y);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      y[2 * i] = cmul(y[2 * i], make_float2(gk[i].x, gk[i].y));
-      y[2 * i + 1] = cmul(y[2 * i + 1], make_float2(gk[i].z, gk[i].w));
-    }
-    dit_stages<16>(y);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) zb[i] = y[i];
-    if (gi == 0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) gk[i] = gn[i];
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < 5; ++t) ub[t] = ldtw(tw + (32 << t) * aa);
-  __syncthreads();
-  TVS_PH(3);
-  // ---- pass B': adjoint of B
-  {
-    float2 *zb = zsm + aa + 544 * ja;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) x[b] = zb[17 * b];
-    twiddle32<true>(x, ub);
-    dit_stages<32>(x);
-#pragma unroll
-    for (int b = 0; b < 32; ++b) zb[17 * b] = x[b];
-  }
-  int kp;   // an opaque copy of tid: keeps pass A's index arithmetic from being kept live (and
-            // spilled) until the outputs
-  asm volatile("mov.u32 %0, %1;" : "=r"(kp) : "r"(tid));
-  float2 bt[5];
-#pragma unroll
-  for (int t = 0; t < 5; ++t) bt[t] = ldtw(tw + (kp << t));
-  __syncthreads();
-  TVS_PH(4);
-  // ---- pass A': adjoint of A; outputs n = kp + 512 m, m <= 16 (n <= M/2 = N - 1)
-  {
-    const float2 *zb = zsm + pz(kp);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = zb[544 * j];
-    twiddle32<true>(x, bt);
-    dit_stages<32>(x);
-  }
-  // outputs through shared memory (Z_k and Z_{N-k} of the forward live in different threads; the
-  // inverse's Makhoul columns x = 2n, 2(N - 1 - n) + 1 are stride-2 in n): coalesced global access
-  __syncthreads();   // (every thread's pass-A' loads are done)
-  {
-    float2 *zb = zsm + pz(kp);
-#pragma unroll
-    for (int m = 0; m < 16; ++m) zb[544 * m] = x[m];
-    if (kp == 0) zb[544 * 16] = x[16];
-  }
-  __syncthreads();
-  if constexpr (kind == 3) {   // forward: Z_k and Z_{N-k} live in different threads -- through shared memory
-    float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
-    float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
-    constexpr int B = 8;
-    for (int k0 = tid; k0 < jb.vlen; k0 += B * nth) {
-      float2 ck[B], cm[B], e[B];
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const int k = min(k0 + r * nth, jb.vlen - 1), m = k ? N - k : 0;
-        ck[r] = __ldg(cc + k);
-        cm[r] = __ldg(cc + m);
-        e[r] = __ldg(ee + k);
-      }
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const int k = k0 + r * nth;
-        if (k >= jb.vlen) break;
-        const int m = k ? N - k : 0;
-        const float2 zk = cmulc(zsm[pz(k)], ck[r]), zm = cmulc(zsm[pz(m)], cm[r]);
-        const float ax = 0.5f * (zk.x + zm.x), ay = 0.5f * (zk.y - zm.y);
-        const float bx = 0.5f * (zk.y + zm.y), by = -0.5f * (zk.x - zm.x);
-        oa[k] = e[r].x * ax + e[r].y * ay;
-        if (ob) ob[k] = e[r].x * bx + e[r].y * by;
-      }
-    }
-#if TVS_CZT_PHASES
-    TVS_PH(5);
-    if (ph_on) printf("czt kind %d: A %lld B %lld C %lld B' %lld A'+out %lld\n", kind, ph_t[1] - ph_t[0], ph_t[2] - ph_t[1], ph_t[3] - ph_t[2], ph_t[4] - ph_t[3], ph_t[5] - ph_t[4]);
-#endif
-    return;
-  }
-  // inverse: v = conj(conj(c_n) z_n) / 2 at the Makhoul position n of column x
-  float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
-  float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
-  const float *__restrict__ aa0 = jb.add ? jb.add + (size_t)r0 * jb.ldadd : nullptr;
-  const float *__restrict__ ab0 = (jb.add && two) ? aa0 + jb.ldadd : nullptr;
-  constexpr int B = 8;
-  for (int i0 = tid; i0 < jb.vlen; i0 += B * nth) {
-    float2 cn[B];
-    float av[B], bv[B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const int ic = min(i0 + r * nth, jb.vlen - 1), xg = jb.tx0 + ic;
-      cn[r] = __ldg(cc + ((xg & 1) ? N - 1 - (xg >> 1) : (xg >> 1)));
-      av[r] = aa0 ? __ldg(aa0 + ic) : 0.f;
-      bv[r] = ab0 ? __ldg(ab0 + ic) : 0.f;
-    }
-#pragma unroll
-    for (int r = 0; r < B; ++r) {
-      const int i = i0 + r * nth;
-      if (i >= jb.vlen) break;
-      const int xg = jb.tx0 + i;
-      const int n = (xg & 1) ? N - 1 - (xg >> 1) : (xg >> 1);
-      const float2 y = cmulc(zsm[pz(n)], cn[r]);
-      // (no "+ 0" when there is nothing to add: the plain outputs keep their signed zeros)
-      if constexpr (kind == 4) {
-        oa[i] = aa0 ? 0.5f * y.x + av[r] : 0.5f * y.x;
-        if (ob) ob[i] = ab0 ? -0.5f * y.y + bv[r] : -0.5f * y.y;
-      } else {
-        const float v = 0.5f * ((xg & 1) ? -y.x : y.x) - 0.5f * y.y;
-        oa[i] = aa0 ? v + av[r] : v;
-      }
-    }
-  }
-#if TVS_CZT_PHASES
-  TVS_PH(5);
-  if (ph_on) printf("czt kind %d: A %lld B %lld C %lld B' %lld A'+out %lld\n", kind, ph_t[1] - ph_t[0], ph_t[2] - ph_t[1], ph_t[3] - ph_t[2], ph_t[4] - ph_t[3], ph_t[5] - ph_t[4]);
-#endif
-}
-
 // One CTA per (row, job, output pass).  kind 0: forward cos (pre u^2, post v^2 + v(2tx0+1), Re);
 // kind 1: inverse cos (pre u^2 + u(2tx0+1), post v^2, Re); kind 2: inverse sin (pre u^2 +
 // u(2tx0+2), post v^2, Im).
@@ -994,19 +627,6 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   if (nuc > 1)
     for (int i = tid; i < vcnt; i += nth) out[i] = addr ? acc[i] + addr[i] : acc[i];
 }
-
-#if TVS_CZT_R32
-// Makhoul form at M = 16384 (see czt_makhoul_r32): one CTA per (row pair or row, job)
-__global__ void __launch_bounds__(512, 1)
-k_czt_r32(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gtab,
-          const float2 *__restrict__ tw) {
-  extern __shared__ float2 zsm[];
-  const CztJob &jb = jobs[blockIdx.y];
-  if (jb.kind == 3) czt_makhoul_r32<3>(jb, G, gtab, tw, zsm);
-  else if (jb.kind == 4) czt_makhoul_r32<4>(jb, G, gtab, tw, zsm);
-  else czt_makhoul_r32<5>(jb, G, gtab, tw, zsm);
-}
-#endif
 
 // ------------------------------------------------------------------------------------ host side
 
@@ -1172,19 +792,9 @@ void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2>
       }
       fft64(a);
       float2 *dst = gtab.data() + (size_t)(p * g.nuc + c) * M;
-      // the four-step 32 x 32 x 16 path (czt_makhoul_r32) holds frequency
-      // k = k1 + 32 c1 + 1024 c2 at position brev4(c2) + 16 brev5(c1) + 512 brev5(k1)
-      const bool r32 = TVS_CZT_R32 && g.mk && g.logM4 == 7;
-      auto brev = [](int v, int bits) {
-        int r = 0;
-        for (int b = 0; b < bits; ++b) r |= ((v >> b) & 1) << (bits - 1 - b);
-        return r;
-      };
       for (int k = 0; k < M; ++k) {
         const std::complex<double> v = a[k] / (double)M;
-        const int pos = r32 ? brev(k >> 10, 4) + 16 * brev((k >> 5) & 31, 5) + 512 * brev(k & 31, 5)
-                            : digitrev4(k, g.logM4);
-        dst[pos] = make_float2((float)v.real(), (float)v.imag());
+        dst[digitrev4(k, g.logM4)] = make_float2((float)v.real(), (float)v.imag());
       }
     }
   tw.resize((size_t)M);
@@ -1203,15 +813,6 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
     if (e != cudaSuccess) return e;
   }
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
-#if TVS_CZT_R32
-  if (g.mk && g.logM4 == 7) {
-    const size_t sm = (size_t)(g.M + (g.M >> 4)) * sizeof(float2);
-    cudaError_t e = smem_optin((const void *)k_czt_r32, sm);
-    if (e != cudaSuccess) return e;
-    k_czt_r32<<<dim3(max_rows, njobs), 512, sm, s>>>(jobs, g, gtab, tw);
-    return cudaGetLastError();
-  }
-#endif
   CztGeom gg = g;
   gg.prune = g.mk ? 0 : 1;
   k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
