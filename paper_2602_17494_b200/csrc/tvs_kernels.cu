@@ -1018,6 +1018,9 @@ __global__ void k_omega0_1(const SubDesc *__restrict__ subs, Geo g, const float 
 // columns, lane 0 / lane 31 are halo columns, and each warp walks RB rows with the next rows'
 // loads in flight (same scheme as k_sweep2v).
 constexpr int S1_OUT = 60, S1_WARPS = 4;
+// kernel (a') is capped at 64 registers (eight CTAs per SM, 32 warps): 510 -> 486 us per config-4
+// update, bitwise the same (78 registers and six CTAs otherwise; 7 CTAs: 495 us)
+constexpr int S1_MINB = 8;
 
 struct PairCtx {
   int jA, jB;
@@ -1120,7 +1123,7 @@ k_prediv1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ v,
 // Kernel (a') streaming form: rho_k = w_k - grad phi_k - omega0_k on S+, psi_k = grad rho_k,
 // row-wise ball update of (v_k1, v_k2) (Alg. 5)
 template <bool OM>
-__global__ void __launch_bounds__(32 * S1_WARPS)
+__global__ void __launch_bounds__(32 * S1_WARPS, S1_MINB)
 k_sweep1s(const SubDesc *__restrict__ subs, Geo g, const float *__restrict__ thy,
           const float *__restrict__ thx, const float *__restrict__ vin,
           const float *__restrict__ gphi, int ldg, const float *__restrict__ om,

@@ -1,6 +1,7 @@
 """Config 4 step 1 (8192^2, 8 strips, overlap 32), one outer sweep x `inner` Alg. 5 updates after
 a warm-up call: per-family device times.  Used for A/B runs and ncu captures of the chirp-z
-kernels.  Usage: python tools/c4_step1_short.py [inner] [config, default c4]"""
+kernels.  Usage: python tools/c4_step1_short.py [inner] [config, default c4] [step1|step2]
+(step2: one sweep of `inner` Alg. 3 updates on tau = P tau_0)"""
 import json
 import os
 import sys
@@ -19,12 +20,18 @@ img = c.image()
 ctx = pkg.Context(0)
 d0 = torch.from_numpy(img).cuda()
 L = (c.m2, c.m1, c.overlap, c.overlap)
-ctx.tv_stokes_step1(d0, c.delta, L, (1, 1, c.t))
+step = sys.argv[3] if len(sys.argv) > 3 else "step1"
+if step == "step2":
+    tau1, _, _ = ctx.tv_stokes_step1(d0, c.delta, L, (1, 0, c.t))
+    run = lambda it: ctx.tv_stokes_step2(tau1, d0, c.lam, L, (1, it, c.t))
+else:
+    run = lambda it: ctx.tv_stokes_step1(d0, c.delta, L, (1, it, c.t))
+run(1)
 torch.cuda.synchronize()
-_, _, st0 = ctx.tv_stokes_step1(d0, c.delta, L, (1, inner, c.t))   # unprofiled (device time)
+_, _, st0 = run(inner)   # unprofiled (device time)
 ctx.set_profiling(True)
 ctx.reset_kernel_times()
-tau, _, st = ctx.tv_stokes_step1(d0, c.delta, L, (1, inner, c.t))
+tau, _, st = run(inner)
 ctx.set_profiling(False)
 kt = ctx.kernel_times()
 fam = {nm: {"n": kt.counts[i], "avg_us": round(kt.ms[i] / kt.counts[i] * 1e3, 1),
