@@ -415,7 +415,10 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   const int h = (N + 1) >> 1;
   // loads are issued in batches of B per thread (all loads of a batch before any use: the
   // kernel is latency-bound on them otherwise)
-  constexpr int B = 8;
+  // B = 9: 9 x 512 x 2 >= N = 8193 -- two batches per thread; with 8 a third batch leaves one thread
+  // waiting out a load latency alone before the barrier (config 4: forward 630 -> 603 us, inverse
+  // 1838 -> 1792 us)
+  constexpr int B = 9;
   // only indices 0 .. N - 1 = M/2 are written when the HALF first FFT pair runs (M >= 64); the
   // smaller transforms read every index, so the tail is zero-filled for them
   const int nw = G.logM4 >= 3 ? N : M;
@@ -499,10 +502,10 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
       float2 ck[B], cm[B], e[B];
 #pragma unroll
       for (int r = 0; r < B; ++r) {
-        const int k = min(k0 + r * nth, jb.vlen - 1), m = k ? N - k : 0;
-        ck[r] = __ldg(cc + k);
-        cm[r] = __ldg(cc + m);
+        const int k = min(k0 + r * nth, jb.vlen - 1);
+        ck[r] = __ldg(cc + k);   // c_{N-k} = (-1)^N c_k = -c_k (N = M/2 + 1 odd), c_0 for k = 0
         e[r] = __ldg(ee + k);
+        cm[r] = k ? make_float2(-ck[r].x, -ck[r].y) : ck[r];
       }
 #pragma unroll
       for (int r = 0; r < B; ++r) {
