@@ -2376,7 +2376,7 @@ int solve_nseg(int AT) {
   return std::min(SSEG_MAX, std::max(1, (AT + ls - 1) / ls));
 }
 // column block width of solve4: 16 for tiles up to 512 rows (four CTAs per SM instead of two:
-// config 3 -3 %), else 32; TVS_SOLVE_J=16|32 forces one
+// config 3 -3 %), else 32
 static int solve_j(int AT) {
   return AT <= 512 ? 16 : 32;
 }
