@@ -201,6 +201,7 @@ struct ProjBatch {
   CztJob *d_fj = nullptr, *d_ij = nullptr;
   CztJob *d_ij_add = nullptr;   // inverse jobs writing grad phi + omega0 (the inner loop's)
   int nfj = 0, nij = 0, fj_rows = 0, ij_rows = 0;
+  bool x6 = false;   // Makhoul inverse x jobs of kind 6 (row pairs) instead of kind 5
   float2 *gtab_f = nullptr, *gtab_i = nullptr, *tw_f = nullptr, *tw_i = nullptr;
   // algorithmic work per launch: contraction flops (dense 2MNK), FFT flops of the chirp-z form
   // (2 x 5 M log2 M per FFT pair and row chunk), and the y-solve's HBM bytes
@@ -345,6 +346,7 @@ struct tvs_ctx {
   cudaStream_t pipe_s = nullptr;
   cudaEvent_t ev_pf = nullptr, ev_pj = nullptr;
   bool makhoul = true;           // Makhoul form of the chirp-z where M = 2N - 2 is a power of 4
+  bool czt_x6 = true;            // local projections: x-gradient by differencing phi (kind 6)
                                  // (TVS_CZT_MAKHOUL=0: the general chirp-z form everywhere)
   double *h_energy = nullptr;   // pinned slot for dual energies
   bool sweep2x2 = true;          // kernel (a): two inner updates per pass (TVS_SWEEP2X2=0: off)
@@ -590,6 +592,11 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     B.ij_rows = std::max(B.ij_rows, g.no);
   }
   const bool mk = ctx->makhoul && czt_makhoul_geometry(n1t, ctx->czt_max_m, &B.gf);
+  // the x-gradient of the local (group-scratch) projections by differencing phi (kind 6, one DFT
+  // per row pair); the global projection keeps the sine form (kind 5): its error enters tau --
+  // and step 2's integration of tau -- directly
+  const bool x6 = mk && om && ctx->czt_x6;   // om: the batch of the local solves
+  B.x6 = x6;
   if (mk) {
     B.gi = B.gf;
   } else {
@@ -602,9 +609,11 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
   for (int i = 0; i < B.ntiles; ++i) {
     const Geom &g = gm[i];
     // FFT flops per launch: one FFT pair per CTA (Makhoul form: forward per row pair, inverse
-    // per row pair (y) plus per row (x); general form: per row, chunk and pass, two jobs inverse)
+    // per row pair (y) plus per row pair (x, local batches) or per row (x, global); general
+    // form: per row, chunk and pass, two jobs inverse)
     tf[i] = mk ? (double)((g.nt + 1) / 2) * f1 : (double)g.nt * B.gf.nvp * B.gf.nuc * f1;
-    ti[i] = mk ? (double)((g.no + 1) / 2 + g.no) * f2 : 2.0 * g.no * B.gi.nvp * B.gi.nuc * f2;
+    ti[i] = mk ? (double)((g.no + 1) / 2 + (x6 ? (g.no + 1) / 2 : g.no)) * f2
+               : 2.0 * g.no * B.gi.nvp * B.gi.nuc * f2;
     // algorithmic work: the contraction flops (2MNK of each partial x-DCT) and, for the y-solve,
     // Q-hat read (4 B) per (T row, frequency) plus the two fp32 gradient planes written (8 B)
     // per (output row, frequency); the fp64 pivots are added once per chain below
@@ -710,7 +719,7 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
                       B.qhat + (sl * B.AT + g.f0) * B.ldn, g.nt, ldq, B.ldn, t.tx0, g.bt, n1t,
                       mk ? 3 : 0});
         ij.push_back({B.phx + sl * B.AP * B.ldn, G + io * B.AP * ldG + goff, g.no, B.ldn,
-                      ldG, t.tx0, n1t, g.bo, mk ? 5 : 2});
+                      ldG, t.tx0, n1t, g.bo, mk ? (B.x6 ? 6 : 5) : 2});
         ij.push_back({B.phy + sl * B.AP * B.ldn, G + gplane + io * B.AP * ldG + goff, g.no,
                       B.ldn, ldG, t.tx0, n1t, g.bo, mk ? 4 : 1});
       }
@@ -725,12 +734,15 @@ tvs_status build_proj(tvs_ctx *ctx, Plan &P, ProjBatch &B, const std::vector<Pro
     TRY(upload(ctx, P.bufs, &B.tw_i, tw));
     if (mk) {   // Makhoul form: the axis tables c_n, e_k shared by every job
       std::vector<float2> ct, et;
-      czt_makhoul_tables(n1t, ct, et);
+      std::vector<float> xt;
+      czt_makhoul_tables(n1t, ct, et, xt);
       float2 *dc = nullptr, *de = nullptr;
+      float *dx = nullptr;
       TRY(upload(ctx, P.bufs, &dc, ct));
       TRY(upload(ctx, P.bufs, &de, et));
+      TRY(upload(ctx, P.bufs, &dx, xt));
       for (auto &j : fj) j.pre = dc, j.post = de;
-      for (auto &j : ij) j.pre = dc, j.post = de;
+      for (auto &j : ij) j.pre = dc, j.post = de, j.xs = dx;
     } else {   // chirp tables: one device buffer for both job lists
       std::vector<size_t> pf, qf, pi, qi;
       std::vector<float2> tfw = czt_chirp_tables(B.gf.N, fj, pf, qf);
@@ -1273,7 +1285,7 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
   if (B.czt) {   // chirp-z form of the two partial x-DCTs (full-width strips, large N)
     TRY(run(ctx, s, F_CZT_FWD, 0, B.gfwd[k], [&] {
       return launch_czt(B.d_fj + t0, nt, B.gf.mk ? (B.fj_rows + 1) / 2 : B.fj_rows, B.gf,
-                        B.gtab_f, B.tw_f, s);
+                        B.gtab_f, B.tw_f, s, true);
     }));
   } else {       // dense 3xTF32 tcgen05 contraction (persistent, A in tensor memory)
     TRY(run(ctx, s, F_FWD, 0, B.fwd_flops, [&] {
@@ -1309,8 +1321,9 @@ tvs_status project_group(tvs_ctx *ctx, Plan &P, ProjBatch &B, int k, cudaStream_
   }
   if (B.czt)
     return run(ctx, s, F_CZT_INV, 0, B.ginv[k], [&] {
-      return launch_czt((add_om ? B.d_ij_add : B.d_ij) + 2 * t0, 2 * nt, B.ij_rows, B.gi, B.gtab_i,
-                        B.tw_i, s);
+      return launch_czt((add_om ? B.d_ij_add : B.d_ij) + 2 * t0, 2 * nt,
+                        B.x6 ? (B.ij_rows + 1) / 2 : B.ij_rows, B.gi, B.gtab_i,
+                        B.tw_i, s, false);
     });
   return run(ctx, s, F_INV, 0, B.inv_flops, [&] {
     return launch_gemm_tma_ts(B.d_inv, 2 * B.nstack, B.tcM_inv, B.invN, 144, s);
@@ -1779,6 +1792,7 @@ tvs_status tvs_create(tvs_ctx **out, int rank, int world, const uint8_t *nccl_id
   if (const char *ov = getenv("TVS_OVERLAP")) c->overlap = atoi(ov) != 0;
   if (const char *pg = getenv("TVS_PROJ_GROUP")) c->proj_group = std::max(0, atoi(pg));
   if (const char *mk = getenv("TVS_CZT_MAKHOUL")) c->makhoul = atoi(mk) != 0;
+  if (const char *x6 = getenv("TVS_CZT_X6")) c->czt_x6 = atoi(x6) != 0;
   if (const char *pp = getenv("TVS_PIPE")) c->pipe = atoi(pp) != 0;
   const char *dm = getenv("TVS_DCT");
   c->dct_mode = !dm ? 0 : strcmp(dm, "gemm") == 0 ? 1 : strcmp(dm, "czt") == 0 ? 2 : 0;

@@ -30,8 +30,16 @@
 //   kind 5, inverse x, one row: sum_j b_j sin(theta j (2x+2)) = (-1)^x T(c)[x] + T(d)[x] with
 //     c_k = b_{N-k} cos(delta_{N-k}) (c_0 = 0), d_k = b_k sin(delta_k), delta_k = pi k/(2N)
 //     (sin(theta j (2x+2)) = sin(A_j + delta_j) and sin A_j = (-1)^x cos A_{N-j}), both DCT-IIIs
-//     packed in one DFT.
-// Per pair of rows: 1 transform forward (general form: 2) and 3 inverse (general form: 4).
+//     packed in one DFT -- the global projection's form (its error enters tau directly);
+//   kind 6, inverse x, rows r and r+1 -- the local projections of the inner loop: sum_j b_j sin(theta j (2x+2)) = phi(x+1) - phi(x) with
+//     phi = T(a), a_j = b_j xs_j, xs_j = -1 / (2 sin(pi j/(2N))) (xs_0 = 0: the constant mode has
+//     no x-derivative) -- b_j sin(theta j (2x+2)) = a_j (cos(theta j (2x+3)) - cos(theta j (2x+1)));
+//     the DCT-III by the kind-4 map, phi(x+1) from the neighbouring lane.  phi is formed in fp32
+//     shared memory and differenced (never stored): on the config-3 P tau_0 field the error is
+//     ~2x that of the direct sine form (4e-7 vs 2e-7 of max |D+_x phi|),
+//     for one DFT per row pair instead of one per row.
+// Per pair of rows: 1 transform forward (general form: 2); inverse 2 (local, kind 6) or 3 (global,
+// kind 5; general form: 4).
 #include "tvs_internal.h"
 
 #include <cmath>
@@ -396,12 +404,13 @@ __device__ __forceinline__ void czt_fft_pair(float2 *z, int logM4, const Tw &tw,
 
 // Makhoul form (see the file header): one CTA per (row pair or row, job).  pre = c table,
 // post = e table (n, k < N).
+template <int KSET>   // 1: forward (kind 3 only), 2: inverse (kinds 4, 5, 6)
 __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
                                             const float2 *__restrict__ gtab,
                                             const float2 *__restrict__ tw, float2 *zsm, int MP) {
   const int N = G.N, M = G.M, tid = threadIdx.x, nth = blockDim.x;
-  const int kind = jb.kind;
-  const int r0 = kind == 5 ? blockIdx.x : 2 * blockIdx.x;
+  const int kind = KSET == 1 ? 3 : jb.kind;
+  const int r0 = kind == 5 ? blockIdx.x : 2 * blockIdx.x;   // kind 5: one row, else a row pair
   if (r0 >= jb.rows) return;
   const bool two = kind != 5 && r0 + 1 < jb.rows;
   float2 *tfine = zsm + MP, *tcoarse = tfine + 256;
@@ -452,11 +461,18 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
         const int km = nz ? N - k : 0;   // N - k in [1, N - 1] (index N reads as 0)
         e[r] = in ? __ldg(ee + k) : make_float2(0.f, 0.f);
         c[r] = in ? __ldg(cc + k) : make_float2(0.f, 0.f);
-        if (kind == 4) {   // V_a = e (a''_k - i a''_{N-k}), V_b likewise
+        if (kind != 5) {   // V_a = e (a''_k - i a''_{N-k}), V_b likewise; kind 6: a = Phi_x xs
           p[r] = in ? __ldg(ia + k) : 0.f;
           q[r] = nz ? __ldg(ia + km) : 0.f;
           r_[r] = in && ib ? __ldg(ib + k) : 0.f;
           s[r] = nz && ib ? __ldg(ib + km) : 0.f;
+          if (kind == 6) {
+            const float xk = in ? __ldg(jb.xs + k) : 0.f, xm = nz ? __ldg(jb.xs + km) : 0.f;
+            p[r] *= xk;
+            r_[r] *= xk;
+            q[r] *= xm;
+            s[r] *= xm;
+          }
         } else {           // b_k, b_{N-k} and e_{N-k} of one Phi_x row (cos / sin of delta)
           p[r] = in ? __ldg(ia + k) : 0.f;
           q[r] = nz ? __ldg(ia + km) : 0.f;
@@ -470,7 +486,7 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
         const int k = k0 + r * nth;
         if (k >= nw) break;
         float pp, qq, rr, ss;
-        if (kind == 4) {
+        if (kind != 5) {
           pp = k == 0 ? 2.f * p[r] : p[r];   // a''_0 = 2 a_0
           qq = q[r];
           rr = k == 0 ? 2.f * r_[r] : r_[r];
@@ -520,6 +536,40 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
         if (ob) ob[k] = e[r].x * bx + e[r].y * by;
       }
     }
+  } else if (kind == 6) {   // phi(x) = conj(conj(c_n) z_n) / 2; out = phi(x + 1) - phi(x)
+    // the lanes hold consecutive columns: phi(x + 1) comes from the next lane (lane 31 forms it)
+    const int lane = tid & 31;
+    auto col_n = [&](int x) { return (x & 1) ? N - 1 - (x >> 1) : (x >> 1); };
+    for (int i0 = tid - lane; i0 < jb.vlen; i0 += B * nth) {   // warp-uniform trip count
+      float2 cn[B], cn1[B];
+      float av[B], bv[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int i = i0 + lane + r * nth, x = jb.tx0 + i;
+        const bool ok = i < jb.vlen;
+        cn[r] = x < N ? __ldg(cc + col_n(x)) : make_float2(0.f, 0.f);
+        cn1[r] = (lane == 31 && x + 1 < N) ? __ldg(cc + col_n(x + 1)) : make_float2(0.f, 0.f);
+        av[r] = ok && aa ? __ldg(aa + i) : 0.f;
+        bv[r] = ok && ab ? __ldg(ab + i) : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int i = i0 + lane + r * nth, x = jb.tx0 + i;
+        const float2 y = x < N ? cmulc(zsm[pz(col_n(x))], cn[r]) : make_float2(0.f, 0.f);
+        float fa = 0.5f * y.x, fb = -0.5f * y.y;   // phi_a(x), phi_b(x)
+        float na = __shfl_down_sync(0xffffffffu, fa, 1), nb = __shfl_down_sync(0xffffffffu, fb, 1);
+        if (lane == 31) {
+          const float2 y1 = x + 1 < N ? cmulc(zsm[pz(col_n(x + 1))], cn1[r]) : make_float2(0.f, 0.f);
+          na = 0.5f * y1.x;
+          nb = -0.5f * y1.y;
+        }
+        if (i >= jb.vlen) continue;
+        // D+_x phi = 0 on the last column (sin(pi j) = 0 in the spectral form)
+        const float da = x < N - 1 ? na - fa : 0.f, db = x < N - 1 ? nb - fb : 0.f;
+        oa[i] = aa ? da + av[r] : da;
+        if (ob) ob[i] = ab ? db + bv[r] : db;
+      }
+    }
   } else {           // v = conj(conj(c_n) z_n) / 2 at the Makhoul position of column x
     for (int i0 = tid; i0 < jb.vlen; i0 += B * nth) {
       float2 cn[B];
@@ -554,6 +604,9 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
 // One CTA per (row, job, output pass).  kind 0: forward cos (pre u^2, post v^2 + v(2tx0+1), Re);
 // kind 1: inverse cos (pre u^2 + u(2tx0+1), post v^2, Re); kind 2: inverse sin (pre u^2 +
 // u(2tx0+2), post v^2, Im).
+// KSET (compile time): 0 general form, 1 Makhoul forward, 2 Makhoul inverse -- separate
+// instantiations, so the forward's register allocation does not carry the inverse's paths.
+template <int KSET>
 __global__ void __launch_bounds__(CZT_THREADS)
 k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gtab,
       const float2 *__restrict__ tw) {
@@ -563,7 +616,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   float *acc = reinterpret_cast<float *>(tcoarse + (G.M >> 8) + 1);
   const CztJob jb = jobs[blockIdx.y];
   if (G.mk) {
-    czt_makhoul(jb, G, gtab, tw, zsm, MP);
+    if constexpr (KSET != 0) czt_makhoul<KSET>(jb, G, gtab, tw, zsm, MP);
     return;
   }
   const int row = blockIdx.x;
@@ -721,9 +774,12 @@ bool czt_makhoul_geometry(int N, int max_m, CztGeom *g) {
   return true;
 }
 
-void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab) {
+void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab,
+                        std::vector<float> &xtab) {
   ctab.resize(N);
   etab.resize(N);
+  xtab.assign(N, 0.f);   // kind 6: xs_k = -1 / (2 sin(pi k/(2N))), xs_0 = 0
+  for (int k = 1; k < N; ++k) xtab[k] = (float)(-0.5 / std::sin(M_PI * (double)k / (2.0 * N)));
   const long long n2 = 2LL * N;
   for (long long n = 0; n < N; ++n) {
     const long long r = (n * n) % n2;   // e^{i pi n^2 / N}: n^2 mod 2N exactly
@@ -808,17 +864,21 @@ void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2>
 }
 
 cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
-                       const float2 *gtab, const float2 *tw, cudaStream_t s) {
+                       const float2 *gtab, const float2 *tw, cudaStream_t s, bool fwd) {
   const size_t smem = (size_t)(g.M + (g.M >> 4) + 256 + (g.M >> 8) + 1) * sizeof(float2) +
                       (size_t)g.Vp * sizeof(float);
+  const void *fn = !g.mk ? (const void *)k_czt<0> : fwd ? (const void *)k_czt<1> : (const void *)k_czt<2>;
   if (smem > 48 * 1024) {
-    cudaError_t e = smem_optin((const void *)k_czt, smem);
+    cudaError_t e = smem_optin(fn, smem);
     if (e != cudaSuccess) return e;
   }
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
   CztGeom gg = g;
   gg.prune = g.mk ? 0 : 1;
-  k_czt<<<dim3(max_rows, njobs, g.nvp), CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
+  const dim3 grid(max_rows, njobs, g.nvp);
+  if (!g.mk) k_czt<0><<<grid, CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
+  else if (fwd) k_czt<1><<<grid, CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
+  else k_czt<2><<<grid, CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
   return cudaGetLastError();
 }
 

@@ -97,6 +97,8 @@ struct CztJob {
   // grad phi + omega0 so kernel (a') reads one field instead of two (bitwise the same sum)
   const float *add = nullptr;
   int ldadd = 0;
+  // kind 6 (Makhoul inverse x): per-frequency scale Phi_x -> the cosine coefficients of phi
+  const float *xs = nullptr;
 };
 // host: fill the chirp tables of every job (deduplicated by (c, length)); returns the table
 std::vector<float2> czt_chirp_tables(int N, std::vector<CztJob> &jobs, std::vector<size_t> &pre_off,
@@ -108,16 +110,18 @@ struct CztGeom {
   int nuc, nvp;   // numbers of chunks / passes for the largest job
   int prune = 1;  // pruned first / last FFT passes for narrow jobs (general form)
   int mk = 0;     // 1: Makhoul form -- the partial x-DCTs as DFT_N's of packed real sequences by
-                  // Bluestein with M = 2N - 2 (job kinds 3, 4, 5; see tvs_czt.cu)
+                  // Bluestein with M = 2N - 2 (job kinds 3, 4, 6; see tvs_czt.cu)
 };
 bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g);
 // Makhoul form on an axis of N (any tile): M = 2N - 2 must be a power of 4 <= max_m.
 bool czt_makhoul_geometry(int N, int max_m, CztGeom *g);
 // its per-axis tables: c[n] = e^{i pi n^2 / N} and e[k] = e^{i pi k / (2N)}, n, k < N
-void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab);
+// and xs[k] = -1 / (2 sin(pi k/(2N))) (xs[0] = 0), the kind-6 scale
+void czt_makhoul_tables(int N, std::vector<float2> &ctab, std::vector<float2> &etab,
+                        std::vector<float> &xtab);
 void czt_tables(const CztGeom &g, std::vector<float2> &gtab, std::vector<float2> &tw);
 cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeom &g,
-                       const float2 *gtab, const float2 *tw, cudaStream_t s);
+                       const float2 *gtab, const float2 *tw, cudaStream_t s, bool fwd);   // fwd: Makhoul forward jobs (kind 3)
 
 // Uniform per-subdomain buffer geometry (every subdomain uses the max dims, row pitch `ld`).
 struct Geo {

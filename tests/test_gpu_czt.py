@@ -141,6 +141,32 @@ def test_step1_makhoul_form(ctx, ctx_general, shape, L):
     assert float((t1 - t2).abs().max()) < 2e-5
 
 
+@pytest.fixture(scope="module")
+def ctx_nox6():
+    """The sine form (kind 5) for every Makhoul inverse-x job (TVS_CZT_X6=0)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = _context(TVS_DCT="czt", TVS_CZT_X6="0")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("shape,L", [((40, 32), (2, 2, 4, 4)), ((33, 128), (3, 1, 4, 0)),
+                                     ((129, 512), (2, 4, 6, 8)), ((65, 512), (1, 1, 0, 0))])
+def test_step1_makhoul_x6_ab(ctx, ctx_nox6, shape, L):
+    """The local projections' x-gradient by differencing phi (kind 6, row pairs) against the sine
+    form (kind 5): both match the oracle, and agree with each other to fp32 rounding, on even and
+    odd row counts and single-domain layouts."""
+    img = random_image(*shape, seed=shape[0] * 7 + shape[1] + 11)
+    check_step1(ctx, img, 0.05, L, 3, 4)
+    check_step1(ctx_nox6, img, 0.05, L, 3, 4)
+    d0 = torch.from_numpy(img).cuda()
+    t1, _, _ = ctx.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125))
+    t2, _, _ = ctx_nox6.tv_stokes_step1(d0, 0.05, L, (3, 4, 0.125))
+    torch.cuda.synchronize()
+    assert float((t1 - t2).abs().max()) < 2e-5
+
+
 def test_pipelined_groups_bitwise(ctx):
     """Two subdomain groups in flight on two streams with separate scratch (TVS_PIPE=1) give
     bitwise the serial schedule's tau and p, also with more than two groups (TVS_PROJ_GROUP) and
