@@ -404,9 +404,26 @@ __device__ __forceinline__ void czt_fft_pair(float2 *z, int logM4, const Tw &tw,
 
 // Makhoul form (see the file header): one CTA per (row pair or row, job).  pre = c table,
 // post = e table (n, k < N).
+// L2 prefetch (TVS_CZT_L2PF): one CTA per SM and nothing to overlap its load / output phases with,
+// so while the FFT pair runs, four threads ask L2 for (a) this item's omega0 rows (read by the
+// output phase, TVS ncu: the output phase's first uses are long-scoreboard stalls) and (b) the
+// input rows of the item one wave ahead (linear CTA id + G.ahead): its load phase then waits on
+// L2 instead of DRAM.  No shared memory or registers held (the staged variant's carve-out cost the
+// tables their L1); results bitwise the same.
+#ifndef TVS_CZT_L2PF
+#define TVS_CZT_L2PF 1
+#endif
+__device__ __forceinline__ void l2_prefetch(const float *p, int n) {
+  if (!p || n <= 0) return;
+  const unsigned long long a = reinterpret_cast<unsigned long long>(p), lo = a & ~15ull;
+  const unsigned long long hi = (a + 4ull * (unsigned long long)n + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((unsigned)(hi - lo))
+               : "memory");
+}
+
 template <int KSET>   // 1: forward (kind 3 only), 2: inverse (kinds 4, 5, 6)
-__device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
-                                            const float2 *__restrict__ gtab,
+__device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztJob *__restrict__ jobs,
+                                            const CztGeom &G, const float2 *__restrict__ gtab,
                                             const float2 *__restrict__ tw, float2 *zsm, int MP) {
   const int N = G.N, M = G.M, tid = threadIdx.x, nth = blockDim.x;
   const int kind = KSET == 1 ? 3 : jb.kind;
@@ -507,6 +524,22 @@ __device__ __forceinline__ void czt_makhoul(const CztJob &jb, const CztGeom &G,
   }
   __syncthreads();
   const CztIo io{nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, false, false, true};
+#if TVS_CZT_L2PF
+  if (tid < 4 && G.ahead > 0) {
+    if (tid < 2) {   // this item's omega0 rows (output phase)
+      if (jb.add && (tid == 0 || two)) l2_prefetch(jb.add + (size_t)(r0 + tid) * jb.ldadd, jb.vlen);
+    } else {         // the input rows of the item one wave ahead
+      const long long ln = (long long)blockIdx.y * gridDim.x + blockIdx.x + G.ahead;
+      if (ln < (long long)gridDim.x * gridDim.y) {
+        const CztJob &jn = jobs[ln / gridDim.x];
+        const int bxn = (int)(ln % gridDim.x), kn = KSET == 1 ? 3 : jn.kind;
+        const int rn = (kn == 5 ? bxn : 2 * bxn) + (tid - 2);
+        if ((tid == 2 || kn != 5) && rn < jn.rows)
+          l2_prefetch(jn.in + (size_t)rn * jn.ldin, kn == 3 ? jn.ulen : N);
+      }
+    }
+  }
+#endif
   czt_fft_pair(zsm, G.logM4, twd, gtab, io);
   float *__restrict__ oa = jb.out + (size_t)r0 * jb.ldout;
   float *__restrict__ ob = two ? oa + jb.ldout : nullptr;
@@ -616,7 +649,7 @@ k_czt(const CztJob *__restrict__ jobs, CztGeom G, const float2 *__restrict__ gta
   float *acc = reinterpret_cast<float *>(tcoarse + (G.M >> 8) + 1);
   const CztJob jb = jobs[blockIdx.y];
   if (G.mk) {
-    if constexpr (KSET != 0) czt_makhoul<KSET>(jb, G, gtab, tw, zsm, MP);
+    if constexpr (KSET != 0) czt_makhoul<KSET>(jb, jobs, G, gtab, tw, zsm, MP);
     return;
   }
   const int row = blockIdx.x;
@@ -875,6 +908,7 @@ cudaError_t launch_czt(const CztJob *jobs, int njobs, int max_rows, const CztGeo
   if (max_rows <= 0 || njobs <= 0) return cudaSuccess;
   CztGeom gg = g;
   gg.prune = g.mk ? 0 : 1;
+  gg.ahead = sm_count();   // one CTA per SM: the next wave starts ~one SM count later
   const dim3 grid(max_rows, njobs, g.nvp);
   if (!g.mk) k_czt<0><<<grid, CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);
   else if (fwd) k_czt<1><<<grid, CZT_THREADS, smem, s>>>(jobs, gg, gtab, tw);

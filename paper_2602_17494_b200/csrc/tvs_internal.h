@@ -111,6 +111,7 @@ struct CztGeom {
   int prune = 1;  // pruned first / last FFT passes for narrow jobs (general form)
   int mk = 0;     // 1: Makhoul form -- the partial x-DCTs as DFT_N's of packed real sequences by
                   // Bluestein with M = 2N - 2 (job kinds 3, 4, 6; see tvs_czt.cu)
+  int ahead = 0;  // Makhoul form: L2 prefetch of the item this many CTAs ahead (set by launch_czt)
 };
 bool czt_geometry(int N, int ulen_max, int vlen_max, int max_m, CztGeom *g);
 // Makhoul form on an axis of N (any tile): M = 2N - 2 must be a power of 4 <= max_m.

@@ -241,3 +241,52 @@ def test_config5_weak1_step1_sampled(ctx):
     e_div = np.abs(ops.div(tau_g.cpu().numpy().astype(np.float64))).max()
     _log("c5w1_step1_div_tau", div=e_div)
     assert e_div <= TOL, e_div
+
+
+def test_config4_bench_schedule_energies_oracle_evaluated(ctx):
+    """The bench workload exactly (config 4, 30 x 20 per step, both steps, bench.py's headline):
+    the library's E_1, D_1, gap_1 (step 1) and E_2, D_2, gap_2 (step 2) -- fixed-order fp64
+    reductions on the device -- against the oracle's energy functions evaluated in fp64 on the
+    library's own outputs tau, p^1, d, p^2 (E_1 P:249, D_TFS P:675 with f = P tau_0 / delta from
+    the oracle's global projection, E_2 P:475-479 with g from the oracle's integration of tau, D_IRV2
+    P:679, gap SURVEY C-15), at the north star's 1e-4 relative; and weak duality G <= E for both
+    steps with the oracle's dual objectives (Cor. tfsdual P:240-250, the ROF dual P:504-510)."""
+    c = CONFIGS["c4"]
+    d0 = _image("c4")
+    L = _layout(c)
+    d0_dev = torch.from_numpy(d0).cuda()
+    tau_g, p1_g, s1 = ctx.tv_stokes_step1(d0_dev, c.delta, L, (c.sweeps, c.inner, c.t), want_p=True)
+    d_g, p2_g, s2 = ctx.tv_stokes_step2(tau_g, d0_dev, c.lam, L, (c.sweeps, c.inner, c.t), want_p=True)
+    torch.cuda.synchronize()
+    assert s1.pixel_updates > 0 and s2.pixel_updates > 0
+    tau = tau_g.cpu().numpy().astype(np.float64)
+    p1 = p1_g.cpu().numpy().astype(np.float64).reshape(2, 2, *tau.shape[1:])
+    d = d_g.cpu().numpy().astype(np.float64)
+    p2 = p2_g.cpu().numpy().astype(np.float64)
+    del tau_g, p1_g, d_g, p2_g
+    d0 = d0.astype(np.float64)
+    ptau0 = spectral.project(S.tau0(d0))
+    e1 = S.primal_energy_tfs(tau, ptau0, c.delta)
+    dd1 = S.dual_energy_tfs(p1, ptau0 / c.delta)
+    g1 = S.duality_gap(tau, p1)
+    G1 = S.dual_value_tfs(p1, ptau0, c.delta)
+    del ptau0
+    alpha, g, f2 = S.irv2_data(d0, tau, c.lam)
+    e2 = S.primal_energy_irv2(d, d0, g, alpha)
+    dd2 = S.dual_energy_irv2(p2, f2)
+    g2 = S.duality_gap(d - g, p2)
+    G2 = S.dual_value_irv2(p2, d0, g, alpha)
+    r = {"E1": _rel_(s1.primal_energy, e1), "D1": _rel_(s1.dual_energy, dd1),
+         "E2": _rel_(s2.primal_energy, e2), "D2": _rel_(s2.dual_energy, dd2)}
+    _log("c4_bench_schedule_energies", gap1=s1.gap, gap1_ref=g1, gap2=s2.gap, gap2_ref=g2,
+         G1=G1, G2=G2, **{k + "_rel": v for k, v in r.items()})
+    assert all(v <= TOL for v in r.values()), r
+    assert abs(s1.gap - g1) <= TOL * e1, (s1.gap, g1)
+    assert abs(s2.gap - g2) <= TOL * e2, (s2.gap, g2)
+    # weak duality on the oracle's side (fp64): the dual objective never exceeds the primal
+    assert G1 <= e1 * (1 + 1e-12), (G1, e1)
+    assert G2 <= e2 * (1 + 1e-12), (G2, e2)
+
+
+def _rel_(a, b):
+    return abs(a - b) / abs(b)
